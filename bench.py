@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark: unique valid SAT solutions per second (BASELINE.json metric).
+
+Workload (configs[1], SURVEY.md section 8 "C2"): the ISCAS89-shaped synthetic
+CNF encode(random_circuit(15850, 600, 40, 240, 7)) -- 10,200 vars, 31,685
+clauses, 21,895-node circuit -- sampled at batch 65,536 rows per GPU with the
+reference hyper-parameters (GD, lr 10, 5 iterations, seed 1, f32).
+
+One "step" = one restart of satgrad::run: init_soft_inputs, the iteration-0
+harvest, then 5 x (embed+forward+loss+backward+GD, harvest) over the whole
+batch.  K steps run back to back inside one sgx_run (ReinitOnExhaust with a
+restart budget of K), W warm-up restarts before.  Inputs (tape 3.5 GB, V 135
+MB) exceed the 126 MB L2, so no explicit flush is needed between steps.
+
+  value   unique solutions found in the timed restarts / device time
+          (CUDA events on the sampler stream, max over ranks)
+  e2e     the same metric through the public API run() from host buffers:
+          circuit upload (H2D), the run, and fetching every solution key (D2H)
+  --impl reference   the reference's own CPU sampler (oracle/_ref, built from
+          /root/reference sources) on the host cores.
+
+Multi-GPU (torchrun): rank g samples global rows [g*B, (g+1)*B) (RNG keyed by
+global row, so shards are disjoint slices of one big batch); solutions are
+deduplicated across ranks by an all-gather of 64-bit fingerprints.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "unique valid solutions/sec"
+UNIT = "solutions/s"
+WORKLOADS = {
+    # name: (instance file, default batch, reference-arm batch)
+    "c2_iscas": ("c2_iscas", 65536, 2048),
+    "c4_blasted": ("c4_blasted", 65536, 512),
+    "c3a_or50": ("c3a_or50", 1 << 20, 20000),
+    "c3b_or100": ("c3b_or100", 1 << 20, 20000),
+    "c1b_random": ("c1b_random", 1024, 1024),
+}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            if self.thread:
+                self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl" if args.impl != "reference" else "gloo")
+        pg = dist
+    return world, rank, local, pg
+
+
+def cpu_reference(inst_name, batch, iterations, seed, steps=1, timeout_s=0.0):
+    """The reference's satgrad::run on the host cores (oracle/_ref); falls back
+    to the C port (oracle/libsgx_oracle.so) when the reference was not built."""
+    from paper_2502_08673_b200 import load_instance, write_dimacs
+    from oracle.oracle import PortLib, RefInstance, ref_available
+    cores = os.cpu_count() or 1
+    inst = load_instance(inst_name)
+    uniq, wall = 0, 0.0
+    if ref_available():
+        ri = RefInstance.from_dimacs(write_dimacs(inst.cnf))
+        kind = "reference"
+        for _ in range(steps):
+            r = ri.run(batch=batch, iterations=iterations, seed=seed, threads=cores,
+                       use_f32=True, timeout_s=timeout_s)
+            uniq += r.unique
+            wall += r.wall
+    else:
+        kind, cores = "port", 1
+        for _ in range(steps):
+            r = PortLib().run(inst, batch=batch, iterations=iterations, seed=seed,
+                              timeout_s=timeout_s)
+            uniq += r.unique
+            wall += r.wall
+    return {"value": uniq / wall if wall > 0 else 0.0, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{steps} x satgrad::run(batch={batch}, iterations={iterations}, seed={seed}, "
+                      f"f32, threads={cores}) on {inst_name}: rows are independent, so unique/s "
+                      f"per row is batch-invariant; {uniq} unique in {wall:.2f} s",
+            "unique": uniq, "wall_s": wall}
+
+
+def run_reference_arm(args, world, rank):
+    name, batch, ref_batch = WORKLOADS[args.workload]
+    batch = args.batch or batch
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        cpu_reference(name, ref_batch, args.iterations, 1, steps=1)
+    res = cpu_reference(name, ref_batch, args.iterations, 1, steps=args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * res["wall_s"] / max(1, args.steps), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": name, "batch": batch, "iterations": args.iterations,
+                   "reference_sample_batch": ref_batch, "lr": 10.0, "seed": 1},
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200_arm(args, world, rank, local, dist):
+    import torch
+    from paper_2502_08673_b200 import (DeviceCircuit, RestartPolicy, Sampler, SamplerConfig,
+                                       load_instance, run_instance)
+    name, batch, ref_batch = WORKLOADS[args.workload]
+    batch = args.batch or batch
+    dev = local
+    torch.cuda.set_device(dev)
+    inst = load_instance(name)
+    dc = DeviceCircuit.from_instance(inst, device=dev)
+    info = dc.info()
+
+    def cfg_for(restarts):
+        return SamplerConfig(batch=batch, iterations=args.iterations, seed=1,
+                             restart=RestartPolicy.REINIT_ON_EXHAUST if restarts > 1 else
+                             RestartPolicy.NONE, max_restarts=max(1, restarts - 1),
+                             row_offset=rank * batch)
+
+    sampler = Sampler(dc, cfg_for(max(1, args.warmup)))
+    if args.warmup > 0:
+        sampler.run()
+    sampler.close()
+    sampler = Sampler(dc, cfg_for(args.steps))
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev) as clk:
+        t0 = time.perf_counter()
+        st = sampler.run()
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t0
+    if dist:
+        dist.barrier()
+    keys = sampler.fetch()
+    local_unique = len(keys)
+    device_s = st.device_ms / 1000.0
+    restarts_done = st.restarts + 1
+    # global dedup across ranks by 64-bit fingerprint (outside the timed region)
+    fp = np.zeros(0, np.uint64)
+    if len(keys):
+        h = np.full(len(keys), 0x243F6A8885A308D3, np.uint64)
+        for q in range(keys.shape[1]):
+            h = (h ^ keys[:, q]) * np.uint64(0x100000001B3)
+        fp = h
+    if dist:
+        import torch.distributed as tdist
+        t_dev = torch.tensor([device_s], dtype=torch.float64, device=f"cuda:{dev}")
+        tdist.all_reduce(t_dev, op=tdist.ReduceOp.MAX)
+        device_s = float(t_dev.item())
+        n = torch.tensor([len(fp)], dtype=torch.int64, device=f"cuda:{dev}")
+        ns = [torch.zeros_like(n) for _ in range(world)]
+        tdist.all_gather(ns, n)
+        mx = max(int(x.item()) for x in ns)
+        buf = torch.zeros(mx, dtype=torch.int64, device=f"cuda:{dev}")
+        buf[:len(fp)] = torch.from_numpy(fp.view(np.int64)).to(buf.device)
+        bufs = [torch.zeros_like(buf) for _ in range(world)]
+        tdist.all_gather(bufs, buf)
+        allfp = np.concatenate([b[:int(c.item())].cpu().numpy() for b, c in zip(bufs, ns)])
+        global_unique = len(np.unique(allfp))
+    else:
+        global_unique = local_unique
+    sampler.close()
+
+    if rank != 0:
+        return
+    value = global_unique / device_s if device_s > 0 else 0.0
+    ph = st.phase_ms
+    n_steps = args.steps * args.iterations
+    # Dominant kernel roofline (SURVEY.md 8(d) compulsory-tape model).
+    ncone, cpi = info["cone_nodes"], info["cpi"]
+    kernels = {
+        "k_forward": (ph["forward"], n_steps, 4 * (cpi + ncone) * batch),
+        "k_backward": (ph["backward"], n_steps, 4 * (ncone + 2 * cpi) * batch),
+    }
+    dom = max(kernels, key=lambda k: kernels[k][0])
+    t_ms, nl, bytes_per_launch = kernels[dom]
+    avg_s = (t_ms / max(1, nl)) / 1000.0
+    peak, peak_kind = peaks()
+    achieved = bytes_per_launch / avg_s / 1e9 if avg_s > 0 else 0.0
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"ncu_{name}.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get(dom, {}).get("dram_bytes_per_launch")
+
+    # e2e through the public API from host buffers (upload + run + fetch).
+    e2e_cfg = cfg_for(args.steps)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    res = run_instance(inst, e2e_cfg, device=dev)
+    e2e_wall = time.perf_counter() - t0
+    h2d = sum(x.nbytes for x in (inst.kind, inst.a, inst.b, inst.var, inst.out_var, inst.out_tgt,
+                                 inst.cpi, inst.ucpi, inst.clause_ptr, inst.clause_lit))
+    d2h = res.solutions.keys.nbytes
+    e2e = {"value": res.stats.unique_count / e2e_wall, "unit": UNIT,
+           "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
+           "wall_s": e2e_wall}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference(name, ref_batch, args.iterations, 1, steps=1)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * device_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": name, "batch": batch, "global_batch": batch * world,
+                   "iterations": args.iterations, "lr": 10.0, "seed": 1,
+                   "parallelism": f"sample-shard x{world}",
+                   "l2": "inputs > L2 (tape %.1f GB)" % (4 * ncone * batch / 1e9)},
+        "unique": global_unique, "restarts": restarts_done, "attempts": st.attempts,
+        "wall_s": wall, "device_s": device_s,
+        "phase_ms": {k: round(v, 3) for k, v in ph.items()},
+        "gpu_launches": st.launches,
+        "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "avg_launch_ms": avg_s * 1000.0},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c2_iscas", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--iterations", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local, dist = dist_setup(args)
+    try:
+        if args.impl == "reference":
+            run_reference_arm(args, world, rank)
+        else:
+            run_b200_arm(args, world, rank, local, dist)
+    finally:
+        if dist:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

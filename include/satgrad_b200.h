@@ -1,0 +1,173 @@
+/*
+ * satgrad_b200 -- C-ABI of the B200-native (sm_100a) sampling loop.
+ *
+ * This is the drop-in boundary for the reference's data-parallel sampling
+ * path (satgrad, arXiv 2502.08673).  Everything below this header runs on the
+ * GPU; everything above it (CNF parsing, circuit extraction, path
+ * classification) stays in the caller.  Plain C types only: no C++ or torch
+ * types cross the boundary, arrays are host pointers with explicit sizes, and
+ * every function returns 0 on success or a negative SGX_E* code, with a
+ * thread-local message in sgx_last_error().
+ *
+ * Which reference interface each entry point replaces (paths relative to
+ * /root/reference/proj):
+ *
+ *   sgx_circuit_upload   Circuit + CnfFormula + PathClassification as consumed
+ *                        by run() (include/satgrad/circuit.hpp:20-40,
+ *                        include/satgrad/cnf.hpp:27-38,
+ *                        include/satgrad/extract.hpp:58-63); adds the
+ *                        levelization / device-layout pass the reference lacks.
+ *   sgx_sampler_create   SamplerConfig (include/satgrad/sampler.hpp:23-33).
+ *   sgx_run              satgrad::run (include/satgrad/sampler.hpp:79-81,
+ *                        src/sampler.cpp:89-203), f32 instantiation.
+ *   sgx_init             init_soft_inputs (sampler.hpp:76-77, sampler.cpp:54-64)
+ *                        + the double->S cast at sampler.cpp:156-159.
+ *   sgx_step             embed + forward + loss + backward + gd_step
+ *                        (autodiff.hpp:31-82, autodiff.cpp:57-290) fused.
+ *   sgx_harvest          the harvest lambda (sampler.cpp:124-153): harden,
+ *                        free bits, eval_discrete (circuit.cpp:124-152), PO
+ *                        check, eval_cnf (cnf.cpp:129-147), dedupe_key +
+ *                        SolutionSet::insert (sampler.cpp:18-44).
+ *   sgx_fetch_solutions  SolutionSet keys in insertion order
+ *                        (sampler.hpp:37-55), packed like dedupe_key.
+ *   sgx_forward /        forward<float> / backward<float> (autodiff.hpp:52-78)
+ *   sgx_backward         as parity taps, in the reference's layouts.
+ */
+#ifndef SATGRAD_B200_H
+#define SATGRAD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGX_OK 0
+#define SGX_E_INVALID (-1)  /* std::invalid_argument in the reference */
+#define SGX_E_CUDA (-2)     /* CUDA runtime / device failure          */
+#define SGX_E_NOMEM (-3)    /* device allocation failed               */
+#define SGX_E_STATE (-4)    /* call out of order                      */
+
+/* GateKind order of circuit.hpp:20-22. */
+enum sgx_gate_kind {
+  SGX_INPUT = 0, SGX_CONST0, SGX_CONST1, SGX_BUF, SGX_NOT,
+  SGX_AND2, SGX_OR2, SGX_XOR2, SGX_XNOR2
+};
+
+/* RestartPolicy, sampler.hpp:21. */
+enum sgx_restart_policy { SGX_RESTART_NONE = 0, SGX_RESTART_REINIT_ON_EXHAUST = 1 };
+
+typedef struct sgx_ctx sgx_ctx;
+typedef struct sgx_circuit sgx_circuit;
+typedef struct sgx_sampler sgx_sampler;
+
+/* The reference's hot-path inputs, host-owned, copied by sgx_circuit_upload. */
+typedef struct {
+  /* Circuit::nodes in topological order: operands always at lower ids. */
+  int32_t n_nodes;
+  const int32_t* kind; /* sgx_gate_kind                                  */
+  const int32_t* a;    /* operand node ids, -1 if unused                  */
+  const int32_t* b;
+  const int32_t* var;  /* variable owned by the node, 0 = internal        */
+  int32_t num_vars;    /* CnfFormula::num_vars (aux vars are above it)    */
+  /* Circuit::outputs (PoEntry list, incl. aux outputs), in order. */
+  int32_t n_outputs;
+  const int32_t* out_var;
+  const uint8_t* out_target;
+  /* PathClassification: V column order and free-bit order. */
+  int32_t n_cpi;
+  const int32_t* cpi;
+  int32_t n_ucpi;
+  const int32_t* ucpi;
+  /* CnfFormula::clauses as CSR of DIMACS literals (+v / -v). */
+  int64_t n_clauses;
+  const int64_t* clause_ptr; /* n_clauses + 1 */
+  const int32_t* clause_lit;
+  /* ExtractionResult::unsat: run() returns immediately with a note. */
+  int32_t unsat;
+} sgx_circuit_desc;
+
+/* SamplerConfig plus the sharding fields the multi-GPU path needs. */
+typedef struct {
+  int32_t batch;           /* rows on this device                        */
+  int32_t iterations;
+  double learning_rate;
+  uint64_t seed;
+  int64_t max_solutions;   /* 0 = no quota                               */
+  double timeout_s;        /* 0 = none; checked between iterations       */
+  int32_t restart_policy;  /* sgx_restart_policy                         */
+  int64_t row_offset;      /* global row of local row 0 (RNG coordinates)*/
+  int64_t solution_capacity; /* initial device solution store, 0 = auto  */
+  int32_t max_restarts;    /* safety valve, reference uses 1000          */
+  int32_t reserved;
+} sgx_sampler_cfg;
+
+typedef struct {
+  int64_t unique_count;
+  int64_t attempts;
+  double wall_time_s;
+  double throughput;
+  int32_t restarts;
+  int32_t timed_out;
+  int32_t n_loss;     /* entries in the loss trace                       */
+  int32_t n_harvest;  /* entries in the new-unique trace                 */
+  int32_t unsat;      /* run skipped: instance unsatisfiable             */
+  int32_t reserved;
+  double device_ms;   /* CUDA-event time of the whole run on its stream  */
+  int64_t launches;   /* kernels launched by the run                      */
+} sgx_run_stats;
+
+const char* sgx_last_error(void);
+const char* sgx_version(void);
+
+int sgx_open(int device, sgx_ctx** out);
+int sgx_close(sgx_ctx* ctx);
+
+int sgx_circuit_upload(sgx_ctx* ctx, const sgx_circuit_desc* desc, sgx_circuit** out);
+/* info[0..15]: nodes, cone nodes, cone edges, soft levels, bit levels,
+ * fwd ops, bwd ops, bit ops, clauses, literals, key words, cpi, ucpi,
+ * outputs, num_vars, unsat */
+int sgx_circuit_info(const sgx_circuit* c, int64_t* info16);
+int sgx_circuit_free(sgx_circuit* c);
+
+/* Host-only layout compiler (no device calls): the same levelization and
+ * device program construction sgx_circuit_upload performs.  For CPU tests. */
+int sgx_layout_stats(const sgx_circuit_desc* desc, int64_t* info16);
+
+int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler** out);
+int sgx_sampler_free(sgx_sampler* s);
+
+/* One restart's building blocks (what sgx_run loops over). */
+int sgx_init(sgx_sampler* s, int32_t restart);
+int sgx_step(sgx_sampler* s, double* loss_total);
+int sgx_harvest(sgx_sampler* s, int32_t restart, int32_t iter, int64_t* attempts,
+                int64_t* added);
+
+/* satgrad::run: the whole restart x iteration loop with quota, timeout and
+ * restart policy; solutions stay on the device until fetched. */
+int sgx_run(sgx_sampler* s, sgx_run_stats* stats);
+int sgx_run_traces(sgx_sampler* s, double* loss_trace, int64_t* new_unique);
+int64_t sgx_solution_count(const sgx_sampler* s);
+int32_t sgx_key_words(const sgx_sampler* s);
+int sgx_fetch_solutions(sgx_sampler* s, int64_t first, int64_t count, uint64_t* keys);
+/* Device time of the last sgx_run by phase, milliseconds:
+ * [init, step(fwd+bwd), harvest, fwd, bwd, eval, keys, commit] */
+int sgx_phase_times(const sgx_sampler* s, double* ms8);
+
+/* Parity taps over ALL nodes, reference layouts: p / v / dv / dp are [batch][n_cpi]
+ * row-major, tape is [n_nodes][batch] in reference node order, y is
+ * [batch][n_outputs]. */
+int sgx_forward(sgx_circuit* c, const float* p, int32_t batch, float* tape, float* y);
+int sgx_backward(sgx_circuit* c, const float* tape, int32_t batch, const float* v,
+                 float* dv, float* dp);
+/* embed (autodiff.cpp:57-62): clamped sigmoid of a host array, on device. */
+int sgx_embed(sgx_ctx* ctx, const float* v, int64_t n, float* p);
+
+/* Bit-exact device sigmoid / expf over a host array (parity of the glibc
+ * expf restatement used by embed/backward). */
+int sgx_expf(sgx_ctx* ctx, const float* x, int64_t n, float* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SATGRAD_B200_H */

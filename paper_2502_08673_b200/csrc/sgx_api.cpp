@@ -1,0 +1,751 @@
+// C-ABI implementation: device context, circuit upload, the sampler and its
+// run loop (a restatement of run_impl, sampler.cpp:89-194, driving the
+// kernels in sgx_kernels.cu), and the parity taps.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/satgrad_b200.h"
+#include "sgx_kernels.cuh"
+#include "sgx_launch.hpp"
+#include "sgx_layout.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NoMem : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct StateError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));                \
+  } while (0)
+
+// glibc __exp2f_data.tab (see sgx_kernels.cuh expf_glibc).
+const uint64_t kExpTab[32] = {
+    0x3ff0000000000000ull, 0x3fefd9b0d3158574ull, 0x3fefb5586cf9890full, 0x3fef9301d0125b51ull,
+    0x3fef72b83c7d517bull, 0x3fef54873168b9aaull, 0x3fef387a6e756238ull, 0x3fef1e9df51fdee1ull,
+    0x3fef06fe0a31b715ull, 0x3feef1a7373aa9cbull, 0x3feedea64c123422ull, 0x3feece086061892dull,
+    0x3feebfdad5362a27ull, 0x3feeb42b569d4f82ull, 0x3feeab07dd485429ull, 0x3feea47eb03a5585ull,
+    0x3feea09e667f3bcdull, 0x3fee9f75e8ec5f74ull, 0x3feea11473eb0187ull, 0x3feea589994cce13ull,
+    0x3feeace5422aa0dbull, 0x3feeb737b0cdc5e5ull, 0x3feec49182a3f090ull, 0x3feed503b23e255dull,
+    0x3feee89f995ad3adull, 0x3feeff76f2fb5e47ull, 0x3fef199bdd85529cull, 0x3fef3720dcef9069ull,
+    0x3fef5818dcfba487ull, 0x3fef7c97337b9b5full, 0x3fefa4afa2a490daull, 0x3fefd0765b6e4540ull};
+
+// Owning device buffer.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    reset();
+    size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      throw NoMem("cudaMalloc(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e));
+    }
+    n = count;
+  }
+  void upload(const std::vector<T>& v, cudaStream_t st) {
+    alloc(v.size());
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  }
+  void swap(DBuf& o) {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+  }
+};
+
+int round_up(long long x, int m) { return static_cast<int>((x + m - 1) / m * m); }
+
+uint64_t next_pow2(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+std::vector<int4> to_int4(const std::vector<sgx::I4>& v) {
+  std::vector<int4> out(v.size());
+  for (size_t i = 0; i < v.size(); ++i) out[i] = make_int4(v[i].x, v[i].y, v[i].z, v[i].w);
+  return out;
+}
+
+struct DevSoft {
+  DBuf<int4> fwd, bwd;
+  DBuf<int> out_row;
+  int n_fwd_chunks = 0, n_bwd_chunks = 0, n_rows = 0;
+  void upload(const sgx::SoftProgram& P, cudaStream_t st) {
+    fwd.upload(to_int4(P.fwd), st);
+    bwd.upload(to_int4(P.bwd), st);
+    out_row.upload(P.out_row, st);
+    n_fwd_chunks = static_cast<int>(P.fwd.size() / sgx::kU);
+    n_bwd_chunks = static_cast<int>(P.bwd.size() / sgx::kU);
+    n_rows = P.n_rows;
+  }
+};
+
+}  // namespace
+
+struct sgx_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  DBuf<uint64_t> exp_tab;
+};
+
+struct sgx_circuit {
+  sgx_ctx* ctx = nullptr;
+  sgx::Layout L;
+  bool layout_ok = false;
+  DevSoft cone, full;
+  DBuf<int4> bit_ops;
+  DBuf<int> bit_lvl_ptr, cpi_bit_row, ucpi_bit_row, out_bit_row, clause_ptr, clause_enc, key_bit_row;
+  DBuf<uint8_t> out_tgt;
+  int n_bit_levels = 0;
+};
+
+struct sgx_sampler {
+  sgx_circuit* c = nullptr;
+  sgx_sampler_cfg cfg{};
+  cudaStream_t st = nullptr;
+  int Bp = 0, W = 0, wpc = 8, n_partial = 148;
+  DBuf<float> V, tape, adj, row_loss;
+  DBuf<double> partial;
+  DBuf<uint32_t> BT, valid, newmask;
+  DBuf<int> slot_of_row, block_count;
+  DBuf<uint64_t> K, store;
+  DBuf<unsigned long long> tkeys, tmeta;
+  uint64_t tcap = 0;
+  long long table_count = 0;
+  long long store_cap = 0, n_solutions = 0;
+  uint64_t epoch = 0;
+  long long launches = 0;
+  DBuf<sgx::HarvestOut> hout;
+  sgx::HarvestOut* hpin = nullptr;
+  // last run
+  std::vector<double> loss_trace;
+  std::vector<int64_t> new_unique;
+  sgx_run_stats stats{};
+  double phase_ms[8] = {0};
+  cudaEvent_t ev[8] = {nullptr};
+};
+
+namespace {
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return SGX_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return SGX_E_INVALID;
+  } catch (const NoMem& e) {
+    g_err = e.what();
+    return SGX_E_NOMEM;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return SGX_E_CUDA;
+  } catch (const StateError& e) {
+    g_err = e.what();
+    return SGX_E_STATE;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SGX_E_INVALID;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw std::invalid_argument(std::string(what) + " is null");
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.0f;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  return ms;
+}
+
+// ---------------------------------------------------------------- sampler ops
+void sampler_init(sgx_sampler* s, int restart) {
+  const auto& L = s->c->L;
+  uint64_t prefix = sgx::fold(sgx::fold(sgx::fold(sgx::kPi, s->cfg.seed), sgx::kInitTag),
+                              static_cast<uint64_t>(static_cast<int64_t>(restart)));
+  sgx::launch_init_v(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, prefix, s->cfg.row_offset);
+  s->launches += L.cpi.empty() ? 0 : 1;
+  CK(cudaGetLastError());
+}
+
+void sampler_step(sgx_sampler* s) {
+  sgx_circuit* c = s->c;
+  const uint64_t* tab = c->ctx->exp_tab.p;
+  CK(cudaEventRecord(s->ev[0], s->st));
+  sgx::launch_forward(s->st, c->cone.fwd.p, c->cone.n_fwd_chunks, s->V.p, s->tape.p, s->Bp, 0, tab);
+  CK(cudaEventRecord(s->ev[1], s->st));
+  sgx::launch_backward(s->st, c->cone.bwd.p, c->cone.n_bwd_chunks, s->tape.p, s->adj.p, s->V.p, nullptr,
+                       nullptr, s->Bp, static_cast<float>(s->cfg.learning_rate), c->cone.out_row.p,
+                       c->out_tgt.p, static_cast<int>(c->L.out_node.size()), s->row_loss.p, tab);
+  sgx::launch_loss(s->st, s->row_loss.p, s->cfg.batch, s->partial.p, s->n_partial, s->hout.p);
+  s->launches += 4;
+  CK(cudaEventRecord(s->ev[2], s->st));
+  CK(cudaGetLastError());
+}
+
+void ensure_table(sgx_sampler* s) {
+  // Keep the load factor under 1/2 even if every row of this harvest is new.
+  uint64_t want = static_cast<uint64_t>(s->table_count + s->Bp) * 2;
+  if (want <= s->tcap) return;
+  uint64_t ncap = next_pow2(std::max<uint64_t>(want * 2, 1u << 16));
+  DBuf<unsigned long long> nk, nm;
+  nk.alloc(ncap);
+  nm.alloc(ncap);
+  CK(cudaMemsetAsync(nk.p, 0, ncap * sizeof(unsigned long long), s->st));
+  CK(cudaMemsetAsync(nm.p, 0xff, ncap * sizeof(unsigned long long), s->st));
+  if (s->tcap) {
+    sgx::launch_rehash(s->st, s->tkeys.p, s->tmeta.p, s->tcap, nk.p, nm.p, ncap - 1);
+    s->launches += 1;
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s->st));
+  s->tkeys.swap(nk);
+  s->tmeta.swap(nm);
+  s->tcap = ncap;
+}
+
+void grow_store(sgx_sampler* s, long long need_rows) {
+  long long ncap = std::max<long long>(need_rows, s->store_cap * 2);
+  const size_t kw = static_cast<size_t>(s->c->L.key_words);
+  DBuf<uint64_t> ns;
+  ns.alloc(static_cast<size_t>(ncap) * kw);
+  if (s->n_solutions)
+    CK(cudaMemcpyAsync(ns.p, s->store.p, static_cast<size_t>(s->n_solutions) * kw * sizeof(uint64_t),
+                       cudaMemcpyDeviceToDevice, s->st));
+  CK(cudaStreamSynchronize(s->st));
+  s->store.swap(ns);
+  s->store_cap = ncap;
+}
+
+// The harvest lambda of sampler.cpp:124-153 for one (restart, iter).
+// quota_left < 0 means no quota.  Returns rows attempted and solutions added.
+void sampler_harvest(sgx_sampler* s, int restart, int iter, long long quota_left, long long* attempts,
+                     long long* added) {
+  sgx_circuit* c = s->c;
+  const auto& L = c->L;
+  ensure_table(s);
+  CK(cudaEventRecord(s->ev[3], s->st));
+  uint64_t fprefix = sgx::fold(
+      sgx::fold(sgx::fold(sgx::fold(sgx::kPi, s->cfg.seed), sgx::kFreeTag), static_cast<uint64_t>(static_cast<int64_t>(restart))),
+      static_cast<uint64_t>(static_cast<int64_t>(iter)));
+  sgx::launch_harden(s->st, s->V.p, static_cast<int>(L.cpi.size()), static_cast<int>(L.ucpi.size()),
+                     c->cpi_bit_row.p, c->ucpi_bit_row.p, s->BT.p, s->W, s->Bp, fprefix, s->cfg.row_offset);
+  sgx::launch_bit_eval(s->st, s->wpc, c->bit_ops.p, c->bit_lvl_ptr.p, c->n_bit_levels, s->BT.p, s->W,
+                       c->out_bit_row.p, c->out_tgt.p, static_cast<int>(L.out_node.size()), c->clause_ptr.p,
+                       c->clause_enc.p, static_cast<int>(L.clause_ptr.size()) - 1, s->valid.p, s->cfg.batch);
+  CK(cudaEventRecord(s->ev[4], s->st));
+  s->epoch += 1;
+  sgx::launch_keys(s->st, s->BT.p, s->W, c->key_bit_row.p, L.key_words, s->valid.p, s->Bp, s->K.p,
+                   s->slot_of_row.p, s->tkeys.p, s->tmeta.p, s->tcap - 1, s->epoch);
+  CK(cudaEventRecord(s->ev[5], s->st));
+  sgx::launch_commit(s->st, s->valid.p, s->slot_of_row.p, s->tmeta.p, s->epoch, s->Bp, s->newmask.p,
+                     s->block_count.p, quota_left, s->hout.p);
+  sgx::launch_append(s->st, s->newmask.p, s->block_count.p, s->K.p, L.key_words, s->Bp, s->store.p,
+                     s->n_solutions, s->store_cap, s->hout.p);
+  s->launches += (L.cpi.size() + L.ucpi.size() ? 1 : 0) + 5;
+  CK(cudaEventRecord(s->ev[6], s->st));
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->st));
+  CK(cudaStreamSynchronize(s->st));
+  if (s->hpin->overflow) {
+    grow_store(s, s->n_solutions + s->hpin->accepted);
+    sgx::launch_append(s->st, s->newmask.p, s->block_count.p, s->K.p, L.key_words, s->Bp, s->store.p,
+                       s->n_solutions, s->store_cap, s->hout.p);
+    s->launches += 1;
+    CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    if (s->hpin->overflow) throw CudaError("solution store overflow after growth");
+  }
+  const sgx::HarvestOut& h = *s->hpin;
+  s->table_count += h.new_rows;
+  s->n_solutions += h.accepted;
+  *added = h.accepted;
+  // Quota met inside this harvest: the reference stops at the row after the
+  // one that filled it (sampler.cpp:129).
+  if (quota_left >= 0 && h.accepted == quota_left && h.accepted > 0)
+    *attempts = h.last_row + 1;
+  else
+    *attempts = s->cfg.batch;
+  s->phase_ms[2] += elapsed(s->ev[3], s->ev[6]);
+  s->phase_ms[5] += elapsed(s->ev[3], s->ev[4]);
+  s->phase_ms[6] += elapsed(s->ev[4], s->ev[5]);
+  s->phase_ms[7] += elapsed(s->ev[5], s->ev[6]);
+}
+
+// run_impl<float> (sampler.cpp:89-194).
+void sampler_run(sgx_sampler* s) {
+  using clock = std::chrono::steady_clock;
+  const auto t0 = clock::now();
+  auto now_s = [&] { return std::chrono::duration<double>(clock::now() - t0).count(); };
+  const sgx_sampler_cfg& cfg = s->cfg;
+  s->loss_trace.clear();
+  s->new_unique.clear();
+  s->stats = sgx_run_stats{};
+  std::fill(s->phase_ms, s->phase_ms + 8, 0.0);
+  s->launches = 0;
+  if (s->c->L.unsat) {
+    s->stats.unsat = 1;
+    s->stats.wall_time_s = now_s();
+    return;
+  }
+  const bool quota = cfg.max_solutions > 0;
+  auto quota_met = [&] { return quota && s->n_solutions >= cfg.max_solutions; };
+  auto out_of_time = [&] { return cfg.timeout_s > 0.0 && now_s() >= cfg.timeout_s; };
+  auto harvest = [&](int restart, int iter) {
+    long long att = 0, add = 0;
+    sampler_harvest(s, restart, iter, quota ? cfg.max_solutions - s->n_solutions : -1, &att, &add);
+    s->stats.attempts += att;
+    s->new_unique.push_back(add);
+  };
+  const int max_restarts = cfg.max_restarts > 0 ? cfg.max_restarts : 1000;
+  bool timed_out = false;
+  cudaEvent_t e0, e1, r0, r1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventCreate(&r0));
+  CK(cudaEventCreate(&r1));
+  CK(cudaEventRecord(r0, s->st));
+  for (int restart = 0;; ++restart) {
+    CK(cudaEventRecord(e0, s->st));
+    sampler_init(s, restart);
+    CK(cudaEventRecord(e1, s->st));
+    const long long before = s->n_solutions;
+    harvest(restart, 0);
+    s->phase_ms[0] += elapsed(e0, e1);
+    for (int iter = 1; iter <= cfg.iterations && !quota_met(); ++iter) {
+      if (out_of_time()) {
+        timed_out = true;
+        break;
+      }
+      sampler_step(s);
+      harvest(restart, iter);
+      s->loss_trace.push_back(s->hpin->loss_total / cfg.batch);
+      s->phase_ms[1] += elapsed(s->ev[0], s->ev[2]);
+      s->phase_ms[3] += elapsed(s->ev[0], s->ev[1]);
+      s->phase_ms[4] += elapsed(s->ev[1], s->ev[2]);
+    }
+    if (quota_met() || timed_out) break;
+    if (cfg.restart_policy != SGX_RESTART_REINIT_ON_EXHAUST) break;
+    if (s->n_solutions == before) break;
+    if (restart >= max_restarts) break;
+    if (out_of_time()) {
+      timed_out = true;
+      break;
+    }
+    s->stats.restarts = restart + 1;
+  }
+  CK(cudaEventRecord(r1, s->st));
+  CK(cudaEventSynchronize(r1));
+  s->stats.device_ms = elapsed(r0, r1);
+  s->stats.launches = s->launches;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(r0);
+  cudaEventDestroy(r1);
+  s->stats.timed_out = timed_out ? 1 : 0;
+  s->stats.unique_count = s->n_solutions;
+  s->stats.wall_time_s = now_s();
+  s->stats.throughput = s->stats.wall_time_s > 0.0 ? s->n_solutions / s->stats.wall_time_s : 0.0;
+  s->stats.n_loss = static_cast<int32_t>(s->loss_trace.size());
+  s->stats.n_harvest = static_cast<int32_t>(s->new_unique.size());
+}
+
+void reset_solutions(sgx_sampler* s) {
+  s->n_solutions = 0;
+  s->table_count = 0;
+  s->epoch = 0;
+  if (s->tcap) {
+    CK(cudaMemsetAsync(s->tkeys.p, 0, s->tcap * sizeof(unsigned long long), s->st));
+    CK(cudaMemsetAsync(s->tmeta.p, 0xff, s->tcap * sizeof(unsigned long long), s->st));
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sgx_last_error(void) { return g_err.c_str(); }
+const char* sgx_version(void) { return "satgrad_b200 0.1 (sm_100a)"; }
+
+int sgx_open(int device, sgx_ctx** out) {
+  return guard([&] {
+    need(out, "out");
+    auto ctx = std::make_unique<sgx_ctx>();
+    ctx->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    std::vector<uint64_t> tab(kExpTab, kExpTab + 32);
+    ctx->exp_tab.upload(tab, ctx->stream);
+    CK(cudaStreamSynchronize(ctx->stream));
+    *out = ctx.release();
+  });
+}
+
+int sgx_close(sgx_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    ctx->exp_tab.reset();
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int sgx_layout_stats(const sgx_circuit_desc* desc, int64_t* info16) {
+  return guard([&] {
+    need(desc, "desc");
+    need(info16, "info16");
+    sgx::Layout L = sgx::build_layout(*desc);
+    sgx::layout_info(L, info16);
+  });
+}
+
+int sgx_circuit_upload(sgx_ctx* ctx, const sgx_circuit_desc* d, sgx_circuit** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(d, "desc");
+    need(out, "out");
+    CK(cudaSetDevice(ctx->device));
+    auto c = std::make_unique<sgx_circuit>();
+    c->ctx = ctx;
+    if (d->unsat) {
+      // run() returns before touching the circuit (sampler.cpp:105-110).
+      try {
+        c->L = sgx::build_layout(*d);
+        c->layout_ok = true;
+      } catch (const std::invalid_argument&) {
+        c->L = sgx::Layout{};
+        c->L.unsat = true;
+        c->L.num_vars = d->num_vars;
+        c->L.key_words = (d->num_vars + 63) / 64;
+      }
+    } else {
+      c->L = sgx::build_layout(*d);
+      c->layout_ok = true;
+    }
+    if (c->layout_ok) {
+      cudaStream_t st = ctx->stream;
+      const auto& L = c->L;
+      c->cone.upload(L.cone, st);
+      c->full.upload(L.full, st);
+      c->bit_ops.upload(to_int4(L.bit_ops), st);
+      c->bit_lvl_ptr.upload(L.bit_lvl_ptr, st);
+      c->n_bit_levels = static_cast<int>(L.bit_lvl_ptr.size()) - 1;
+      c->cpi_bit_row.upload(L.cpi_bit_row, st);
+      c->ucpi_bit_row.upload(L.ucpi_bit_row, st);
+      c->out_bit_row.upload(L.out_bit_row, st);
+      c->out_tgt.upload(L.out_tgt, st);
+      c->clause_ptr.upload(L.clause_ptr32, st);
+      c->clause_enc.upload(L.clause_enc, st);
+      c->key_bit_row.upload(L.key_bit_row, st);
+      CK(cudaStreamSynchronize(st));
+    }
+    *out = c.release();
+  });
+}
+
+int sgx_circuit_info(const sgx_circuit* c, int64_t* info16) {
+  return guard([&] {
+    need(c, "circuit");
+    need(info16, "info16");
+    sgx::layout_info(c->L, info16);
+  });
+}
+
+int sgx_circuit_free(sgx_circuit* c) {
+  return guard([&] {
+    if (!c) return;
+    cudaSetDevice(c->ctx->device);
+    delete c;
+  });
+}
+
+int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler** out) {
+  return guard([&] {
+    need(c, "circuit");
+    need(cfg, "cfg");
+    need(out, "out");
+    if (cfg->batch < 1) throw std::invalid_argument("batch must be positive");  // sampler.cpp:93
+    if (cfg->iterations < 0) throw std::invalid_argument("iterations must be non-negative");
+    CK(cudaSetDevice(c->ctx->device));
+    auto s = std::make_unique<sgx_sampler>();
+    s->c = c;
+    s->cfg = *cfg;
+    CK(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+    for (auto& e : s->ev) CK(cudaEventCreate(&e));
+    CK(cudaMallocHost(&s->hpin, sizeof(sgx::HarvestOut)));
+    std::memset(s->hpin, 0, sizeof(sgx::HarvestOut));
+    s->hout.alloc(1);
+    if (c->layout_ok && !c->L.unsat) {
+      const auto& L = c->L;
+      s->Bp = round_up(cfg->batch, 1024);
+      s->W = s->Bp / 32;
+      s->wpc = s->W / 32 >= 2 * 148 ? 32 : (s->W / 16 >= 2 * 148 ? 16 : 8);
+      const size_t Bp = static_cast<size_t>(s->Bp);
+      s->V.alloc(L.cpi.size() * Bp);
+      s->tape.alloc(static_cast<size_t>(L.cone.n_rows) * Bp);
+      s->adj.alloc(static_cast<size_t>(L.cone.n_rows) * Bp);
+      s->row_loss.alloc(Bp);
+      s->partial.alloc(s->n_partial);
+      s->BT.alloc(static_cast<size_t>(L.n_bit_rows) * s->W);
+      s->valid.alloc(s->W);
+      s->newmask.alloc(s->W);
+      s->slot_of_row.alloc(Bp);
+      s->block_count.alloc(Bp / sgx::kThreads);
+      s->K.alloc(static_cast<size_t>(L.key_words) * Bp);
+      s->store_cap = cfg->solution_capacity > 0 ? cfg->solution_capacity : 2 * static_cast<long long>(Bp);
+      s->store.alloc(static_cast<size_t>(s->store_cap) * L.key_words);
+      CK(cudaMemsetAsync(s->V.p, 0, s->V.n * sizeof(float), s->st));
+      ensure_table(s.get());
+      CK(cudaStreamSynchronize(s->st));
+    }
+    *out = s.release();
+  });
+}
+
+int sgx_sampler_free(sgx_sampler* s) {
+  return guard([&] {
+    if (!s) return;
+    cudaSetDevice(s->c->ctx->device);
+    if (s->st) cudaStreamSynchronize(s->st);
+    for (auto& e : s->ev)
+      if (e) cudaEventDestroy(e);
+    if (s->hpin) cudaFreeHost(s->hpin);
+    cudaStream_t st = s->st;
+    delete s;
+    if (st) cudaStreamDestroy(st);
+  });
+}
+
+static void need_ready(sgx_sampler* s) {
+  need(s, "sampler");
+  if (!s->c->layout_ok || s->c->L.unsat) throw StateError("instance is unsatisfiable by construction");
+}
+
+int sgx_init(sgx_sampler* s, int32_t restart) {
+  return guard([&] {
+    need_ready(s);
+    CK(cudaSetDevice(s->c->ctx->device));
+    sampler_init(s, restart);
+    CK(cudaStreamSynchronize(s->st));
+  });
+}
+
+int sgx_step(sgx_sampler* s, double* loss_total) {
+  return guard([&] {
+    need_ready(s);
+    CK(cudaSetDevice(s->c->ctx->device));
+    sampler_step(s);
+    CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    if (loss_total) *loss_total = s->hpin->loss_total;
+  });
+}
+
+int sgx_harvest(sgx_sampler* s, int32_t restart, int32_t iter, int64_t* attempts, int64_t* added) {
+  return guard([&] {
+    need_ready(s);
+    CK(cudaSetDevice(s->c->ctx->device));
+    long long quota_left = s->cfg.max_solutions > 0 ? s->cfg.max_solutions - s->n_solutions : -1;
+    if (quota_left == 0) {
+      if (attempts) *attempts = 0;
+      if (added) *added = 0;
+      return;
+    }
+    long long att = 0, add = 0;
+    sampler_harvest(s, restart, iter, quota_left, &att, &add);
+    if (attempts) *attempts = att;
+    if (added) *added = add;
+  });
+}
+
+int sgx_run(sgx_sampler* s, sgx_run_stats* stats) {
+  return guard([&] {
+    need(s, "sampler");
+    CK(cudaSetDevice(s->c->ctx->device));
+    if (s->c->layout_ok && !s->c->L.unsat) reset_solutions(s);
+    else s->n_solutions = 0;
+    sampler_run(s);
+    if (stats) *stats = s->stats;
+  });
+}
+
+int sgx_run_traces(sgx_sampler* s, double* loss_trace, int64_t* new_unique) {
+  return guard([&] {
+    need(s, "sampler");
+    if (loss_trace && !s->loss_trace.empty())
+      std::memcpy(loss_trace, s->loss_trace.data(), s->loss_trace.size() * sizeof(double));
+    if (new_unique && !s->new_unique.empty())
+      std::memcpy(new_unique, s->new_unique.data(), s->new_unique.size() * sizeof(int64_t));
+  });
+}
+
+int64_t sgx_solution_count(const sgx_sampler* s) { return s ? s->n_solutions : -1; }
+
+int32_t sgx_key_words(const sgx_sampler* s) { return s ? s->c->L.key_words : -1; }
+
+int sgx_fetch_solutions(sgx_sampler* s, int64_t first, int64_t count, uint64_t* keys) {
+  return guard([&] {
+    need(s, "sampler");
+    if (first < 0 || count < 0 || first + count > s->n_solutions)
+      throw std::invalid_argument("solution range out of bounds");
+    if (count == 0) return;
+    need(keys, "keys");
+    CK(cudaSetDevice(s->c->ctx->device));
+    const size_t kw = static_cast<size_t>(s->c->L.key_words);
+    CK(cudaMemcpyAsync(keys, s->store.p + static_cast<size_t>(first) * kw,
+                       static_cast<size_t>(count) * kw * sizeof(uint64_t), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+  });
+}
+
+int sgx_phase_times(const sgx_sampler* s, double* ms8) {
+  return guard([&] {
+    need(s, "sampler");
+    need(ms8, "ms8");
+    std::memcpy(ms8, s->phase_ms, sizeof(s->phase_ms));
+  });
+}
+
+// ------------------------------------------------------------------ taps
+int sgx_forward(sgx_circuit* c, const float* p, int32_t batch, float* tape, float* y) {
+  return guard([&] {
+    need(c, "circuit");
+    if (!c->layout_ok) throw StateError("circuit has no device layout");
+    if (batch < 0) throw std::invalid_argument("batch must be non-negative");
+    const auto& L = c->L;
+    const size_t ncpi = L.cpi.size();
+    if (batch * ncpi) need(p, "p");
+    for (size_t i = 0; i < batch * ncpi; ++i)  // autodiff.cpp:71-73
+      if (!(p[i] >= 0.0f && p[i] <= 1.0f)) throw std::invalid_argument("probabilities must lie in [0, 1]");
+    if (batch == 0) return;
+    CK(cudaSetDevice(c->ctx->device));
+    cudaStream_t st = c->ctx->stream;
+    const int Bp = round_up(batch, sgx::kThreads);
+    std::vector<float> src(ncpi * Bp, 0.5f);
+    for (int r = 0; r < batch; ++r)
+      for (size_t j = 0; j < ncpi; ++j) src[j * Bp + r] = p[r * ncpi + j];
+    DBuf<float> dsrc, dtape;
+    dsrc.upload(src, st);
+    dtape.alloc(static_cast<size_t>(L.full.n_rows) * Bp);
+    sgx::launch_forward(st, c->full.fwd.p, c->full.n_fwd_chunks, dsrc.p, dtape.p, Bp, 1, c->ctx->exp_tab.p);
+    CK(cudaGetLastError());
+    std::vector<float> h(static_cast<size_t>(L.full.n_rows) * Bp);
+    CK(cudaMemcpyAsync(h.data(), dtape.p, h.size() * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int i = 0; i < L.n_nodes; ++i) {
+      const float* rowp = h.data() + static_cast<size_t>(L.full.row_of_node[i]) * Bp;
+      if (tape) std::memcpy(tape + static_cast<size_t>(i) * batch, rowp, sizeof(float) * batch);
+    }
+    if (y) {
+      const size_t m = L.out_node.size();
+      for (size_t o = 0; o < m; ++o) {
+        const float* rowp = h.data() + static_cast<size_t>(L.full.row_of_node[L.out_node[o]]) * Bp;
+        for (int r = 0; r < batch; ++r) y[r * m + o] = rowp[r];
+      }
+    }
+  });
+}
+
+int sgx_backward(sgx_circuit* c, const float* tape, int32_t batch, const float* v, float* dv, float* dp) {
+  return guard([&] {
+    need(c, "circuit");
+    if (!c->layout_ok) throw StateError("circuit has no device layout");
+    if (batch < 0) throw std::invalid_argument("batch must be non-negative");
+    if (batch == 0) return;
+    need(tape, "tape");
+    const auto& L = c->L;
+    const size_t ncpi = L.cpi.size();
+    if (ncpi) need(v, "v");
+    CK(cudaSetDevice(c->ctx->device));
+    cudaStream_t st = c->ctx->stream;
+    const int Bp = round_up(batch, sgx::kThreads);
+    std::vector<float> ht(static_cast<size_t>(L.full.n_rows) * Bp, 0.5f);
+    for (int i = 0; i < L.n_nodes; ++i)
+      std::memcpy(ht.data() + static_cast<size_t>(L.full.row_of_node[i]) * Bp, tape + static_cast<size_t>(i) * batch,
+                  sizeof(float) * batch);
+    std::vector<float> hv(std::max<size_t>(ncpi * Bp, 1), 0.0f);
+    for (int r = 0; r < batch; ++r)
+      for (size_t j = 0; j < ncpi; ++j) hv[j * Bp + r] = v[r * ncpi + j];
+    DBuf<float> dt, dadj, dV, ddv, ddp;
+    dt.upload(ht, st);
+    dV.upload(hv, st);
+    dadj.alloc(static_cast<size_t>(L.full.n_rows) * Bp);
+    ddv.alloc(std::max<size_t>(ncpi * Bp, 1));
+    ddp.alloc(std::max<size_t>(ncpi * Bp, 1));
+    CK(cudaMemsetAsync(ddv.p, 0, ddv.n * sizeof(float), st));
+    CK(cudaMemsetAsync(ddp.p, 0, ddp.n * sizeof(float), st));
+    sgx::launch_backward(st, c->full.bwd.p, c->full.n_bwd_chunks, dt.p, dadj.p, dV.p, ddv.p, ddp.p, Bp, 0.0f,
+                         c->full.out_row.p, c->out_tgt.p, static_cast<int>(L.out_node.size()), nullptr,
+                         c->ctx->exp_tab.p);
+    CK(cudaGetLastError());
+    std::vector<float> hdv(ddv.n), hdp(ddp.n);
+    CK(cudaMemcpyAsync(hdv.data(), ddv.p, hdv.size() * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hdp.data(), ddp.p, hdp.size() * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int r = 0; r < batch; ++r)
+      for (size_t j = 0; j < ncpi; ++j) {
+        if (dv) dv[r * ncpi + j] = hdv[j * Bp + r];
+        if (dp) dp[r * ncpi + j] = hdp[j * Bp + r];
+      }
+  });
+}
+
+static int device_unary(sgx_ctx* ctx, const float* x, int64_t n, float* out, int sigmoid) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (n < 0) throw std::invalid_argument("n must be non-negative");
+    if (n == 0) return;
+    need(x, "x");
+    need(out, "out");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    DBuf<float> dx, dy;
+    dx.alloc(n);
+    dy.alloc(n);
+    CK(cudaMemcpyAsync(dx.p, x, n * sizeof(float), cudaMemcpyHostToDevice, st));
+    sgx::launch_expf(st, dx.p, n, dy.p, ctx->exp_tab.p, sigmoid);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, dy.p, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int sgx_embed(sgx_ctx* ctx, const float* v, int64_t n, float* p) { return device_unary(ctx, v, n, p, 1); }
+
+int sgx_expf(sgx_ctx* ctx, const float* x, int64_t n, float* out) { return device_unary(ctx, x, n, out, 0); }
+
+}  // extern "C"

@@ -1,0 +1,599 @@
+#include <cuda_runtime.h>
+
+#include "sgx_kernels.cuh"
+#include "sgx_launch.hpp"
+
+namespace sgx {
+
+// ---------------------------------------------------------------------------
+// K1: V0 = (float)(2 * u01(hash{seed, 'init', restart, row, col}) - 1)
+// Layout [col][Bp]; consecutive threads take consecutive rows of one column.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+k_init_v(float* __restrict__ V, int ncols, int Bp, uint64_t prefix, long long row_offset) {
+  const long long total = static_cast<long long>(ncols) * Bp;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    int c = static_cast<int>(i / Bp);
+    int r = static_cast<int>(i - static_cast<long long>(c) * Bp);
+    uint64_t h = fold(fold(prefix, static_cast<uint64_t>(row_offset + r)), static_cast<uint64_t>(c));
+    double u = static_cast<double>(h >> 11) * 0x1.0p-53;  // u01, rng.hpp:28-30
+    V[i] = __double2float_rn(__dsub_rn(__dmul_rn(2.0, u), 1.0));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: forward over the soft program.  One thread = one sample; ops arrive in
+// chunks of kU independent ops (a chunk never crosses a level), so each
+// thread issues all 2*kU operand loads of a chunk before it computes.  Every
+// lane runs the same op stream: control flow is warp-uniform and the op
+// records are broadcast loads.  tape is [row][Bp]: each warp load/store is
+// one 128-byte line.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+k_forward(const int4* __restrict__ ops, int n_chunks, const float* __restrict__ src, float* tape,
+          int Bp, int src_is_prob, const uint64_t* __restrict__ exp_tab) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= Bp) return;
+  const size_t B = static_cast<size_t>(Bp);
+  for (int c = 0; c < n_chunks; ++c) {
+    int4 op[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) op[k] = __ldg(ops + static_cast<size_t>(c) * kU + k);
+    float x[kU], y[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const int code = op[k].x;
+      x[k] = 0.0f;
+      y[k] = 0.0f;
+      if (code == SGX_INPUT) {
+        if (op[k].z >= 0) x[k] = src[op[k].z * B + s];
+      } else if (code >= SGX_BUF && code <= SGX_XNOR2) {
+        x[k] = tape[op[k].z * B + s];
+        if (code >= SGX_AND2) y[k] = tape[op[k].w * B + s];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const int code = op[k].x;
+      const float a = x[k], b = y[k];
+      float r;
+      switch (code) {
+        case SGX_INPUT:
+          r = op[k].z < 0 ? 0.5f : (src_is_prob ? a : sigmoid_ref(a, exp_tab));
+          break;
+        case SGX_CONST0: r = 0.0f; break;
+        case SGX_CONST1: r = 1.0f; break;
+        case SGX_BUF: r = a; break;
+        case SGX_NOT: r = __fsub_rn(1.0f, a); break;
+        case SGX_AND2: r = __fmul_rn(a, b); break;
+        case SGX_OR2: r = __fsub_rn(1.0f, __fmul_rn(__fsub_rn(1.0f, a), __fsub_rn(1.0f, b))); break;
+        case SGX_XOR2:
+          r = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, a), b), __fmul_rn(a, __fsub_rn(1.0f, b)));
+          break;
+        case SGX_XNOR2:
+          r = __fadd_rn(__fmul_rn(a, b), __fmul_rn(__fsub_rn(1.0f, a), __fsub_rn(1.0f, b)));
+          break;
+        default: r = 0.0f; break;
+      }
+      if (code != kNop) tape[op[k].y * B + s] = r;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3+K4: per-row loss, pull-style backward and the fused GD step.  The micro
+// op stream is BEGIN (seed) / EDGE* (one per fan-out slot, consumers in
+// descending reference id) / END (store adjoint, or for a V column: dV and
+// V -= lr * dV).  No atomics: every adjoint is produced by exactly one thread
+// of the owning sample, in one pass.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+k_backward(const int4* __restrict__ ops, int n_chunks, const float* tape, float* adj, float* V,
+           float* dv_out, float* dp_out, int Bp, float lr, const int* __restrict__ out_row,
+           const uint8_t* __restrict__ out_tgt, int n_out, float* __restrict__ row_loss,
+           const uint64_t* __restrict__ exp_tab) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= Bp) return;
+  const size_t B = static_cast<size_t>(Bp);
+  if (row_loss) {  // loss (autodiff.cpp:160-166): outputs in order
+    float l = 0.0f;
+    for (int m = 0; m < n_out; ++m) {
+      float d = __fsub_rn(tape[static_cast<size_t>(__ldg(out_row + m)) * B + s],
+                          __ldg(out_tgt + m) ? 1.0f : 0.0f);
+      l = __fadd_rn(l, __fmul_rn(d, d));
+    }
+    row_loss[s] = l;
+  }
+  float acc = 0.0f;
+  for (int c = 0; c < n_chunks; ++c) {
+    int4 op[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) op[k] = __ldg(ops + static_cast<size_t>(c) * kU + k);
+    float x[kU], y[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const int code = op[k].x & 0xff;
+      x[k] = 0.0f;
+      y[k] = 0.0f;
+      if (code == kBegin) {
+        if (op[k].x & kSeedBit) x[k] = tape[op[k].y * B + s];
+      } else if (code == kEdge) {
+        x[k] = adj[op[k].y * B + s];
+        if (op[k].z >= 0) y[k] = tape[op[k].z * B + s];
+      } else if (code == kEnd) {
+        if (op[k].z >= 0) x[k] = V[op[k].z * B + s];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const int code = op[k].x & 0xff;
+      if (code == kBegin) {
+        acc = 0.0f;
+        if (op[k].x & kSeedBit)  // adj[out] += 2 (y - t)  (autodiff.cpp:206)
+          acc = __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(x[k], (op[k].x & kTargetBit) ? 1.0f : 0.0f)));
+      } else if (code == kEdge) {
+        const float g = x[k], vo = y[k];
+        switch ((op[k].x >> kKindShift) & 0xf) {  // autodiff.cpp:225-277
+          case SGX_BUF: acc = __fadd_rn(acc, g); break;
+          case SGX_NOT: acc = __fsub_rn(acc, g); break;
+          case SGX_AND2: acc = __fadd_rn(acc, __fmul_rn(g, vo)); break;
+          case SGX_OR2: acc = __fadd_rn(acc, __fmul_rn(g, __fsub_rn(1.0f, vo))); break;
+          case SGX_XOR2:
+            acc = __fadd_rn(acc, __fmul_rn(g, __fsub_rn(1.0f, __fmul_rn(2.0f, vo))));
+            break;
+          case SGX_XNOR2:
+            acc = __fadd_rn(acc, __fmul_rn(g, __fsub_rn(__fmul_rn(2.0f, vo), 1.0f)));
+            break;
+          default: break;
+        }
+      } else if (code == kEnd) {
+        if (op[k].y >= 0) adj[op[k].y * B + s] = acc;
+        if (op[k].z >= 0) {  // autodiff.cpp:212-221 then gd_step :285-290
+          const float v = x[k];
+          const float p = sigmoid_ref(v, exp_tab);
+          const float dv = __fmul_rn(__fmul_rn(acc, p), __fsub_rn(1.0f, p));
+          const size_t at = op[k].z * B + s;
+          if (dv_out) {
+            dv_out[at] = dv;
+            dp_out[at] = acc;
+          } else {
+            V[at] = __fsub_rn(v, __fmul_rn(lr, dv));
+          }
+        }
+      }
+    }
+  }
+}
+
+// Deterministic loss total: fixed per-block partial sums in double, then one
+// block folds the partials in block order.
+__global__ void __launch_bounds__(kThreads)
+k_loss_partial(const float* __restrict__ row_loss, int batch, double* __restrict__ partial) {
+  __shared__ double sh[kThreads];
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < batch; i += gridDim.x * blockDim.x)
+    acc += static_cast<double>(row_loss[i]);
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void k_loss_final(const double* __restrict__ partial, int n, HarvestOut* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += partial[i];
+    out->loss_total = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5a: harden + free bits.  One warp per (input, 32-row word): lane = row.
+// Constrained column c: ballot(V >= 0) (ties -> 1, NaN -> 0).  Free input k:
+// ballot(hash{seed, 'free', restart, iter, row, k} & 1).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+k_harden(const float* __restrict__ V, int ncpi, int nucpi, const int* __restrict__ cpi_row,
+         const int* __restrict__ ucpi_row, uint32_t* __restrict__ BT, int W, int Bp,
+         uint64_t free_prefix, long long row_offset) {
+  const int lane = threadIdx.x & 31;
+  const long long total = static_cast<long long>(ncpi + nucpi) * W;
+  for (long long gw = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; gw < total;
+       gw += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+    const int input = static_cast<int>(gw / W);
+    const int w = static_cast<int>(gw - static_cast<long long>(input) * W);
+    const int r = w * 32 + lane;
+    bool bit;
+    int row;
+    if (input < ncpi) {
+      bit = V[static_cast<size_t>(input) * Bp + r] >= 0.0f;
+      row = __ldg(cpi_row + input);
+    } else {
+      const int k = input - ncpi;
+      bit = fold(fold(free_prefix, static_cast<uint64_t>(row_offset + r)), static_cast<uint64_t>(k)) & 1;
+      row = __ldg(ucpi_row + k);
+    }
+    const uint32_t word = __ballot_sync(kFull, bit);
+    if (lane == 0) BT[static_cast<size_t>(row) * W + w] = word;
+  }
+}
+
+__device__ __forceinline__ uint32_t bit_gate(int kind, uint32_t a, uint32_t b) {
+  switch (kind) {  // circuit.cpp:137-144 on 32 rows at once
+    case SGX_CONST0: return 0u;
+    case SGX_CONST1: return kFull;
+    case SGX_BUF: return a;
+    case SGX_NOT: return ~a;
+    case SGX_AND2: return a & b;
+    case SGX_OR2: return a | b;
+    case SGX_XOR2: return a ^ b;
+    case SGX_XNOR2: return ~(a ^ b);
+    default: return 0u;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5b+K6: bit-sliced eval of every node, then PO check and CNF check.  A CTA
+// owns WPC consecutive words (32*WPC rows); its threads are (slot, word)
+// pairs, slots split each level's nodes, __syncthreads between levels.
+// Output valid[w]: bit r set iff row 32w+r hits every output target and
+// satisfies every clause.
+// ---------------------------------------------------------------------------
+template <int WPC>
+__global__ void __launch_bounds__(kThreads)
+k_bit_eval(const int4* __restrict__ ops, const int* __restrict__ lvl_ptr, int n_levels,
+           uint32_t* BT, int W, const int* __restrict__ out_row, const uint8_t* __restrict__ out_tgt,
+           int n_out, const int* __restrict__ clause_ptr, const int* __restrict__ clause_enc,
+           int n_clauses, uint32_t* __restrict__ valid, int batch) {
+  constexpr int S = kThreads / WPC;
+  const int lw = threadIdx.x % WPC, slot = threadIdx.x / WPC;
+  const int w = blockIdx.x * WPC + lw;
+  const size_t Wz = static_cast<size_t>(W);
+  for (int l = 0; l < n_levels; ++l) {
+    const int e = __ldg(lvl_ptr + l + 1);
+    for (int i = __ldg(lvl_ptr + l) + slot; i < e; i += 4 * S) {
+      int4 op[4];
+      uint32_t xa[4], xb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int ii = i + u * S;
+        op[u] = ii < e ? __ldg(ops + ii) : make_int4(SGX_CONST0, -1, 0, 0);
+        xa[u] = op[u].y >= 0 ? BT[op[u].z * Wz + w] : 0u;
+        xb[u] = op[u].y >= 0 ? BT[op[u].w * Wz + w] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (op[u].y >= 0) BT[op[u].y * Wz + w] = bit_gate(op[u].x, xa[u], xb[u]);
+    }
+    __syncthreads();
+  }
+  uint32_t ok = kFull;
+  for (int m = slot; m < n_out; m += S) {  // sampler.cpp:140-146
+    const uint32_t x = BT[static_cast<size_t>(__ldg(out_row + m)) * Wz + w];
+    ok &= __ldg(out_tgt + m) ? x : ~x;
+  }
+  // eval_cnf (cnf.cpp:136-145): this slot's contiguous clause range, as a
+  // flat literal stream so the loads pipeline.
+  const int c0 = static_cast<int>(static_cast<long long>(n_clauses) * slot / S);
+  const int c1 = static_cast<int>(static_cast<long long>(n_clauses) * (slot + 1) / S);
+  const int l1 = __ldg(clause_ptr + c1);
+  uint32_t any = 0u;
+#pragma unroll 8
+  for (int l = __ldg(clause_ptr + c0); l < l1; ++l) {
+    const int e = __ldg(clause_enc + l);
+    const uint32_t x = BT[static_cast<size_t>(e >> 2) * Wz + w];
+    any |= (e & 1) ? ~x : x;
+    if (e & 2) {
+      ok &= any;
+      any = 0u;
+    }
+  }
+  __shared__ uint32_t red[kThreads];
+  red[threadIdx.x] = ok;
+  __syncthreads();
+  if (slot == 0) {
+#pragma unroll
+    for (int j = 1; j < S; ++j) ok &= red[j * WPC + lw];
+    const int r0 = w * 32;
+    uint32_t mask = r0 + 32 <= batch ? kFull : (r0 >= batch ? 0u : ((1u << (batch - r0)) - 1u));
+    valid[w] = ok & mask;
+  }
+}
+
+// 32x32 bit transpose across a warp: lane i holds row i on entry, column i on
+// exit (bit k of lane i <-> bit i of lane k).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+  const uint32_t masks[5] = {0x0000ffffu, 0x00ff00ffu, 0x0f0f0f0fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int t = 0; t < 5; ++t) {
+    const int j = 16 >> t;
+    const uint32_t m = masks[t];
+    const uint32_t o = __shfl_xor_sync(kFull, x, j);
+    x = (lane & j) ? ((x & ~m) | ((o >> j) & m)) : ((x & m) | ((o & m) << j));
+  }
+  return x;
+}
+
+// ---------------------------------------------------------------------------
+// K7: dedupe keys + fingerprints + table insert.  A warp owns 8 consecutive
+// words (256 rows).  For each group of 32 variables, lane k loads the 8 words
+// of variable 32g+k (one 32-byte sector) and 8 warp transposes turn them into
+// per-row variable bits.  Key word q packs vars 64q+1..64q+64 LSB first
+// (dedupe_key, sampler.cpp:18-26).  Valid rows: K[q][row] = key word,
+// fp = splitmix chain over the key words, then the first-row-wins insert:
+// meta = min over rows of (epoch << 32 | row) for fingerprints first seen in
+// this epoch; older fingerprints keep a smaller meta, so they never win.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+k_keys(const uint32_t* __restrict__ BT, int W, const int* __restrict__ key_row, int key_words,
+       const uint32_t* __restrict__ valid, int Bp, uint64_t* __restrict__ K, int* __restrict__ slot_of_row,
+       unsigned long long* tkeys, unsigned long long* tmeta, uint64_t tmask, uint64_t epoch) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int w0 = warp * 8;
+  if (w0 >= W) return;
+  uint32_t vm[8];
+  uint32_t anyv = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    vm[j] = __ldg(valid + w0 + j);
+    anyv |= vm[j];
+  }
+  if (anyv == 0) return;  // warp-uniform
+  uint64_t h[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) h[j] = kPi;
+  const size_t Wz = static_cast<size_t>(W);
+  for (int q = 0; q < key_words; ++q) {
+    uint32_t half[2][8];
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const int row = __ldg(key_row + (2 * q + hf) * 32 + lane);
+      uint4 A = make_uint4(0, 0, 0, 0), Bv = make_uint4(0, 0, 0, 0);
+      if (row >= 0) {
+        const uint4* p = reinterpret_cast<const uint4*>(BT + row * Wz + w0);
+        A = __ldg(p);
+        Bv = __ldg(p + 1);
+      }
+      uint32_t x[8] = {A.x, A.y, A.z, A.w, Bv.x, Bv.y, Bv.z, Bv.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) half[hf][j] = transpose32(x[j], lane);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint64_t kw = static_cast<uint64_t>(half[0][j]) | (static_cast<uint64_t>(half[1][j]) << 32);
+      h[j] = mix64(h[j] ^ kw);
+      if ((vm[j] >> lane) & 1u) K[static_cast<size_t>(q) * Bp + (w0 + j) * 32 + lane] = kw;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (!((vm[j] >> lane) & 1u)) continue;
+    const int r = (w0 + j) * 32 + lane;
+    const unsigned long long fp = h[j] ? h[j] : 1ull;  // 0 marks an empty slot
+    uint64_t idx = (fp ^ (fp >> 29)) & tmask;
+    for (;;) {
+      unsigned long long cur = tkeys[idx];
+      if (cur == fp) break;
+      if (cur == 0ull) {
+        cur = atomicCAS(tkeys + idx, 0ull, fp);
+        if (cur == 0ull || cur == fp) break;
+      }
+      idx = (idx + 1) & tmask;
+    }
+    atomicMin(tmeta + idx, static_cast<unsigned long long>((epoch << 32) | static_cast<uint32_t>(r)));
+    slot_of_row[r] = static_cast<int>(idx);
+  }
+}
+
+// new[w] bit r: valid row whose fingerprint this epoch first saw at this row.
+// Per-block counts for the row-order scan.
+__global__ void __launch_bounds__(kThreads)
+k_new_rows(const uint32_t* __restrict__ valid, const int* __restrict__ slot_of_row,
+           const unsigned long long* __restrict__ tmeta, uint64_t epoch, int Bp,
+           uint32_t* __restrict__ newmask, int* __restrict__ block_count) {
+  __shared__ int warp_cnt[kThreads / 32];
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  bool is_new = false;
+  if (r < Bp && ((__ldg(valid + (r >> 5)) >> lane) & 1u)) {
+    const int idx = slot_of_row[r];
+    is_new = tmeta[idx] == ((epoch << 32) | static_cast<uint32_t>(r));
+  }
+  const uint32_t m = __ballot_sync(kFull, is_new);
+  if (lane == 0) {
+    if (r < Bp) newmask[r >> 5] = m;
+    warp_cnt[wid] = __popc(m);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int i = 0; i < kThreads / 32; ++i) t += warp_cnt[i];
+    block_count[blockIdx.x] = t;
+  }
+}
+
+// Exclusive scan of the block counts (single CTA, sequential chunks), then
+// the quota cut: accepted = min(new_rows, quota_left) (quota_left < 0 = none).
+__global__ void __launch_bounds__(1024)
+k_scan_blocks(int* __restrict__ block_count, int n_blocks, long long quota_left, HarvestOut* out) {
+  __shared__ int sh[1024];
+  __shared__ long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n_blocks; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = i < n_blocks ? block_count[i] : 0;
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+      const int t = threadIdx.x >= off ? sh[threadIdx.x - off] : 0;
+      __syncthreads();
+      sh[threadIdx.x] += t;
+      __syncthreads();
+    }
+    if (i < n_blocks) block_count[i] = static_cast<int>(carry) + sh[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += sh[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out->new_rows = carry;
+    out->accepted = quota_left < 0 ? carry : (carry < quota_left ? carry : quota_left);
+    out->last_row = -1;
+    out->overflow = 0;
+  }
+}
+
+// Append accepted new rows, in row order, to the row-major solution store.
+__global__ void __launch_bounds__(kThreads)
+k_append(const uint32_t* __restrict__ newmask, const int* __restrict__ block_off, const uint64_t* __restrict__ K,
+         int key_words, int Bp, uint64_t* __restrict__ store, long long store_base, long long store_cap,
+         HarvestOut* out) {
+  __shared__ int warp_off[kThreads / 32];
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t m = r < Bp ? __ldg(newmask + (r >> 5)) : 0u;
+  if (lane == 0) warp_off[wid] = __popc(m);
+  __syncthreads();
+  if (!((m >> lane) & 1u)) return;
+  int pos = __ldg(block_off + blockIdx.x);
+  for (int i = 0; i < wid; ++i) pos += warp_off[i];
+  pos += __popc(m & ((1u << lane) - 1u));
+  const long long accepted = out->accepted;
+  if (pos >= accepted) return;
+  if (pos == accepted - 1) out->last_row = r;
+  const long long dst = store_base + pos;
+  if (dst >= store_cap) {
+    out->overflow = 1;
+    return;
+  }
+  for (int q = 0; q < key_words; ++q)
+    store[static_cast<size_t>(dst) * key_words + q] = K[static_cast<size_t>(q) * Bp + r];
+}
+
+// Move every occupied slot of the old table into the new one.
+__global__ void __launch_bounds__(kThreads)
+k_rehash(const unsigned long long* __restrict__ okeys, const unsigned long long* __restrict__ ometa,
+         uint64_t ocap, unsigned long long* nkeys, unsigned long long* nmeta, uint64_t nmask) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < ocap;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long fp = okeys[i];
+    if (fp == 0ull) continue;
+    uint64_t idx = (fp ^ (fp >> 29)) & nmask;
+    for (;;) {
+      const unsigned long long cur = atomicCAS(nkeys + idx, 0ull, fp);
+      if (cur == 0ull) break;
+      idx = (idx + 1) & nmask;
+    }
+    nmeta[idx] = ometa[i];
+  }
+}
+
+__global__ void k_expf(const float* __restrict__ x, long long n, float* __restrict__ out,
+                       const uint64_t* __restrict__ tab, int sigmoid) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[i] = sigmoid ? sigmoid_ref(x[i], tab) : expf_glibc(x[i], tab);
+}
+
+// ---------------------------------------------------------------------------
+// Host launch wrappers.
+// ---------------------------------------------------------------------------
+static int grid_for(long long n, int per_block, int cap) {
+  long long g = (n + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<int>(g);
+}
+
+void launch_init_v(cudaStream_t st, float* V, int ncols, int Bp, uint64_t prefix, long long row_offset) {
+  if (ncols == 0) return;
+  k_init_v<<<grid_for(static_cast<long long>(ncols) * Bp, kThreads, 148 * 64), kThreads, 0, st>>>(
+      V, ncols, Bp, prefix, row_offset);
+}
+
+void launch_forward(cudaStream_t st, const int4* ops, int n_chunks, const float* src, float* tape,
+                    int Bp, int src_is_prob, const uint64_t* exp_tab) {
+  k_forward<<<Bp / kThreads, kThreads, 0, st>>>(ops, n_chunks, src, tape, Bp, src_is_prob, exp_tab);
+}
+
+void launch_backward(cudaStream_t st, const int4* ops, int n_chunks, const float* tape, float* adj,
+                     float* V, float* dv_out, float* dp_out, int Bp, float lr, const int* out_row,
+                     const uint8_t* out_tgt, int n_out, float* row_loss, const uint64_t* exp_tab) {
+  k_backward<<<Bp / kThreads, kThreads, 0, st>>>(ops, n_chunks, tape, adj, V, dv_out, dp_out, Bp, lr,
+                                                 out_row, out_tgt, n_out, row_loss, exp_tab);
+}
+
+void launch_loss(cudaStream_t st, const float* row_loss, int batch, double* partial, int n_partial,
+                 HarvestOut* out) {
+  k_loss_partial<<<n_partial, kThreads, 0, st>>>(row_loss, batch, partial);
+  k_loss_final<<<1, 32, 0, st>>>(partial, n_partial, out);
+}
+
+void launch_harden(cudaStream_t st, const float* V, int ncpi, int nucpi, const int* cpi_row,
+                   const int* ucpi_row, uint32_t* BT, int W, int Bp, uint64_t free_prefix,
+                   long long row_offset) {
+  const long long warps = static_cast<long long>(ncpi + nucpi) * W;
+  if (warps == 0) return;
+  k_harden<<<grid_for(warps * 32, kThreads, 148 * 64), kThreads, 0, st>>>(
+      V, ncpi, nucpi, cpi_row, ucpi_row, BT, W, Bp, free_prefix, row_offset);
+}
+
+void launch_bit_eval(cudaStream_t st, int wpc, const int4* ops, const int* lvl_ptr, int n_levels,
+                     uint32_t* BT, int W, const int* out_row, const uint8_t* out_tgt, int n_out,
+                     const int* clause_ptr, const int* clause_enc, int n_clauses, uint32_t* valid,
+                     int batch) {
+  switch (wpc) {
+    case 8:
+      k_bit_eval<8><<<W / 8, kThreads, 0, st>>>(ops, lvl_ptr, n_levels, BT, W, out_row, out_tgt, n_out,
+                                                clause_ptr, clause_enc, n_clauses, valid, batch);
+      break;
+    case 16:
+      k_bit_eval<16><<<W / 16, kThreads, 0, st>>>(ops, lvl_ptr, n_levels, BT, W, out_row, out_tgt, n_out,
+                                                  clause_ptr, clause_enc, n_clauses, valid, batch);
+      break;
+    default:
+      k_bit_eval<32><<<W / 32, kThreads, 0, st>>>(ops, lvl_ptr, n_levels, BT, W, out_row, out_tgt, n_out,
+                                                  clause_ptr, clause_enc, n_clauses, valid, batch);
+      break;
+  }
+}
+
+void launch_keys(cudaStream_t st, const uint32_t* BT, int W, const int* key_row, int key_words,
+                 const uint32_t* valid, int Bp, uint64_t* K, int* slot_of_row, unsigned long long* tkeys,
+                 unsigned long long* tmeta, uint64_t tmask, uint64_t epoch) {
+  const int warps = W / 8;
+  k_keys<<<grid_for(static_cast<long long>(warps) * 32, kThreads, 1 << 30), kThreads, 0, st>>>(
+      BT, W, key_row, key_words, valid, Bp, K, slot_of_row, tkeys, tmeta, tmask, epoch);
+}
+
+void launch_commit(cudaStream_t st, const uint32_t* valid, const int* slot_of_row,
+                   const unsigned long long* tmeta, uint64_t epoch, int Bp, uint32_t* newmask,
+                   int* block_count, long long quota_left, HarvestOut* out) {
+  const int nb = Bp / kThreads;
+  k_new_rows<<<nb, kThreads, 0, st>>>(valid, slot_of_row, tmeta, epoch, Bp, newmask, block_count);
+  k_scan_blocks<<<1, 1024, 0, st>>>(block_count, nb, quota_left, out);
+}
+
+void launch_append(cudaStream_t st, const uint32_t* newmask, const int* block_off, const uint64_t* K,
+                   int key_words, int Bp, uint64_t* store, long long base, long long cap,
+                   HarvestOut* out) {
+  k_append<<<Bp / kThreads, kThreads, 0, st>>>(newmask, block_off, K, key_words, Bp, store, base, cap, out);
+}
+
+void launch_rehash(cudaStream_t st, const unsigned long long* okeys, const unsigned long long* ometa,
+                   uint64_t ocap, unsigned long long* nkeys, unsigned long long* nmeta, uint64_t nmask) {
+  k_rehash<<<grid_for(static_cast<long long>(ocap), kThreads, 148 * 32), kThreads, 0, st>>>(
+      okeys, ometa, ocap, nkeys, nmeta, nmask);
+}
+
+void launch_expf(cudaStream_t st, const float* x, long long n, float* out, const uint64_t* tab, int sigmoid) {
+  k_expf<<<grid_for(n, kThreads, 148 * 32), kThreads, 0, st>>>(x, n, out, tab, sigmoid);
+}
+
+}  // namespace sgx

@@ -1,0 +1,40 @@
+// Host-callable launch wrappers for the kernels in sgx_kernels.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sgx {
+
+struct HarvestOut;
+
+void launch_init_v(cudaStream_t st, float* V, int ncols, int Bp, uint64_t prefix, long long row_offset);
+void launch_forward(cudaStream_t st, const int4* ops, int n_chunks, const float* src, float* tape,
+                    int Bp, int src_is_prob, const uint64_t* exp_tab);
+void launch_backward(cudaStream_t st, const int4* ops, int n_chunks, const float* tape, float* adj,
+                     float* V, float* dv_out, float* dp_out, int Bp, float lr, const int* out_row,
+                     const uint8_t* out_tgt, int n_out, float* row_loss, const uint64_t* exp_tab);
+void launch_loss(cudaStream_t st, const float* row_loss, int batch, double* partial, int n_partial,
+                 HarvestOut* out);
+void launch_harden(cudaStream_t st, const float* V, int ncpi, int nucpi, const int* cpi_row,
+                   const int* ucpi_row, uint32_t* BT, int W, int Bp, uint64_t free_prefix,
+                   long long row_offset);
+void launch_bit_eval(cudaStream_t st, int wpc, const int4* ops, const int* lvl_ptr, int n_levels,
+                     uint32_t* BT, int W, const int* out_row, const uint8_t* out_tgt, int n_out,
+                     const int* clause_ptr, const int* clause_enc, int n_clauses, uint32_t* valid,
+                     int batch);
+void launch_keys(cudaStream_t st, const uint32_t* BT, int W, const int* key_row, int key_words,
+                 const uint32_t* valid, int Bp, uint64_t* K, int* slot_of_row, unsigned long long* tkeys,
+                 unsigned long long* tmeta, uint64_t tmask, uint64_t epoch);
+void launch_commit(cudaStream_t st, const uint32_t* valid, const int* slot_of_row,
+                   const unsigned long long* tmeta, uint64_t epoch, int Bp, uint32_t* newmask,
+                   int* block_count, long long quota_left, HarvestOut* out);
+void launch_append(cudaStream_t st, const uint32_t* newmask, const int* block_off, const uint64_t* K,
+                   int key_words, int Bp, uint64_t* store, long long base, long long cap,
+                   HarvestOut* out);
+void launch_rehash(cudaStream_t st, const unsigned long long* okeys, const unsigned long long* ometa,
+                   uint64_t ocap, unsigned long long* nkeys, unsigned long long* nmeta, uint64_t nmask);
+void launch_expf(cudaStream_t st, const float* x, long long n, float* out, const uint64_t* tab, int sigmoid);
+
+}  // namespace sgx

@@ -1,0 +1,97 @@
+// Host-side levelizer and device-layout compiler.
+//
+// The reference evaluates its circuit in plain node-id order
+// (autodiff.cpp:87-143, circuit.cpp:126-146); it has no levelization.  This
+// pass turns the reference's topological node array (circuit.hpp:20-40) into
+// the programs the sm_100a kernels execute:
+//
+//  * a SOFT program over the primary-output cone (or every node, for the
+//    parity taps): tape rows sorted by (ASAP level, node id); a forward op
+//    stream and a pull-style backward micro-op stream, both cut into chunks of
+//    kU ops that never cross a level boundary, so every op in a chunk is
+//    independent of the others and all of a chunk's loads can be in flight
+//    at once;
+//  * a BIT program over every node for the bit-sliced harvest (32 samples per
+//    word): level pointers for a level-synchronous sweep, the CNF as bit-row
+//    literals, the output checks and the dedupe-key variable map.
+//
+// Summation order is the reference's by construction: an adjoint is seeded
+// first (autodiff.cpp:201-207) and then pulls its fan-out in descending
+// consumer id, a-slot before b-slot (the push order of :208-280).  Consumers
+// outside the cone carry an exactly-zero adjoint, so pruning them changes no
+// bits.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/satgrad_b200.h"
+
+namespace sgx {
+
+constexpr int kU = 8;  // ops per chunk (loads in flight per thread)
+
+// Forward op (int4): {code, out_row, a, b}.  INPUT: a = V column or -1 (=0.5).
+// Backward micro-op (int4), opcode in the low byte:
+//   BEGIN {kBegin | seed<<8 | target<<9, row, 0, 0}
+//   EDGE  {kEdge | consumer_kind<<12, adj_row_of_consumer, other_row (-1), 0}
+//   END   {kEnd, adj_row_to_store (-1), V column (-1), 0}
+// Bit op (int4): {kind, out_row, a_row, b_row}.
+// Clause literal (int32): bit_row << 2 | last_in_clause << 1 | negated.
+enum OpCode : int32_t { kNop = 15, kBegin = 16, kEdge = 17, kEnd = 18 };
+constexpr int32_t kSeedBit = 1 << 8, kTargetBit = 1 << 9, kKindShift = 12;
+
+struct I4 {
+  int32_t x, y, z, w;
+};
+
+struct SoftProgram {
+  int32_t n_rows = 0;                // tape rows
+  int32_t n_levels = 0;
+  int64_t n_edges = 0;               // operand edges inside the program
+  std::vector<int32_t> row_of_node;  // -1 if the node is not in the program
+  std::vector<int32_t> node_of_row;
+  std::vector<I4> fwd;               // multiple of kU
+  std::vector<I4> bwd;               // multiple of kU
+  std::vector<int32_t> out_row;      // tape row of each output
+  std::vector<int32_t> col_row;      // tape row of each V column's INPUT node
+};
+
+struct Layout {
+  // Reference inputs (validated copies).
+  int32_t n_nodes = 0, num_vars = 0, max_var = 0;
+  std::vector<int32_t> kind, a, b, var;
+  std::vector<int32_t> node_of_var;  // max_var + 1, -1 = no node
+  std::vector<int32_t> out_var, out_node;
+  std::vector<uint8_t> out_tgt;
+  std::vector<int32_t> cpi, ucpi;
+  std::vector<int64_t> clause_ptr;
+  std::vector<int32_t> clause_lit;
+  bool unsat = false;
+  std::vector<int32_t> level;        // ASAP level per node
+
+  SoftProgram cone;                  // sampling
+  SoftProgram full;                  // parity taps (every node)
+
+  // Bit-sliced harvest program over every node.
+  int32_t n_bit_rows = 0;
+  std::vector<int32_t> bit_row_of_node;
+  std::vector<I4> bit_ops;           // non-INPUT nodes, level-sorted
+  std::vector<int32_t> bit_lvl_ptr;  // into bit_ops
+  std::vector<int32_t> cpi_bit_row, ucpi_bit_row;
+  std::vector<int32_t> out_bit_row;
+  std::vector<int32_t> clause_ptr32; // n_clauses + 1
+  std::vector<int32_t> clause_enc;   // bit_row << 1 | negated
+  int32_t key_words = 0;             // (num_vars + 63) / 64
+  std::vector<int32_t> key_bit_row;  // key_words * 64, -1 = padding
+
+  int64_t n_lits() const { return static_cast<int64_t>(clause_lit.size()); }
+};
+
+// Throws std::invalid_argument with the reference's wording where one exists.
+Layout build_layout(const sgx_circuit_desc& d);
+
+void layout_info(const Layout& L, int64_t* info16);
+
+}  // namespace sgx

@@ -1,0 +1,273 @@
+"""``run`` and friends: the reference's sampler API over the sm_100a library.
+
+Mirrors include/satgrad/sampler.hpp: ``SamplerConfig`` (:23-33),
+``SolutionSet`` (:39-55), ``RunStats`` (:57-67), ``RunResult`` (:69-72) and
+``run`` (:79-81, sampler.cpp:89-203).  Every call goes through the C-ABI of
+``libsatgrad_b200.so``; nothing here computes a sample.
+
+The device implements the reference's single-precision instantiation
+(``use_f32 = true``) bit for bit; asking for the double-precision path raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .circuit import Circuit, Instance, PathClassification
+from .cnf import CnfFormula, format_solution_line, key_to_assignment
+
+
+class RestartPolicy(enum.IntEnum):
+    NONE = 0
+    REINIT_ON_EXHAUST = 1
+
+
+@dataclass
+class SamplerConfig:
+    batch: int = 1024
+    iterations: int = 5
+    learning_rate: float = 10.0
+    seed: int = 1
+    max_solutions: int = 0
+    timeout_s: float = 0.0
+    restart: RestartPolicy = RestartPolicy.NONE
+    threads: int = 1          # accepted for API parity; the device ignores it
+    use_f32: bool = True      # the device path is the f32 instantiation
+    row_offset: int = 0       # global row of local row 0 (sample sharding)
+    max_restarts: int = 1000  # sampler.cpp:180 safety valve
+    solution_capacity: int = 0
+
+
+@dataclass
+class RunStats:
+    unique_count: int = 0
+    attempts: int = 0
+    wall_time_s: float = 0.0
+    throughput: float = 0.0
+    loss_trace: list = field(default_factory=list)
+    new_unique: list = field(default_factory=list)
+    restarts: int = 0
+    timed_out: bool = False
+    note: str = ""
+    phase_ms: dict = field(default_factory=dict)
+
+
+class SolutionSet:
+    """Insertion-ordered unique solutions as packed dedupe keys."""
+
+    def __init__(self, num_vars: int, keys: np.ndarray | None = None):
+        self.num_vars = num_vars
+        words = (num_vars + 63) // 64
+        self.keys = keys if keys is not None else np.zeros((0, words), np.uint64)
+
+    def size(self) -> int:
+        return int(self.keys.shape[0])
+
+    __len__ = size
+
+    def assignment(self, i: int) -> np.ndarray:
+        return key_to_assignment(self.keys[i], self.num_vars)
+
+    def format(self) -> str:  # format_solutions, sampler.cpp:78-85
+        return "".join(format_solution_line(k, self.num_vars) + "\n" for k in self.keys)
+
+
+@dataclass
+class RunResult:
+    solutions: SolutionSet
+    stats: RunStats
+
+
+_ctx: dict[int, int] = {}
+
+
+def device_context(device: int = 0) -> int:
+    L = _lib.load()
+    if device not in _ctx:
+        h = C.c_void_p()
+        _lib.check(L.sgx_open(device, C.byref(h)))
+        _ctx[device] = h.value
+    return _ctx[device]
+
+
+class DeviceCircuit:
+    """A circuit + CNF uploaded and levelized on one GPU (sgx_circuit_upload)."""
+
+    def __init__(self, cnf: CnfFormula, circuit: Circuit, paths: PathClassification,
+                 unsat: bool = False, device: int = 0):
+        self.L = _lib.load()
+        self.num_vars = cnf.num_vars
+        self.circuit = circuit
+        self.paths = paths
+        self._keep = [np.ascontiguousarray(x) for x in (
+            circuit.kind, circuit.a, circuit.b, circuit.var, circuit.out_var, circuit.out_tgt,
+            paths.constrained_pi, paths.unconstrained_pi, cnf.clause_ptr, cnf.clause_lit)]
+        self.desc = make_desc(cnf, circuit, paths, unsat, self._keep)
+        h = C.c_void_p()
+        _lib.check(self.L.sgx_circuit_upload(device_context(device), C.byref(self.desc), C.byref(h)))
+        self.h = h.value
+        self.device = device
+
+    @classmethod
+    def from_instance(cls, inst: Instance, device: int = 0) -> "DeviceCircuit":
+        return cls(inst.cnf, inst.circuit, inst.paths, inst.unsat, device)
+
+    def info(self) -> dict:
+        out = np.zeros(16, np.int64)
+        _lib.check(self.L.sgx_circuit_info(self.h, _lib.ptr(out, C.c_int64)))
+        keys = ["nodes", "cone_nodes", "cone_edges", "soft_levels", "bit_levels", "fwd_ops",
+                "bwd_ops", "bit_ops", "clauses", "literals", "key_words", "cpi", "ucpi",
+                "outputs", "num_vars", "unsat"]
+        return dict(zip(keys, (int(x) for x in out)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.sgx_circuit_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def make_desc(cnf, circuit, paths, unsat, keep) -> _lib.CircuitDesc:
+    kind, a, b, var, out_var, out_tgt, cpi, ucpi, cptr, clit = keep
+    d = _lib.CircuitDesc()
+    d.n_nodes = len(kind)
+    d.kind, d.a, d.b, d.var = (_lib.ptr(x, C.c_int32) for x in (kind, a, b, var))
+    d.num_vars = cnf.num_vars
+    d.n_outputs = len(out_var)
+    d.out_var = _lib.ptr(out_var, C.c_int32)
+    d.out_target = _lib.ptr(out_tgt, C.c_uint8)
+    d.n_cpi, d.cpi = len(cpi), _lib.ptr(cpi, C.c_int32)
+    d.n_ucpi, d.ucpi = len(ucpi), _lib.ptr(ucpi, C.c_int32)
+    d.n_clauses = len(cptr) - 1
+    d.clause_ptr = _lib.ptr(cptr, C.c_int64)
+    d.clause_lit = _lib.ptr(clit, C.c_int32)
+    d.unsat = 1 if unsat else 0
+    return d
+
+
+def layout_stats(cnf, circuit, paths, unsat=False) -> dict:
+    """Host-only levelization (no GPU needed)."""
+    L = _lib.load()
+    keep = [np.ascontiguousarray(x) for x in (
+        circuit.kind, circuit.a, circuit.b, circuit.var, circuit.out_var, circuit.out_tgt,
+        paths.constrained_pi, paths.unconstrained_pi, cnf.clause_ptr, cnf.clause_lit)]
+    d = make_desc(cnf, circuit, paths, unsat, keep)
+    out = np.zeros(16, np.int64)
+    _lib.check(L.sgx_layout_stats(C.byref(d), _lib.ptr(out, C.c_int64)))
+    keys = ["nodes", "cone_nodes", "cone_edges", "soft_levels", "bit_levels", "fwd_ops",
+            "bwd_ops", "bit_ops", "clauses", "literals", "key_words", "cpi", "ucpi", "outputs",
+            "num_vars", "unsat"]
+    return dict(zip(keys, (int(x) for x in out)))
+
+
+class Sampler:
+    """sgx_sampler: device buffers for one batch shape + the run loop."""
+
+    def __init__(self, dc: DeviceCircuit, cfg: SamplerConfig):
+        if not cfg.use_f32:
+            raise ValueError("the B200 path implements the reference's f32 instantiation "
+                             "(SamplerConfig.use_f32 = True)")
+        self.L = _lib.load()
+        self.dc = dc
+        self.cfg = cfg
+        c = _lib.SamplerCfg()
+        c.batch = cfg.batch
+        c.iterations = cfg.iterations
+        c.learning_rate = cfg.learning_rate
+        c.seed = cfg.seed
+        c.max_solutions = cfg.max_solutions
+        c.timeout_s = cfg.timeout_s
+        c.restart_policy = int(cfg.restart)
+        c.row_offset = cfg.row_offset
+        c.solution_capacity = cfg.solution_capacity
+        c.max_restarts = cfg.max_restarts
+        self._cfg = c
+        h = C.c_void_p()
+        _lib.check(self.L.sgx_sampler_create(dc.h, C.byref(c), C.byref(h)))
+        self.h = h.value
+
+    def run(self) -> RunStats:
+        st = _lib.RunStatsC()
+        _lib.check(self.L.sgx_run(self.h, C.byref(st)))
+        loss = np.zeros(max(1, st.n_loss), np.float64)
+        nu = np.zeros(max(1, st.n_harvest), np.int64)
+        _lib.check(self.L.sgx_run_traces(self.h, _lib.ptr(loss, C.c_double),
+                                         _lib.ptr(nu, C.c_int64)))
+        ph = np.zeros(8, np.float64)
+        _lib.check(self.L.sgx_phase_times(self.h, _lib.ptr(ph, C.c_double)))
+        names = ["init", "step", "harvest", "forward", "backward", "eval", "keys", "commit"]
+        note = ""
+        if st.unsat:
+            note = getattr(self.dc, "unsat_note", "") or "unsatisfiable by construction"
+        return RunStats(unique_count=st.unique_count, attempts=st.attempts,
+                        wall_time_s=st.wall_time_s, throughput=st.throughput,
+                        loss_trace=[float(x) for x in loss[:st.n_loss]],
+                        new_unique=[int(x) for x in nu[:st.n_harvest]], restarts=st.restarts,
+                        timed_out=bool(st.timed_out), note=note,
+                        phase_ms=dict(zip(names, (float(x) for x in ph))))
+
+    def solution_count(self) -> int:
+        return int(self.L.sgx_solution_count(self.h))
+
+    def fetch(self, first: int = 0, count: int | None = None) -> np.ndarray:
+        n = self.solution_count()
+        if count is None:
+            count = n - first
+        words = int(self.L.sgx_key_words(self.h))
+        out = np.zeros((count, words), np.uint64)
+        _lib.check(self.L.sgx_fetch_solutions(self.h, first, count,
+                                              _lib.ptr(out, C.c_uint64) if count else None))
+        return out
+
+    # building blocks ----------------------------------------------------------
+    def init(self, restart: int):
+        _lib.check(self.L.sgx_init(self.h, restart))
+
+    def step(self) -> float:
+        x = C.c_double()
+        _lib.check(self.L.sgx_step(self.h, C.byref(x)))
+        return x.value
+
+    def harvest(self, restart: int, it: int) -> tuple[int, int]:
+        att, add = C.c_int64(), C.c_int64()
+        _lib.check(self.L.sgx_harvest(self.h, restart, it, C.byref(att), C.byref(add)))
+        return att.value, add.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.sgx_sampler_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run(cnf: CnfFormula, circuit: Circuit, paths: PathClassification, cfg: SamplerConfig,
+        unsat: bool = False, unsat_note: str = "", device: int = 0) -> RunResult:
+    """satgrad::run (sampler.hpp:79-81): upload, sample, fetch every solution."""
+    dc = DeviceCircuit(cnf, circuit, paths, unsat, device)
+    dc.unsat_note = unsat_note
+    s = Sampler(dc, cfg)
+    try:
+        stats = s.run()
+        keys = s.fetch()
+    finally:
+        s.close()
+        dc.close()
+    return RunResult(SolutionSet(cnf.num_vars, keys), stats)
+
+
+def run_instance(inst: Instance, cfg: SamplerConfig, device: int = 0) -> RunResult:
+    return run(inst.cnf, inst.circuit, inst.paths, cfg, inst.unsat, inst.unsat_note, device)
