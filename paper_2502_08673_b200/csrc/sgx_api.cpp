@@ -282,6 +282,7 @@ void sampler_harvest(sgx_sampler* s, int restart, int iter, long long quota_left
   CK(cudaStreamSynchronize(s->st));
   if (s->hpin->overflow) {
     grow_store(s, s->n_solutions + s->hpin->accepted);
+    CK(cudaMemsetAsync(&s->hout.p->overflow, 0, sizeof(long long), s->st));
     sgx::launch_append(s->st, s->newmask.p, s->block_count.p, s->K.p, L.key_words, s->Bp, s->store.p,
                        s->n_solutions, s->store_cap, s->hout.p);
     s->launches += 1;

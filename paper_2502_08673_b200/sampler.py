@@ -54,6 +54,8 @@ class RunStats:
     timed_out: bool = False
     note: str = ""
     phase_ms: dict = field(default_factory=dict)
+    device_ms: float = 0.0   # CUDA-event time of the run on the sampler stream
+    launches: int = 0        # kernels the run launched
 
 
 class SolutionSet:
@@ -213,7 +215,8 @@ class Sampler:
                         loss_trace=[float(x) for x in loss[:st.n_loss]],
                         new_unique=[int(x) for x in nu[:st.n_harvest]], restarts=st.restarts,
                         timed_out=bool(st.timed_out), note=note,
-                        phase_ms=dict(zip(names, (float(x) for x in ph))))
+                        phase_ms=dict(zip(names, (float(x) for x in ph))),
+                        device_ms=st.device_ms, launches=st.launches)
 
     def solution_count(self) -> int:
         return int(self.L.sgx_solution_count(self.h))

