@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -85,6 +86,12 @@ struct DBuf {
 
 int round_up(long long x, int m) { return static_cast<int>((x + m - 1) / m * m); }
 
+// Tile-major index (parity taps run with 32-sample tiles): sample r, row j of
+// a [tile][rows][32] array.
+size_t tile_index(int r, size_t j, size_t rows) {
+  return (static_cast<size_t>(r / 32) * rows + j) * 32 + static_cast<size_t>(r % 32);
+}
+
 uint64_t next_pow2(uint64_t x) {
   uint64_t p = 1;
   while (p < x) p <<= 1;
@@ -97,16 +104,25 @@ std::vector<int4> to_int4(const std::vector<sgx::I4>& v) {
   return out;
 }
 
+std::vector<int2> to_int2(const std::vector<int32_t>& v) {
+  std::vector<int2> out(v.size() / 2);
+  for (size_t i = 0; i < out.size(); ++i) out[i] = make_int2(v[2 * i], v[2 * i + 1]);
+  return out;
+}
+
 struct DevSoft {
   DBuf<int4> fwd, bwd;
-  DBuf<int> out_row;
-  int n_fwd_chunks = 0, n_bwd_chunks = 0, n_rows = 0;
+  DBuf<int2> fwd_lvl, bwd_lvl;
+  DBuf<int> out_enc;
+  int n_fwd_levels = 0, n_bwd_levels = 0, n_rows = 0;
   void upload(const sgx::SoftProgram& P, cudaStream_t st) {
     fwd.upload(to_int4(P.fwd), st);
     bwd.upload(to_int4(P.bwd), st);
-    out_row.upload(P.out_row, st);
-    n_fwd_chunks = static_cast<int>(P.fwd.size() / sgx::kU);
-    n_bwd_chunks = static_cast<int>(P.bwd.size() / sgx::kU);
+    fwd_lvl.upload(to_int2(P.fwd_lvl), st);
+    bwd_lvl.upload(to_int2(P.bwd_lvl), st);
+    out_enc.upload(P.out_enc, st);
+    n_fwd_levels = static_cast<int>(P.fwd_lvl.size() / (2 * sgx::kWarps));
+    n_bwd_levels = static_cast<int>(P.bwd_lvl.size() / (2 * sgx::kWarps));
     n_rows = P.n_rows;
   }
 };
@@ -134,7 +150,7 @@ struct sgx_sampler {
   sgx_circuit* c = nullptr;
   sgx_sampler_cfg cfg{};
   cudaStream_t st = nullptr;
-  int Bp = 0, W = 0, wpc = 8, n_partial = 148;
+  int Bp = 0, W = 0, wpc = 8, vec = 2, n_partial = 148;
   DBuf<float> V, tape, adj, row_loss;
   DBuf<double> partial;
   DBuf<uint32_t> BT, valid, newmask;
@@ -196,7 +212,8 @@ void sampler_init(sgx_sampler* s, int restart) {
   const auto& L = s->c->L;
   uint64_t prefix = sgx::fold(sgx::fold(sgx::fold(sgx::kPi, s->cfg.seed), sgx::kInitTag),
                               static_cast<uint64_t>(static_cast<int64_t>(restart)));
-  sgx::launch_init_v(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, prefix, s->cfg.row_offset);
+  sgx::launch_init_v(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, 32 * s->vec, prefix,
+                     s->cfg.row_offset);
   s->launches += L.cpi.empty() ? 0 : 1;
   CK(cudaGetLastError());
 }
@@ -205,10 +222,13 @@ void sampler_step(sgx_sampler* s) {
   sgx_circuit* c = s->c;
   const uint64_t* tab = c->ctx->exp_tab.p;
   CK(cudaEventRecord(s->ev[0], s->st));
-  sgx::launch_forward(s->st, c->cone.fwd.p, c->cone.n_fwd_chunks, s->V.p, s->tape.p, s->Bp, 0, tab);
+  const int ncpi = static_cast<int>(c->L.cpi.size());
+  sgx::launch_forward(s->st, s->vec, c->cone.fwd.p, c->cone.fwd_lvl.p, c->cone.n_fwd_levels, s->V.p, ncpi,
+                      s->tape.p, c->cone.n_rows, s->Bp, 0, tab);
   CK(cudaEventRecord(s->ev[1], s->st));
-  sgx::launch_backward(s->st, c->cone.bwd.p, c->cone.n_bwd_chunks, s->tape.p, s->adj.p, s->V.p, nullptr,
-                       nullptr, s->Bp, static_cast<float>(s->cfg.learning_rate), c->cone.out_row.p,
+  sgx::launch_backward(s->st, s->vec, c->cone.bwd.p, c->cone.bwd_lvl.p, c->cone.n_bwd_levels, s->tape.p, s->adj.p,
+                       s->V.p, ncpi, c->cone.n_rows, nullptr, nullptr, s->Bp,
+                       static_cast<float>(s->cfg.learning_rate), c->cone.out_enc.p,
                        c->out_tgt.p, static_cast<int>(c->L.out_node.size()), s->row_loss.p, tab);
   sgx::launch_loss(s->st, s->row_loss.p, s->cfg.batch, s->partial.p, s->n_partial, s->hout.p);
   s->launches += 4;
@@ -262,7 +282,8 @@ void sampler_harvest(sgx_sampler* s, int restart, int iter, long long quota_left
       sgx::fold(sgx::fold(sgx::fold(sgx::kPi, s->cfg.seed), sgx::kFreeTag), static_cast<uint64_t>(static_cast<int64_t>(restart))),
       static_cast<uint64_t>(static_cast<int64_t>(iter)));
   sgx::launch_harden(s->st, s->V.p, static_cast<int>(L.cpi.size()), static_cast<int>(L.ucpi.size()),
-                     c->cpi_bit_row.p, c->ucpi_bit_row.p, s->BT.p, s->W, s->Bp, fprefix, s->cfg.row_offset);
+                     c->cpi_bit_row.p, c->ucpi_bit_row.p, s->BT.p, s->W, 32 * s->vec, fprefix,
+                     s->cfg.row_offset);
   sgx::launch_bit_eval(s->st, s->wpc, c->bit_ops.p, c->bit_lvl_ptr.p, c->n_bit_levels, s->BT.p, s->W,
                        c->out_bit_row.p, c->out_tgt.p, static_cast<int>(L.out_node.size()), c->clause_ptr.p,
                        c->clause_enc.p, static_cast<int>(L.clause_ptr.size()) - 1, s->valid.p, s->cfg.batch);
@@ -515,6 +536,13 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       s->Bp = round_up(cfg->batch, 1024);
       s->W = s->Bp / 32;
       s->wpc = s->W / 32 >= 2 * 148 ? 32 : (s->W / 16 >= 2 * 148 ? 16 : 8);
+      // Widest samples-per-thread that still leaves >= 3 tiles per SM
+      // (SGX_VEC overrides, for tuning).
+      s->vec = s->Bp / 128 >= 3 * 148 ? 4 : (s->Bp / 64 >= 3 * 148 ? 2 : 1);
+      if (const char* e = std::getenv("SGX_VEC")) {
+        int v = std::atoi(e);
+        if (v == 1 || v == 2 || v == 4) s->vec = v;
+      }
       const size_t Bp = static_cast<size_t>(s->Bp);
       s->V.alloc(L.cpi.size() * Bp);
       s->tape.alloc(static_cast<size_t>(L.cone.n_rows) * Bp);
@@ -656,27 +684,38 @@ int sgx_forward(sgx_circuit* c, const float* p, int32_t batch, float* tape, floa
     CK(cudaSetDevice(c->ctx->device));
     cudaStream_t st = c->ctx->stream;
     const int Bp = round_up(batch, sgx::kThreads);
-    std::vector<float> src(ncpi * Bp, 0.5f);
+    const size_t nr = static_cast<size_t>(L.full.n_rows);
+    std::vector<float> src(std::max<size_t>(ncpi * Bp, 1), 0.5f);
     for (int r = 0; r < batch; ++r)
-      for (size_t j = 0; j < ncpi; ++j) src[j * Bp + r] = p[r * ncpi + j];
+      for (size_t j = 0; j < ncpi; ++j) src[tile_index(r, j, ncpi)] = p[r * ncpi + j];
     DBuf<float> dsrc, dtape;
     dsrc.upload(src, st);
-    dtape.alloc(static_cast<size_t>(L.full.n_rows) * Bp);
-    sgx::launch_forward(st, c->full.fwd.p, c->full.n_fwd_chunks, dsrc.p, dtape.p, Bp, 1, c->ctx->exp_tab.p);
+    dtape.alloc(nr * Bp);
+    sgx::launch_forward(st, 1, c->full.fwd.p, c->full.fwd_lvl.p, c->full.n_fwd_levels, dsrc.p,
+                        static_cast<int>(ncpi), dtape.p, L.full.n_rows, Bp, 1, c->ctx->exp_tab.p);
     CK(cudaGetLastError());
-    std::vector<float> h(static_cast<size_t>(L.full.n_rows) * Bp);
+    std::vector<float> h(nr * Bp);
     CK(cudaMemcpyAsync(h.data(), dtape.p, h.size() * sizeof(float), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    for (int i = 0; i < L.n_nodes; ++i) {
-      const float* rowp = h.data() + static_cast<size_t>(L.full.row_of_node[i]) * Bp;
-      if (tape) std::memcpy(tape + static_cast<size_t>(i) * batch, rowp, sizeof(float) * batch);
-    }
+    // Reference node order; a folded node is recomputed from its operand with
+    // the same float operation the device applies on read.
+    auto value = [&](int node, int r) {
+      int row = L.full.row_of_node[node];
+      bool neg = false;
+      if (row < 0) {
+        row = L.full.virt_base[node];
+        neg = L.full.virt_neg[node] != 0;
+      }
+      float x = h[tile_index(r, row, nr)];
+      return neg ? 1.0f - x : x;
+    };
+    if (tape)
+      for (int i = 0; i < L.n_nodes; ++i)
+        for (int r = 0; r < batch; ++r) tape[static_cast<size_t>(i) * batch + r] = value(i, r);
     if (y) {
       const size_t m = L.out_node.size();
-      for (size_t o = 0; o < m; ++o) {
-        const float* rowp = h.data() + static_cast<size_t>(L.full.row_of_node[L.out_node[o]]) * Bp;
-        for (int r = 0; r < batch; ++r) y[r * m + o] = rowp[r];
-      }
+      for (size_t o = 0; o < m; ++o)
+        for (int r = 0; r < batch; ++r) y[r * m + o] = value(L.out_node[o], r);
     }
   });
 }
@@ -694,24 +733,29 @@ int sgx_backward(sgx_circuit* c, const float* tape, int32_t batch, const float* 
     CK(cudaSetDevice(c->ctx->device));
     cudaStream_t st = c->ctx->stream;
     const int Bp = round_up(batch, sgx::kThreads);
-    std::vector<float> ht(static_cast<size_t>(L.full.n_rows) * Bp, 0.5f);
-    for (int i = 0; i < L.n_nodes; ++i)
-      std::memcpy(ht.data() + static_cast<size_t>(L.full.row_of_node[i]) * Bp, tape + static_cast<size_t>(i) * batch,
-                  sizeof(float) * batch);
+    const size_t nr = static_cast<size_t>(L.full.n_rows);
+    // Only materialized rows are uploaded: folded nodes are re-derived from
+    // their operand on read, exactly as the reference computes them.
+    std::vector<float> ht(nr * Bp, 0.5f);
+    for (int i = 0; i < L.n_nodes; ++i) {
+      const int row = L.full.row_of_node[i];
+      if (row < 0) continue;
+      for (int r = 0; r < batch; ++r) ht[tile_index(r, row, nr)] = tape[static_cast<size_t>(i) * batch + r];
+    }
     std::vector<float> hv(std::max<size_t>(ncpi * Bp, 1), 0.0f);
     for (int r = 0; r < batch; ++r)
-      for (size_t j = 0; j < ncpi; ++j) hv[j * Bp + r] = v[r * ncpi + j];
+      for (size_t j = 0; j < ncpi; ++j) hv[tile_index(r, j, ncpi)] = v[r * ncpi + j];
     DBuf<float> dt, dadj, dV, ddv, ddp;
     dt.upload(ht, st);
     dV.upload(hv, st);
-    dadj.alloc(static_cast<size_t>(L.full.n_rows) * Bp);
+    dadj.alloc(nr * Bp);
     ddv.alloc(std::max<size_t>(ncpi * Bp, 1));
     ddp.alloc(std::max<size_t>(ncpi * Bp, 1));
     CK(cudaMemsetAsync(ddv.p, 0, ddv.n * sizeof(float), st));
     CK(cudaMemsetAsync(ddp.p, 0, ddp.n * sizeof(float), st));
-    sgx::launch_backward(st, c->full.bwd.p, c->full.n_bwd_chunks, dt.p, dadj.p, dV.p, ddv.p, ddp.p, Bp, 0.0f,
-                         c->full.out_row.p, c->out_tgt.p, static_cast<int>(L.out_node.size()), nullptr,
-                         c->ctx->exp_tab.p);
+    sgx::launch_backward(st, 1, c->full.bwd.p, c->full.bwd_lvl.p, c->full.n_bwd_levels, dt.p, dadj.p, dV.p,
+                         static_cast<int>(ncpi), L.full.n_rows, ddv.p, ddp.p, Bp, 0.0f, c->full.out_enc.p,
+                         c->out_tgt.p, static_cast<int>(L.out_node.size()), nullptr, c->ctx->exp_tab.p);
     CK(cudaGetLastError());
     std::vector<float> hdv(ddv.n), hdp(ddp.n);
     CK(cudaMemcpyAsync(hdv.data(), ddv.p, hdv.size() * sizeof(float), cudaMemcpyDeviceToHost, st));
@@ -719,8 +763,8 @@ int sgx_backward(sgx_circuit* c, const float* tape, int32_t batch, const float* 
     CK(cudaStreamSynchronize(st));
     for (int r = 0; r < batch; ++r)
       for (size_t j = 0; j < ncpi; ++j) {
-        if (dv) dv[r * ncpi + j] = hdv[j * Bp + r];
-        if (dp) dp[r * ncpi + j] = hdp[j * Bp + r];
+        if (dv) dv[r * ncpi + j] = hdv[tile_index(r, j, ncpi)];
+        if (dp) dp[r * ncpi + j] = hdp[tile_index(r, j, ncpi)];
       }
   });
 }

@@ -9,160 +9,303 @@ namespace sgx {
 // K1: V0 = (float)(2 * u01(hash{seed, 'init', restart, row, col}) - 1)
 // Layout [col][Bp]; consecutive threads take consecutive rows of one column.
 // ---------------------------------------------------------------------------
+// V is tile-major like the tape: [tile][col][tile_rows]; i walks it in
+// memory order.
 __global__ void __launch_bounds__(kThreads)
-k_init_v(float* __restrict__ V, int ncols, int Bp, uint64_t prefix, long long row_offset) {
+k_init_v(float* __restrict__ V, int ncols, int Bp, int tile_rows, uint64_t prefix, long long row_offset) {
   const long long total = static_cast<long long>(ncols) * Bp;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    int c = static_cast<int>(i / Bp);
-    int r = static_cast<int>(i - static_cast<long long>(c) * Bp);
+    const long long tile = i / (static_cast<long long>(ncols) * tile_rows);
+    const int within = static_cast<int>(i - tile * ncols * tile_rows);
+    const int c = within / tile_rows;
+    const int r = static_cast<int>(tile * tile_rows) + within % tile_rows;
     uint64_t h = fold(fold(prefix, static_cast<uint64_t>(row_offset + r)), static_cast<uint64_t>(c));
     double u = static_cast<double>(h >> 11) * 0x1.0p-53;  // u01, rng.hpp:28-30
     V[i] = __double2float_rn(__dsub_rn(__dmul_rn(2.0, u), 1.0));
   }
 }
 
-// ---------------------------------------------------------------------------
-// K2: forward over the soft program.  One thread = one sample; ops arrive in
-// chunks of kU independent ops (a chunk never crosses a level), so each
-// thread issues all 2*kU operand loads of a chunk before it computes.  Every
-// lane runs the same op stream: control flow is warp-uniform and the op
-// records are broadcast loads.  tape is [row][Bp]: each warp load/store is
-// one 128-byte line.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads)
-k_forward(const int4* __restrict__ ops, int n_chunks, const float* __restrict__ src, float* tape,
-          int Bp, int src_is_prob, const uint64_t* __restrict__ exp_tab) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= Bp) return;
-  const size_t B = static_cast<size_t>(Bp);
-  for (int c = 0; c < n_chunks; ++c) {
-    int4 op[kU];
+// Vector access of V consecutive samples of one tape row.
+template <int V>
+__device__ __forceinline__ void vload(const float* p, float (&o)[V]) {
+  if constexpr (V == 1) {
+    o[0] = *p;
+  } else if constexpr (V == 2) {
+    const float2 t = *reinterpret_cast<const float2*>(p);
+    o[0] = t.x;
+    o[1] = t.y;
+  } else {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    o[0] = t.x;
+    o[1] = t.y;
+    o[2] = t.z;
+    o[3] = t.w;
+  }
+}
+
+template <int V>
+__device__ __forceinline__ void vstore(float* p, const float (&o)[V]) {
+  if constexpr (V == 1) {
+    *p = o[0];
+  } else if constexpr (V == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(o[0], o[1]);
+  } else {
+    *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// autodiff.cpp:99-141, one node value.
+__device__ __forceinline__ float gate_value(int code, float a, float b) {
+  switch (code) {
+    case SGX_CONST0: return 0.0f;
+    case SGX_CONST1: return 1.0f;
+    case SGX_BUF: return a;
+    case SGX_NOT: return __fsub_rn(1.0f, a);
+    case SGX_AND2: return __fmul_rn(a, b);
+    case SGX_OR2: return __fsub_rn(1.0f, __fmul_rn(__fsub_rn(1.0f, a), __fsub_rn(1.0f, b)));
+    case SGX_XOR2: return __fadd_rn(__fmul_rn(__fsub_rn(1.0f, a), b), __fmul_rn(a, __fsub_rn(1.0f, b)));
+    case SGX_XNOR2: return __fadd_rn(__fmul_rn(a, b), __fmul_rn(__fsub_rn(1.0f, a), __fsub_rn(1.0f, b)));
+    default: return 0.0f;
+  }
+}
+
+// autodiff.cpp:225-277, one fan-out contribution pulled into acc.
+__device__ __forceinline__ float pull(int ck, float acc, float g, float vo) {
+  switch (ck) {
+    case SGX_BUF: return __fadd_rn(acc, g);
+    case SGX_NOT: return __fsub_rn(acc, g);
+    case SGX_AND2: return __fadd_rn(acc, __fmul_rn(g, vo));
+    case SGX_OR2: return __fadd_rn(acc, __fmul_rn(g, __fsub_rn(1.0f, vo)));
+    case SGX_XOR2: return __fadd_rn(acc, __fmul_rn(g, __fsub_rn(1.0f, __fmul_rn(2.0f, vo))));
+    case SGX_XNOR2: return __fadd_rn(acc, __fmul_rn(g, __fsub_rn(__fmul_rn(2.0f, vo), 1.0f)));
+    default: return acc;
+  }
+}
+
+// Folded-operand read: row << 1 | negate (a folded NOT reads 1 - x, exactly
+// the reference's NOT, autodiff.cpp:112).
+template <int V>
+__device__ __forceinline__ void load_operand(const float* T, int enc, float (&o)[V]) {
+  vload<V>(T + static_cast<size_t>(enc >> 1) * (32 * V), o);
+  if (enc & 1) {
 #pragma unroll
-    for (int k = 0; k < kU; ++k) op[k] = __ldg(ops + static_cast<size_t>(c) * kU + k);
-    float x[kU], y[kU];
+    for (int v = 0; v < V; ++v) o[v] = __fsub_rn(1.0f, o[v]);
+  }
+}
+
+// Backward pull coefficients per consumer kind: contribution = g * (c0 + c1*v)
+// with c1*v exact, so one fma reproduces the reference's (1 - v), (1 - 2v),
+// (2v - 1), v, +1, -1 factors bit for bit (autodiff.cpp:225-277).
+__constant__ float kPullC0[9] = {0.f, 0.f, 0.f, 1.f, -1.f, 0.f, 1.f, 1.f, -1.f};
+__constant__ float kPullC1[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 1.f, -1.f, -2.f, 2.f};
+
+// ---------------------------------------------------------------------------
+// K2: forward over the soft program (NOT/BUF folded into operand reads).  A
+// CTA owns a tile of 32*V samples; its tape slice is [row][32*V] contiguous
+// (tile-major), so one warp access is 128*V contiguous bytes and an address
+// is one multiply-add.  kWarps warps split each level; __syncthreads()
+// separates levels.  Work arrives as kind-homogeneous groups of <= kGroup
+// ops: one uniform dispatch per group, then straight-line code that issues
+// every operand load of the group before computing.
+// ---------------------------------------------------------------------------
+template <int V>
+__global__ void __launch_bounds__(32 * kWarps)
+k_forward(const int4* __restrict__ grp, const int2* __restrict__ lvl, int n_levels,
+          const float* __restrict__ src, int ncols, float* tape, int n_rows, int src_is_prob,
+          const uint64_t* __restrict__ exp_tab) {
+  constexpr int TILE = 32 * V;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* T = tape + static_cast<size_t>(blockIdx.x) * n_rows * TILE + lane * V;
+  const float* S = src + static_cast<size_t>(blockIdx.x) * ncols * TILE + lane * V;
+  for (int l = 0; l < n_levels; ++l) {
+    const int2 L = __ldg(lvl + l * kWarps + warp);
+    for (int g = 0; g < L.y; ++g) {
+      const int4* rec = grp + static_cast<size_t>(L.x + g) * kGroupRecs;
+      const int4 h = __ldg(rec);
+      int opd[2 * kGroup];
 #pragma unroll
-    for (int k = 0; k < kU; ++k) {
-      const int code = op[k].x;
-      x[k] = 0.0f;
-      y[k] = 0.0f;
-      if (code == SGX_INPUT) {
-        if (op[k].z >= 0) x[k] = src[op[k].z * B + s];
-      } else if (code >= SGX_BUF && code <= SGX_XNOR2) {
-        x[k] = tape[op[k].z * B + s];
-        if (code >= SGX_AND2) y[k] = tape[op[k].w * B + s];
+      for (int q = 0; q < kGroup / 2; ++q) {
+        const int4 t = __ldg(rec + 1 + q);
+        opd[4 * q] = t.x;
+        opd[4 * q + 1] = t.y;
+        opd[4 * q + 2] = t.z;
+        opd[4 * q + 3] = t.w;
+      }
+      const int kind = h.x, n = h.y;
+      float* out = T + static_cast<size_t>(h.z) * TILE;
+      float x[kGroup][V], y[kGroup][V];
+      if (kind >= SGX_AND2) {
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k)
+          if (k < n) {
+            load_operand<V>(T, opd[2 * k], x[k]);
+            load_operand<V>(T, opd[2 * k + 1], y[k]);
+          }
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k)
+          if (k < n) {
+            float r[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) r[v] = gate_value(kind, x[k][v], y[k][v]);
+            vstore<V>(out + k * TILE, r);
+          }
+      } else if (kind == SGX_NOT || kind == SGX_BUF) {
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k)
+          if (k < n) load_operand<V>(T, opd[2 * k], x[k]);
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k)
+          if (k < n) {
+            float r[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) r[v] = kind == SGX_NOT ? __fsub_rn(1.0f, x[k][v]) : x[k][v];
+            vstore<V>(out + k * TILE, r);
+          }
+      } else if (kind == SGX_INPUT) {
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k)
+          if (k < n && opd[2 * k] >= 0) vload<V>(S + static_cast<size_t>(opd[2 * k]) * TILE, x[k]);
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k)
+          if (k < n) {
+            float r[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+              r[v] = opd[2 * k] < 0 ? 0.5f : (src_is_prob ? x[k][v] : sigmoid_ref(x[k][v], exp_tab));
+            vstore<V>(out + k * TILE, r);
+          }
+      } else {  // CONST0 / CONST1
+        float r[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) r[v] = kind == SGX_CONST1 ? 1.0f : 0.0f;
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k)
+          if (k < n) vstore<V>(out + k * TILE, r);
       }
     }
-#pragma unroll
-    for (int k = 0; k < kU; ++k) {
-      const int code = op[k].x;
-      const float a = x[k], b = y[k];
-      float r;
-      switch (code) {
-        case SGX_INPUT:
-          r = op[k].z < 0 ? 0.5f : (src_is_prob ? a : sigmoid_ref(a, exp_tab));
-          break;
-        case SGX_CONST0: r = 0.0f; break;
-        case SGX_CONST1: r = 1.0f; break;
-        case SGX_BUF: r = a; break;
-        case SGX_NOT: r = __fsub_rn(1.0f, a); break;
-        case SGX_AND2: r = __fmul_rn(a, b); break;
-        case SGX_OR2: r = __fsub_rn(1.0f, __fmul_rn(__fsub_rn(1.0f, a), __fsub_rn(1.0f, b))); break;
-        case SGX_XOR2:
-          r = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, a), b), __fmul_rn(a, __fsub_rn(1.0f, b)));
-          break;
-        case SGX_XNOR2:
-          r = __fadd_rn(__fmul_rn(a, b), __fmul_rn(__fsub_rn(1.0f, a), __fsub_rn(1.0f, b)));
-          break;
-        default: r = 0.0f; break;
-      }
-      if (code != kNop) tape[op[k].y * B + s] = r;
-    }
+    __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------------------
-// K3+K4: per-row loss, pull-style backward and the fused GD step.  The micro
-// op stream is BEGIN (seed) / EDGE* (one per fan-out slot, consumers in
-// descending reference id) / END (store adjoint, or for a V column: dV and
-// V -= lr * dV).  No atomics: every adjoint is produced by exactly one thread
-// of the owning sample, in one pass.
+// K3+K4: per-row loss, pull-style backward and the fused GD step.  Same tile
+// and level split as the forward, levels high to low.  Each warp runs its
+// own micro-op stream in chunks of U records (all loads of a chunk issued
+// first): BEGIN (seed) / EDGE* (fan-out slots, consumers in descending
+// reference id) / SUB_BEGIN EDGE* SUB_END (a folded NOT/BUF consumer's
+// adjoint, summed in its own order, then subtracted/added) / END (store the
+// adjoint; for a V column: dV and V -= lr * dV).  No atomics: every adjoint
+// is produced once, by the warp that owns the node.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads)
-k_backward(const int4* __restrict__ ops, int n_chunks, const float* tape, float* adj, float* V,
-           float* dv_out, float* dp_out, int Bp, float lr, const int* __restrict__ out_row,
+template <int V, int U>
+__global__ void __launch_bounds__(32 * kWarps)
+k_backward(const int4* __restrict__ ops, const int2* __restrict__ lvl, int n_levels,
+           const float* tape, float* adj, float* Vp, int ncols, int n_rows, float* dv_out,
+           float* dp_out, float lr, const int* __restrict__ out_enc,
            const uint8_t* __restrict__ out_tgt, int n_out, float* __restrict__ row_loss,
            const uint64_t* __restrict__ exp_tab) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= Bp) return;
-  const size_t B = static_cast<size_t>(Bp);
-  if (row_loss) {  // loss (autodiff.cpp:160-166): outputs in order
-    float l = 0.0f;
+  constexpr int TILE = 32 * V;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t tbase = static_cast<size_t>(blockIdx.x) * n_rows * TILE + lane * V;
+  const float* T = tape + tbase;
+  float* A = adj + tbase;
+  const size_t vbase = static_cast<size_t>(blockIdx.x) * ncols * TILE + lane * V;
+  if (row_loss && warp == 0) {  // loss (autodiff.cpp:160-166): outputs in order
+    float l[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) l[v] = 0.0f;
     for (int m = 0; m < n_out; ++m) {
-      float d = __fsub_rn(tape[static_cast<size_t>(__ldg(out_row + m)) * B + s],
-                          __ldg(out_tgt + m) ? 1.0f : 0.0f);
-      l = __fadd_rn(l, __fmul_rn(d, d));
-    }
-    row_loss[s] = l;
-  }
-  float acc = 0.0f;
-  for (int c = 0; c < n_chunks; ++c) {
-    int4 op[kU];
+      float yv[V];
+      load_operand<V>(T, __ldg(out_enc + m), yv);
+      const float t = __ldg(out_tgt + m) ? 1.0f : 0.0f;
 #pragma unroll
-    for (int k = 0; k < kU; ++k) op[k] = __ldg(ops + static_cast<size_t>(c) * kU + k);
-    float x[kU], y[kU];
-#pragma unroll
-    for (int k = 0; k < kU; ++k) {
-      const int code = op[k].x & 0xff;
-      x[k] = 0.0f;
-      y[k] = 0.0f;
-      if (code == kBegin) {
-        if (op[k].x & kSeedBit) x[k] = tape[op[k].y * B + s];
-      } else if (code == kEdge) {
-        x[k] = adj[op[k].y * B + s];
-        if (op[k].z >= 0) y[k] = tape[op[k].z * B + s];
-      } else if (code == kEnd) {
-        if (op[k].z >= 0) x[k] = V[op[k].z * B + s];
+      for (int v = 0; v < V; ++v) {
+        const float d = __fsub_rn(yv[v], t);
+        l[v] = __fadd_rn(l[v], __fmul_rn(d, d));
       }
     }
+    vstore<V>(row_loss + static_cast<size_t>(blockIdx.x) * TILE + lane * V, l);
+  }
+  float acc[V], acc2[V];
 #pragma unroll
-    for (int k = 0; k < kU; ++k) {
-      const int code = op[k].x & 0xff;
-      if (code == kBegin) {
-        acc = 0.0f;
-        if (op[k].x & kSeedBit)  // adj[out] += 2 (y - t)  (autodiff.cpp:206)
-          acc = __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(x[k], (op[k].x & kTargetBit) ? 1.0f : 0.0f)));
-      } else if (code == kEdge) {
-        const float g = x[k], vo = y[k];
-        switch ((op[k].x >> kKindShift) & 0xf) {  // autodiff.cpp:225-277
-          case SGX_BUF: acc = __fadd_rn(acc, g); break;
-          case SGX_NOT: acc = __fsub_rn(acc, g); break;
-          case SGX_AND2: acc = __fadd_rn(acc, __fmul_rn(g, vo)); break;
-          case SGX_OR2: acc = __fadd_rn(acc, __fmul_rn(g, __fsub_rn(1.0f, vo))); break;
-          case SGX_XOR2:
-            acc = __fadd_rn(acc, __fmul_rn(g, __fsub_rn(1.0f, __fmul_rn(2.0f, vo))));
-            break;
-          case SGX_XNOR2:
-            acc = __fadd_rn(acc, __fmul_rn(g, __fsub_rn(__fmul_rn(2.0f, vo), 1.0f)));
-            break;
-          default: break;
+  for (int v = 0; v < V; ++v) acc[v] = acc2[v] = 0.0f;
+  for (int li = 0; li < n_levels; ++li) {
+    const int2 L = __ldg(lvl + li * kWarps + warp);
+    for (int c = 0; c < L.y; c += U) {
+      int4 op[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        op[k] = c + k < L.y ? __ldg(ops + L.x + c + k) : make_int4(kNop, -1, -1, 0);
+      float x[U][V], y[U][V];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int code = op[k].x & 0xff;
+        if (code == kEdge) {
+          vload<V>(A + static_cast<size_t>(op[k].y) * TILE, x[k]);
+          if (op[k].z >= 0) vload<V>(T + static_cast<size_t>(op[k].z) * TILE, y[k]);
+        } else if (code == kBegin || code == kSubBegin) {
+          if (op[k].x & kSeedBit) vload<V>(T + static_cast<size_t>(op[k].y) * TILE, x[k]);
+        } else if (code == kEnd) {
+          if (op[k].z >= 0) vload<V>(Vp + vbase + static_cast<size_t>(op[k].z) * TILE, x[k]);
         }
-      } else if (code == kEnd) {
-        if (op[k].y >= 0) adj[op[k].y * B + s] = acc;
-        if (op[k].z >= 0) {  // autodiff.cpp:212-221 then gd_step :285-290
-          const float v = x[k];
-          const float p = sigmoid_ref(v, exp_tab);
-          const float dv = __fmul_rn(__fmul_rn(acc, p), __fsub_rn(1.0f, p));
-          const size_t at = op[k].z * B + s;
-          if (dv_out) {
-            dv_out[at] = dv;
-            dp_out[at] = acc;
-          } else {
-            V[at] = __fsub_rn(v, __fmul_rn(lr, dv));
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int f = op[k].x;
+        const int code = f & 0xff;
+        if (code == kEdge) {
+          const int ck = (f >> kKindShift) & 0xf;
+          const float c0 = kPullC0[ck], c1 = kPullC1[ck];
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            float vo = op[k].z >= 0 ? y[k][v] : 0.0f;
+            if (f & kNegOtherBit) vo = __fsub_rn(1.0f, vo);
+            const float p = __fmul_rn(x[k][v], __fmaf_rn(c1, vo, c0));
+            if (f & kInSubBit)
+              acc2[v] = __fadd_rn(acc2[v], p);
+            else
+              acc[v] = __fadd_rn(acc[v], p);
+          }
+        } else if (code == kBegin || code == kSubBegin) {
+          const float t = (f & kTargetBit) ? 1.0f : 0.0f;
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            float yv = x[k][v];
+            if (f & kNegSelfBit) yv = __fsub_rn(1.0f, yv);
+            // adj[out] += 2 (y - t) on a zero adjoint (autodiff.cpp:206)
+            const float sd = (f & kSeedBit) ? __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(yv, t))) : 0.0f;
+            if (code == kBegin)
+              acc[v] = sd;
+            else
+              acc2[v] = sd;
+          }
+        } else if (code == kSubEnd) {
+          const bool is_not = ((f >> kKindShift) & 0xf) == SGX_NOT;
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[v] = is_not ? __fsub_rn(acc[v], acc2[v]) : __fadd_rn(acc[v], acc2[v]);
+        } else if (code == kEnd) {
+          if (op[k].y >= 0) vstore<V>(A + static_cast<size_t>(op[k].y) * TILE, acc);
+          if (op[k].z >= 0) {  // autodiff.cpp:212-221 then gd_step :285-290
+            float dv[V], nv[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              const float p = sigmoid_ref(x[k][v], exp_tab);
+              dv[v] = __fmul_rn(__fmul_rn(acc[v], p), __fsub_rn(1.0f, p));
+              nv[v] = __fsub_rn(x[k][v], __fmul_rn(lr, dv[v]));
+            }
+            const size_t at = vbase + static_cast<size_t>(op[k].z) * TILE;
+            if (dv_out) {
+              vstore<V>(dv_out + at, dv);
+              vstore<V>(dp_out + at, acc);
+            } else {
+              vstore<V>(Vp + at, nv);
+            }
           }
         }
       }
     }
+    __syncthreads();
   }
 }
 
@@ -198,7 +341,7 @@ __global__ void k_loss_final(const double* __restrict__ partial, int n, HarvestO
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads)
 k_harden(const float* __restrict__ V, int ncpi, int nucpi, const int* __restrict__ cpi_row,
-         const int* __restrict__ ucpi_row, uint32_t* __restrict__ BT, int W, int Bp,
+         const int* __restrict__ ucpi_row, uint32_t* __restrict__ BT, int W, int tile_rows,
          uint64_t free_prefix, long long row_offset) {
   const int lane = threadIdx.x & 31;
   const long long total = static_cast<long long>(ncpi + nucpi) * W;
@@ -210,7 +353,8 @@ k_harden(const float* __restrict__ V, int ncpi, int nucpi, const int* __restrict
     bool bit;
     int row;
     if (input < ncpi) {
-      bit = V[static_cast<size_t>(input) * Bp + r] >= 0.0f;
+      const size_t tile = static_cast<size_t>(r / tile_rows);
+      bit = V[(tile * ncpi + input) * tile_rows + r % tile_rows] >= 0.0f;
       row = __ldg(cpi_row + input);
     } else {
       const int k = input - ncpi;
@@ -511,22 +655,47 @@ static int grid_for(long long n, int per_block, int cap) {
   return static_cast<int>(g);
 }
 
-void launch_init_v(cudaStream_t st, float* V, int ncols, int Bp, uint64_t prefix, long long row_offset) {
+void launch_init_v(cudaStream_t st, float* V, int ncols, int Bp, int tile_rows, uint64_t prefix,
+                   long long row_offset) {
   if (ncols == 0) return;
   k_init_v<<<grid_for(static_cast<long long>(ncols) * Bp, kThreads, 148 * 64), kThreads, 0, st>>>(
-      V, ncols, Bp, prefix, row_offset);
+      V, ncols, Bp, tile_rows, prefix, row_offset);
 }
 
-void launch_forward(cudaStream_t st, const int4* ops, int n_chunks, const float* src, float* tape,
-                    int Bp, int src_is_prob, const uint64_t* exp_tab) {
-  k_forward<<<Bp / kThreads, kThreads, 0, st>>>(ops, n_chunks, src, tape, Bp, src_is_prob, exp_tab);
+void launch_forward(cudaStream_t st, int vec, const int4* grp, const int2* lvl, int n_levels,
+                    const float* src, int ncols, float* tape, int n_rows, int Bp, int src_is_prob,
+                    const uint64_t* exp_tab) {
+  const int tiles = Bp / (32 * vec);
+  switch (vec) {
+    case 4:
+      k_forward<4><<<tiles, 32 * kWarps, 0, st>>>(grp, lvl, n_levels, src, ncols, tape, n_rows, src_is_prob, exp_tab);
+      break;
+    case 2:
+      k_forward<2><<<tiles, 32 * kWarps, 0, st>>>(grp, lvl, n_levels, src, ncols, tape, n_rows, src_is_prob, exp_tab);
+      break;
+    default:
+      k_forward<1><<<tiles, 32 * kWarps, 0, st>>>(grp, lvl, n_levels, src, ncols, tape, n_rows, src_is_prob, exp_tab);
+  }
 }
 
-void launch_backward(cudaStream_t st, const int4* ops, int n_chunks, const float* tape, float* adj,
-                     float* V, float* dv_out, float* dp_out, int Bp, float lr, const int* out_row,
-                     const uint8_t* out_tgt, int n_out, float* row_loss, const uint64_t* exp_tab) {
-  k_backward<<<Bp / kThreads, kThreads, 0, st>>>(ops, n_chunks, tape, adj, V, dv_out, dp_out, Bp, lr,
-                                                 out_row, out_tgt, n_out, row_loss, exp_tab);
+void launch_backward(cudaStream_t st, int vec, const int4* ops, const int2* lvl, int n_levels,
+                     const float* tape, float* adj, float* V, int ncols, int n_rows, float* dv_out,
+                     float* dp_out, int Bp, float lr, const int* out_enc, const uint8_t* out_tgt,
+                     int n_out, float* row_loss, const uint64_t* exp_tab) {
+  const int tiles = Bp / (32 * vec);
+  switch (vec) {
+    case 4:
+      k_backward<4, 4><<<tiles, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows, dv_out,
+                                                      dp_out, lr, out_enc, out_tgt, n_out, row_loss, exp_tab);
+      break;
+    case 2:
+      k_backward<2, 8><<<tiles, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows, dv_out,
+                                                      dp_out, lr, out_enc, out_tgt, n_out, row_loss, exp_tab);
+      break;
+    default:
+      k_backward<1, 8><<<tiles, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows, dv_out,
+                                                      dp_out, lr, out_enc, out_tgt, n_out, row_loss, exp_tab);
+  }
 }
 
 void launch_loss(cudaStream_t st, const float* row_loss, int batch, double* partial, int n_partial,
@@ -536,12 +705,12 @@ void launch_loss(cudaStream_t st, const float* row_loss, int batch, double* part
 }
 
 void launch_harden(cudaStream_t st, const float* V, int ncpi, int nucpi, const int* cpi_row,
-                   const int* ucpi_row, uint32_t* BT, int W, int Bp, uint64_t free_prefix,
+                   const int* ucpi_row, uint32_t* BT, int W, int tile_rows, uint64_t free_prefix,
                    long long row_offset) {
   const long long warps = static_cast<long long>(ncpi + nucpi) * W;
   if (warps == 0) return;
   k_harden<<<grid_for(warps * 32, kThreads, 148 * 64), kThreads, 0, st>>>(
-      V, ncpi, nucpi, cpi_row, ucpi_row, BT, W, Bp, free_prefix, row_offset);
+      V, ncpi, nucpi, cpi_row, ucpi_row, BT, W, tile_rows, free_prefix, row_offset);
 }
 
 void launch_bit_eval(cudaStream_t st, int wpc, const int4* ops, const int* lvl_ptr, int n_levels,

@@ -9,16 +9,19 @@ namespace sgx {
 
 struct HarvestOut;
 
-void launch_init_v(cudaStream_t st, float* V, int ncols, int Bp, uint64_t prefix, long long row_offset);
-void launch_forward(cudaStream_t st, const int4* ops, int n_chunks, const float* src, float* tape,
-                    int Bp, int src_is_prob, const uint64_t* exp_tab);
-void launch_backward(cudaStream_t st, const int4* ops, int n_chunks, const float* tape, float* adj,
-                     float* V, float* dv_out, float* dp_out, int Bp, float lr, const int* out_row,
-                     const uint8_t* out_tgt, int n_out, float* row_loss, const uint64_t* exp_tab);
+void launch_init_v(cudaStream_t st, float* V, int ncols, int Bp, int tile_rows, uint64_t prefix,
+                   long long row_offset);
+void launch_forward(cudaStream_t st, int vec, const int4* grp, const int2* lvl, int n_levels,
+                    const float* src, int ncols, float* tape, int n_rows, int Bp, int src_is_prob,
+                    const uint64_t* exp_tab);
+void launch_backward(cudaStream_t st, int vec, const int4* ops, const int2* lvl, int n_levels,
+                     const float* tape, float* adj, float* V, int ncols, int n_rows, float* dv_out,
+                     float* dp_out, int Bp, float lr, const int* out_enc, const uint8_t* out_tgt,
+                     int n_out, float* row_loss, const uint64_t* exp_tab);
 void launch_loss(cudaStream_t st, const float* row_loss, int batch, double* partial, int n_partial,
                  HarvestOut* out);
 void launch_harden(cudaStream_t st, const float* V, int ncpi, int nucpi, const int* cpi_row,
-                   const int* ucpi_row, uint32_t* BT, int W, int Bp, uint64_t free_prefix,
+                   const int* ucpi_row, uint32_t* BT, int W, int tile_rows, uint64_t free_prefix,
                    long long row_offset);
 void launch_bit_eval(cudaStream_t st, int wpc, const int4* ops, const int* lvl_ptr, int n_levels,
                      uint32_t* BT, int W, const int* out_row, const uint8_t* out_tgt, int n_out,

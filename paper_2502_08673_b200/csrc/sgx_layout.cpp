@@ -24,58 +24,108 @@ int operand_count(int32_t k) {
 
 std::string xv(int v) { return "x" + std::to_string(v); }
 
-void pad_chunk(std::vector<I4>& ops) {
-  while (ops.size() % kU) ops.push_back({kNop, -1, -1, -1});
-}
-
 // Soft program over the nodes with in_set[i] != 0 (closed under operands).
+//
+// NOT / BUF folding: a NOT or BUF node whose operand is materialized is
+// VIRTUAL -- it owns no tape row; consumers read its operand's row and apply
+// 1 - x (NOT) on the fly, which is the exact operation the reference performs
+// (autodiff.cpp:110-113), so values stay bit-identical.  In the backward pass
+// a virtual consumer j of node i contributes -adj[j] (NOT) / +adj[j] (BUF),
+// where adj[j] is summed first, in its own order, by a nested SUB run
+// (autodiff.cpp:225-233 pushed in descending id order).  A NOT/BUF whose
+// operand is itself virtual stays materialized, so nesting depth is one.
 SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
   SoftProgram P;
   const int n = L.n_nodes;
   P.row_of_node.assign(n, -1);
-  std::vector<int32_t> order;
+
+  std::vector<uint8_t> virt(n, 0);
   for (int i = 0; i < n; ++i)
-    if (in_set[i]) order.push_back(i);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int x, int y) { return L.level[x] < L.level[y]; });
-  P.node_of_row = order;
-  P.n_rows = static_cast<int32_t>(order.size());
-  for (int r = 0; r < P.n_rows; ++r) P.row_of_node[order[r]] = r;
+    if (in_set[i] && (L.kind[i] == SGX_NOT || L.kind[i] == SGX_BUF) && !virt[L.a[i]]) virt[i] = 1;
+  // Operand reference: (materialized base node, negate).
+  auto base_of = [&](int x) { return virt[x] ? L.a[x] : x; };
+  auto neg_of = [&](int x) { return virt[x] && L.kind[x] == SGX_NOT; };
+
+  // Levels over the materialized DAG.
+  std::vector<int32_t> lev(n, 0);
   int max_level = -1;
-  for (int i : order) max_level = std::max(max_level, L.level[i]);
+  for (int i = 0; i < n; ++i) {
+    if (!in_set[i] || virt[i]) continue;
+    int oc = operand_count(L.kind[i]);
+    if (oc >= 1) lev[i] = lev[base_of(L.a[i])] + 1;
+    if (oc == 2) lev[i] = std::max(lev[i], lev[base_of(L.b[i])] + 1);
+    max_level = std::max(max_level, lev[i]);
+  }
   P.n_levels = max_level + 1;
+  std::vector<std::vector<int32_t>> by_level(P.n_levels);
+  for (int i = 0; i < n; ++i)
+    if (in_set[i] && !virt[i]) by_level[lev[i]].push_back(i);
 
   std::vector<int32_t> col_of_node(n, -1);
   for (size_t j = 0; j < L.cpi.size(); ++j) col_of_node[L.node_of_var[L.cpi[j]]] = static_cast<int32_t>(j);
-  P.col_row.assign(L.cpi.size(), -1);
-  for (size_t j = 0; j < L.cpi.size(); ++j) P.col_row[j] = P.row_of_node[L.node_of_var[L.cpi[j]]];
-
   std::vector<int32_t> seed_of_node(n, -1);
   for (size_t m = 0; m < L.out_node.size(); ++m)
     if (in_set[L.out_node[m]]) seed_of_node[L.out_node[m]] = static_cast<int32_t>(m);
-  P.out_row.resize(L.out_node.size());
-  for (size_t m = 0; m < L.out_node.size(); ++m) P.out_row[m] = P.row_of_node[L.out_node[m]];
 
-  // Level buckets (rows are level-sorted, so buckets are row ranges).
-  std::vector<int32_t> lvl_begin(P.n_levels + 1, P.n_rows);
-  for (int r = P.n_rows - 1; r >= 0; --r) lvl_begin[L.level[order[r]]] = r;
-  lvl_begin[P.n_levels] = P.n_rows;
-  for (int l = P.n_levels - 1; l >= 0; --l)
-    if (lvl_begin[l] > lvl_begin[l + 1]) lvl_begin[l] = lvl_begin[l + 1];
-
-  // Forward ops, level by level.
+  // Forward: per level, nodes dealt round-robin to kWarps warps (after
+  // sorting by kind), each warp's list cut into kind-homogeneous groups of at
+  // most kGroup ops.  Rows are assigned in emission order, so a group's
+  // outputs are consecutive rows.
+  int32_t next_row = 0;
+  auto enc = [&](int x) {  // operand encoding: row << 1 | negate
+    int bse = base_of(x);
+    return (P.row_of_node[bse] << 1) | (neg_of(x) ? 1 : 0);
+  };
   for (int l = 0; l < P.n_levels; ++l) {
-    for (int r = lvl_begin[l]; r < lvl_begin[l + 1]; ++r) {
-      int i = order[r];
-      int32_t k = L.kind[i];
-      I4 op{k, r, -1, -1};
-      if (k == SGX_INPUT) op.z = col_of_node[i];
-      if (operand_count(k) >= 1) op.z = P.row_of_node[L.a[i]];
-      if (operand_count(k) == 2) op.w = P.row_of_node[L.b[i]];
-      P.fwd.push_back(op);
+    std::vector<int32_t> nodes = by_level[l];
+    std::stable_sort(nodes.begin(), nodes.end(), [&](int x, int y) { return L.kind[x] < L.kind[y]; });
+    std::vector<std::vector<int32_t>> per(kWarps);
+    for (size_t t = 0; t < nodes.size(); ++t) per[t % kWarps].push_back(nodes[t]);
+    for (int w = 0; w < kWarps; ++w) {
+      const auto& lst = per[w];
+      int32_t first = static_cast<int32_t>(P.fwd.size() / kGroupRecs);
+      int32_t groups = 0;
+      for (size_t t = 0; t < lst.size();) {
+        const int32_t k = L.kind[lst[t]];
+        size_t e = t;
+        while (e < lst.size() && L.kind[lst[e]] == k && e - t < static_cast<size_t>(kGroup)) ++e;
+        const int32_t cnt = static_cast<int32_t>(e - t);
+        I4 head{k, cnt, next_row, 0};
+        std::vector<int32_t> operands(2 * kGroup, 0);
+        for (size_t u = t; u < e; ++u) {
+          const int i = lst[u];
+          P.row_of_node[i] = next_row++;
+          P.node_of_row.push_back(i);
+          int oc = operand_count(k);
+          if (k == SGX_INPUT) operands[2 * (u - t)] = col_of_node[i];
+          if (oc >= 1) operands[2 * (u - t)] = enc(L.a[i]);
+          if (oc == 2) operands[2 * (u - t) + 1] = enc(L.b[i]);
+        }
+        P.fwd.push_back(head);
+        for (int q = 0; q < kGroup / 2; ++q)
+          P.fwd.push_back({operands[4 * q], operands[4 * q + 1], operands[4 * q + 2], operands[4 * q + 3]});
+        ++groups;
+        t = e;
+      }
+      P.fwd_lvl.push_back(first);
+      P.fwd_lvl.push_back(groups);
     }
-    pad_chunk(P.fwd);
   }
+  P.n_rows = next_row;
+  for (int i = 0; i < n; ++i) P.n_set += in_set[i] ? 1 : 0;
+  // Virtual nodes read as their base row (for the taps / outputs).
+  P.virt_base.assign(n, -1);
+  P.virt_neg.assign(n, 0);
+  for (int i = 0; i < n; ++i)
+    if (in_set[i] && virt[i]) {
+      P.virt_base[i] = P.row_of_node[L.a[i]];
+      P.virt_neg[i] = neg_of(i) ? 1 : 0;
+    }
+  P.out_enc.resize(L.out_node.size());
+  for (size_t m = 0; m < L.out_node.size(); ++m)
+    P.out_enc[m] = in_set[L.out_node[m]] ? enc(L.out_node[m]) : -1;
+  P.col_row.assign(L.cpi.size(), -1);
+  for (size_t j = 0; j < L.cpi.size(); ++j) P.col_row[j] = P.row_of_node[L.node_of_var[L.cpi[j]]];
 
   // Fan-out lists inside the set: consumers in descending id, a-slot first.
   std::vector<int32_t> fo_cnt(n + 1, 0);
@@ -99,28 +149,66 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
     if (oc >= 1) fo[fill[L.a[j]]++] = {j, oc == 2 ? L.b[j] : -1};
     if (oc == 2) fo[fill[L.b[j]]++] = {j, L.a[j]};
   }
+  auto seed_flags = [&](int node) {
+    int32_t m = seed_of_node[node];
+    return m >= 0 ? (kSeedBit | (L.out_tgt[m] ? kTargetBit : 0)) : 0;
+  };
+  // EDGE from materialized consumer j; `sub` marks edges inside a SUB run.
+  auto edge = [&](std::vector<I4>& run, const Edge& e, int32_t sub) {
+    int32_t ck = L.kind[e.consumer];
+    int32_t x = kEdge | (ck << kKindShift) | sub;
+    int32_t other = -1;
+    if (e.other >= 0) {
+      other = P.row_of_node[base_of(e.other)];
+      if (neg_of(e.other)) x |= kNegOtherBit;
+    }
+    run.push_back({x, P.row_of_node[e.consumer], other, 0});
+  };
 
-  // Backward micro-ops, levels high to low.
+  // Backward micro-op runs, levels high to low; a run is kept whole inside
+  // one warp's stream, runs go longest-first to the least loaded warp.
   for (int l = P.n_levels - 1; l >= 0; --l) {
-    for (int r = lvl_begin[l + 1] - 1; r >= lvl_begin[l]; --r) {
-      int i = order[r];
+    std::vector<std::vector<I4>> runs;
+    for (int i : by_level[l]) {
       int32_t k = L.kind[i];
       bool is_col_input = k == SGX_INPUT && col_of_node[i] >= 0;
       bool has_operands = operand_count(k) > 0;
       if (!is_col_input && !has_operands) continue;  // CONST / 0.5-input: adjoint unused
-      int32_t m = seed_of_node[i];
-      int32_t begin_code = kBegin;
-      if (m >= 0) begin_code |= kSeedBit | (L.out_tgt[m] ? kTargetBit : 0);
-      P.bwd.push_back({begin_code, r, 0, 0});
+      const int32_t r = P.row_of_node[i];
+      std::vector<I4> run;
+      run.push_back({kBegin | seed_flags(i), r, 0, 0});
       for (int64_t e = fo_ptr[i]; e < fo_ptr[i + 1]; ++e) {
-        int32_t ck = L.kind[fo[e].consumer];
-        P.bwd.push_back({kEdge | (ck << kKindShift), P.row_of_node[fo[e].consumer],
-                         fo[e].other >= 0 ? P.row_of_node[fo[e].other] : -1, 0});
+        const int j = fo[e].consumer;
+        if (!virt[j]) {
+          edge(run, fo[e], 0);
+          continue;
+        }
+        // adj[j] for virtual j (its value is T(v_i)), then -/+ into acc.
+        int32_t sb = kSubBegin | seed_flags(j) | (L.kind[j] == SGX_NOT ? kNegSelfBit : 0);
+        run.push_back({sb, r, 0, 0});
+        for (int64_t f = fo_ptr[j]; f < fo_ptr[j + 1]; ++f) edge(run, fo[f], kInSubBit);
+        run.push_back({kSubEnd | (L.kind[j] << kKindShift), 0, 0, 0});
       }
-      P.bwd.push_back({kEnd, has_operands ? r : -1, is_col_input ? col_of_node[i] : -1, 0});
+      run.push_back({kEnd, has_operands ? r : -1, is_col_input ? col_of_node[i] : -1, 0});
+      runs.push_back(std::move(run));
     }
-    pad_chunk(P.bwd);
+    std::stable_sort(runs.begin(), runs.end(),
+                     [](const auto& x, const auto& y) { return x.size() > y.size(); });
+    std::vector<std::vector<I4>> per(kWarps);
+    for (auto& run : runs) {
+      int best = 0;
+      for (int w = 1; w < kWarps; ++w)
+        if (per[w].size() < per[best].size()) best = w;
+      per[best].insert(per[best].end(), run.begin(), run.end());
+    }
+    for (int w = 0; w < kWarps; ++w) {
+      P.bwd_lvl.push_back(static_cast<int32_t>(P.bwd.size()));
+      P.bwd_lvl.push_back(static_cast<int32_t>(per[w].size()));
+      P.bwd.insert(P.bwd.end(), per[w].begin(), per[w].end());
+    }
   }
+  // Slack so a chunk of kU records may read past the last op.
+  for (int k = 0; k < kU; ++k) P.bwd.push_back({kNop, -1, -1, 0});
   return P;
 }
 
@@ -274,11 +362,11 @@ Layout build_layout(const sgx_circuit_desc& d) {
 
 void layout_info(const Layout& L, int64_t* info) {
   info[0] = L.n_nodes;
-  info[1] = L.cone.n_rows;
+  info[1] = L.cone.n_set;   // cone nodes (SURVEY 8(d) N_c)
   info[2] = L.cone.n_edges;
   info[3] = L.cone.n_levels;
   info[4] = static_cast<int64_t>(L.bit_lvl_ptr.size()) - 1;
-  info[5] = static_cast<int64_t>(L.cone.fwd.size());
+  info[5] = L.cone.n_rows;  // materialized (tape) rows after NOT/BUF folding
   info[6] = static_cast<int64_t>(L.cone.bwd.size());
   info[7] = static_cast<int64_t>(L.bit_ops.size());
   info[8] = static_cast<int64_t>(L.clause_ptr.size()) - 1;

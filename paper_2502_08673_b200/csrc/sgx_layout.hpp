@@ -30,32 +30,48 @@
 
 namespace sgx {
 
-constexpr int kU = 8;  // ops per chunk (loads in flight per thread)
+constexpr int kU = 8;      // ops per chunk (loads in flight per thread)
+constexpr int kWarps = 4;  // warps per CTA sharing one sample tile (node split)
 
-// Forward op (int4): {code, out_row, a, b}.  INPUT: a = V column or -1 (=0.5).
+// Forward group: kGroupRecs int4 records.  Header {kind, n, first_out_row, 0},
+// then kGroup operand pairs (a, b) packed two per int4; an operand is
+// row << 1 | negate (negate = read through a folded NOT).  INPUT: a = V
+// column or -1 (= 0.5).  The group's outputs are rows first_out_row + [0, n).
 // Backward micro-op (int4), opcode in the low byte:
-//   BEGIN {kBegin | seed<<8 | target<<9, row, 0, 0}
-//   EDGE  {kEdge | consumer_kind<<12, adj_row_of_consumer, other_row (-1), 0}
-//   END   {kEnd, adj_row_to_store (-1), V column (-1), 0}
+//   BEGIN     {kBegin | seed | target, row, 0, 0}
+//   EDGE      {kEdge | consumer_kind << 12 | neg_other | in_sub,
+//              adj_row_of_consumer, other_row (-1), 0}
+//   SUB_BEGIN {kSubBegin | seed | target | neg_self, row of the folded node's
+//              operand, 0, 0}      -- opens adj[j] of a folded NOT/BUF j
+//   SUB_END   {kSubEnd | kind(j) << 12}   -- acc -= adj[j] (NOT) / += (BUF)
+//   END       {kEnd, adj_row_to_store (-1), V column (-1), 0}
 // Bit op (int4): {kind, out_row, a_row, b_row}.
 // Clause literal (int32): bit_row << 2 | last_in_clause << 1 | negated.
-enum OpCode : int32_t { kNop = 15, kBegin = 16, kEdge = 17, kEnd = 18 };
-constexpr int32_t kSeedBit = 1 << 8, kTargetBit = 1 << 9, kKindShift = 12;
+enum OpCode : int32_t { kNop = 15, kBegin = 16, kEdge = 17, kEnd = 18, kSubBegin = 19, kSubEnd = 20 };
+constexpr int32_t kSeedBit = 1 << 8, kTargetBit = 1 << 9, kNegOtherBit = 1 << 10,
+                  kNegSelfBit = 1 << 11, kKindShift = 12, kInSubBit = 1 << 16;
+constexpr int kGroup = 4;                      // ops per forward group
+constexpr int kGroupRecs = 1 + kGroup / 2;     // int4 records per group
 
 struct I4 {
   int32_t x, y, z, w;
 };
 
 struct SoftProgram {
-  int32_t n_rows = 0;                // tape rows
+  int32_t n_rows = 0;                // tape rows (materialized nodes)
+  int32_t n_set = 0;                 // nodes in the program's set (cone)
   int32_t n_levels = 0;
   int64_t n_edges = 0;               // operand edges inside the program
   std::vector<int32_t> row_of_node;  // -1 if the node is not in the program
   std::vector<int32_t> node_of_row;
-  std::vector<I4> fwd;               // multiple of kU
-  std::vector<I4> bwd;               // multiple of kU
-  std::vector<int32_t> out_row;      // tape row of each output
+  std::vector<I4> fwd;               // groups, kGroupRecs records each
+  std::vector<I4> bwd;               // micro-ops
+  std::vector<int32_t> fwd_lvl;      // per (level, warp): first group, group count
+  std::vector<int32_t> bwd_lvl;      // per (level high to low, warp): first op, op count
+  std::vector<int32_t> out_enc;      // each output as row << 1 | negate (-1: not in set)
   std::vector<int32_t> col_row;      // tape row of each V column's INPUT node
+  std::vector<int32_t> virt_base;    // folded node -> row of its operand (-1 otherwise)
+  std::vector<uint8_t> virt_neg;     // folded node is a NOT
 };
 
 struct Layout {
