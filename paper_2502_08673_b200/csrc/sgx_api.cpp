@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -74,6 +75,24 @@ struct DBuf {
     }
     n = count;
   }
+  // Stream-ordered (pool) allocation: no device-wide synchronisation, so the
+  // sampler can grow its table / solution store between kernels.
+  void alloc_async(size_t count, cudaStream_t st) {
+    reset_async(st);
+    size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, st);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      throw NoMem("cudaMallocAsync(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e));
+    }
+    n = count;
+  }
+  void reset_async(cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+    n = 0;
+  }
   void upload(const std::vector<T>& v, cudaStream_t st) {
     alloc(v.size());
     if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
@@ -86,10 +105,12 @@ struct DBuf {
 
 int round_up(long long x, int m) { return static_cast<int>((x + m - 1) / m * m); }
 
-// Tile-major index (parity taps run with 32-sample tiles): sample r, row j of
-// a [tile][rows][32] array.
+// Parity taps run the sampler's kernels with 128-sample tiles (4 per lane).
+constexpr int kTapVec = 4, kTapTile = 32 * kTapVec;
+
+// Tile-major index: sample r, row j of a [tile][rows][kTapTile] array.
 size_t tile_index(int r, size_t j, size_t rows) {
-  return (static_cast<size_t>(r / 32) * rows + j) * 32 + static_cast<size_t>(r % 32);
+  return (static_cast<size_t>(r / kTapTile) * rows + j) * kTapTile + static_cast<size_t>(r % kTapTile);
 }
 
 uint64_t next_pow2(uint64_t x) {
@@ -169,6 +190,7 @@ struct sgx_sampler {
   std::vector<int64_t> new_unique;
   sgx_run_stats stats{};
   double phase_ms[8] = {0};
+  double host_ms[4] = {0};  // harvest wall, table growth, store growth, (spare)
   cudaEvent_t ev[8] = {nullptr};
 };
 
@@ -242,8 +264,8 @@ void ensure_table(sgx_sampler* s) {
   if (want <= s->tcap) return;
   uint64_t ncap = next_pow2(std::max<uint64_t>(want * 2, 1u << 16));
   DBuf<unsigned long long> nk, nm;
-  nk.alloc(ncap);
-  nm.alloc(ncap);
+  nk.alloc_async(ncap, s->st);
+  nm.alloc_async(ncap, s->st);
   CK(cudaMemsetAsync(nk.p, 0, ncap * sizeof(unsigned long long), s->st));
   CK(cudaMemsetAsync(nm.p, 0xff, ncap * sizeof(unsigned long long), s->st));
   if (s->tcap) {
@@ -251,22 +273,24 @@ void ensure_table(sgx_sampler* s) {
     s->launches += 1;
   }
   CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(s->st));
   s->tkeys.swap(nk);
   s->tmeta.swap(nm);
+  nk.reset_async(s->st);  // the old table, after the rehash in stream order
+  nm.reset_async(s->st);
   s->tcap = ncap;
 }
 
+// Stream-ordered growth of the row-major solution store (no host sync).
 void grow_store(sgx_sampler* s, long long need_rows) {
   long long ncap = std::max<long long>(need_rows, s->store_cap * 2);
   const size_t kw = static_cast<size_t>(s->c->L.key_words);
   DBuf<uint64_t> ns;
-  ns.alloc(static_cast<size_t>(ncap) * kw);
+  ns.alloc_async(static_cast<size_t>(ncap) * kw, s->st);
   if (s->n_solutions)
     CK(cudaMemcpyAsync(ns.p, s->store.p, static_cast<size_t>(s->n_solutions) * kw * sizeof(uint64_t),
                        cudaMemcpyDeviceToDevice, s->st));
-  CK(cudaStreamSynchronize(s->st));
   s->store.swap(ns);
+  ns.reset_async(s->st);
   s->store_cap = ncap;
 }
 
@@ -276,7 +300,11 @@ void sampler_harvest(sgx_sampler* s, int restart, int iter, long long quota_left
                      long long* added) {
   sgx_circuit* c = s->c;
   const auto& L = c->L;
-  ensure_table(s);
+  {
+    const auto t0 = std::chrono::steady_clock::now();
+    ensure_table(s);
+    s->host_ms[1] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
   CK(cudaEventRecord(s->ev[3], s->st));
   uint64_t fprefix = sgx::fold(
       sgx::fold(sgx::fold(sgx::fold(sgx::kPi, s->cfg.seed), sgx::kFreeTag), static_cast<uint64_t>(static_cast<int64_t>(restart))),
@@ -302,7 +330,9 @@ void sampler_harvest(sgx_sampler* s, int restart, int iter, long long quota_left
   CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->st));
   CK(cudaStreamSynchronize(s->st));
   if (s->hpin->overflow) {
+    const auto t0 = std::chrono::steady_clock::now();
     grow_store(s, s->n_solutions + s->hpin->accepted);
+    s->host_ms[2] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     CK(cudaMemsetAsync(&s->hout.p->overflow, 0, sizeof(long long), s->st));
     sgx::launch_append(s->st, s->newmask.p, s->block_count.p, s->K.p, L.key_words, s->Bp, s->store.p,
                        s->n_solutions, s->store_cap, s->hout.p);
@@ -315,6 +345,8 @@ void sampler_harvest(sgx_sampler* s, int restart, int iter, long long quota_left
   s->table_count += h.new_rows;
   s->n_solutions += h.accepted;
   *added = h.accepted;
+  // Grow ahead of need, in stream order, so the next harvest never overflows.
+  if (s->store_cap - s->n_solutions < s->Bp) grow_store(s, s->n_solutions + 2LL * s->Bp);
   // Quota met inside this harvest: the reference stops at the row after the
   // one that filled it (sampler.cpp:129).
   if (quota_left >= 0 && h.accepted == quota_left && h.accepted > 0)
@@ -337,6 +369,7 @@ void sampler_run(sgx_sampler* s) {
   s->new_unique.clear();
   s->stats = sgx_run_stats{};
   std::fill(s->phase_ms, s->phase_ms + 8, 0.0);
+  std::fill(s->host_ms, s->host_ms + 4, 0.0);
   s->launches = 0;
   if (s->c->L.unsat) {
     s->stats.unsat = 1;
@@ -348,7 +381,9 @@ void sampler_run(sgx_sampler* s) {
   auto out_of_time = [&] { return cfg.timeout_s > 0.0 && now_s() >= cfg.timeout_s; };
   auto harvest = [&](int restart, int iter) {
     long long att = 0, add = 0;
+    const auto h0 = clock::now();
     sampler_harvest(s, restart, iter, quota ? cfg.max_solutions - s->n_solutions : -1, &att, &add);
+    s->host_ms[0] += std::chrono::duration<double, std::milli>(clock::now() - h0).count();
     s->stats.attempts += att;
     s->new_unique.push_back(add);
   };
@@ -393,6 +428,10 @@ void sampler_run(sgx_sampler* s) {
   CK(cudaEventSynchronize(r1));
   s->stats.device_ms = elapsed(r0, r1);
   s->stats.launches = s->launches;
+  if (std::getenv("SGX_TRACE"))
+    std::fprintf(stderr, "[sgx] device %.2f ms; harvest wall %.2f ms (table growth %.2f, store growth %.2f); "
+                 "phases init %.2f step %.2f harvest %.2f\n", s->stats.device_ms, s->host_ms[0], s->host_ms[1],
+                 s->host_ms[2], s->phase_ms[0], s->phase_ms[1], s->phase_ms[2]);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaEventDestroy(r0);
@@ -431,6 +470,12 @@ int sgx_open(int device, sgx_ctx** out) {
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     std::vector<uint64_t> tab(kExpTab, kExpTab + 32);
     ctx->exp_tab.upload(tab, ctx->stream);
+    // Keep freed stream-ordered allocations in the pool (table / store growth).
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     CK(cudaStreamSynchronize(ctx->stream));
     *out = ctx.release();
   });
@@ -691,7 +736,7 @@ int sgx_forward(sgx_circuit* c, const float* p, int32_t batch, float* tape, floa
     DBuf<float> dsrc, dtape;
     dsrc.upload(src, st);
     dtape.alloc(nr * Bp);
-    sgx::launch_forward(st, 1, c->full.fwd.p, c->full.fwd_lvl.p, c->full.n_fwd_levels, dsrc.p,
+    sgx::launch_forward(st, kTapVec, c->full.fwd.p, c->full.fwd_lvl.p, c->full.n_fwd_levels, dsrc.p,
                         static_cast<int>(ncpi), dtape.p, L.full.n_rows, Bp, 1, c->ctx->exp_tab.p);
     CK(cudaGetLastError());
     std::vector<float> h(nr * Bp);
@@ -753,7 +798,7 @@ int sgx_backward(sgx_circuit* c, const float* tape, int32_t batch, const float* 
     ddp.alloc(std::max<size_t>(ncpi * Bp, 1));
     CK(cudaMemsetAsync(ddv.p, 0, ddv.n * sizeof(float), st));
     CK(cudaMemsetAsync(ddp.p, 0, ddp.n * sizeof(float), st));
-    sgx::launch_backward(st, 1, c->full.bwd.p, c->full.bwd_lvl.p, c->full.n_bwd_levels, dt.p, dadj.p, dV.p,
+    sgx::launch_backward(st, kTapVec, c->full.bwd.p, c->full.bwd_lvl.p, c->full.n_bwd_levels, dt.p, dadj.p, dV.p,
                          static_cast<int>(ncpi), L.full.n_rows, ddv.p, ddp.p, Bp, 0.0f, c->full.out_enc.p,
                          c->out_tgt.p, static_cast<int>(L.out_node.size()), nullptr, c->ctx->exp_tab.p);
     CK(cudaGetLastError());

@@ -309,6 +309,259 @@ k_backward(const int4* __restrict__ ops, const int2* __restrict__ lvl, int n_lev
   }
 }
 
+// ---------------------------------------------------------------------------
+// v4: the same forward / backward, with every operand row staged through
+// shared memory by cp.async (LDGSTS, 16 B per lane = the lane's 4 samples).
+// Each warp keeps kStages groups (forward) or kU-op chunks (backward) in
+// flight without spending registers on them, so the loads of the next three
+// groups overlap the arithmetic of the current one.  Lanes only ever read
+// their own staged bytes, so per-thread cp.async.wait_group is the only
+// synchronisation inside a level.
+// ---------------------------------------------------------------------------
+#ifndef SGX_STAGES
+#define SGX_STAGES 3
+#endif
+constexpr int kStages = SGX_STAGES;      // groups / chunks in flight per warp
+constexpr int kSlots = 2 * kGroup;       // staged rows per stage (= 2 * kAsyncU)
+constexpr int kAsyncU = 4;               // backward micro-ops per chunk
+constexpr int kAsyncSmem = kWarps * kStages * kSlots * 32 * 16;  // bytes per CTA
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void f4(const float4& t, float (&o)[4]) {
+  o[0] = t.x;
+  o[1] = t.y;
+  o[2] = t.z;
+  o[3] = t.w;
+}
+
+__global__ void __launch_bounds__(32 * kWarps)
+k_forward_async(const int4* __restrict__ grp, const int2* __restrict__ lvl, int n_levels,
+                const float* __restrict__ src, int ncols, float* tape, int n_rows, int src_is_prob,
+                const uint64_t* __restrict__ exp_tab) {
+  constexpr int TILE = 128;
+  extern __shared__ float4 stage_mem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* T = tape + static_cast<size_t>(blockIdx.x) * n_rows * TILE + lane * 4;
+  const float* S = src + static_cast<size_t>(blockIdx.x) * ncols * TILE + lane * 4;
+  float4* my = stage_mem + warp * kStages * kSlots * 32 + lane;  // slot (d, j): my[(d*kSlots + j) * 32]
+  auto issue = [&](int g, int d) {
+    const int4* rec = grp + static_cast<size_t>(g) * kGroupRecs;
+    const int4 h = __ldg(rec), o0 = __ldg(rec + 1), o1 = __ldg(rec + 2);
+    const int opd[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+    const int kind = h.x, n = h.y;
+    float4* base = my + d * kSlots * 32;
+#pragma unroll
+    for (int k = 0; k < kGroup; ++k) {
+      if (k >= n) break;
+      if (kind >= SGX_AND2) {
+        cp_async16(base + (2 * k) * 32, T + static_cast<size_t>(opd[2 * k] >> 1) * TILE);
+        cp_async16(base + (2 * k + 1) * 32, T + static_cast<size_t>(opd[2 * k + 1] >> 1) * TILE);
+      } else if (kind == SGX_NOT || kind == SGX_BUF) {
+        cp_async16(base + (2 * k) * 32, T + static_cast<size_t>(opd[2 * k] >> 1) * TILE);
+      } else if (kind == SGX_INPUT && opd[2 * k] >= 0) {
+        cp_async16(base + (2 * k) * 32, S + static_cast<size_t>(opd[2 * k]) * TILE);
+      }
+    }
+    cp_async_commit();
+  };
+  for (int l = 0; l < n_levels; ++l) {
+    const int2 L = __ldg(lvl + l * kWarps + warp);
+#pragma unroll
+    for (int i = 0; i < kStages - 1; ++i) {
+      if (i < L.y)
+        issue(L.x + i, i);
+      else
+        cp_async_commit();
+    }
+    for (int i = 0; i < L.y; ++i) {
+      const int nxt = i + kStages - 1;
+      if (nxt < L.y)
+        issue(L.x + nxt, nxt % kStages);
+      else
+        cp_async_commit();
+      cp_async_wait<kStages - 1>();
+      const int4* rec = grp + static_cast<size_t>(L.x + i) * kGroupRecs;
+      const int4 h = __ldg(rec), o0 = __ldg(rec + 1), o1 = __ldg(rec + 2);
+      const int opd[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+      const int kind = h.x, n = h.y;
+      const float4* base = my + (i % kStages) * kSlots * 32;
+      float* out = T + static_cast<size_t>(h.z) * TILE;
+#pragma unroll
+      for (int k = 0; k < kGroup; ++k) {
+        if (k >= n) break;
+        float a[4], b[4], r[4];
+        if (kind >= SGX_AND2) {
+          f4(base[(2 * k) * 32], a);
+          f4(base[(2 * k + 1) * 32], b);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const float av = (opd[2 * k] & 1) ? __fsub_rn(1.0f, a[v]) : a[v];
+            const float bv = (opd[2 * k + 1] & 1) ? __fsub_rn(1.0f, b[v]) : b[v];
+            r[v] = gate_value(kind, av, bv);
+          }
+        } else if (kind == SGX_NOT || kind == SGX_BUF) {
+          f4(base[(2 * k) * 32], a);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const float av = (opd[2 * k] & 1) ? __fsub_rn(1.0f, a[v]) : a[v];
+            r[v] = kind == SGX_NOT ? __fsub_rn(1.0f, av) : av;
+          }
+        } else if (kind == SGX_INPUT) {
+          if (opd[2 * k] >= 0) f4(base[(2 * k) * 32], a);
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            r[v] = opd[2 * k] < 0 ? 0.5f : (src_is_prob ? a[v] : sigmoid_ref(a[v], exp_tab));
+        } else {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) r[v] = kind == SGX_CONST1 ? 1.0f : 0.0f;
+        }
+        vstore<4>(out + k * TILE, r);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(32 * kWarps)
+k_backward_async(const int4* __restrict__ ops, const int2* __restrict__ lvl, int n_levels,
+                 const float* tape, float* adj, float* Vp, int ncols, int n_rows, float* dv_out,
+                 float* dp_out, float lr, const int* __restrict__ out_enc,
+                 const uint8_t* __restrict__ out_tgt, int n_out, float* __restrict__ row_loss,
+                 const uint64_t* __restrict__ exp_tab) {
+  constexpr int TILE = 128, U = kAsyncU;
+  extern __shared__ float4 stage_mem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t tbase = static_cast<size_t>(blockIdx.x) * n_rows * TILE + lane * 4;
+  const float* T = tape + tbase;
+  float* A = adj + tbase;
+  const size_t vbase = static_cast<size_t>(blockIdx.x) * ncols * TILE + lane * 4;
+  float4* my = stage_mem + warp * kStages * kSlots * 32 + lane;
+  if (row_loss && warp == 0) {  // loss (autodiff.cpp:160-166): outputs in order
+    float l[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    for (int m = 0; m < n_out; ++m) {
+      float yv[4];
+      load_operand<4>(T, __ldg(out_enc + m), yv);
+      const float t = __ldg(out_tgt + m) ? 1.0f : 0.0f;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const float d = __fsub_rn(yv[v], t);
+        l[v] = __fadd_rn(l[v], __fmul_rn(d, d));
+      }
+    }
+    vstore<4>(row_loss + static_cast<size_t>(blockIdx.x) * TILE + lane * 4, l);
+  }
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f}, acc2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  for (int li = 0; li < n_levels; ++li) {
+    const int2 L = __ldg(lvl + li * kWarps + warp);
+    const int nch = (L.y + U - 1) / U;
+    auto issue = [&](int c, int d) {
+      float4* base = my + d * kSlots * 32;
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        if (c * U + k >= L.y) break;
+        const int4 op = __ldg(ops + L.x + c * U + k);
+        const int code = op.x & 0xff;
+        if (code == kEdge) {
+          cp_async16(base + (2 * k) * 32, A + static_cast<size_t>(op.y) * TILE);
+          if (op.z >= 0) cp_async16(base + (2 * k + 1) * 32, T + static_cast<size_t>(op.z) * TILE);
+        } else if (code == kBegin || code == kSubBegin) {
+          if (op.x & kSeedBit) cp_async16(base + (2 * k) * 32, T + static_cast<size_t>(op.y) * TILE);
+        } else if (code == kEnd) {
+          if (op.z >= 0) cp_async16(base + (2 * k) * 32, Vp + vbase + static_cast<size_t>(op.z) * TILE);
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int i = 0; i < kStages - 1; ++i) {
+      if (i < nch)
+        issue(i, i);
+      else
+        cp_async_commit();
+    }
+    for (int c = 0; c < nch; ++c) {
+      const int nxt = c + kStages - 1;
+      if (nxt < nch)
+        issue(nxt, nxt % kStages);
+      else
+        cp_async_commit();
+      cp_async_wait<kStages - 1>();
+      const float4* base = my + (c % kStages) * kSlots * 32;
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        if (c * U + k >= L.y) break;
+        const int4 op = __ldg(ops + L.x + c * U + k);
+        const int f = op.x;
+        const int code = f & 0xff;
+        if (code == kEdge) {
+          const int ck = (f >> kKindShift) & 0xf;
+          const float c0 = kPullC0[ck], c1 = kPullC1[ck];
+          float g[4], y[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          f4(base[(2 * k) * 32], g);
+          if (op.z >= 0) f4(base[(2 * k + 1) * 32], y);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            float vo = y[v];
+            if (f & kNegOtherBit) vo = __fsub_rn(1.0f, vo);
+            const float p = __fmul_rn(g[v], __fmaf_rn(c1, vo, c0));
+            if (f & kInSubBit)
+              acc2[v] = __fadd_rn(acc2[v], p);
+            else
+              acc[v] = __fadd_rn(acc[v], p);
+          }
+        } else if (code == kBegin || code == kSubBegin) {
+          const float t = (f & kTargetBit) ? 1.0f : 0.0f;
+          float x[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          if (f & kSeedBit) f4(base[(2 * k) * 32], x);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            float yv = x[v];
+            if (f & kNegSelfBit) yv = __fsub_rn(1.0f, yv);
+            const float sd = (f & kSeedBit) ? __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(yv, t))) : 0.0f;
+            if (code == kBegin)
+              acc[v] = sd;
+            else
+              acc2[v] = sd;
+          }
+        } else if (code == kSubEnd) {
+          const bool is_not = ((f >> kKindShift) & 0xf) == SGX_NOT;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[v] = is_not ? __fsub_rn(acc[v], acc2[v]) : __fadd_rn(acc[v], acc2[v]);
+        } else if (code == kEnd) {
+          if (op.y >= 0) vstore<4>(A + static_cast<size_t>(op.y) * TILE, acc);
+          if (op.z >= 0) {  // autodiff.cpp:212-221 then gd_step :285-290
+            float x[4], dv[4], nv[4];
+            f4(base[(2 * k) * 32], x);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const float p = sigmoid_ref(x[v], exp_tab);
+              dv[v] = __fmul_rn(__fmul_rn(acc[v], p), __fsub_rn(1.0f, p));
+              nv[v] = __fsub_rn(x[v], __fmul_rn(lr, dv[v]));
+            }
+            const size_t at = vbase + static_cast<size_t>(op.z) * TILE;
+            if (dv_out) {
+              vstore<4>(dv_out + at, dv);
+              vstore<4>(dp_out + at, acc);
+            } else {
+              vstore<4>(Vp + at, nv);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Deterministic loss total: fixed per-block partial sums in double, then one
 // block folds the partials in block order.
 __global__ void __launch_bounds__(kThreads)
@@ -662,10 +915,35 @@ void launch_init_v(cudaStream_t st, float* V, int ncols, int Bp, int tile_rows, 
       V, ncols, Bp, tile_rows, prefix, row_offset);
 }
 
+// Kernel variant per pass (measured on B200, c2_iscas @ 64k rows): the
+// cp.async-staged forward beats the register one (1.41 vs 1.78 ms), the
+// register backward beats the staged one (3.35 vs 4.27 ms).  SGX_SOFT=3
+// forces register kernels for both passes, SGX_SOFT=4 staged for both.
+static int soft_mode() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = std::getenv("SGX_SOFT");
+    m = (e && (e[0] == '3' || e[0] == '4')) ? e[0] - '0' : 0;
+  }
+  return m;
+}
+static bool async_enabled_fwd() { return soft_mode() != 3; }
+static bool async_enabled_bwd() { return soft_mode() == 4; }
+
 void launch_forward(cudaStream_t st, int vec, const int4* grp, const int2* lvl, int n_levels,
                     const float* src, int ncols, float* tape, int n_rows, int Bp, int src_is_prob,
                     const uint64_t* exp_tab) {
   const int tiles = Bp / (32 * vec);
+  if (vec == 4 && async_enabled_fwd()) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_forward_async, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsyncSmem);
+      attr = true;
+    }
+    k_forward_async<<<tiles, 32 * kWarps, kAsyncSmem, st>>>(grp, lvl, n_levels, src, ncols, tape, n_rows,
+                                                           src_is_prob, exp_tab);
+    return;
+  }
   switch (vec) {
     case 4:
       k_forward<4><<<tiles, 32 * kWarps, 0, st>>>(grp, lvl, n_levels, src, ncols, tape, n_rows, src_is_prob, exp_tab);
@@ -683,6 +961,17 @@ void launch_backward(cudaStream_t st, int vec, const int4* ops, const int2* lvl,
                      float* dp_out, int Bp, float lr, const int* out_enc, const uint8_t* out_tgt,
                      int n_out, float* row_loss, const uint64_t* exp_tab) {
   const int tiles = Bp / (32 * vec);
+  if (vec == 4 && async_enabled_bwd()) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_backward_async, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsyncSmem);
+      attr = true;
+    }
+    k_backward_async<<<tiles, 32 * kWarps, kAsyncSmem, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows,
+                                                            dv_out, dp_out, lr, out_enc, out_tgt, n_out,
+                                                            row_loss, exp_tab);
+    return;
+  }
   switch (vec) {
     case 4:
       k_backward<4, 4><<<tiles, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows, dv_out,
