@@ -207,79 +207,95 @@ def run_b200_arm(args, world, rank, local, dist):
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(dev) as clk:
-        t0 = time.perf_counter()
-        st = sampler.run()
-        torch.cuda.synchronize(dev)
-        wall = time.perf_counter() - t0
+    if world == 1:
+        # satgrad::run in C++ (sgx_run): device time from CUDA events on the
+        # sampler stream around the whole run.
+        with ClockSampler(dev) as clk:
+            t0 = time.perf_counter()
+            st = sampler.run()
+            torch.cuda.synchronize(dev)
+            wall = time.perf_counter() - t0
+        device_s = st.device_ms / 1000.0
+        global_unique = st.unique_count
+        restarts_done, attempts, launches, ph = st.restarts + 1, st.attempts, st.launches, st.phase_ms
+    else:
+        # Sample sharding with the per-harvest NCCL all-gather of fingerprints
+        # (dist.py); every harvest synchronises the device, so the timed
+        # wall clock is device-bound.  Max over ranks.
+        from paper_2502_08673_b200.dist import DeviceShard, TorchExchange, run_sharded
+        shard = DeviceShard(sampler)
+        ex = TorchExchange(device=f"cuda:{dev}")
+        with ClockSampler(dev) as clk:
+            t0 = time.perf_counter()
+            sst = run_sharded(shard, ex, cfg_for(args.steps), rank, world, shard.stride)
+            torch.cuda.synchronize(dev)
+            wall = time.perf_counter() - t0
+        t_dev = torch.tensor([wall], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
+        device_s = float(t_dev.item())
+        global_unique = sst.unique_count
+        restarts_done, attempts, launches, ph = sst.restarts + 1, sst.attempts, None, None
     if dist:
         dist.barrier()
-    keys = sampler.fetch()
-    local_unique = len(keys)
-    device_s = st.device_ms / 1000.0
-    restarts_done = st.restarts + 1
-    # global dedup across ranks by 64-bit fingerprint (outside the timed region)
-    fp = np.zeros(0, np.uint64)
-    if len(keys):
-        h = np.full(len(keys), 0x243F6A8885A308D3, np.uint64)
-        for q in range(keys.shape[1]):
-            h = (h ^ keys[:, q]) * np.uint64(0x100000001B3)
-        fp = h
-    if dist:
-        import torch.distributed as tdist
-        t_dev = torch.tensor([device_s], dtype=torch.float64, device=f"cuda:{dev}")
-        tdist.all_reduce(t_dev, op=tdist.ReduceOp.MAX)
-        device_s = float(t_dev.item())
-        n = torch.tensor([len(fp)], dtype=torch.int64, device=f"cuda:{dev}")
-        ns = [torch.zeros_like(n) for _ in range(world)]
-        tdist.all_gather(ns, n)
-        mx = max(int(x.item()) for x in ns)
-        buf = torch.zeros(mx, dtype=torch.int64, device=f"cuda:{dev}")
-        buf[:len(fp)] = torch.from_numpy(fp.view(np.int64)).to(buf.device)
-        bufs = [torch.zeros_like(buf) for _ in range(world)]
-        tdist.all_gather(bufs, buf)
-        allfp = np.concatenate([b[:int(c.item())].cpu().numpy() for b, c in zip(bufs, ns)])
-        global_unique = len(np.unique(allfp))
-    else:
-        global_unique = local_unique
     sampler.close()
 
-    if rank != 0:
-        return
-    value = global_unique / device_s if device_s > 0 else 0.0
-    ph = st.phase_ms
-    n_steps = args.steps * args.iterations
-    # Dominant kernel roofline (SURVEY.md 8(d) compulsory-tape model).
-    ncone, cpi = info["cone_nodes"], info["cpi"]
-    kernels = {
-        "k_forward": (ph["forward"], n_steps, 4 * (cpi + ncone) * batch),
-        "k_backward": (ph["backward"], n_steps, 4 * (ncone + 2 * cpi) * batch),
-    }
-    dom = max(kernels, key=lambda k: kernels[k][0])
-    t_ms, nl, bytes_per_launch = kernels[dom]
-    avg_s = (t_ms / max(1, nl)) / 1000.0
-    peak, peak_kind = peaks()
-    achieved = bytes_per_launch / avg_s / 1e9 if avg_s > 0 else 0.0
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", f"ncu_{name}.json")
-    if os.path.exists(prof):
-        with open(prof) as f:
-            traffic = json.load(f).get(dom, {}).get("dram_bytes_per_launch")
-
-    # e2e through the public API from host buffers (upload + run + fetch).
+    # e2e through the public API from host buffers: circuit + CNF upload
+    # (H2D), the run, every solution key fetched to host memory (D2H).
     e2e_cfg = cfg_for(args.steps)
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
-    res = run_instance(inst, e2e_cfg, device=dev)
+    if world == 1:
+        res = run_instance(inst, e2e_cfg, device=dev)
+        e2e_unique, d2h = res.stats.unique_count, res.solutions.keys.nbytes
+    else:
+        from paper_2502_08673_b200.dist import DeviceShard, TorchExchange, run_sharded
+        dc2 = DeviceCircuit.from_instance(inst, device=dev)
+        s2 = Sampler(dc2, e2e_cfg)
+        sh2 = DeviceShard(s2)
+        est = run_sharded(sh2, TorchExchange(device=f"cuda:{dev}"), e2e_cfg, rank, world, sh2.stride)
+        d2h = s2.fetch().nbytes
+        e2e_unique = est.unique_count
+        s2.close()
+        dc2.close()
     e2e_wall = time.perf_counter() - t0
+    if dist:
+        t_e = torch.tensor([e2e_wall], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+        e2e_wall = float(t_e.item())
     h2d = sum(x.nbytes for x in (inst.kind, inst.a, inst.b, inst.var, inst.out_var, inst.out_tgt,
                                  inst.cpi, inst.ucpi, inst.clause_ptr, inst.clause_lit))
-    d2h = res.solutions.keys.nbytes
-    e2e = {"value": res.stats.unique_count / e2e_wall, "unit": UNIT,
+    e2e = {"value": e2e_unique / e2e_wall, "unit": UNIT,
            "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
            "wall_s": e2e_wall}
+
+    if rank != 0:
+        return
+    value = global_unique / device_s if device_s > 0 else 0.0
+    ncone, cpi = info["cone_nodes"], info["cpi"]
+    roofline = None
+    if ph is not None:
+        n_steps = args.steps * args.iterations
+        # Dominant kernel roofline (SURVEY.md 8(d) compulsory-tape model).
+        kernels = {
+            "k_forward": (ph["forward"], n_steps, 4 * (cpi + ncone) * batch),
+            "k_backward": (ph["backward"], n_steps, 4 * (ncone + 2 * cpi) * batch),
+        }
+        dom = max(kernels, key=lambda k: kernels[k][0])
+        t_ms, nl, bytes_per_launch = kernels[dom]
+        avg_s = (t_ms / max(1, nl)) / 1000.0
+        peak, peak_kind = peaks()
+        achieved = bytes_per_launch / avg_s / 1e9 if avg_s > 0 else 0.0
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", f"ncu_{name}.json")
+        if os.path.exists(prof):
+            with open(prof) as f:
+                traffic = json.load(f).get(dom, {}).get("dram_bytes_per_launch")
+        roofline = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak,
+                    "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": traffic, "algorithmic_bytes_per_launch": bytes_per_launch,
+                    "avg_launch_ms": avg_s * 1000.0}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -295,14 +311,11 @@ def run_b200_arm(args, world, rank, local, dist):
                    "iterations": args.iterations, "lr": 10.0, "seed": 1,
                    "parallelism": f"sample-shard x{world}",
                    "l2": "inputs > L2 (tape %.1f GB)" % (4 * ncone * batch / 1e9)},
-        "unique": global_unique, "restarts": restarts_done, "attempts": st.attempts,
+        "unique": global_unique, "restarts": restarts_done, "attempts": attempts,
         "wall_s": wall, "device_s": device_s,
-        "phase_ms": {k: round(v, 3) for k, v in ph.items()},
-        "gpu_launches": st.launches,
-        "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "avg_launch_ms": avg_s * 1000.0},
+        "phase_ms": {k: round(v, 3) for k, v in ph.items()} if ph else None,
+        "gpu_launches": launches,
+        "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "clocks": clk.summary(),

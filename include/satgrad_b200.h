@@ -143,6 +143,27 @@ int sgx_step(sgx_sampler* s, double* loss_total);
 int sgx_harvest(sgx_sampler* s, int32_t restart, int32_t iter, int64_t* attempts,
                 int64_t* added);
 
+/* Multi-GPU harvest (sample sharding: rank g owns global rows [g*B, (g+1)*B)
+ * via cfg.row_offset).  sgx_harvest is split around the caller's all-gather:
+ *   sgx_harvest_local   harden, eval, CNF check, keys, local table insert;
+ *                       *n_new = locally-new rows, *fps = DEVICE pointer to
+ *                       their 64-bit fingerprints in row order (stride =
+ *                       sgx_fingerprint_stride entries; valid until commit).
+ *   sgx_harvest_merge   all_fps = DEVICE array [nranks][stride] gathered
+ *                       from every rank, counts = HOST array of each rank's
+ *                       n_new.  A fingerprint found by several ranks stays
+ *                       new only on the lowest one (the reference's row
+ *                       order over the union of the shards); every remote
+ *                       fingerprint joins the local table.  *n_won = rows
+ *                       still new here.
+ *   sgx_harvest_commit  append the first min(n_won, quota_left) of them
+ *                       (quota_left < 0: no quota); attempts as sgx_harvest. */
+int sgx_fingerprint_stride(const sgx_sampler* s);
+int sgx_harvest_local(sgx_sampler* s, int32_t restart, int32_t iter, int64_t* n_new, uint64_t** fps);
+int sgx_harvest_merge(sgx_sampler* s, const uint64_t* all_fps, const int64_t* counts, int32_t nranks,
+                      int32_t rank, int64_t stride, int64_t* n_won);
+int sgx_harvest_commit(sgx_sampler* s, int64_t quota_left, int64_t* attempts, int64_t* added);
+
 /* satgrad::run: the whole restart x iteration loop with quota, timeout and
  * restart policy; solutions stay on the device until fetched. */
 int sgx_run(sgx_sampler* s, sgx_run_stats* stats);

@@ -21,7 +21,8 @@ EXPORTS = [
     "sgx_circuit_info", "sgx_circuit_free", "sgx_layout_stats", "sgx_sampler_create",
     "sgx_sampler_free", "sgx_init", "sgx_step", "sgx_harvest", "sgx_run", "sgx_run_traces",
     "sgx_solution_count", "sgx_key_words", "sgx_fetch_solutions", "sgx_phase_times",
-    "sgx_forward", "sgx_backward", "sgx_embed", "sgx_expf",
+    "sgx_forward", "sgx_backward", "sgx_embed", "sgx_expf", "sgx_fingerprint_stride",
+    "sgx_harvest_local", "sgx_harvest_merge", "sgx_harvest_commit",
 ]
 
 
@@ -106,6 +107,10 @@ def load() -> C.CDLL:
         "sgx_backward": (C.c_int, [vp, f32p, i32, f32p, f32p, f32p]),
         "sgx_embed": (C.c_int, [vp, f32p, i64, f32p]),
         "sgx_expf": (C.c_int, [vp, f32p, i64, f32p]),
+        "sgx_fingerprint_stride": (C.c_int, [vp]),
+        "sgx_harvest_local": (C.c_int, [vp, i32, i32, i64p, C.POINTER(C.c_void_p)]),
+        "sgx_harvest_merge": (C.c_int, [vp, C.c_void_p, i64p, i32, i32, i64, i64p]),
+        "sgx_harvest_commit": (C.c_int, [vp, i64, i64p, i64p]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -177,6 +177,9 @@ struct sgx_sampler {
   DBuf<uint32_t> BT, valid, newmask;
   DBuf<int> slot_of_row, block_count;
   DBuf<uint64_t> K, store;
+  DBuf<unsigned long long> fps_local;  // multi-GPU: this harvest's new fingerprints
+  DBuf<long long> n_of;                // multi-GPU: per-rank counts of the gathered lists
+  int dist_stage = 0;                  // 0 idle, 1 after local, 2 after merge
   DBuf<unsigned long long> tkeys, tmeta;
   uint64_t tcap = 0;
   long long table_count = 0;
@@ -296,8 +299,9 @@ void grow_store(sgx_sampler* s, long long need_rows) {
 
 // The harvest lambda of sampler.cpp:124-153 for one (restart, iter).
 // quota_left < 0 means no quota.  Returns rows attempted and solutions added.
-void sampler_harvest(sgx_sampler* s, int restart, int iter, long long quota_left, long long* attempts,
-                     long long* added) {
+// Front half: harden, bit-sliced eval + PO/CNF check, keys + local insert, the
+// row-order scan of the new rows (quota applied when quota_left >= 0).
+void harvest_front(sgx_sampler* s, int restart, int iter, long long quota_left) {
   sgx_circuit* c = s->c;
   const auto& L = c->L;
   {
@@ -322,9 +326,15 @@ void sampler_harvest(sgx_sampler* s, int restart, int iter, long long quota_left
   CK(cudaEventRecord(s->ev[5], s->st));
   sgx::launch_commit(s->st, s->valid.p, s->slot_of_row.p, s->tmeta.p, s->epoch, s->Bp, s->newmask.p,
                      s->block_count.p, quota_left, s->hout.p);
+  s->launches += (L.cpi.size() + L.ucpi.size() ? 1 : 0) + 4;
+}
+
+// Back half: append the accepted rows (hout->accepted) in row order, one sync.
+void harvest_back(sgx_sampler* s, long long quota_left, long long* attempts, long long* added) {
+  const auto& L = s->c->L;
   sgx::launch_append(s->st, s->newmask.p, s->block_count.p, s->K.p, L.key_words, s->Bp, s->store.p,
                      s->n_solutions, s->store_cap, s->hout.p);
-  s->launches += (L.cpi.size() + L.ucpi.size() ? 1 : 0) + 5;
+  s->launches += 1;
   CK(cudaEventRecord(s->ev[6], s->st));
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->st));
@@ -357,6 +367,14 @@ void sampler_harvest(sgx_sampler* s, int restart, int iter, long long quota_left
   s->phase_ms[5] += elapsed(s->ev[3], s->ev[4]);
   s->phase_ms[6] += elapsed(s->ev[4], s->ev[5]);
   s->phase_ms[7] += elapsed(s->ev[5], s->ev[6]);
+}
+
+// The harvest lambda of sampler.cpp:124-153 for one (restart, iter), single
+// device: quota applied in the scan, one host sync.
+void sampler_harvest(sgx_sampler* s, int restart, int iter, long long quota_left, long long* attempts,
+                     long long* added) {
+  harvest_front(s, restart, iter, quota_left);
+  harvest_back(s, quota_left, attempts, added);
 }
 
 // run_impl<float> (sampler.cpp:89-194).
@@ -711,6 +729,85 @@ int sgx_phase_times(const sgx_sampler* s, double* ms8) {
     need(s, "sampler");
     need(ms8, "ms8");
     std::memcpy(ms8, s->phase_ms, sizeof(s->phase_ms));
+  });
+}
+
+// ------------------------------------------------------- multi-GPU harvest
+int sgx_fingerprint_stride(const sgx_sampler* s) { return s ? s->Bp : -1; }
+
+int sgx_harvest_local(sgx_sampler* s, int32_t restart, int32_t iter, int64_t* n_new, uint64_t** fps) {
+  return guard([&] {
+    need_ready(s);
+    if (s->dist_stage != 0) throw StateError("sgx_harvest_local: previous harvest not committed");
+    CK(cudaSetDevice(s->c->ctx->device));
+    if (!s->fps_local.p) s->fps_local.alloc(s->Bp);
+    harvest_front(s, restart, iter, -1);
+    sgx::launch_compact_new(s->st, s->newmask.p, s->block_count.p, s->slot_of_row.p, s->tkeys.p, s->Bp,
+                            s->fps_local.p);
+    s->launches += 1;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    if (n_new) *n_new = s->hpin->new_rows;
+    if (fps) *fps = reinterpret_cast<uint64_t*>(s->fps_local.p);
+    s->dist_stage = 1;
+  });
+}
+
+int sgx_harvest_merge(sgx_sampler* s, const uint64_t* all_fps, const int64_t* counts, int32_t nranks,
+                      int32_t rank, int64_t stride, int64_t* n_won) {
+  return guard([&] {
+    need_ready(s);
+    if (s->dist_stage != 1) throw StateError("sgx_harvest_merge: call sgx_harvest_local first");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank / nranks");
+    if (nranks > 1) {
+      need(all_fps, "all_fps");
+      need(counts, "counts");
+    }
+    CK(cudaSetDevice(s->c->ctx->device));
+    const long long n_local = s->hpin->new_rows;
+    long long remote = 0;
+    std::vector<long long> cnt(nranks, 0);
+    for (int r = 0; r < nranks; ++r) {
+      cnt[r] = counts ? counts[r] : (r == rank ? n_local : 0);
+      if (cnt[r] < 0 || cnt[r] > stride) throw std::invalid_argument("fingerprint count out of range");
+      if (r != rank) remote += cnt[r];
+    }
+    // Room for every remote fingerprint at load factor <= 1/2.
+    s->table_count += remote;
+    ensure_table(s);
+    if (!s->n_of.p || static_cast<int>(s->n_of.n) < nranks) s->n_of.alloc(std::max(nranks, 64));
+    CK(cudaMemcpyAsync(s->n_of.p, cnt.data(), nranks * sizeof(long long), cudaMemcpyHostToDevice, s->st));
+    sgx::launch_merge_remote(s->st, reinterpret_cast<const unsigned long long*>(all_fps), s->n_of.p,
+                             nranks > 1 ? nranks : 0, rank, stride, s->tkeys.p, s->tmeta.p, s->tcap - 1,
+                             s->epoch, s->newmask.p, s->Bp, s->block_count.p, s->hout.p);
+    s->launches += nranks > 1 ? 3 : 2;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    // Locally-new rows another rank claimed still occupy table slots.
+    s->table_count += n_local - s->hpin->new_rows;
+    if (n_won) *n_won = s->hpin->new_rows;
+    s->dist_stage = 2;
+  });
+}
+
+int sgx_harvest_commit(sgx_sampler* s, int64_t quota_left, int64_t* attempts, int64_t* added) {
+  return guard([&] {
+    need_ready(s);
+    if (s->dist_stage != 2) throw StateError("sgx_harvest_commit: call sgx_harvest_merge first");
+    CK(cudaSetDevice(s->c->ctx->device));
+    sgx::HarvestOut h = *s->hpin;
+    h.accepted = quota_left < 0 ? h.new_rows : std::min<long long>(h.new_rows, quota_left);
+    h.last_row = -1;
+    h.overflow = 0;
+    *s->hpin = h;
+    CK(cudaMemcpyAsync(s->hout.p, s->hpin, sizeof(sgx::HarvestOut), cudaMemcpyHostToDevice, s->st));
+    long long att = 0, add = 0;
+    harvest_back(s, quota_left, &att, &add);  // counts the winners into table_count
+    if (attempts) *attempts = att;
+    if (added) *added = add;
+    s->dist_stage = 0;
   });
 }
 

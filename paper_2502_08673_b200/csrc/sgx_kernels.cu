@@ -873,6 +873,88 @@ k_append(const uint32_t* __restrict__ newmask, const int* __restrict__ block_off
     store[static_cast<size_t>(dst) * key_words + q] = K[static_cast<size_t>(q) * Bp + r];
 }
 
+// ---------------------------------------------------------------------------
+// Multi-GPU exchange (sample sharding): rank g owns global rows
+// [g*B, (g+1)*B).  After the local insert, each rank publishes its new
+// fingerprints in row order; a fingerprint new on several ranks counts for the
+// lowest rank, which is exactly the reference's row order over the union of
+// the shards.
+// ---------------------------------------------------------------------------
+
+// Row-order list of this harvest's locally-new fingerprints.
+__global__ void __launch_bounds__(kThreads)
+k_compact_new(const uint32_t* __restrict__ newmask, const int* __restrict__ block_off,
+              const int* __restrict__ slot_of_row, const unsigned long long* __restrict__ tkeys, int Bp,
+              unsigned long long* __restrict__ out) {
+  __shared__ int warp_off[kThreads / 32];
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t m = r < Bp ? __ldg(newmask + (r >> 5)) : 0u;
+  if (lane == 0) warp_off[wid] = __popc(m);
+  __syncthreads();
+  if (!((m >> lane) & 1u)) return;
+  int pos = __ldg(block_off + blockIdx.x);
+  for (int i = 0; i < wid; ++i) pos += warp_off[i];
+  pos += __popc(m & ((1u << lane) - 1u));
+  out[pos] = tkeys[slot_of_row[r]];
+}
+
+// Remote fingerprints: ones from lower ranks that this epoch first saw at a
+// local row take that row out of the new set; every remote fingerprint not
+// yet in the table is inserted with an unmatchable row tag so later epochs
+// see it as old.  all_fps is [nranks][stride], counts on the host side are
+// folded into n_of[rank].
+__global__ void __launch_bounds__(kThreads)
+k_merge_remote(const unsigned long long* __restrict__ all_fps, const long long* __restrict__ n_of,
+               int nranks, int me, long long stride, unsigned long long* tkeys, unsigned long long* tmeta,
+               uint64_t tmask, uint64_t epoch, uint32_t* newmask) {
+  const long long total = static_cast<long long>(nranks) * stride;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int rank = static_cast<int>(i / stride);
+    const long long j = i - static_cast<long long>(rank) * stride;
+    if (rank == me || j >= n_of[rank]) continue;
+    const unsigned long long fp = all_fps[i];
+    uint64_t idx = (fp ^ (fp >> 29)) & tmask;
+    for (;;) {
+      unsigned long long cur = tkeys[idx];
+      if (cur == fp) break;
+      if (cur == 0ull) {
+        cur = atomicCAS(tkeys + idx, 0ull, fp);
+        if (cur == 0ull) {
+          atomicMin(tmeta + idx, static_cast<unsigned long long>((epoch << 32) | 0xffffffffull));
+          cur = fp;
+          idx = ~0ull;  // freshly inserted: nothing local to revoke
+          break;
+        }
+        if (cur == fp) break;
+      }
+      idx = (idx + 1) & tmask;
+    }
+    if (idx == ~0ull || rank > me) continue;
+    const unsigned long long meta = tmeta[idx];
+    if ((meta >> 32) == epoch && (meta & 0xffffffffull) != 0xffffffffull) {
+      const uint32_t row = static_cast<uint32_t>(meta & 0xffffffffull);
+      atomicAnd(newmask + (row >> 5), ~(1u << (row & 31)));
+    }
+  }
+}
+
+// Block counts of the (possibly revoked) new mask, for the row-order scan.
+__global__ void __launch_bounds__(kThreads)
+k_count_new(const uint32_t* __restrict__ newmask, int Bp, int* __restrict__ block_count) {
+  __shared__ int warp_cnt[kThreads / 32];
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) warp_cnt[wid] = r < Bp ? __popc(newmask[r >> 5]) : 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int i = 0; i < kThreads / 32; ++i) t += warp_cnt[i];
+    block_count[blockIdx.x] = t;
+  }
+}
+
 // Move every occupied slot of the old table into the new one.
 __global__ void __launch_bounds__(kThreads)
 k_rehash(const unsigned long long* __restrict__ okeys, const unsigned long long* __restrict__ ometa,
@@ -1042,6 +1124,24 @@ void launch_append(cudaStream_t st, const uint32_t* newmask, const int* block_of
                    int key_words, int Bp, uint64_t* store, long long base, long long cap,
                    HarvestOut* out) {
   k_append<<<Bp / kThreads, kThreads, 0, st>>>(newmask, block_off, K, key_words, Bp, store, base, cap, out);
+}
+
+void launch_compact_new(cudaStream_t st, const uint32_t* newmask, const int* block_off, const int* slot_of_row,
+                        const unsigned long long* tkeys, int Bp, unsigned long long* out) {
+  k_compact_new<<<Bp / kThreads, kThreads, 0, st>>>(newmask, block_off, slot_of_row, tkeys, Bp, out);
+}
+
+void launch_merge_remote(cudaStream_t st, const unsigned long long* all_fps, const long long* n_of, int nranks,
+                         int me, long long stride, unsigned long long* tkeys, unsigned long long* tmeta,
+                         uint64_t tmask, uint64_t epoch, uint32_t* newmask, int Bp, int* block_count,
+                         HarvestOut* out) {
+  const long long total = static_cast<long long>(nranks) * stride;
+  if (total > 0)
+    k_merge_remote<<<grid_for(total, kThreads, 148 * 32), kThreads, 0, st>>>(all_fps, n_of, nranks, me, stride,
+                                                                          tkeys, tmeta, tmask, epoch, newmask);
+  const int nb = Bp / kThreads;
+  k_count_new<<<nb, kThreads, 0, st>>>(newmask, Bp, block_count);
+  k_scan_blocks<<<1, 1024, 0, st>>>(block_count, nb, -1, out);
 }
 
 void launch_rehash(cudaStream_t st, const unsigned long long* okeys, const unsigned long long* ometa,

@@ -36,6 +36,12 @@ void launch_commit(cudaStream_t st, const uint32_t* valid, const int* slot_of_ro
 void launch_append(cudaStream_t st, const uint32_t* newmask, const int* block_off, const uint64_t* K,
                    int key_words, int Bp, uint64_t* store, long long base, long long cap,
                    HarvestOut* out);
+void launch_compact_new(cudaStream_t st, const uint32_t* newmask, const int* block_off, const int* slot_of_row,
+                        const unsigned long long* tkeys, int Bp, unsigned long long* out);
+void launch_merge_remote(cudaStream_t st, const unsigned long long* all_fps, const long long* n_of, int nranks,
+                         int me, long long stride, unsigned long long* tkeys, unsigned long long* tmeta,
+                         uint64_t tmask, uint64_t epoch, uint32_t* newmask, int Bp, int* block_count,
+                         HarvestOut* out);
 void launch_rehash(cudaStream_t st, const unsigned long long* okeys, const unsigned long long* ometa,
                    uint64_t ocap, unsigned long long* nkeys, unsigned long long* nmeta, uint64_t nmask);
 void launch_expf(cudaStream_t st, const float* x, long long n, float* out, const uint64_t* tab, int sigmoid);

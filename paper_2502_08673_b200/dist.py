@@ -1,0 +1,181 @@
+"""Multi-GPU sampling: sample sharding with a per-harvest fingerprint exchange.
+
+The reference is one process; rows are independent
+and every random draw is keyed by (seed, restart, [iter,] row, col)
+(sampler.cpp:54-64, :132-137).  So rank g of N samples global rows
+[g*B, (g+1)*B) with cfg.row_offset = g*B, and the union of the shards is
+exactly a one-device run at batch N*B.  The only data-path collective is the
+all-gather of each harvest's new 64-bit solution fingerprints (NCCL over
+NVLink when the group is NCCL), which keeps uniqueness global: a solution
+found by several ranks in the same harvest counts once, for the lowest rank
+(the reference's row order), and every rank's table learns every
+fingerprint.  Quota, "restart found nothing" and timeout decisions use
+all-gathered counters so every rank takes the same branch (run_impl,
+sampler.cpp:89-194, restated over the union).
+
+``run_sharded`` is written against two small interfaces so its control flow
+can be exercised on CPU (gloo) with a stand-in sampler:
+  * a sampler with init(restart) / step() / harvest_local(restart, it) ->
+    (n_new, fps) / harvest_merge(gathered, counts, world, rank) -> n_won /
+    harvest_commit(quota_left) -> (attempts, added);
+  * an exchange with all_gather_int(x) -> list[int] and
+    all_gather_fps(fps, stride) -> gathered.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+from . import _lib
+
+
+class _DevArray:
+    """Zero-copy view of a library-owned device buffer for torch."""
+
+    def __init__(self, ptr: int, n: int, device: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False),
+                                         "version": 3}
+
+
+class DeviceShard:
+    """A Sampler driven through the split harvest of the C-ABI."""
+
+    def __init__(self, sampler):
+        self.s = sampler
+        self.L = _lib.load()
+        self.stride = int(self.L.sgx_fingerprint_stride(sampler.h))
+        self.device = sampler.dc.device
+
+    def init(self, restart: int):
+        self.s.init(restart)
+
+    def step(self) -> float:
+        return self.s.step()
+
+    def harvest_local(self, restart: int, it: int):
+        import torch
+        n = C.c_int64()
+        ptr = C.c_void_p()
+        _lib.check(self.L.sgx_harvest_local(self.s.h, restart, it, C.byref(n), C.byref(ptr)))
+        fps = torch.as_tensor(_DevArray(ptr.value, self.stride, self.device),
+                              device=f"cuda:{self.device}")
+        return n.value, fps
+
+    def harvest_merge(self, gathered, counts, world: int, rank: int) -> int:
+        import numpy as np
+        won = C.c_int64()
+        cnt = np.ascontiguousarray(counts, np.int64)
+        _lib.check(self.L.sgx_harvest_merge(self.s.h, C.c_void_p(gathered.data_ptr()),
+                                            _lib.ptr(cnt, C.c_int64), world, rank, self.stride,
+                                            C.byref(won)))
+        return won.value
+
+    def harvest_commit(self, quota_left: int):
+        att, add = C.c_int64(), C.c_int64()
+        _lib.check(self.L.sgx_harvest_commit(self.s.h, quota_left, C.byref(att), C.byref(add)))
+        return att.value, add.value
+
+
+class TorchExchange:
+    """torch.distributed collectives (NCCL on GPU tensors, gloo on CPU)."""
+
+    def __init__(self, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.device = torch.device(device) if device is not None else torch.device("cpu")
+        self.torch = torch
+
+    def all_gather_int(self, x: int) -> list[int]:
+        t = self.torch.tensor([int(x)], dtype=self.torch.int64, device=self.device)
+        out = self.torch.zeros(self.world, dtype=self.torch.int64, device=self.device)
+        self.dist.all_gather_into_tensor(out, t, group=self.group)
+        return [int(v) for v in out.cpu()]
+
+    def all_gather_fps(self, fps, stride: int):
+        out = self.torch.empty(self.world * stride, dtype=self.torch.int64, device=fps.device)
+        self.dist.all_gather_into_tensor(out, fps[:stride].contiguous(), group=self.group)
+        if out.is_cuda:
+            self.torch.cuda.current_stream(out.device).synchronize()
+        return out
+
+
+@dataclass
+class ShardStats:
+    unique_count: int = 0           # global unique solutions (all ranks)
+    local_count: int = 0            # solutions this rank holds
+    attempts: int = 0               # global rows pushed through verification
+    restarts: int = 0
+    timed_out: bool = False
+    loss_trace: list = field(default_factory=list)   # this rank's mean loss per step
+    new_unique: list = field(default_factory=list)   # global new per harvest
+    wall_time_s: float = 0.0
+
+
+def run_sharded(shard, ex, cfg, rank: int, world: int, stride: int) -> ShardStats:
+    """run_impl (sampler.cpp:89-194) over the union of `world` shards."""
+    st = ShardStats()
+    t0 = time.perf_counter()
+    quota = cfg.max_solutions > 0
+
+    def quota_met():
+        return quota and st.unique_count >= cfg.max_solutions
+
+    def out_of_time():
+        # every rank must take the same branch: any rank over time stops all
+        late = cfg.timeout_s > 0 and time.perf_counter() - t0 >= cfg.timeout_s
+        return max(ex.all_gather_int(1 if late else 0)) > 0 if cfg.timeout_s > 0 else False
+
+    def harvest(restart, it):
+        n_new, fps = shard.harvest_local(restart, it)
+        counts = ex.all_gather_int(n_new)
+        gathered = ex.all_gather_fps(fps, stride)
+        won = shard.harvest_merge(gathered, counts, world, rank)
+        wons = ex.all_gather_int(won)
+        left = cfg.max_solutions - st.unique_count if quota else None
+        before = sum(wons[:rank])
+        my_left = max(0, left - before) if quota else -1
+        att, add = shard.harvest_commit(my_left)
+        if quota and my_left == 0:
+            att = 0  # a lower rank filled the quota: these rows come after the cut
+        # global accepted, in rank order (identical on every rank)
+        acc = 0
+        for w in wons:
+            take = w if not quota else max(0, min(w, left - acc))
+            acc += take
+        st.unique_count += acc
+        st.local_count += add
+        st.attempts += sum(ex.all_gather_int(att))
+        st.new_unique.append(acc)
+
+    restart = 0
+    while True:
+        shard.init(restart)
+        before = st.unique_count
+        harvest(restart, 0)
+        for it in range(1, cfg.iterations + 1):
+            if quota_met():
+                break
+            if out_of_time():
+                st.timed_out = True
+                break
+            st.loss_trace.append(shard.step() / cfg.batch)
+            harvest(restart, it)
+        if quota_met() or st.timed_out:
+            break
+        if int(cfg.restart) != 1:
+            break
+        if st.unique_count == before:
+            break
+        if restart >= (cfg.max_restarts if cfg.max_restarts > 0 else 1000):
+            break
+        if out_of_time():
+            st.timed_out = True
+            break
+        st.restarts = restart + 1
+        restart += 1
+    st.wall_time_s = time.perf_counter() - t0
+    return st
