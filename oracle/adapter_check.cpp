@@ -1,0 +1,61 @@
+// TEST INFRASTRUCTURE ONLY.  Proves the reference-side binding
+// (include/satgrad_b200_adapter.hpp) is a drop-in: the UNMODIFIED reference
+// pipeline (parse_dimacs -> extract -> build -> classify_paths) feeds both
+// satgrad::run (CPU, f32) and satgrad_b200::run (B200), and the two
+// RunResults must agree: same solutions in the same order (format_solutions
+// byte-identical), same counters, loss traces within f32 summation error.
+// Built by `make -C oracle adapter` into oracle/_ref/adapter_check; run by
+// tests/test_gpu_parity.py::test_reference_adapter_drop_in.
+#include <cmath>
+#include <cstdio>
+#include <fstream>
+#include <sstream>
+
+#include "satgrad/sampler.hpp"
+#include "satgrad_b200_adapter.hpp"
+
+int main(int argc, char** argv) {
+  if (argc < 2) {
+    std::fprintf(stderr, "usage: adapter_check <cnf> [batch iters seed quota restart]\n");
+    return 2;
+  }
+  std::ifstream in(argv[1], std::ios::binary);
+  std::stringstream ss;
+  ss << in.rdbuf();
+  satgrad::CnfFormula cnf = satgrad::parse_dimacs(ss.str());
+  satgrad::ExtractionResult res = satgrad::extract(cnf);
+  satgrad::Circuit c = satgrad::build(res);
+  satgrad::PathClassification paths = satgrad::classify_paths(res);
+  satgrad::SamplerConfig cfg;
+  cfg.use_f32 = true;
+  if (argc > 2) cfg.batch = std::atoi(argv[2]);
+  if (argc > 3) cfg.iterations = std::atoi(argv[3]);
+  if (argc > 4) cfg.seed = std::strtoull(argv[4], nullptr, 10);
+  if (argc > 5) cfg.max_solutions = std::atoll(argv[5]);
+  if (argc > 6 && std::atoi(argv[6])) cfg.restart = satgrad::RestartPolicy::ReinitOnExhaust;
+
+  satgrad::RunResult cpu = satgrad::run(cnf, c, res, paths, cfg);
+  satgrad::RunResult gpu = satgrad_b200::run(cnf, c, res, paths, cfg);
+
+  int bad = 0;
+  auto expect = [&](bool ok, const char* what) {
+    if (!ok) {
+      std::printf("MISMATCH %s\n", what);
+      ++bad;
+    }
+  };
+  expect(satgrad::format_solutions(cpu.solutions) == satgrad::format_solutions(gpu.solutions), "solutions");
+  expect(cpu.stats.unique_count == gpu.stats.unique_count, "unique_count");
+  expect(cpu.stats.attempts == gpu.stats.attempts, "attempts");
+  expect(cpu.stats.new_unique == gpu.stats.new_unique, "new_unique");
+  expect(cpu.stats.restarts == gpu.stats.restarts, "restarts");
+  expect(cpu.stats.timed_out == gpu.stats.timed_out, "timed_out");
+  expect(cpu.stats.loss_trace.size() == gpu.stats.loss_trace.size(), "loss_trace length");
+  for (size_t i = 0; i < cpu.stats.loss_trace.size() && i < gpu.stats.loss_trace.size(); ++i) {
+    double a = cpu.stats.loss_trace[i], b = gpu.stats.loss_trace[i];
+    expect(std::fabs(a - b) <= 1e-4 * std::fmax(std::fabs(a), 1e-30), "loss_trace value");
+  }
+  std::printf("%s: %lld unique (cpu %.3f s, b200 %.3f s)\n", bad ? "adapter MISMATCH" : "adapter ok",
+              static_cast<long long>(gpu.stats.unique_count), cpu.stats.wall_time_s, gpu.stats.wall_time_s);
+  return bad ? 1 : 0;
+}

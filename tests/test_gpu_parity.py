@@ -190,6 +190,28 @@ def test_full_size_shard_union(gpu, name, batch):
     assert union == {k.tobytes() for k in keys}
 
 
+ADAPTER = __import__("os").path.join(__import__("helpers").ROOT, "oracle", "_ref", "adapter_check")
+
+
+@pytest.mark.skipif(not __import__("os").path.exists(ADAPTER), reason="adapter check not built")
+@pytest.mark.parametrize("name,args", [("mux_chain14", ["64", "5", "3", "1000", "1"]),
+                                       ("c3a_or50", ["10000", "5", "1"]),
+                                       ("c1b_random", ["1024", "5", "1", "1000", "1"]),
+                                       ("c2_iscas", ["256", "2", "1"])])
+def test_reference_adapter_drop_in(gpu, tmp_path, name, args):
+    """include/satgrad_b200_adapter.hpp inside the UNMODIFIED reference pipeline:
+    satgrad_b200::run == satgrad::run (f32), solutions byte-identical."""
+    import gzip
+    import subprocess
+    from helpers import ROOT
+    src = __import__("os").path.join(ROOT, "data", "instances", name + ".cnf.gz")
+    cnf = tmp_path / (name + ".cnf")
+    cnf.write_bytes(gzip.open(src).read())
+    r = subprocess.run([ADAPTER, str(cnf), *args], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "adapter ok" in r.stdout
+
+
 def test_sampler_building_blocks(gpu):
     """sgx_init / sgx_step / sgx_harvest reproduce run() for one restart."""
     i = inst("c3a_or50")
