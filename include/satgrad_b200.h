@@ -171,6 +171,9 @@ int sgx_run_traces(sgx_sampler* s, double* loss_trace, int64_t* new_unique);
 int64_t sgx_solution_count(const sgx_sampler* s);
 int32_t sgx_key_words(const sgx_sampler* s);
 int sgx_fetch_solutions(sgx_sampler* s, int64_t first, int64_t count, uint64_t* keys);
+/* The sampler's current logits V as [batch][n_cpi] row-major (the reference's
+ * Mat<float> v of run_impl, sampler.cpp:157-173): trajectory parity tap. */
+int sgx_read_logits(sgx_sampler* s, float* v);
 /* Device time of the last sgx_run by phase, milliseconds:
  * [init, step(fwd+bwd), harvest, fwd, bwd, eval, keys, commit] */
 int sgx_phase_times(const sgx_sampler* s, double* ms8);

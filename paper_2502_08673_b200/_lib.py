@@ -22,7 +22,7 @@ EXPORTS = [
     "sgx_sampler_free", "sgx_init", "sgx_step", "sgx_harvest", "sgx_run", "sgx_run_traces",
     "sgx_solution_count", "sgx_key_words", "sgx_fetch_solutions", "sgx_phase_times",
     "sgx_forward", "sgx_backward", "sgx_embed", "sgx_expf", "sgx_fingerprint_stride",
-    "sgx_harvest_local", "sgx_harvest_merge", "sgx_harvest_commit",
+    "sgx_harvest_local", "sgx_harvest_merge", "sgx_harvest_commit", "sgx_read_logits",
 ]
 
 
@@ -111,6 +111,7 @@ def load() -> C.CDLL:
         "sgx_harvest_local": (C.c_int, [vp, i32, i32, i64p, C.POINTER(C.c_void_p)]),
         "sgx_harvest_merge": (C.c_int, [vp, C.c_void_p, i64p, i32, i32, i64, i64p]),
         "sgx_harvest_commit": (C.c_int, [vp, i64, i64p, i64p]),
+        "sgx_read_logits": (C.c_int, [vp, f32p]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -732,6 +732,23 @@ int sgx_phase_times(const sgx_sampler* s, double* ms8) {
   });
 }
 
+int sgx_read_logits(sgx_sampler* s, float* v) {
+  return guard([&] {
+    need_ready(s);
+    const size_t ncpi = s->c->L.cpi.size();
+    if (!ncpi) return;
+    need(v, "v");
+    CK(cudaSetDevice(s->c->ctx->device));
+    std::vector<float> h(ncpi * s->Bp);
+    CK(cudaMemcpyAsync(h.data(), s->V.p, h.size() * sizeof(float), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    const int tile = 32 * s->vec;
+    for (int r = 0; r < s->cfg.batch; ++r)
+      for (size_t j = 0; j < ncpi; ++j)
+        v[static_cast<size_t>(r) * ncpi + j] = h[(static_cast<size_t>(r / tile) * ncpi + j) * tile + r % tile];
+  });
+}
+
 // ------------------------------------------------------- multi-GPU harvest
 int sgx_fingerprint_stride(const sgx_sampler* s) { return s ? s->Bp : -1; }
 

@@ -257,15 +257,20 @@ k_backward(const int4* __restrict__ ops, const int2* __restrict__ lvl, int n_lev
         if (code == kEdge) {
           const int ck = (f >> kKindShift) & 0xf;
           const float c0 = kPullC0[ck], c1 = kPullC1[ck];
+          const bool neg = f & kNegOtherBit;
+          const float ns = neg ? -1.0f : 1.0f, no = neg ? 1.0f : 0.0f;
+          float p[V];
 #pragma unroll
-          for (int v = 0; v < V; ++v) {
-            float vo = op[k].z >= 0 ? y[k][v] : 0.0f;
-            if (f & kNegOtherBit) vo = __fsub_rn(1.0f, vo);
-            const float p = __fmul_rn(x[k][v], __fmaf_rn(c1, vo, c0));
-            if (f & kInSubBit)
-              acc2[v] = __fadd_rn(acc2[v], p);
-            else
-              acc[v] = __fadd_rn(acc[v], p);
+          for (int v = 0; v < V; ++v) {  // BUF/NOT consumers have no other operand (c1 = 0)
+            const float vo = op[k].z >= 0 ? __fmaf_rn(ns, y[k][v], no) : 0.0f;
+            p[v] = __fmul_rn(x[k][v], __fmaf_rn(c1, vo, c0));
+          }
+          if (f & kInSubBit) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc2[v] = __fadd_rn(acc2[v], p[v]);
+          } else {
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[v] = __fadd_rn(acc[v], p[v]);
           }
         } else if (code == kBegin || code == kSubBegin) {
           const float t = (f & kTargetBit) ? 1.0f : 0.0f;
@@ -343,6 +348,51 @@ __device__ __forceinline__ void f4(const float4& t, float (&o)[4]) {
   o[3] = t.w;
 }
 
+// Folded NOT on read without a branch: fma(-1, x, 1) rounds 1 - x exactly as
+// __fsub_rn(1, x) does; fma(1, x, 0) = x.
+__device__ __forceinline__ float fold_read(float x, int enc) {
+  const bool neg = enc & 1;
+  return __fmaf_rn(neg ? -1.0f : 1.0f, x, neg ? 1.0f : 0.0f);
+}
+
+template <int KIND>
+__device__ __forceinline__ void group_binary(const float4* base, const int (&opd)[8], int n, float* out) {
+#pragma unroll
+  for (int k = 0; k < kGroup; ++k) {
+    if (k >= n) break;
+    float a[4], b[4], r[4];
+    f4(base[(2 * k) * 32], a);
+    f4(base[(2 * k + 1) * 32], b);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const float x = fold_read(a[v], opd[2 * k]), y = fold_read(b[v], opd[2 * k + 1]);
+      if constexpr (KIND == SGX_AND2) r[v] = __fmul_rn(x, y);
+      if constexpr (KIND == SGX_OR2) r[v] = __fsub_rn(1.0f, __fmul_rn(__fsub_rn(1.0f, x), __fsub_rn(1.0f, y)));
+      if constexpr (KIND == SGX_XOR2)
+        r[v] = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, x), y), __fmul_rn(x, __fsub_rn(1.0f, y)));
+      if constexpr (KIND == SGX_XNOR2)
+        r[v] = __fadd_rn(__fmul_rn(x, y), __fmul_rn(__fsub_rn(1.0f, x), __fsub_rn(1.0f, y)));
+    }
+    vstore<4>(out + k * 128, r);
+  }
+}
+
+template <bool NOT>
+__device__ __forceinline__ void group_unary(const float4* base, const int (&opd)[8], int n, float* out) {
+#pragma unroll
+  for (int k = 0; k < kGroup; ++k) {
+    if (k >= n) break;
+    float a[4], r[4];
+    f4(base[(2 * k) * 32], a);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const float x = fold_read(a[v], opd[2 * k]);
+      r[v] = NOT ? __fsub_rn(1.0f, x) : x;
+    }
+    vstore<4>(out + k * 128, r);
+  }
+}
+
 __global__ void __launch_bounds__(32 * kWarps)
 k_forward_async(const int4* __restrict__ grp, const int2* __restrict__ lvl, int n_levels,
                 const float* __restrict__ src, int ncols, float* tape, int n_rows, int src_is_prob,
@@ -395,36 +445,35 @@ k_forward_async(const int4* __restrict__ grp, const int2* __restrict__ lvl, int 
       const int kind = h.x, n = h.y;
       const float4* base = my + (i % kStages) * kSlots * 32;
       float* out = T + static_cast<size_t>(h.z) * TILE;
+      // One dispatch per group; the per-sample loops below are branch-free.
+      switch (kind) {
+        case SGX_AND2: group_binary<SGX_AND2>(base, opd, n, out); break;
+        case SGX_OR2: group_binary<SGX_OR2>(base, opd, n, out); break;
+        case SGX_XOR2: group_binary<SGX_XOR2>(base, opd, n, out); break;
+        case SGX_XNOR2: group_binary<SGX_XNOR2>(base, opd, n, out); break;
+        case SGX_NOT: group_unary<true>(base, opd, n, out); break;
+        case SGX_BUF: group_unary<false>(base, opd, n, out); break;
+        case SGX_INPUT:
 #pragma unroll
-      for (int k = 0; k < kGroup; ++k) {
-        if (k >= n) break;
-        float a[4], b[4], r[4];
-        if (kind >= SGX_AND2) {
-          f4(base[(2 * k) * 32], a);
-          f4(base[(2 * k + 1) * 32], b);
+          for (int k = 0; k < kGroup; ++k) {
+            if (k >= n) break;
+            float a[4] = {0.0f, 0.0f, 0.0f, 0.0f}, r[4];
+            if (opd[2 * k] >= 0) f4(base[(2 * k) * 32], a);
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const float av = (opd[2 * k] & 1) ? __fsub_rn(1.0f, a[v]) : a[v];
-            const float bv = (opd[2 * k + 1] & 1) ? __fsub_rn(1.0f, b[v]) : b[v];
-            r[v] = gate_value(kind, av, bv);
+            for (int v = 0; v < 4; ++v)
+              r[v] = opd[2 * k] < 0 ? 0.5f : (src_is_prob ? a[v] : sigmoid_ref(a[v], exp_tab));
+            vstore<4>(out + k * TILE, r);
           }
-        } else if (kind == SGX_NOT || kind == SGX_BUF) {
-          f4(base[(2 * k) * 32], a);
+          break;
+        default: {
+          const float c = kind == SGX_CONST1 ? 1.0f : 0.0f;
+          const float r[4] = {c, c, c, c};
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const float av = (opd[2 * k] & 1) ? __fsub_rn(1.0f, a[v]) : a[v];
-            r[v] = kind == SGX_NOT ? __fsub_rn(1.0f, av) : av;
+          for (int k = 0; k < kGroup; ++k) {
+            if (k >= n) break;
+            vstore<4>(out + k * TILE, r);
           }
-        } else if (kind == SGX_INPUT) {
-          if (opd[2 * k] >= 0) f4(base[(2 * k) * 32], a);
-#pragma unroll
-          for (int v = 0; v < 4; ++v)
-            r[v] = opd[2 * k] < 0 ? 0.5f : (src_is_prob ? a[v] : sigmoid_ref(a[v], exp_tab));
-        } else {
-#pragma unroll
-          for (int v = 0; v < 4; ++v) r[v] = kind == SGX_CONST1 ? 1.0f : 0.0f;
         }
-        vstore<4>(out + k * TILE, r);
       }
     }
     __syncthreads();

@@ -232,6 +232,14 @@ class Sampler:
         return out
 
     # building blocks ----------------------------------------------------------
+    def logits(self) -> np.ndarray:
+        """Current V, [batch][n_cpi] (trajectory parity tap)."""
+        ncpi = len(self.dc.paths.constrained_pi)
+        v = np.zeros((self.cfg.batch, ncpi), np.float32)
+        if v.size:
+            _lib.check(self.L.sgx_read_logits(self.h, _lib.ptr(v, C.c_float)))
+        return v
+
     def init(self, restart: int):
         _lib.check(self.L.sgx_init(self.h, restart))
 

@@ -190,6 +190,30 @@ def test_full_size_shard_union(gpu, name, batch):
     assert union == {k.tobytes() for k in keys}
 
 
+@pytest.mark.parametrize("name,batch", [("c1b_random", 3000), ("c3a_or50", 3000),
+                                        ("c3a_or50", 65536), ("c3b_or100", 65536),
+                                        ("mux_chain14", 70000)])
+def test_logit_trajectory_bit_exact(gpu, name, batch):
+    """The sampler's own V after init and after each fused step equals the
+    reference computation (init_soft_inputs, embed, forward, backward,
+    gd_step) bit for bit -- at small batches (1 sample per lane) and at bench
+    batches (4 samples per lane, cp.async-staged forward)."""
+    i = inst(name)
+    P = PortLib()
+    s = Sampler(DeviceCircuit.from_instance(i), SamplerConfig(batch=batch, seed=3, iterations=3))
+    s.init(1)
+    v = P.init_soft_inputs(batch, len(i.cpi), 3, 1).astype(np.float32)
+    assert np.array_equal(s.logits().view(np.uint32), v.view(np.uint32))
+    for _ in range(3):
+        s.step()
+        tape, _ = P.forward(i, i.cpi, P.embed(v))
+        dv, _ = P.backward(i, i.cpi, tape, v)
+        v = (v - np.float32(10.0) * dv).astype(np.float32)
+        got = s.logits()
+        bad = np.nonzero(got.view(np.uint32) != v.view(np.uint32))
+        assert bad[0].size == 0, f"{bad[0].size} logits differ, first at row {bad[0][0]} col {bad[1][0]}"
+
+
 ADAPTER = __import__("os").path.join(__import__("helpers").ROOT, "oracle", "_ref", "adapter_check")
 
 
