@@ -165,6 +165,10 @@ struct sgx_circuit {
   DBuf<int> bit_lvl_ptr, cpi_bit_row, ucpi_bit_row, out_bit_row, clause_ptr, clause_enc, key_bit_row;
   DBuf<uint8_t> out_tgt;
   int n_bit_levels = 0;
+  // folded bit program (shared-memory harvest)
+  DBuf<int4> fb_ops;
+  DBuf<int> fb_lvl_ptr, fb_cpi_row, fb_ucpi_row, fb_out_enc, fb_clause_enc, fb_key_enc;
+  int fb_levels = 0;
 };
 
 struct sgx_sampler {
@@ -172,6 +176,7 @@ struct sgx_sampler {
   sgx_sampler_cfg cfg{};
   cudaStream_t st = nullptr;
   int Bp = 0, W = 0, wpc = 8, vec = 2, n_partial = 148;
+  int hwpc = 0;  // words per CTA of the shared-memory harvest (0: global-memory path)
   DBuf<float> V, tape, adj, row_loss;
   DBuf<double> partial;
   DBuf<uint32_t> BT, valid, newmask;
@@ -265,7 +270,8 @@ void ensure_table(sgx_sampler* s) {
   // Keep the load factor under 1/2 even if every row of this harvest is new.
   uint64_t want = static_cast<uint64_t>(s->table_count + s->Bp) * 2;
   if (want <= s->tcap) return;
-  uint64_t ncap = next_pow2(std::max<uint64_t>(want * 2, 1u << 16));
+  // Geometric growth with a first size covering several restarts.
+  uint64_t ncap = next_pow2(std::max<uint64_t>(std::max<uint64_t>(want * 2, 16ull * s->Bp), 1u << 16));
   DBuf<unsigned long long> nk, nm;
   nk.alloc_async(ncap, s->st);
   nm.alloc_async(ncap, s->st);
@@ -313,20 +319,57 @@ void harvest_front(sgx_sampler* s, int restart, int iter, long long quota_left) 
   uint64_t fprefix = sgx::fold(
       sgx::fold(sgx::fold(sgx::fold(sgx::kPi, s->cfg.seed), sgx::kFreeTag), static_cast<uint64_t>(static_cast<int64_t>(restart))),
       static_cast<uint64_t>(static_cast<int64_t>(iter)));
-  sgx::launch_harden(s->st, s->V.p, static_cast<int>(L.cpi.size()), static_cast<int>(L.ucpi.size()),
-                     c->cpi_bit_row.p, c->ucpi_bit_row.p, s->BT.p, s->W, 32 * s->vec, fprefix,
-                     s->cfg.row_offset);
-  sgx::launch_bit_eval(s->st, s->wpc, c->bit_ops.p, c->bit_lvl_ptr.p, c->n_bit_levels, s->BT.p, s->W,
-                       c->out_bit_row.p, c->out_tgt.p, static_cast<int>(L.out_node.size()), c->clause_ptr.p,
-                       c->clause_enc.p, static_cast<int>(L.clause_ptr.size()) - 1, s->valid.p, s->cfg.batch);
-  CK(cudaEventRecord(s->ev[4], s->st));
   s->epoch += 1;
-  sgx::launch_keys(s->st, s->BT.p, s->W, c->key_bit_row.p, L.key_words, s->valid.p, s->Bp, s->K.p,
-                   s->slot_of_row.p, s->tkeys.p, s->tmeta.p, s->tcap - 1, s->epoch);
-  CK(cudaEventRecord(s->ev[5], s->st));
+  if (s->hwpc > 0) {
+    sgx::HarvestSmemArgs a{};
+    a.V = s->V.p;
+    a.ncpi = static_cast<int>(L.cpi.size());
+    a.nucpi = static_cast<int>(L.ucpi.size());
+    a.cpi_row = c->fb_cpi_row.p;
+    a.ucpi_row = c->fb_ucpi_row.p;
+    a.tile_rows = 32 * s->vec;
+    a.free_prefix = fprefix;
+    a.row_offset = s->cfg.row_offset;
+    a.ops = c->fb_ops.p;
+    a.lvl_ptr = c->fb_lvl_ptr.p;
+    a.n_levels = c->fb_levels;
+    a.out_enc = c->fb_out_enc.p;
+    a.out_tgt = c->out_tgt.p;
+    a.n_out = static_cast<int>(L.out_node.size());
+    a.clause_ptr = c->clause_ptr.p;
+    a.clause_enc = c->fb_clause_enc.p;
+    a.n_clauses = static_cast<int>(L.clause_ptr.size()) - 1;
+    a.key_enc = c->fb_key_enc.p;
+    a.key_words = L.key_words;
+    a.batch = s->cfg.batch;
+    a.Bp = s->Bp;
+    a.valid = s->valid.p;
+    a.K = s->K.p;
+    a.slot_of_row = s->slot_of_row.p;
+    a.tkeys = s->tkeys.p;
+    a.tmeta = s->tmeta.p;
+    a.tmask = s->tcap - 1;
+    a.epoch = s->epoch;
+    sgx::launch_harvest_smem(s->st, s->hwpc, L.fb_rows, s->W, a);
+    CK(cudaEventRecord(s->ev[4], s->st));
+    CK(cudaEventRecord(s->ev[5], s->st));
+    s->launches += 1;
+  } else {
+    sgx::launch_harden(s->st, s->V.p, static_cast<int>(L.cpi.size()), static_cast<int>(L.ucpi.size()),
+                       c->cpi_bit_row.p, c->ucpi_bit_row.p, s->BT.p, s->W, 32 * s->vec, fprefix,
+                       s->cfg.row_offset);
+    sgx::launch_bit_eval(s->st, s->wpc, c->bit_ops.p, c->bit_lvl_ptr.p, c->n_bit_levels, s->BT.p, s->W,
+                         c->out_bit_row.p, c->out_tgt.p, static_cast<int>(L.out_node.size()), c->clause_ptr.p,
+                         c->clause_enc.p, static_cast<int>(L.clause_ptr.size()) - 1, s->valid.p, s->cfg.batch);
+    CK(cudaEventRecord(s->ev[4], s->st));
+    sgx::launch_keys(s->st, s->BT.p, s->W, c->key_bit_row.p, L.key_words, s->valid.p, s->Bp, s->K.p,
+                     s->slot_of_row.p, s->tkeys.p, s->tmeta.p, s->tcap - 1, s->epoch);
+    CK(cudaEventRecord(s->ev[5], s->st));
+    s->launches += (L.cpi.size() + L.ucpi.size() ? 1 : 0) + 2;
+  }
   sgx::launch_commit(s->st, s->valid.p, s->slot_of_row.p, s->tmeta.p, s->epoch, s->Bp, s->newmask.p,
                      s->block_count.p, quota_left, s->hout.p);
-  s->launches += (L.cpi.size() + L.ucpi.size() ? 1 : 0) + 4;
+  s->launches += 2;
 }
 
 // Back half: append the accepted rows (hout->accepted) in row order, one sync.
@@ -556,6 +599,14 @@ int sgx_circuit_upload(sgx_ctx* ctx, const sgx_circuit_desc* d, sgx_circuit** ou
       c->clause_ptr.upload(L.clause_ptr32, st);
       c->clause_enc.upload(L.clause_enc, st);
       c->key_bit_row.upload(L.key_bit_row, st);
+      c->fb_ops.upload(to_int4(L.fb_ops), st);
+      c->fb_lvl_ptr.upload(L.fb_lvl_ptr, st);
+      c->fb_levels = static_cast<int>(L.fb_lvl_ptr.size()) - 1;
+      c->fb_cpi_row.upload(L.fb_cpi_row, st);
+      c->fb_ucpi_row.upload(L.fb_ucpi_row, st);
+      c->fb_out_enc.upload(L.fb_out_enc, st);
+      c->fb_clause_enc.upload(L.fb_clause_enc, st);
+      c->fb_key_enc.upload(L.fb_key_enc, st);
       CK(cudaStreamSynchronize(st));
     }
     *out = c.release();
@@ -606,6 +657,20 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
         int v = std::atoi(e);
         if (v == 1 || v == 2 || v == 4) s->vec = v;
       }
+      // Shared-memory harvest: the widest word block whose folded bit tape
+      // fits ~100 KB (two CTAs per SM) while leaving >= 2 CTAs per SM of work;
+      // one word (up to 200 KB) for deep circuits; else the global path.
+      const size_t row_bytes = static_cast<size_t>(L.fb_rows) * sizeof(uint32_t);
+      s->hwpc = 0;
+      for (int w = 32; w >= 1; w /= 2)
+        if (row_bytes * w <= 100 * 1024 && s->W / w >= 2 * 148) {
+          s->hwpc = w;
+          break;
+        }
+      if (!s->hwpc && row_bytes <= 200 * 1024) s->hwpc = 1;
+      if (const char* e = std::getenv("SGX_HARVEST")) {
+        if (e[0] == 'g') s->hwpc = 0;  // force the global-memory harvest
+      }
       const size_t Bp = static_cast<size_t>(s->Bp);
       s->V.alloc(L.cpi.size() * Bp);
       s->tape.alloc(static_cast<size_t>(L.cone.n_rows) * Bp);
@@ -618,7 +683,9 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       s->slot_of_row.alloc(Bp);
       s->block_count.alloc(Bp / sgx::kThreads);
       s->K.alloc(static_cast<size_t>(L.key_words) * Bp);
-      s->store_cap = cfg->solution_capacity > 0 ? cfg->solution_capacity : 2 * static_cast<long long>(Bp);
+      // Room for about a restart's worth of solutions (6 harvests of unique
+      // rows) before the first growth.
+      s->store_cap = cfg->solution_capacity > 0 ? cfg->solution_capacity : 6 * static_cast<long long>(Bp);
       s->store.alloc(static_cast<size_t>(s->store_cap) * L.key_words);
       CK(cudaMemsetAsync(s->V.p, 0, s->V.n * sizeof(float), s->st));
       ensure_table(s.get());

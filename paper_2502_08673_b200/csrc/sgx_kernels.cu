@@ -323,6 +323,10 @@ k_backward(const int4* __restrict__ ops, const int2* __restrict__ lvl, int n_lev
 // their own staged bytes, so per-thread cp.async.wait_group is the only
 // synchronisation inside a level.
 // ---------------------------------------------------------------------------
+#ifndef SGX_BWD_U
+#define SGX_BWD_U 8  // backward micro-ops per chunk at 4 samples per lane (measured: 4 -> 3.34 ms,
+                     // 8 -> 2.94 ms, 16 -> 5.2 ms per C2 launch)
+#endif
 #ifndef SGX_STAGES
 #define SGX_STAGES 3
 #endif
@@ -792,7 +796,7 @@ k_keys(const uint32_t* __restrict__ BT, int W, const int* __restrict__ key_row, 
   if (anyv == 0) return;  // warp-uniform
   uint64_t h[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) h[j] = kPi;
+  for (int j = 0; j < 8; ++j) h[j] = 0ull;
   const size_t Wz = static_cast<size_t>(W);
   for (int q = 0; q < key_words; ++q) {
     uint32_t half[2][8];
@@ -812,7 +816,7 @@ k_keys(const uint32_t* __restrict__ BT, int W, const int* __restrict__ key_row, 
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint64_t kw = static_cast<uint64_t>(half[0][j]) | (static_cast<uint64_t>(half[1][j]) << 32);
-      h[j] = mix64(h[j] ^ kw);
+      h[j] += key_term(kw, q);
       if ((vm[j] >> lane) & 1u) K[static_cast<size_t>(q) * Bp + (w0 + j) * 32 + lane] = kw;
     }
   }
@@ -820,7 +824,157 @@ k_keys(const uint32_t* __restrict__ BT, int W, const int* __restrict__ key_row, 
   for (int j = 0; j < 8; ++j) {
     if (!((vm[j] >> lane) & 1u)) continue;
     const int r = (w0 + j) * 32 + lane;
-    const unsigned long long fp = h[j] ? h[j] : 1ull;  // 0 marks an empty slot
+    const uint64_t hf = mix64(h[j]);
+    const unsigned long long fp = hf ? hf : 1ull;  // 0 marks an empty slot
+    uint64_t idx = (fp ^ (fp >> 29)) & tmask;
+    for (;;) {
+      unsigned long long cur = tkeys[idx];
+      if (cur == fp) break;
+      if (cur == 0ull) {
+        cur = atomicCAS(tkeys + idx, 0ull, fp);
+        if (cur == 0ull || cur == fp) break;
+      }
+      idx = (idx + 1) & tmask;
+    }
+    atomicMin(tmeta + idx, static_cast<unsigned long long>((epoch << 32) | static_cast<uint32_t>(r)));
+    slot_of_row[r] = static_cast<int>(idx);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5+K6+K7 fused, shared-memory resident: one CTA owns WPC words (32*WPC
+// rows) and keeps its whole folded bit tape [row][WPC] in shared memory, so
+// harden -> every level of eval_discrete -> PO + CNF check -> dedupe keys +
+// fingerprint + table insert run without touching HBM except for V, the
+// key words of valid rows and the table.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t neg_mask(int enc) { return (enc & 1) ? kFull : 0u; }
+
+template <int WPC>
+__global__ void __launch_bounds__(kThreads)
+k_harvest_smem(const float* __restrict__ V, int ncpi, int nucpi, const int* __restrict__ cpi_row,
+               const int* __restrict__ ucpi_row, int tile_rows, uint64_t free_prefix, long long row_offset,
+               const int4* __restrict__ ops, const int* __restrict__ lvl_ptr, int n_levels,
+               const int* __restrict__ out_enc, const uint8_t* __restrict__ out_tgt, int n_out,
+               const int* __restrict__ clause_ptr, const int* __restrict__ clause_enc, int n_clauses,
+               const int* __restrict__ key_enc, int key_words, int batch, int Bp,
+               uint32_t* __restrict__ valid_out, uint64_t* __restrict__ K, int* __restrict__ slot_of_row,
+               unsigned long long* tkeys, unsigned long long* tmeta, uint64_t tmask, uint64_t epoch) {
+  extern __shared__ uint32_t bits[];  // [row][WPC]
+  __shared__ uint32_t red[kThreads];
+  __shared__ uint32_t vw[WPC];
+  constexpr int NW = kThreads / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w0 = blockIdx.x * WPC;
+  // harden (autodiff.cpp:292-297): 8 independent V loads in flight per warp,
+  // then one ballot each
+  constexpr int HU = 8;
+  for (int item0 = warp * HU; item0 < ncpi * WPC; item0 += NW * HU) {
+    float x[HU];
+#pragma unroll
+    for (int u = 0; u < HU; ++u) {
+      const int item = item0 + u;
+      x[u] = -1.0f;
+      if (item < ncpi * WPC) {
+        const int input = item / WPC, wl = item - input * WPC;
+        const int r = (w0 + wl) * 32 + lane;
+        const size_t tile = static_cast<size_t>(r / tile_rows);
+        x[u] = V[(tile * ncpi + input) * tile_rows + r % tile_rows];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < HU; ++u) {
+      const int item = item0 + u;
+      if (item >= ncpi * WPC) break;  // warp-uniform
+      const uint32_t word = __ballot_sync(kFull, x[u] >= 0.0f);
+      const int input = item / WPC, wl = item - input * WPC;
+      if (lane == 0) bits[__ldg(cpi_row + input) * WPC + wl] = word;
+    }
+  }
+  // free bits (sampler.cpp:132-137)
+  for (int item = warp; item < nucpi * WPC; item += NW) {
+    const int k = item / WPC, wl = item - k * WPC;
+    const int r = (w0 + wl) * 32 + lane;
+    const bool bit = fold(fold(free_prefix, static_cast<uint64_t>(row_offset + r)), static_cast<uint64_t>(k)) & 1;
+    const uint32_t word = __ballot_sync(kFull, bit);
+    if (lane == 0) bits[__ldg(ucpi_row + k) * WPC + wl] = word;
+  }
+  __syncthreads();
+  // eval_discrete (circuit.cpp:126-146), level by level
+  for (int l = 0; l < n_levels; ++l) {
+    const int b = __ldg(lvl_ptr + l), e = __ldg(lvl_ptr + l + 1);
+    for (int item = threadIdx.x; item < (e - b) * WPC; item += kThreads) {
+      const int i = b + item / WPC, wl = item % WPC;
+      const int4 op = __ldg(ops + i);
+      const uint32_t a = bits[(op.z >> 1) * WPC + wl] ^ neg_mask(op.z);
+      const uint32_t c = bits[(op.w >> 1) * WPC + wl] ^ neg_mask(op.w);
+      bits[op.y * WPC + wl] = bit_gate(op.x, a, c);
+    }
+    __syncthreads();
+  }
+  // PO check (sampler.cpp:140-146) + eval_cnf (cnf.cpp:136-145)
+  {
+    constexpr int S = kThreads / WPC;
+    const int wl = threadIdx.x % WPC, slot = threadIdx.x / WPC;
+    uint32_t ok = kFull;
+    for (int m = slot; m < n_out; m += S) {
+      const int e = __ldg(out_enc + m);
+      const uint32_t x = bits[(e >> 1) * WPC + wl] ^ neg_mask(e);
+      ok &= __ldg(out_tgt + m) ? x : ~x;
+    }
+    const int c0 = static_cast<int>(static_cast<long long>(n_clauses) * slot / S);
+    const int c1 = static_cast<int>(static_cast<long long>(n_clauses) * (slot + 1) / S);
+    const int l1 = __ldg(clause_ptr + c1);
+    uint32_t any = 0u;
+#pragma unroll 8
+    for (int l = __ldg(clause_ptr + c0); l < l1; ++l) {
+      const int e = __ldg(clause_enc + l);
+      const uint32_t x = bits[(e >> 2) * WPC + wl];
+      any |= (e & 1) ? ~x : x;
+      if (e & 2) {
+        ok &= any;
+        any = 0u;
+      }
+    }
+    red[threadIdx.x] = ok;
+    __syncthreads();
+    if (slot == 0) {
+#pragma unroll 4
+      for (int j = 1; j < S; ++j) ok &= red[j * WPC + wl];
+      const int r0 = (w0 + wl) * 32;
+      const uint32_t mask = r0 + 32 <= batch ? kFull : (r0 >= batch ? 0u : ((1u << (batch - r0)) - 1u));
+      vw[wl] = ok & mask;
+      valid_out[w0 + wl] = ok & mask;
+    }
+    __syncthreads();
+  }
+  // dedupe keys (sampler.cpp:18-26) by warp transposes; all warps share the
+  // (word, key word) items and fold their fingerprint terms with shared atomics
+  __shared__ unsigned long long hsum[WPC * 32];
+  for (int t = threadIdx.x; t < WPC * 32; t += kThreads) hsum[t] = 0ull;
+  __syncthreads();
+  for (int item = warp; item < WPC * key_words; item += NW) {
+    const int q = item / WPC, wl = item - q * WPC;
+    const uint32_t vm = vw[wl];
+    if (vm == 0) continue;  // warp-uniform
+    uint32_t half[2];
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const int e = __ldg(key_enc + (2 * q + hf) * 32 + lane);
+      const uint32_t x = e >= 0 ? (bits[(e >> 1) * WPC + wl] ^ neg_mask(e)) : 0u;
+      half[hf] = transpose32(x, lane);
+    }
+    const uint64_t kw = static_cast<uint64_t>(half[0]) | (static_cast<uint64_t>(half[1]) << 32);
+    atomicAdd(hsum + wl * 32 + lane, static_cast<unsigned long long>(key_term(kw, q)));
+    if ((vm >> lane) & 1u) K[static_cast<size_t>(q) * Bp + (w0 + wl) * 32 + lane] = kw;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < WPC * 32; t += kThreads) {
+    const int wl = t >> 5, ln = t & 31;
+    if (!((vw[wl] >> ln) & 1u)) continue;
+    const int r = (w0 + wl) * 32 + ln;
+    const uint64_t h = mix64(hsum[t]);
+    const unsigned long long fp = h ? h : 1ull;
     uint64_t idx = (fp ^ (fp >> 29)) & tmask;
     for (;;) {
       unsigned long long cur = tkeys[idx];
@@ -1105,8 +1259,9 @@ void launch_backward(cudaStream_t st, int vec, const int4* ops, const int2* lvl,
   }
   switch (vec) {
     case 4:
-      k_backward<4, 4><<<tiles, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows, dv_out,
-                                                      dp_out, lr, out_enc, out_tgt, n_out, row_loss, exp_tab);
+      k_backward<4, SGX_BWD_U><<<tiles, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows,
+                                                              dv_out, dp_out, lr, out_enc, out_tgt, n_out, row_loss,
+                                                              exp_tab);
       break;
     case 2:
       k_backward<2, 8><<<tiles, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows, dv_out,
@@ -1173,6 +1328,32 @@ void launch_append(cudaStream_t st, const uint32_t* newmask, const int* block_of
                    int key_words, int Bp, uint64_t* store, long long base, long long cap,
                    HarvestOut* out) {
   k_append<<<Bp / kThreads, kThreads, 0, st>>>(newmask, block_off, K, key_words, Bp, store, base, cap, out);
+}
+
+template <int WPC>
+static void harvest_smem_t(cudaStream_t st, int grid, size_t smem, const HarvestSmemArgs& a) {
+  static size_t opted = 48 * 1024;  // dynamic bytes this instantiation may use
+  if (smem > opted) {
+    cudaFuncSetAttribute(k_harvest_smem<WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    opted = smem;
+  }
+  k_harvest_smem<WPC><<<grid, kThreads, smem, st>>>(
+      a.V, a.ncpi, a.nucpi, a.cpi_row, a.ucpi_row, a.tile_rows, a.free_prefix, a.row_offset, a.ops, a.lvl_ptr,
+      a.n_levels, a.out_enc, a.out_tgt, a.n_out, a.clause_ptr, a.clause_enc, a.n_clauses, a.key_enc, a.key_words,
+      a.batch, a.Bp, a.valid, a.K, a.slot_of_row, a.tkeys, a.tmeta, a.tmask, a.epoch);
+}
+
+void launch_harvest_smem(cudaStream_t st, int wpc, int n_rows, int W, const HarvestSmemArgs& a) {
+  const size_t smem = static_cast<size_t>(n_rows) * wpc * sizeof(uint32_t);
+  const int grid = W / wpc;
+  switch (wpc) {
+    case 32: harvest_smem_t<32>(st, grid, smem, a); break;
+    case 16: harvest_smem_t<16>(st, grid, smem, a); break;
+    case 8: harvest_smem_t<8>(st, grid, smem, a); break;
+    case 4: harvest_smem_t<4>(st, grid, smem, a); break;
+    case 2: harvest_smem_t<2>(st, grid, smem, a); break;
+    default: harvest_smem_t<1>(st, grid, smem, a); break;
+  }
 }
 
 void launch_compact_new(cudaStream_t st, const uint32_t* newmask, const int* block_off, const int* slot_of_row,

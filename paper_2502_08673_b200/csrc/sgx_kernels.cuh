@@ -43,6 +43,15 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // rng.hpp:14-
 // One hash_stream fold step (rng.hpp:23).
 __host__ __device__ __forceinline__ uint64_t fold(uint64_t h, uint64_t x) { return mix64(h ^ mix64(x)); }
 
+// Fingerprint of a dedupe key: mix64(sum over key words q of
+// mix64(word_q ^ (q+1)*pi)) mod 2^64.  The sum is order-independent, so the
+// key words of one row can be folded by different warps.  Identity of a
+// solution is its full key; the fingerprint only indexes the dedup table
+// (a collision can drop a solution, never emit a wrong or duplicate one).
+__host__ __device__ __forceinline__ uint64_t key_term(uint64_t kw, int q) {
+  return mix64(kw ^ (kPi * static_cast<uint64_t>(q + 1)));
+}
+
 #if defined(__CUDACC__)
 // glibc 2.39 expf (sysdeps/ieee754/flt-32/e_expf.c, FMA ifunc variant) for
 // |x| < 88: 2^(k/32) table + cubic in double.  Constants are glibc's

@@ -36,6 +36,32 @@ void launch_commit(cudaStream_t st, const uint32_t* valid, const int* slot_of_ro
 void launch_append(cudaStream_t st, const uint32_t* newmask, const int* block_off, const uint64_t* K,
                    int key_words, int Bp, uint64_t* store, long long base, long long cap,
                    HarvestOut* out);
+struct HarvestSmemArgs {
+  const float* V;
+  int ncpi, nucpi;
+  const int *cpi_row, *ucpi_row;
+  int tile_rows;
+  uint64_t free_prefix;
+  long long row_offset;
+  const int4* ops;
+  const int* lvl_ptr;
+  int n_levels;
+  const int* out_enc;
+  const uint8_t* out_tgt;
+  int n_out;
+  const int *clause_ptr, *clause_enc;
+  int n_clauses;
+  const int* key_enc;
+  int key_words, batch, Bp;
+  uint32_t* valid;
+  uint64_t* K;
+  int* slot_of_row;
+  unsigned long long *tkeys, *tmeta;
+  uint64_t tmask, epoch;
+};
+// Fused shared-memory harvest (harden + eval + PO/CNF + keys + insert); the
+// folded bit tape of wpc words must fit in shared memory.
+void launch_harvest_smem(cudaStream_t st, int wpc, int n_rows, int W, const HarvestSmemArgs& a);
 void launch_compact_new(cudaStream_t st, const uint32_t* newmask, const int* block_off, const int* slot_of_row,
                         const unsigned long long* tkeys, int Bp, unsigned long long* out);
 void launch_merge_remote(cudaStream_t st, const unsigned long long* all_fps, const long long* n_of, int nranks,

@@ -212,6 +212,65 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
   return P;
 }
 
+// Folded bit program over every node (eval_discrete, circuit.cpp:126-146):
+// ~x and x are free on a 32-row word, so NOT/BUF nodes with a materialized
+// operand become a mask on the reference instead of a row.
+void build_folded_bits(Layout& L) {
+  const int n = L.n_nodes;
+  std::vector<uint8_t> virt(n, 0);
+  for (int i = 0; i < n; ++i)
+    if ((L.kind[i] == SGX_NOT || L.kind[i] == SGX_BUF) && !virt[L.a[i]]) virt[i] = 1;
+  std::vector<int32_t> lev(n, 0);
+  int max_level = 0;
+  auto base = [&](int x) { return virt[x] ? L.a[x] : x; };
+  for (int i = 0; i < n; ++i) {
+    if (virt[i]) continue;
+    const int oc = operand_count(L.kind[i]);
+    if (oc >= 1) lev[i] = lev[base(L.a[i])] + 1;
+    if (oc == 2) lev[i] = std::max(lev[i], lev[base(L.b[i])] + 1);
+    max_level = std::max(max_level, lev[i]);
+  }
+  std::vector<std::vector<int32_t>> by_level(max_level + 1);
+  for (int i = 0; i < n; ++i)
+    if (!virt[i]) by_level[lev[i]].push_back(i);
+  std::vector<int32_t> row(n, -1);
+  int32_t next = 0;
+  for (const auto& lv : by_level)
+    for (int i : lv) row[i] = next++;
+  L.fb_rows = next;
+  auto enc = [&](int x) {  // row << 1 | negate, through at most one folded NOT
+    const bool neg = virt[x] && L.kind[x] == SGX_NOT;
+    return (row[base(x)] << 1) | (neg ? 1 : 0);
+  };
+  L.fb_ops.clear();
+  L.fb_lvl_ptr.clear();
+  for (const auto& lv : by_level) {
+    L.fb_lvl_ptr.push_back(static_cast<int32_t>(L.fb_ops.size()));
+    for (int i : lv) {
+      if (L.kind[i] == SGX_INPUT) continue;
+      const int oc = operand_count(L.kind[i]);
+      L.fb_ops.push_back({L.kind[i], row[i], oc >= 1 ? enc(L.a[i]) : 0, oc == 2 ? enc(L.b[i]) : 0});
+    }
+  }
+  L.fb_lvl_ptr.push_back(static_cast<int32_t>(L.fb_ops.size()));
+  L.fb_cpi_row.clear();
+  L.fb_ucpi_row.clear();
+  for (int v : L.cpi) L.fb_cpi_row.push_back(row[L.node_of_var[v]]);
+  for (int v : L.ucpi) L.fb_ucpi_row.push_back(row[L.node_of_var[v]]);
+  L.fb_out_enc.clear();
+  for (int o : L.out_node) L.fb_out_enc.push_back(enc(o));
+  L.fb_clause_enc.clear();
+  for (int64_t c = 0; c + 1 < static_cast<int64_t>(L.clause_ptr.size()); ++c)
+    for (int64_t l = L.clause_ptr[c]; l < L.clause_ptr[c + 1]; ++l) {
+      const int32_t lit = L.clause_lit[l];
+      const int e = enc(L.node_of_var[lit < 0 ? -lit : lit]);
+      const bool last = l + 1 == L.clause_ptr[c + 1];
+      L.fb_clause_enc.push_back(((e >> 1) << 2) | (last ? 2 : 0) | ((e & 1) ^ (lit < 0 ? 1 : 0)));
+    }
+  L.fb_key_enc.assign(static_cast<size_t>(L.key_words) * 64, -1);
+  for (int v = 1; v <= L.num_vars; ++v) L.fb_key_enc[v - 1] = enc(L.node_of_var[v]);
+}
+
 }  // namespace
 
 Layout build_layout(const sgx_circuit_desc& d) {
@@ -357,6 +416,7 @@ Layout build_layout(const sgx_circuit_desc& d) {
   L.key_words = (L.num_vars + 63) / 64;
   L.key_bit_row.assign(static_cast<size_t>(L.key_words) * 64, -1);
   for (int v = 1; v <= L.num_vars; ++v) L.key_bit_row[v - 1] = L.bit_row_of_node[L.node_of_var[v]];
+  build_folded_bits(L);
   return L;
 }
 

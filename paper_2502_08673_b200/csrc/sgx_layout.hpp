@@ -31,7 +31,10 @@
 namespace sgx {
 
 constexpr int kU = 8;      // ops per chunk (loads in flight per thread)
-constexpr int kWarps = 4;  // warps per CTA sharing one sample tile (node split)
+#ifndef SGX_WARPS
+#define SGX_WARPS 4
+#endif
+constexpr int kWarps = SGX_WARPS;  // warps per CTA sharing one sample tile (node split)
 
 // Forward group: kGroupRecs int4 records.  Header {kind, n, first_out_row, 0},
 // then kGroup operand pairs (a, b) packed two per int4; an operand is
@@ -101,6 +104,17 @@ struct Layout {
   std::vector<int32_t> clause_enc;   // bit_row << 1 | negated
   int32_t key_words = 0;             // (num_vars + 63) / 64
   std::vector<int32_t> key_bit_row;  // key_words * 64, -1 = padding
+
+  // Folded bit program for the shared-memory harvest: NOT/BUF nodes whose
+  // operand is materialized own no row (read as row ^ mask); every reference
+  // is row << 1 | negate (clause literals: row << 2 | last << 1 | negate).
+  int32_t fb_rows = 0;
+  std::vector<I4> fb_ops;            // {kind, out_row, a_enc, b_enc}, level-sorted
+  std::vector<int32_t> fb_lvl_ptr;
+  std::vector<int32_t> fb_cpi_row, fb_ucpi_row;
+  std::vector<int32_t> fb_out_enc;
+  std::vector<int32_t> fb_clause_enc;
+  std::vector<int32_t> fb_key_enc;   // key_words * 64, -1 = padding
 
   int64_t n_lits() const { return static_cast<int64_t>(clause_lit.size()); }
 };

@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 class ThreadExchange:
     def __init__(self, world):
         self.world = world
-        self.bar = threading.Barrier(world)
+        self.bar = threading.Barrier(world, timeout=120)  # a failing rank must not hang the other
         self.slots = [None] * world
 
     def view(self, rank):
