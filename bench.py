@@ -159,6 +159,43 @@ def cpu_reference(inst_name, batch, iterations, seed, steps=1, timeout_s=0.0):
             "unique": uniq, "wall_s": wall}
 
 
+def time_to_1k(dev, with_cpu=True, name="c3a_or50", batch=1 << 20):
+    """BASELINE.json's second metric: time to 1,000 unique valid solutions on
+    the or-50 shape at a 1M-row batch (quota 1000, ReinitOnExhaust, as the
+    reference's `bench` subcommand runs it, satgrad_main.cpp:319-327)."""
+    from paper_2502_08673_b200 import (DeviceCircuit, RestartPolicy, Sampler, SamplerConfig,
+                                       load_instance, run_instance)
+    inst = load_instance(name)
+    cfg = SamplerConfig(batch=batch, iterations=5, seed=1, max_solutions=1000,
+                        restart=RestartPolicy.REINIT_ON_EXHAUST)
+    dc = DeviceCircuit.from_instance(inst, device=dev)
+    s = Sampler(dc, cfg)
+    s.run()  # warm-up
+    dev_ms = []
+    for _ in range(5):
+        st = s.run()
+        assert st.unique_count == 1000
+        dev_ms.append(st.device_ms)
+    s.close()
+    t0 = time.perf_counter()
+    res = run_instance(inst, cfg, device=dev)  # public API: upload, run, fetch
+    e2e_ms = 1000.0 * (time.perf_counter() - t0)
+    out = {"workload": name, "batch": batch, "quota": 1000,
+           "device_ms": statistics.median(dev_ms), "e2e_ms": e2e_ms,
+           "unique": res.stats.unique_count}
+    if with_cpu:
+        from paper_2502_08673_b200 import write_dimacs
+        from oracle.oracle import RefInstance, ref_available
+        if ref_available():
+            ri = RefInstance.from_dimacs(write_dimacs(inst.cnf))
+            r = ri.run(batch=batch, iterations=5, seed=1, max_solutions=1000, restart=True,
+                       threads=os.cpu_count() or 1, use_f32=True)
+            out["cpu_reference_s"] = r.wall
+            out["cpu_cores"] = os.cpu_count()
+            out["speedup_e2e"] = r.wall / (e2e_ms / 1000.0)
+    return out
+
+
 def run_reference_arm(args, world, rank):
     name, batch, ref_batch = WORKLOADS[args.workload]
     batch = args.batch or batch
@@ -301,6 +338,9 @@ def run_b200_arm(args, world, rank, local, dist):
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference(name, ref_batch, args.iterations, 1, steps=1)
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    ttk = None
+    if world == 1 and not args.no_ttk:
+        ttk = time_to_1k(dev, with_cpu=not args.no_cpu_baseline)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -317,6 +357,7 @@ def run_b200_arm(args, world, rank, local, dist):
         "gpu_launches": launches,
         "roofline": roofline,
         "cpu_baseline": cpu,
+        "time_to_1k": ttk,
         "e2e": e2e,
         "clocks": clk.summary(),
     }
@@ -333,6 +374,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--iterations", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ttk", action="store_true", help="skip the time-to-1k measurement")
     args = ap.parse_args()
     world, rank, local, dist = dist_setup(args)
     try:

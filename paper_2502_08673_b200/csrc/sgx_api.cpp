@@ -271,7 +271,8 @@ void ensure_table(sgx_sampler* s) {
   uint64_t want = static_cast<uint64_t>(s->table_count + s->Bp) * 2;
   if (want <= s->tcap) return;
   // Geometric growth with a first size covering several restarts.
-  uint64_t ncap = next_pow2(std::max<uint64_t>(std::max<uint64_t>(want * 2, 16ull * s->Bp), 1u << 16));
+  const uint64_t first = s->cfg.max_solutions > 0 ? 0 : 16ull * s->Bp;  // quota runs stay small
+  uint64_t ncap = next_pow2(std::max<uint64_t>(std::max<uint64_t>(want * 2, first), 1u << 16));
   DBuf<unsigned long long> nk, nm;
   nk.alloc_async(ncap, s->st);
   nm.alloc_async(ncap, s->st);
@@ -588,7 +589,6 @@ int sgx_circuit_upload(sgx_ctx* ctx, const sgx_circuit_desc* d, sgx_circuit** ou
       cudaStream_t st = ctx->stream;
       const auto& L = c->L;
       c->cone.upload(L.cone, st);
-      c->full.upload(L.full, st);
       c->bit_ops.upload(to_int4(L.bit_ops), st);
       c->bit_lvl_ptr.upload(L.bit_lvl_ptr, st);
       c->n_bit_levels = static_cast<int>(L.bit_lvl_ptr.size()) - 1;
@@ -671,22 +671,27 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       if (const char* e = std::getenv("SGX_HARVEST")) {
         if (e[0] == 'g') s->hwpc = 0;  // force the global-memory harvest
       }
+      // Stream-ordered pool allocations: a sampler created after another one
+      // reuses its memory without cudaMalloc / cudaFree round trips.
       const size_t Bp = static_cast<size_t>(s->Bp);
-      s->V.alloc(L.cpi.size() * Bp);
-      s->tape.alloc(static_cast<size_t>(L.cone.n_rows) * Bp);
-      s->adj.alloc(static_cast<size_t>(L.cone.n_rows) * Bp);
-      s->row_loss.alloc(Bp);
-      s->partial.alloc(s->n_partial);
-      s->BT.alloc(static_cast<size_t>(L.n_bit_rows) * s->W);
-      s->valid.alloc(s->W);
-      s->newmask.alloc(s->W);
-      s->slot_of_row.alloc(Bp);
-      s->block_count.alloc(Bp / sgx::kThreads);
-      s->K.alloc(static_cast<size_t>(L.key_words) * Bp);
+      cudaStream_t st = s->st;
+      s->V.alloc_async(L.cpi.size() * Bp, st);
+      s->tape.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
+      s->adj.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
+      s->row_loss.alloc_async(Bp, st);
+      s->partial.alloc_async(s->n_partial, st);
+      if (!s->hwpc) s->BT.alloc_async(static_cast<size_t>(L.n_bit_rows) * s->W, st);
+      s->valid.alloc_async(s->W, st);
+      s->newmask.alloc_async(s->W, st);
+      s->slot_of_row.alloc_async(Bp, st);
+      s->block_count.alloc_async(Bp / sgx::kThreads, st);
+      s->K.alloc_async(static_cast<size_t>(L.key_words) * Bp, st);
       // Room for about a restart's worth of solutions (6 harvests of unique
-      // rows) before the first growth.
-      s->store_cap = cfg->solution_capacity > 0 ? cfg->solution_capacity : 6 * static_cast<long long>(Bp);
-      s->store.alloc(static_cast<size_t>(s->store_cap) * L.key_words);
+      // rows) before the first growth; a quota caps it.
+      long long want_rows = 6 * static_cast<long long>(Bp);
+      if (cfg->max_solutions > 0) want_rows = std::min<long long>(want_rows, cfg->max_solutions + Bp);
+      s->store_cap = cfg->solution_capacity > 0 ? cfg->solution_capacity : want_rows;
+      s->store.alloc_async(static_cast<size_t>(s->store_cap) * L.key_words, st);
       CK(cudaMemsetAsync(s->V.p, 0, s->V.n * sizeof(float), s->st));
       ensure_table(s.get());
       CK(cudaStreamSynchronize(s->st));
@@ -699,11 +704,22 @@ int sgx_sampler_free(sgx_sampler* s) {
   return guard([&] {
     if (!s) return;
     cudaSetDevice(s->c->ctx->device);
-    if (s->st) cudaStreamSynchronize(s->st);
+    cudaStream_t st = s->st;
+    if (st) {  // hand the big buffers back to the pool in stream order
+      for (auto* b : {&s->V, &s->tape, &s->adj, &s->row_loss}) b->reset_async(st);
+      s->partial.reset_async(st);
+      for (auto* b : {&s->BT, &s->valid, &s->newmask}) b->reset_async(st);
+      s->slot_of_row.reset_async(st);
+      s->block_count.reset_async(st);
+      s->K.reset_async(st);
+      s->store.reset_async(st);
+      s->tkeys.reset_async(st);
+      s->tmeta.reset_async(st);
+      cudaStreamSynchronize(st);
+    }
     for (auto& e : s->ev)
       if (e) cudaEventDestroy(e);
     if (s->hpin) cudaFreeHost(s->hpin);
-    cudaStream_t st = s->st;
     delete s;
     if (st) cudaStreamDestroy(st);
   });
@@ -896,10 +912,20 @@ int sgx_harvest_commit(sgx_sampler* s, int64_t quota_left, int64_t* attempts, in
 }
 
 // ------------------------------------------------------------------ taps
+// The parity taps run the all-node program, compiled and uploaded on first use.
+static void ensure_full(sgx_circuit* c) {
+  if (c->full.fwd.p) return;
+  sgx::build_full_program(c->L);
+  c->full.upload(c->L.full, c->ctx->stream);
+  CK(cudaStreamSynchronize(c->ctx->stream));
+}
+
 int sgx_forward(sgx_circuit* c, const float* p, int32_t batch, float* tape, float* y) {
   return guard([&] {
     need(c, "circuit");
     if (!c->layout_ok) throw StateError("circuit has no device layout");
+    CK(cudaSetDevice(c->ctx->device));
+    ensure_full(c);
     if (batch < 0) throw std::invalid_argument("batch must be non-negative");
     const auto& L = c->L;
     const size_t ncpi = L.cpi.size();
@@ -950,6 +976,8 @@ int sgx_backward(sgx_circuit* c, const float* tape, int32_t batch, const float* 
   return guard([&] {
     need(c, "circuit");
     if (!c->layout_ok) throw StateError("circuit has no device layout");
+    CK(cudaSetDevice(c->ctx->device));
+    ensure_full(c);
     if (batch < 0) throw std::invalid_argument("batch must be non-negative");
     if (batch == 0) return;
     need(tape, "tape");

@@ -1332,7 +1332,8 @@ void launch_append(cudaStream_t st, const uint32_t* newmask, const int* block_of
 
 template <int WPC>
 static void harvest_smem_t(cudaStream_t st, int grid, size_t smem, const HarvestSmemArgs& a) {
-  static size_t opted = 48 * 1024;  // dynamic bytes this instantiation may use
+  // Opt in whenever static (~10 KB) + dynamic could pass the 48 KB default.
+  static size_t opted = 0;  // dynamic bytes this instantiation may use
   if (smem > opted) {
     cudaFuncSetAttribute(k_harvest_smem<WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     opted = smem;

@@ -373,7 +373,7 @@ Layout build_layout(const sgx_circuit_desc& d) {
     if (oc == 2) cone[L.b[i]] = 1;
   }
   L.cone = build_soft(L, cone);
-  L.full = build_soft(L, all);
+  (void)all;  // the all-node program for the parity taps is built on demand
 
   // Bit program: every node, level-sorted; INPUT rows come from the harden
   // kernel, everything else from bit ops.
@@ -418,6 +418,11 @@ Layout build_layout(const sgx_circuit_desc& d) {
   for (int v = 1; v <= L.num_vars; ++v) L.key_bit_row[v - 1] = L.bit_row_of_node[L.node_of_var[v]];
   build_folded_bits(L);
   return L;
+}
+
+void build_full_program(Layout& L) {
+  if (!L.full.row_of_node.empty() || L.n_nodes == 0) return;
+  L.full = build_soft(L, std::vector<uint8_t>(L.n_nodes, 1));
 }
 
 void layout_info(const Layout& L, int64_t* info) {

@@ -124,4 +124,8 @@ Layout build_layout(const sgx_circuit_desc& d);
 
 void layout_info(const Layout& L, int64_t* info16);
 
+// The all-node soft program of the parity taps (sgx_forward / sgx_backward),
+// built on first use.
+void build_full_program(Layout& L);
+
 }  // namespace sgx
