@@ -231,10 +231,13 @@ def run_b200_arm(args, world, rank, local, dist):
     info = dc.info()
 
     def cfg_for(restarts):
+        # Presize the solution store / table for the run's upper bound (every
+        # harvested row unique), so no growth lands inside the timed region.
+        cap = restarts * (args.iterations + 1) * batch * world
         return SamplerConfig(batch=batch, iterations=args.iterations, seed=1,
                              restart=RestartPolicy.REINIT_ON_EXHAUST if restarts > 1 else
                              RestartPolicy.NONE, max_restarts=max(1, restarts - 1),
-                             row_offset=rank * batch)
+                             row_offset=rank * batch, solution_capacity=cap)
 
     sampler = Sampler(dc, cfg_for(max(1, args.warmup)))
     if args.warmup > 0:

@@ -168,6 +168,7 @@ struct sgx_circuit {
   // folded bit program (shared-memory harvest)
   DBuf<int4> fb_ops;
   DBuf<int> fb_lvl_ptr, fb_cpi_row, fb_ucpi_row, fb_out_enc, fb_clause_enc, fb_key_enc;
+  DBuf<int4> fb_cnf4;
   int fb_levels = 0;
 };
 
@@ -271,7 +272,9 @@ void ensure_table(sgx_sampler* s) {
   uint64_t want = static_cast<uint64_t>(s->table_count + s->Bp) * 2;
   if (want <= s->tcap) return;
   // Geometric growth with a first size covering several restarts.
-  const uint64_t first = s->cfg.max_solutions > 0 ? 0 : 16ull * s->Bp;  // quota runs stay small
+  // quota runs stay small; a declared solution capacity presizes the table
+  uint64_t first = s->cfg.max_solutions > 0 ? 0 : 16ull * s->Bp;
+  if (s->cfg.solution_capacity > 0) first = std::max<uint64_t>(first, 4ull * s->cfg.solution_capacity);
   uint64_t ncap = next_pow2(std::max<uint64_t>(std::max<uint64_t>(want * 2, first), 1u << 16));
   DBuf<unsigned long long> nk, nm;
   nk.alloc_async(ncap, s->st);
@@ -337,9 +340,8 @@ void harvest_front(sgx_sampler* s, int restart, int iter, long long quota_left) 
     a.out_enc = c->fb_out_enc.p;
     a.out_tgt = c->out_tgt.p;
     a.n_out = static_cast<int>(L.out_node.size());
-    a.clause_ptr = c->clause_ptr.p;
-    a.clause_enc = c->fb_clause_enc.p;
-    a.n_clauses = static_cast<int>(L.clause_ptr.size()) - 1;
+    a.cnf4 = c->fb_cnf4.p;
+    a.cnf_steps = L.fb_cnf_steps;
     a.key_enc = c->fb_key_enc.p;
     a.key_words = L.key_words;
     a.batch = s->cfg.batch;
@@ -607,6 +609,7 @@ int sgx_circuit_upload(sgx_ctx* ctx, const sgx_circuit_desc* d, sgx_circuit** ou
       c->fb_out_enc.upload(L.fb_out_enc, st);
       c->fb_clause_enc.upload(L.fb_clause_enc, st);
       c->fb_key_enc.upload(L.fb_key_enc, st);
+      c->fb_cnf4.upload(to_int4(L.fb_cnf4), st);
       CK(cudaStreamSynchronize(st));
     }
     *out = c.release();
@@ -662,7 +665,9 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       // one word (up to 200 KB) for deep circuits; else the global path.
       const size_t row_bytes = static_cast<size_t>(L.fb_rows) * sizeof(uint32_t);
       s->hwpc = 0;
-      for (int w = 32; w >= 1; w /= 2)
+      // (<= 8 words: the CNF check keeps one accumulator pair per word in
+      // registers)
+      for (int w = 8; w >= 1; w /= 2)
         if (row_bytes * w <= 100 * 1024 && s->W / w >= 2 * 148) {
           s->hwpc = w;
           break;

@@ -856,7 +856,7 @@ k_harvest_smem(const float* __restrict__ V, int ncpi, int nucpi, const int* __re
                const int* __restrict__ ucpi_row, int tile_rows, uint64_t free_prefix, long long row_offset,
                const int4* __restrict__ ops, const int* __restrict__ lvl_ptr, int n_levels,
                const int* __restrict__ out_enc, const uint8_t* __restrict__ out_tgt, int n_out,
-               const int* __restrict__ clause_ptr, const int* __restrict__ clause_enc, int n_clauses,
+               const int4* __restrict__ cnf4, int cnf_steps,
                const int* __restrict__ key_enc, int key_words, int batch, int Bp,
                uint32_t* __restrict__ valid_out, uint64_t* __restrict__ K, int* __restrict__ slot_of_row,
                unsigned long long* tkeys, unsigned long long* tmeta, uint64_t tmask, uint64_t epoch) {
@@ -912,39 +912,58 @@ k_harvest_smem(const float* __restrict__ V, int ncpi, int nucpi, const int* __re
     }
     __syncthreads();
   }
-  // PO check (sampler.cpp:140-146) + eval_cnf (cnf.cpp:136-145)
+  // PO check (sampler.cpp:140-146) + eval_cnf (cnf.cpp:136-145).  Each
+  // thread owns whole clauses as int4 literal records stored transposed, so a
+  // step's reads are coalesced; every record serves all WPC words.
   {
-    constexpr int S = kThreads / WPC;
-    const int wl = threadIdx.x % WPC, slot = threadIdx.x / WPC;
-    uint32_t ok = kFull;
-    for (int m = slot; m < n_out; m += S) {
-      const int e = __ldg(out_enc + m);
-      const uint32_t x = bits[(e >> 1) * WPC + wl] ^ neg_mask(e);
-      ok &= __ldg(out_tgt + m) ? x : ~x;
+    uint32_t ok[WPC], any[WPC];
+#pragma unroll
+    for (int wl = 0; wl < WPC; ++wl) {
+      ok[wl] = kFull;
+      any[wl] = 0u;
     }
-    const int c0 = static_cast<int>(static_cast<long long>(n_clauses) * slot / S);
-    const int c1 = static_cast<int>(static_cast<long long>(n_clauses) * (slot + 1) / S);
-    const int l1 = __ldg(clause_ptr + c1);
-    uint32_t any = 0u;
-#pragma unroll 8
-    for (int l = __ldg(clause_ptr + c0); l < l1; ++l) {
-      const int e = __ldg(clause_enc + l);
-      const uint32_t x = bits[(e >> 2) * WPC + wl];
-      any |= (e & 1) ? ~x : x;
-      if (e & 2) {
-        ok &= any;
-        any = 0u;
+    for (int m = threadIdx.x; m < n_out; m += kThreads) {
+      const int e = __ldg(out_enc + m);
+      const uint32_t t = __ldg(out_tgt + m) ? 0u : kFull;
+#pragma unroll
+      for (int wl = 0; wl < WPC; ++wl) ok[wl] &= bits[(e >> 1) * WPC + wl] ^ neg_mask(e) ^ t;
+    }
+    for (int j = 0; j < cnf_steps; ++j) {
+      const int4 rec = __ldg(cnf4 + static_cast<size_t>(j) * kThreads + threadIdx.x);
+      const int lit[4] = {rec.x, rec.y, rec.z, rec.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = lit[u];
+        if (e < 0) continue;
+#pragma unroll
+        for (int wl = 0; wl < WPC; ++wl) {
+          const uint32_t x = bits[(e >> 2) * WPC + wl];
+          any[wl] |= (e & 1) ? ~x : x;
+        }
+        if (e & 2) {
+#pragma unroll
+          for (int wl = 0; wl < WPC; ++wl) {
+            ok[wl] &= any[wl];
+            any[wl] = 0u;
+          }
+        }
       }
     }
-    red[threadIdx.x] = ok;
+#pragma unroll
+    for (int wl = 0; wl < WPC; ++wl) {
+      const uint32_t v = __reduce_and_sync(kFull, ok[wl]);
+      if (lane == 0) red[warp * WPC + wl] = v;
+    }
     __syncthreads();
-    if (slot == 0) {
-#pragma unroll 4
-      for (int j = 1; j < S; ++j) ok &= red[j * WPC + wl];
+    if (threadIdx.x < WPC) {
+      const int wl = threadIdx.x;
+      uint32_t v = kFull;
+#pragma unroll
+      for (int j = 0; j < NW; ++j) v &= red[j * WPC + wl];
       const int r0 = (w0 + wl) * 32;
       const uint32_t mask = r0 + 32 <= batch ? kFull : (r0 >= batch ? 0u : ((1u << (batch - r0)) - 1u));
-      vw[wl] = ok & mask;
-      valid_out[w0 + wl] = ok & mask;
+      vw[wl] = v & mask;
+      valid_out[w0 + wl] = v & mask;
     }
     __syncthreads();
   }
@@ -1340,7 +1359,7 @@ static void harvest_smem_t(cudaStream_t st, int grid, size_t smem, const Harvest
   }
   k_harvest_smem<WPC><<<grid, kThreads, smem, st>>>(
       a.V, a.ncpi, a.nucpi, a.cpi_row, a.ucpi_row, a.tile_rows, a.free_prefix, a.row_offset, a.ops, a.lvl_ptr,
-      a.n_levels, a.out_enc, a.out_tgt, a.n_out, a.clause_ptr, a.clause_enc, a.n_clauses, a.key_enc, a.key_words,
+      a.n_levels, a.out_enc, a.out_tgt, a.n_out, a.cnf4, a.cnf_steps, a.key_enc, a.key_words,
       a.batch, a.Bp, a.valid, a.K, a.slot_of_row, a.tkeys, a.tmeta, a.tmask, a.epoch);
 }
 

@@ -49,8 +49,8 @@ struct HarvestSmemArgs {
   const int* out_enc;
   const uint8_t* out_tgt;
   int n_out;
-  const int *clause_ptr, *clause_enc;
-  int n_clauses;
+  const int4* cnf4;
+  int cnf_steps;
   const int* key_enc;
   int key_words, batch, Bp;
   uint32_t* valid;

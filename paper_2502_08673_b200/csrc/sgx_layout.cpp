@@ -269,6 +269,37 @@ void build_folded_bits(Layout& L) {
     }
   L.fb_key_enc.assign(static_cast<size_t>(L.key_words) * 64, -1);
   for (int v = 1; v <= L.num_vars; ++v) L.fb_key_enc[v - 1] = enc(L.node_of_var[v]);
+
+  // CNF records: each clause as ceil(len/4) int4 records (the last literal
+  // carries the clause-end flag); whole clauses dealt to kCnfThreads threads,
+  // longest-first to the least loaded, then padded and transposed.
+  const int64_t n_clauses = static_cast<int64_t>(L.clause_ptr.size()) - 1;
+  std::vector<std::vector<I4>> recs(n_clauses);
+  for (int64_t c = 0; c < n_clauses; ++c) {
+    std::vector<int32_t> lits(L.fb_clause_enc.begin() + L.clause_ptr[c],
+                              L.fb_clause_enc.begin() + L.clause_ptr[c + 1]);
+    while (lits.size() % 4) lits.push_back(-1);
+    for (size_t k = 0; k < lits.size(); k += 4) recs[c].push_back({lits[k], lits[k + 1], lits[k + 2], lits[k + 3]});
+  }
+  std::vector<int64_t> order(n_clauses);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int64_t x, int64_t y) { return recs[x].size() > recs[y].size(); });
+  std::vector<std::vector<I4>> per(kCnfThreads);
+  std::vector<size_t> load(kCnfThreads, 0);
+  for (int64_t c : order) {
+    int best = 0;
+    for (int t = 1; t < kCnfThreads; ++t)
+      if (load[t] < load[best]) best = t;
+    per[best].insert(per[best].end(), recs[c].begin(), recs[c].end());
+    load[best] += recs[c].size();
+  }
+  size_t steps = 0;
+  for (const auto& p : per) steps = std::max(steps, p.size());
+  L.fb_cnf_steps = static_cast<int32_t>(steps);
+  L.fb_cnf4.assign(steps * kCnfThreads, I4{-1, -1, -1, -1});
+  for (int t = 0; t < kCnfThreads; ++t)
+    for (size_t j = 0; j < per[t].size(); ++j) L.fb_cnf4[j * kCnfThreads + t] = per[t][j];
 }
 
 }  // namespace

@@ -53,6 +53,7 @@ constexpr int kWarps = SGX_WARPS;  // warps per CTA sharing one sample tile (nod
 enum OpCode : int32_t { kNop = 15, kBegin = 16, kEdge = 17, kEnd = 18, kSubBegin = 19, kSubEnd = 20 };
 constexpr int32_t kSeedBit = 1 << 8, kTargetBit = 1 << 9, kNegOtherBit = 1 << 10,
                   kNegSelfBit = 1 << 11, kKindShift = 12, kInSubBit = 1 << 16;
+constexpr int kCnfThreads = 256;               // threads of the shared-memory harvest CTA
 constexpr int kGroup = 4;                      // ops per forward group
 constexpr int kGroupRecs = 1 + kGroup / 2;     // int4 records per group
 
@@ -115,6 +116,11 @@ struct Layout {
   std::vector<int32_t> fb_out_enc;
   std::vector<int32_t> fb_clause_enc;
   std::vector<int32_t> fb_key_enc;   // key_words * 64, -1 = padding
+  // CNF as int4 records of up to 4 literals (-1 = none), clauses kept whole
+  // per thread and stored transposed [step][kCnfThreads] so that at every
+  // step the CTA's threads read consecutive records.
+  int32_t fb_cnf_steps = 0;
+  std::vector<I4> fb_cnf4;
 
   int64_t n_lits() const { return static_cast<int64_t>(clause_lit.size()); }
 };
