@@ -233,7 +233,9 @@ def run_b200_arm(args, world, rank, local, dist):
     def cfg_for(restarts):
         # Presize the solution store / table for the run's upper bound (every
         # harvested row unique), so no growth lands inside the timed region.
-        cap = restarts * (args.iterations + 1) * batch * world
+        # (sized from the timed run for the warm-up too, so the timed sampler
+        # reuses the warm-up's pool memory instead of mapping fresh pages).
+        cap = max(1, args.steps) * (args.iterations + 1) * batch * world
         return SamplerConfig(batch=batch, iterations=args.iterations, seed=1,
                              restart=RestartPolicy.REINIT_ON_EXHAUST if restarts > 1 else
                              RestartPolicy.NONE, max_restarts=max(1, restarts - 1),
@@ -282,6 +284,7 @@ def run_b200_arm(args, world, rank, local, dist):
     # e2e through the public API from host buffers: circuit + CNF upload
     # (H2D), the run, every solution key fetched to host memory (D2H).
     e2e_cfg = cfg_for(args.steps)
+    e2e_cfg.solution_capacity = 0  # library defaults, as a user calling run() gets them
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)

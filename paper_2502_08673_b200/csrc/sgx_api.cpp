@@ -274,7 +274,7 @@ void ensure_table(sgx_sampler* s) {
   // Geometric growth with a first size covering several restarts.
   // quota runs stay small; a declared solution capacity presizes the table
   uint64_t first = s->cfg.max_solutions > 0 ? 0 : 16ull * s->Bp;
-  if (s->cfg.solution_capacity > 0) first = std::max<uint64_t>(first, 4ull * s->cfg.solution_capacity);
+  if (s->cfg.solution_capacity > 0) first = std::max<uint64_t>(first, 2ull * s->cfg.solution_capacity);
   uint64_t ncap = next_pow2(std::max<uint64_t>(std::max<uint64_t>(want * 2, first), 1u << 16));
   DBuf<unsigned long long> nk, nm;
   nk.alloc_async(ncap, s->st);
