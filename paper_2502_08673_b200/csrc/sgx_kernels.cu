@@ -188,6 +188,30 @@ k_forward(const int4* __restrict__ grp, const int2* __restrict__ lvl, int n_leve
   }
 }
 
+// END of a V column: dV = g p (1 - p) with p recomputed from V
+// (autodiff.cpp:212-221), then V -= lr dV (gd_step, :285-290) -- or, for the
+// parity tap, dV and dP out.  (Measured: an out-of-line version forces the
+// ABI to keep the caller's live state in local memory and ran the C2
+// backward 2.6x slower, so it stays inline.)
+template <int V>
+__device__ __forceinline__ void input_end(const float (&x)[V], const float (&acc)[V], float lr,
+                                          const uint64_t* __restrict__ exp_tab, size_t at, float* Vp,
+                                          float* dv_out, float* dp_out) {
+  float dv[V], nv[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const float p = sigmoid_ref(x[v], exp_tab);
+    dv[v] = __fmul_rn(__fmul_rn(acc[v], p), __fsub_rn(1.0f, p));
+    nv[v] = __fsub_rn(x[v], __fmul_rn(lr, dv[v]));
+  }
+  if (dv_out) {
+    vstore<V>(dv_out + at, dv);
+    vstore<V>(dp_out + at, acc);
+  } else {
+    vstore<V>(Vp + at, nv);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K3+K4: per-row loss, pull-style backward and the fused GD step.  Same tile
 // and level split as the forward, levels high to low.  Each warp runs its
@@ -291,22 +315,9 @@ k_backward(const int4* __restrict__ ops, const int2* __restrict__ lvl, int n_lev
           for (int v = 0; v < V; ++v) acc[v] = is_not ? __fsub_rn(acc[v], acc2[v]) : __fadd_rn(acc[v], acc2[v]);
         } else if (code == kEnd) {
           if (op[k].y >= 0) vstore<V>(A + static_cast<size_t>(op[k].y) * TILE, acc);
-          if (op[k].z >= 0) {  // autodiff.cpp:212-221 then gd_step :285-290
-            float dv[V], nv[V];
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-              const float p = sigmoid_ref(x[k][v], exp_tab);
-              dv[v] = __fmul_rn(__fmul_rn(acc[v], p), __fsub_rn(1.0f, p));
-              nv[v] = __fsub_rn(x[k][v], __fmul_rn(lr, dv[v]));
-            }
-            const size_t at = vbase + static_cast<size_t>(op[k].z) * TILE;
-            if (dv_out) {
-              vstore<V>(dv_out + at, dv);
-              vstore<V>(dp_out + at, acc);
-            } else {
-              vstore<V>(Vp + at, nv);
-            }
-          }
+          if (op[k].z >= 0)  // autodiff.cpp:212-221 then gd_step :285-290 (rare: out of line)
+            input_end<V>(x[k], acc, lr, exp_tab, vbase + static_cast<size_t>(op[k].z) * TILE, Vp, dv_out,
+                         dp_out);
         }
       }
     }
@@ -334,6 +345,13 @@ constexpr int kStages = SGX_STAGES;      // groups / chunks in flight per warp
 constexpr int kSlots = 2 * kGroup;       // staged rows per stage (= 2 * kAsyncU)
 constexpr int kAsyncU = 4;               // backward micro-ops per chunk
 constexpr int kAsyncSmem = kWarps * kStages * kSlots * 32 * 16;  // bytes per CTA
+#ifndef SGX_ABWD_U
+#define SGX_ABWD_U 4
+#endif
+#ifndef SGX_ABWD_STAGES
+#define SGX_ABWD_STAGES 3
+#endif
+constexpr int kAsyncSmemBwd = kWarps * SGX_ABWD_STAGES * 2 * SGX_ABWD_U * 32 * 16;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -490,7 +508,8 @@ k_backward_async(const int4* __restrict__ ops, const int2* __restrict__ lvl, int
                  float* dp_out, float lr, const int* __restrict__ out_enc,
                  const uint8_t* __restrict__ out_tgt, int n_out, float* __restrict__ row_loss,
                  const uint64_t* __restrict__ exp_tab) {
-  constexpr int TILE = 128, U = kAsyncU;
+  constexpr int TILE = 128, U = SGX_ABWD_U;
+  constexpr int kStages = SGX_ABWD_STAGES, kSlots = 2 * SGX_ABWD_U;  // shadow the forward's
   extern __shared__ float4 stage_mem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t tbase = static_cast<size_t>(blockIdx.x) * n_rows * TILE + lane * 4;
@@ -1268,10 +1287,10 @@ void launch_backward(cudaStream_t st, int vec, const int4* ops, const int2* lvl,
   if (vec == 4 && async_enabled_bwd()) {
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_backward_async, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsyncSmem);
+      cudaFuncSetAttribute(k_backward_async, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsyncSmemBwd);
       attr = true;
     }
-    k_backward_async<<<tiles, 32 * kWarps, kAsyncSmem, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows,
+    k_backward_async<<<tiles, 32 * kWarps, kAsyncSmemBwd, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows,
                                                             dv_out, dp_out, lr, out_enc, out_tgt, n_out,
                                                             row_loss, exp_tab);
     return;
