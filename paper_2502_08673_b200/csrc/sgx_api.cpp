@@ -132,21 +132,45 @@ std::vector<int2> to_int2(const std::vector<int32_t>& v) {
 }
 
 struct DevSoft {
-  DBuf<int4> fwd, bwd;
-  DBuf<int2> fwd_lvl, bwd_lvl;
-  DBuf<int> out_enc;
+  DBuf<int4> fwd, bwd, rec;
+  DBuf<int2> fwd_lvl, bwd_lvl, rec_lvl;
+  DBuf<int> out_enc, col_row;
   int n_fwd_levels = 0, n_bwd_levels = 0, n_rows = 0;
   void upload(const sgx::SoftProgram& P, cudaStream_t st) {
     fwd.upload(to_int4(P.fwd), st);
     bwd.upload(to_int4(P.bwd), st);
+    rec.upload(to_int4(P.rec), st);
     fwd_lvl.upload(to_int2(P.fwd_lvl), st);
     bwd_lvl.upload(to_int2(P.bwd_lvl), st);
+    rec_lvl.upload(to_int2(P.rec_lvl), st);
     out_enc.upload(P.out_enc, st);
+    col_row.upload(P.col_row, st);
     n_fwd_levels = static_cast<int>(P.fwd_lvl.size() / (2 * sgx::kWarps));
     n_bwd_levels = static_cast<int>(P.bwd_lvl.size() / (2 * sgx::kWarps));
     n_rows = P.n_rows;
   }
 };
+
+// Backward form: edge records (default) or the micro-op interpreter
+// (SGX_BWD=ops, kept for A/B measurement).
+bool bwd_records() {
+  static const bool r = [] {
+    const char* e = std::getenv("SGX_BWD");
+    return !(e && std::string(e) == "ops");
+  }();
+  return r;
+}
+
+void backward(cudaStream_t st, int vec, const DevSoft& P, const float* tape, float* adj, float* V, int ncols,
+              float* dv_out, float* dp_out, int Bp, float lr, const uint8_t* out_tgt, int n_out, float* row_loss,
+              const uint64_t* tab) {
+  if (bwd_records())
+    sgx::launch_backward_rec(st, vec, P.rec.p, P.rec_lvl.p, P.n_bwd_levels, tape, adj, V, ncols, P.n_rows,
+                             P.col_row.p, dv_out, dp_out, Bp, lr, P.out_enc.p, out_tgt, n_out, row_loss, tab);
+  else
+    sgx::launch_backward(st, vec, P.bwd.p, P.bwd_lvl.p, P.n_bwd_levels, tape, adj, V, ncols, P.n_rows, dv_out,
+                         dp_out, Bp, lr, P.out_enc.p, out_tgt, n_out, row_loss, tab);
+}
 
 }  // namespace
 
@@ -257,10 +281,9 @@ void sampler_step(sgx_sampler* s) {
   sgx::launch_forward(s->st, s->vec, c->cone.fwd.p, c->cone.fwd_lvl.p, c->cone.n_fwd_levels, s->V.p, ncpi,
                       s->tape.p, c->cone.n_rows, s->Bp, 0, tab);
   CK(cudaEventRecord(s->ev[1], s->st));
-  sgx::launch_backward(s->st, s->vec, c->cone.bwd.p, c->cone.bwd_lvl.p, c->cone.n_bwd_levels, s->tape.p, s->adj.p,
-                       s->V.p, ncpi, c->cone.n_rows, nullptr, nullptr, s->Bp,
-                       static_cast<float>(s->cfg.learning_rate), c->cone.out_enc.p,
-                       c->out_tgt.p, static_cast<int>(c->L.out_node.size()), s->row_loss.p, tab);
+  backward(s->st, s->vec, c->cone, s->tape.p, s->adj.p, s->V.p, ncpi, nullptr, nullptr, s->Bp,
+           static_cast<float>(s->cfg.learning_rate), c->out_tgt.p, static_cast<int>(c->L.out_node.size()),
+           s->row_loss.p, tab);
   sgx::launch_loss(s->st, s->row_loss.p, s->cfg.batch, s->partial.p, s->n_partial, s->hout.p);
   s->launches += 4;
   CK(cudaEventRecord(s->ev[2], s->st));
@@ -1012,9 +1035,8 @@ int sgx_backward(sgx_circuit* c, const float* tape, int32_t batch, const float* 
     ddp.alloc(std::max<size_t>(ncpi * Bp, 1));
     CK(cudaMemsetAsync(ddv.p, 0, ddv.n * sizeof(float), st));
     CK(cudaMemsetAsync(ddp.p, 0, ddp.n * sizeof(float), st));
-    sgx::launch_backward(st, kTapVec, c->full.bwd.p, c->full.bwd_lvl.p, c->full.n_bwd_levels, dt.p, dadj.p, dV.p,
-                         static_cast<int>(ncpi), L.full.n_rows, ddv.p, ddp.p, Bp, 0.0f, c->full.out_enc.p,
-                         c->out_tgt.p, static_cast<int>(L.out_node.size()), nullptr, c->ctx->exp_tab.p);
+    backward(st, kTapVec, c->full, dt.p, dadj.p, dV.p, static_cast<int>(ncpi), ddv.p, ddp.p, Bp, 0.0f,
+             c->out_tgt.p, static_cast<int>(L.out_node.size()), nullptr, c->ctx->exp_tab.p);
     CK(cudaGetLastError());
     std::vector<float> hdv(ddv.n), hdp(ddp.n);
     CK(cudaMemcpyAsync(hdv.data(), ddv.p, hdv.size() * sizeof(float), cudaMemcpyDeviceToHost, st));

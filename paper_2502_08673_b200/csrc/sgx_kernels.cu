@@ -228,13 +228,15 @@ k_backward(const int4* __restrict__ ops, const int2* __restrict__ lvl, int n_lev
            const float* tape, float* adj, float* Vp, int ncols, int n_rows, float* dv_out,
            float* dp_out, float lr, const int* __restrict__ out_enc,
            const uint8_t* __restrict__ out_tgt, int n_out, float* __restrict__ row_loss,
-           const uint64_t* __restrict__ exp_tab) {
+           const uint64_t* __restrict__ exp_tab, int n_tiles) {
   constexpr int TILE = 32 * V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t tbase = static_cast<size_t>(blockIdx.x) * n_rows * TILE + lane * V;
+  // Persistent over tiles when the grid is smaller than the tile count.
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  const size_t tbase = static_cast<size_t>(tile) * n_rows * TILE + lane * V;
   const float* T = tape + tbase;
   float* A = adj + tbase;
-  const size_t vbase = static_cast<size_t>(blockIdx.x) * ncols * TILE + lane * V;
+  const size_t vbase = static_cast<size_t>(tile) * ncols * TILE + lane * V;
   if (row_loss && warp == 0) {  // loss (autodiff.cpp:160-166): outputs in order
     float l[V];
 #pragma unroll
@@ -249,7 +251,7 @@ k_backward(const int4* __restrict__ ops, const int2* __restrict__ lvl, int n_lev
         l[v] = __fadd_rn(l[v], __fmul_rn(d, d));
       }
     }
-    vstore<V>(row_loss + static_cast<size_t>(blockIdx.x) * TILE + lane * V, l);
+    vstore<V>(row_loss + static_cast<size_t>(tile) * TILE + lane * V, l);
   }
   float acc[V], acc2[V];
 #pragma unroll
@@ -315,13 +317,174 @@ k_backward(const int4* __restrict__ ops, const int2* __restrict__ lvl, int n_lev
           for (int v = 0; v < V; ++v) acc[v] = is_not ? __fsub_rn(acc[v], acc2[v]) : __fadd_rn(acc[v], acc2[v]);
         } else if (code == kEnd) {
           if (op[k].y >= 0) vstore<V>(A + static_cast<size_t>(op[k].y) * TILE, acc);
-          if (op[k].z >= 0)  // autodiff.cpp:212-221 then gd_step :285-290 (rare: out of line)
+          if (op[k].z >= 0)  // autodiff.cpp:212-221 then gd_step :285-290
             input_end<V>(x[k], acc, lr, exp_tab, vbase + static_cast<size_t>(op[k].z) * TILE, Vp, dv_out,
                          dp_out);
         }
       }
     }
     __syncthreads();
+  }
+  }  // tile loop
+}
+
+// Edge-record decode tables (sgx_layout.hpp kR* flags).  kRecC[ck | in_sub<<4]
+// = {c0a, c1a, c0b, c1b}: the pull factor c0 + c1*vo routed to acc (a) or to
+// the SUB accumulator acc2 (b), zero on the other side.  kRecS[neg_other |
+// first<<1 | sub_first<<2] = {ns, no, k, k2}: vo = ns*y + no, acc keeps factor
+// k, acc2 keeps k2.  kRecE[sub_last | sub_not<<1]: acc += e * acc2.
+__constant__ float4 kRecC[32] = {
+    {0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f},  {0.0f, 0.0f, 0.0f, 0.0f},  {1.0f, 0.0f, 0.0f, 0.0f},
+    {-1.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 1.0f, 0.0f, 0.0f}, {1.0f, -1.0f, 0.0f, 0.0f}, {1.0f, -2.0f, 0.0f, 0.0f},
+    {-1.0f, 2.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f},  {0.0f, 0.0f, 0.0f, 0.0f},
+    {0.0f, 0.0f, 0.0f, 0.0f},  {0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f},  {0.0f, 0.0f, 0.0f, 0.0f},
+    {0.0f, 0.0f, 0.0f, 0.0f},  {0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f},  {0.0f, 0.0f, 1.0f, 0.0f},
+    {0.0f, 0.0f, -1.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 1.0f}, {0.0f, 0.0f, 1.0f, -1.0f}, {0.0f, 0.0f, 1.0f, -2.0f},
+    {0.0f, 0.0f, -1.0f, 2.0f}, {0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f},  {0.0f, 0.0f, 0.0f, 0.0f},
+    {0.0f, 0.0f, 0.0f, 0.0f},  {0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f},  {0.0f, 0.0f, 0.0f, 0.0f}};
+__constant__ float4 kRecS[8] = {{1.0f, 0.0f, 1.0f, 1.0f},  {-1.0f, 1.0f, 1.0f, 1.0f}, {1.0f, 0.0f, 0.0f, 1.0f},
+                                {-1.0f, 1.0f, 0.0f, 1.0f}, {1.0f, 0.0f, 1.0f, 0.0f},  {-1.0f, 1.0f, 1.0f, 0.0f},
+                                {1.0f, 0.0f, 0.0f, 0.0f},  {-1.0f, 1.0f, 0.0f, 0.0f}};
+__constant__ float kRecE[4] = {0.0f, 1.0f, 0.0f, -1.0f};
+
+template <int V>
+__device__ __forceinline__ void vload_nc(const float* p, float (&o)[V]) {
+  if constexpr (V == 4) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+    o[0] = t.x;
+    o[1] = t.y;
+    o[2] = t.z;
+    o[3] = t.w;
+  } else {
+    vload<V>(p, o);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3+K4, edge-record form: the same pull-CSR backward as k_backward, but the
+// micro-op control (BEGIN / SUB_BEGIN / SUB_END / END) rides as flag bits on
+// the edges, so every record runs the same branch-free arithmetic:
+//   acc  = acc  * k  + seed        (k = 0 on a node's first record)
+//   acc2 = acc2 * k2 + seed2       (k2 = 0 on a SUB run's first record)
+//   vo = ns * T[other] + no;  acc += g * (c0a + c1a vo);  acc2 += g * (c0b + c1b vo)
+//   acc += e * acc2                (e = -1 / +1 on a SUB run's last record)
+// Bit-exactness: the c's, k's, ns/no and e are in {0, +-1, +-2}, so every
+// product with them is exact and each fma rounds once, exactly like the
+// reference's add / sub; adding a (signed) zero is the identity because an
+// accumulator is never -0 (it starts at +0 and RN sums only give -0 from
+// -0 + -0).  Seeds (output nodes, autodiff.cpp:206) take a rare uniform
+// branch.  Column-input adjoints are stored like any other and the V update
+// (dV = g p (1 - p), V -= lr dV) runs as an epilogue over the tile's columns.
+// ---------------------------------------------------------------------------
+#ifndef SGX_REC_UC
+#define SGX_REC_UC 2
+#endif
+#ifndef SGX_REC_U
+#define SGX_REC_U 4  // records per chunk at 4 samples per lane (C2 backward: 4 -> 40.7, 6 -> 41.9, 8 -> 46.2 ms per 5 restarts)
+#endif
+template <int V, int U>
+__global__ void __launch_bounds__(32 * kWarps, 4)
+k_backward_rec(const int4* __restrict__ rec, const int2* __restrict__ lvl, int n_levels,
+               const float* __restrict__ tape, float* adj, float* Vp, int ncols, int n_rows,
+               const int* __restrict__ col_row, float* dv_out, float* dp_out, float lr,
+               const int* __restrict__ out_enc, const uint8_t* __restrict__ out_tgt, int n_out,
+               float* __restrict__ row_loss, const uint64_t* __restrict__ exp_tab, int n_tiles) {
+  constexpr int TILE = 32 * V;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const size_t tbase = static_cast<size_t>(tile) * n_rows * TILE + lane * V;
+    const float* T = tape + tbase;
+    float* A = adj + tbase;
+    const size_t vbase = static_cast<size_t>(tile) * ncols * TILE + lane * V;
+    if (row_loss && warp == 0) {  // loss (autodiff.cpp:160-166): outputs in order
+      float l[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) l[v] = 0.0f;
+      for (int m = 0; m < n_out; ++m) {
+        float yv[V];
+        load_operand<V>(T, __ldg(out_enc + m), yv);
+        const float t = __ldg(out_tgt + m) ? 1.0f : 0.0f;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const float d = __fsub_rn(yv[v], t);
+          l[v] = __fadd_rn(l[v], __fmul_rn(d, d));
+        }
+      }
+      vstore<V>(row_loss + static_cast<size_t>(tile) * TILE + lane * V, l);
+    }
+    float acc[V], acc2[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = acc2[v] = 0.0f;
+    for (int li = 0; li < n_levels; ++li) {
+      const int2 L = __ldg(lvl + li * kWarps + warp);
+      for (int c = 0; c < L.y; c += U) {
+        int4 r[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) r[k] = c + k < L.y ? __ldg(rec + L.x + c + k) : make_int4(0, -1, -1, 0);
+        float g[U][V], y[U][V];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) g[k][v] = y[k][v] = 0.0f;
+          if (r[k].y >= 0) vload<V>(A + static_cast<size_t>(r[k].y) * TILE, g[k]);
+          if (r[k].z >= 0) vload_nc<V>(T + static_cast<size_t>(r[k].z) * TILE, y[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int f = r[k].x;
+          const float4 C = kRecC[f & 0x1f];
+          const float4 S = kRecS[(f >> 5) & 0x7];
+          const float e = kRecE[(f >> 8) & 0x3];
+          float sd[V], sd2[V];
+#pragma unroll
+          for (int v = 0; v < V; ++v) sd[v] = sd2[v] = 0.0f;
+          if (f & (kRSeed | kRSubSeed)) {  // adj[out] += 2 (y - t) on a zero adjoint (autodiff.cpp:206)
+            float yw[V];
+            vload_nc<V>(T + static_cast<size_t>(r[k].w) * TILE, yw);
+            const float t = (f & kRTarget) ? 1.0f : 0.0f, t2 = (f & kRSubTarget) ? 1.0f : 0.0f;
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              if (f & kRSeed) sd[v] = __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(yw[v], t)));
+              if (f & kRSubSeed) {
+                const float ys = (f & kRNegSelf) ? __fsub_rn(1.0f, yw[v]) : yw[v];
+                sd2[v] = __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(ys, t2)));
+              }
+            }
+          }
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            acc[v] = __fmaf_rn(acc[v], S.z, sd[v]);
+            acc2[v] = __fmaf_rn(acc2[v], S.w, sd2[v]);
+            const float vo = __fmaf_rn(S.x, y[k][v], S.y);
+            const float fa = __fmaf_rn(C.y, vo, C.x), fb = __fmaf_rn(C.w, vo, C.z);
+            acc[v] = __fadd_rn(acc[v], __fmul_rn(g[k][v], fa));
+            acc2[v] = __fadd_rn(acc2[v], __fmul_rn(g[k][v], fb));
+            acc[v] = __fmaf_rn(e, acc2[v], acc[v]);
+          }
+          if (f & kRLast) vstore<V>(A + static_cast<size_t>(r[k].w) * TILE, acc);
+        }
+      }
+      __syncthreads();
+    }
+    // V columns: dV = g p (1 - p) (autodiff.cpp:212-221), V -= lr dV (gd_step, :285-290).
+    constexpr int UC = SGX_REC_UC;
+    for (int j0 = warp * UC; j0 < ncols; j0 += kWarps * UC) {
+      int rw[UC];
+      float x[UC][V], gg[UC][V];
+#pragma unroll
+      for (int q = 0; q < UC; ++q) {
+        rw[q] = j0 + q < ncols ? __ldg(col_row + j0 + q) : -1;
+        if (rw[q] >= 0) {
+          vload<V>(A + static_cast<size_t>(rw[q]) * TILE, gg[q]);
+          vload<V>(Vp + vbase + static_cast<size_t>(j0 + q) * TILE, x[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < UC; ++q)
+        if (rw[q] >= 0)
+          input_end<V>(x[q], gg[q], lr, exp_tab, vbase + static_cast<size_t>(j0 + q) * TILE, Vp, dv_out, dp_out);
+    }
+    if (n_tiles > static_cast<int>(gridDim.x)) __syncthreads();
   }
 }
 
@@ -418,12 +581,12 @@ __device__ __forceinline__ void group_unary(const float4* base, const int (&opd)
 __global__ void __launch_bounds__(32 * kWarps)
 k_forward_async(const int4* __restrict__ grp, const int2* __restrict__ lvl, int n_levels,
                 const float* __restrict__ src, int ncols, float* tape, int n_rows, int src_is_prob,
-                const uint64_t* __restrict__ exp_tab) {
+                const uint64_t* __restrict__ exp_tab, int n_tiles) {
   constexpr int TILE = 128;
   extern __shared__ float4 stage_mem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* T = tape + static_cast<size_t>(blockIdx.x) * n_rows * TILE + lane * 4;
-  const float* S = src + static_cast<size_t>(blockIdx.x) * ncols * TILE + lane * 4;
+  float* T = nullptr;        // this tile's tape slice (set per tile below)
+  const float* S = nullptr;  // this tile's V slice
   float4* my = stage_mem + warp * kStages * kSlots * 32 + lane;  // slot (d, j): my[(d*kSlots + j) * 32]
   auto issue = [&](int g, int d) {
     const int4* rec = grp + static_cast<size_t>(g) * kGroupRecs;
@@ -445,6 +608,10 @@ k_forward_async(const int4* __restrict__ grp, const int2* __restrict__ lvl, int 
     }
     cp_async_commit();
   };
+  // Persistent over tiles when the grid is smaller than the tile count.
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  T = tape + static_cast<size_t>(tile) * n_rows * TILE + lane * 4;
+  S = src + static_cast<size_t>(tile) * ncols * TILE + lane * 4;
   for (int l = 0; l < n_levels; ++l) {
     const int2 L = __ldg(lvl + l * kWarps + warp);
 #pragma unroll
@@ -500,6 +667,7 @@ k_forward_async(const int4* __restrict__ grp, const int2* __restrict__ lvl, int 
     }
     __syncthreads();
   }
+  }  // tile loop
 }
 
 __global__ void __launch_bounds__(32 * kWarps)
@@ -1253,6 +1421,14 @@ static int soft_mode() {
 static bool async_enabled_fwd() { return soft_mode() != 3; }
 static bool async_enabled_bwd() { return soft_mode() == 4; }
 
+// Grid for the tile-looped soft kernels: default one CTA per tile; SGX_GRID_FWD /
+// SGX_GRID_BWD cap it (a persistent grid walks tiles with a stride).
+static int tile_grid(const char* env, int tiles) {
+  const char* e = getenv(env);
+  int g = e ? atoi(e) : 0;
+  return (g > 0 && g < tiles) ? g : tiles;
+}
+
 void launch_forward(cudaStream_t st, int vec, const int4* grp, const int2* lvl, int n_levels,
                     const float* src, int ncols, float* tape, int n_rows, int Bp, int src_is_prob,
                     const uint64_t* exp_tab) {
@@ -1263,8 +1439,10 @@ void launch_forward(cudaStream_t st, int vec, const int4* grp, const int2* lvl, 
       cudaFuncSetAttribute(k_forward_async, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsyncSmem);
       attr = true;
     }
-    k_forward_async<<<tiles, 32 * kWarps, kAsyncSmem, st>>>(grp, lvl, n_levels, src, ncols, tape, n_rows,
-                                                           src_is_prob, exp_tab);
+    static const int gcap = tile_grid("SGX_GRID_FWD", 1 << 30);
+    const int grid = gcap < tiles ? gcap : tiles;
+    k_forward_async<<<grid, 32 * kWarps, kAsyncSmem, st>>>(grp, lvl, n_levels, src, ncols, tape, n_rows,
+                                                          src_is_prob, exp_tab, tiles);
     return;
   }
   switch (vec) {
@@ -1295,19 +1473,46 @@ void launch_backward(cudaStream_t st, int vec, const int4* ops, const int2* lvl,
                                                             row_loss, exp_tab);
     return;
   }
+  static const int gcap = tile_grid("SGX_GRID_BWD", 1 << 30);
+  const int grid = gcap < tiles ? gcap : tiles;
   switch (vec) {
     case 4:
-      k_backward<4, SGX_BWD_U><<<tiles, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows,
-                                                              dv_out, dp_out, lr, out_enc, out_tgt, n_out, row_loss,
-                                                              exp_tab);
+      k_backward<4, SGX_BWD_U><<<grid, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows,
+                                                             dv_out, dp_out, lr, out_enc, out_tgt, n_out, row_loss,
+                                                             exp_tab, tiles);
       break;
     case 2:
-      k_backward<2, 8><<<tiles, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows, dv_out,
-                                                      dp_out, lr, out_enc, out_tgt, n_out, row_loss, exp_tab);
+      k_backward<2, 8><<<grid, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows, dv_out,
+                                                     dp_out, lr, out_enc, out_tgt, n_out, row_loss, exp_tab, tiles);
       break;
     default:
-      k_backward<1, 8><<<tiles, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows, dv_out,
-                                                      dp_out, lr, out_enc, out_tgt, n_out, row_loss, exp_tab);
+      k_backward<1, 8><<<grid, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows, dv_out,
+                                                     dp_out, lr, out_enc, out_tgt, n_out, row_loss, exp_tab, tiles);
+  }
+}
+
+void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* lvl, int n_levels,
+                         const float* tape, float* adj, float* V, int ncols, int n_rows, const int* col_row,
+                         float* dv_out, float* dp_out, int Bp, float lr, const int* out_enc,
+                         const uint8_t* out_tgt, int n_out, float* row_loss, const uint64_t* exp_tab) {
+  const int tiles = Bp / (32 * vec);
+  static const int gcap = tile_grid("SGX_GRID_BWD", 1 << 30);
+  const int grid = gcap < tiles ? gcap : tiles;
+  switch (vec) {
+    case 4:
+      k_backward_rec<4, SGX_REC_U><<<grid, 32 * kWarps, 0, st>>>(rec, lvl, n_levels, tape, adj, V, ncols, n_rows,
+                                                                 col_row, dv_out, dp_out, lr, out_enc, out_tgt,
+                                                                 n_out, row_loss, exp_tab, tiles);
+      break;
+    case 2:
+      k_backward_rec<2, 8><<<grid, 32 * kWarps, 0, st>>>(rec, lvl, n_levels, tape, adj, V, ncols, n_rows, col_row,
+                                                         dv_out, dp_out, lr, out_enc, out_tgt, n_out, row_loss,
+                                                         exp_tab, tiles);
+      break;
+    default:
+      k_backward_rec<1, 8><<<grid, 32 * kWarps, 0, st>>>(rec, lvl, n_levels, tape, adj, V, ncols, n_rows, col_row,
+                                                         dv_out, dp_out, lr, out_enc, out_tgt, n_out, row_loss,
+                                                         exp_tab, tiles);
   }
 }
 

@@ -24,6 +24,49 @@ int operand_count(int32_t k) {
 
 std::string xv(int v) { return "x" + std::to_string(v); }
 
+// One node's micro-op run (BEGIN ... END) as edge records (kR* flags): the
+// BEGIN / SUB_BEGIN / SUB_END / END control rides on the neighbouring edge.
+void run_records(const std::vector<I4>& run, std::vector<I4>& out) {
+  const int32_t w = run.front().y;
+  const int32_t b = run.front().x;
+  int32_t pend = kRFirst | ((b & kSeedBit) ? kRSeed : 0) | ((b & kTargetBit) ? kRTarget : 0);
+  int32_t spend = 0;
+  bool sub_has = false;
+  const size_t start = out.size();
+  for (size_t t = 1; t < run.size(); ++t) {
+    const I4& o = run[t];
+    const int32_t code = o.x & 0xff;
+    if (code == kEdge) {
+      int32_t f = ((o.x >> kKindShift) & 0xf) | ((o.x & kNegOtherBit) ? kRNegOther : 0) | pend;
+      pend = 0;
+      if (o.x & kInSubBit) {
+        f |= kRInSub | spend;
+        spend = 0;
+        sub_has = true;
+      }
+      out.push_back({f, o.y, o.z, w});
+    } else if (code == kSubBegin) {
+      spend = kRSubFirst | ((o.x & kSeedBit) ? kRSubSeed : 0) | ((o.x & kTargetBit) ? kRSubTarget : 0) |
+              ((o.x & kNegSelfBit) ? kRNegSelf : 0);
+      sub_has = false;
+    } else if (code == kSubEnd) {
+      const int32_t se = kRSubLast | ((((o.x >> kKindShift) & 0xf) == SGX_NOT) ? kRSubNot : 0);
+      if (sub_has) {
+        out.back().x |= se;
+      } else {  // empty SUB run (a seeded folded output with no consumers)
+        out.push_back({kRInSub | spend | pend | se, -1, -1, w});
+        spend = pend = 0;
+      }
+    } else if (code == kEnd) {
+      if (out.size() == start) {  // no edge at all
+        out.push_back({pend, -1, -1, w});
+        pend = 0;
+      }
+      if (o.y >= 0 || o.z >= 0) out.back().x |= kRLast;
+    }
+  }
+}
+
 // Soft program over the nodes with in_set[i] != 0 (closed under operands).
 //
 // NOT / BUF folding: a NOT or BUF node whose operand is materialized is
@@ -206,9 +249,31 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
       P.bwd_lvl.push_back(static_cast<int32_t>(per[w].size()));
       P.bwd.insert(P.bwd.end(), per[w].begin(), per[w].end());
     }
+    // The same runs as edge records, balanced by record count.
+    std::vector<std::vector<I4>> recs;
+    for (const auto& run : runs) {
+      std::vector<I4> r;
+      run_records(run, r);
+      recs.push_back(std::move(r));
+    }
+    std::stable_sort(recs.begin(), recs.end(),
+                     [](const auto& x, const auto& y) { return x.size() > y.size(); });
+    std::vector<std::vector<I4>> rper(kWarps);
+    for (auto& r : recs) {
+      int best = 0;
+      for (int w = 1; w < kWarps; ++w)
+        if (rper[w].size() < rper[best].size()) best = w;
+      rper[best].insert(rper[best].end(), r.begin(), r.end());
+    }
+    for (int w = 0; w < kWarps; ++w) {
+      P.rec_lvl.push_back(static_cast<int32_t>(P.rec.size()));
+      P.rec_lvl.push_back(static_cast<int32_t>(rper[w].size()));
+      P.rec.insert(P.rec.end(), rper[w].begin(), rper[w].end());
+    }
   }
   // Slack so a chunk of kU records may read past the last op.
   for (int k = 0; k < kU; ++k) P.bwd.push_back({kNop, -1, -1, 0});
+  for (int k = 0; k < kU; ++k) P.rec.push_back({0, -1, -1, 0});
   return P;
 }
 

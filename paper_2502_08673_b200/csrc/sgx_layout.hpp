@@ -53,6 +53,21 @@ constexpr int kWarps = SGX_WARPS;  // warps per CTA sharing one sample tile (nod
 enum OpCode : int32_t { kNop = 15, kBegin = 16, kEdge = 17, kEnd = 18, kSubBegin = 19, kSubEnd = 20 };
 constexpr int32_t kSeedBit = 1 << 8, kTargetBit = 1 << 9, kNegOtherBit = 1 << 10,
                   kNegSelfBit = 1 << 11, kKindShift = 12, kInSubBit = 1 << 16;
+// Backward edge record (int4) {flags, adj_row_of_consumer (-1), other_row (-1),
+// own_row}: one record per fan-out edge, with the micro-ops' control folded
+// into flag bits so the kernel runs every record through the same
+// straight-line arithmetic (acc = acc*k + seed; acc += g*fa; acc2 += g*fb;
+// acc += s*acc2; see k_backward_rec).  A record without an edge (y = -1)
+// carries an empty node / empty SUB run.  Flags:
+//   bits 0-3 consumer kind, kRInSub (edge of a SUB run: feeds acc2),
+//   kRNegOther (other operand read through a folded NOT),
+//   kRFirst / kRSubFirst (reset acc / acc2 to the seed or +0 first),
+//   kRSubLast (+ kRSubNot: then acc -= acc2, else acc += acc2),
+//   kRSeed|kRTarget, kRSubSeed|kRSubTarget|kRNegSelf (output seeds from T[own_row]),
+//   kRLast (store acc to adj[own_row]).
+constexpr int32_t kRInSub = 1 << 4, kRNegOther = 1 << 5, kRFirst = 1 << 6, kRSubFirst = 1 << 7,
+                  kRSubLast = 1 << 8, kRSubNot = 1 << 9, kRSeed = 1 << 10, kRTarget = 1 << 11,
+                  kRSubSeed = 1 << 12, kRSubTarget = 1 << 13, kRNegSelf = 1 << 14, kRLast = 1 << 15;
 constexpr int kCnfThreads = 256;               // threads of the shared-memory harvest CTA
 constexpr int kGroup = 4;                      // ops per forward group
 constexpr int kGroupRecs = 1 + kGroup / 2;     // int4 records per group
@@ -72,6 +87,8 @@ struct SoftProgram {
   std::vector<I4> bwd;               // micro-ops
   std::vector<int32_t> fwd_lvl;      // per (level, warp): first group, group count
   std::vector<int32_t> bwd_lvl;      // per (level high to low, warp): first op, op count
+  std::vector<I4> rec;               // edge records (same runs as bwd)
+  std::vector<int32_t> rec_lvl;      // per (level high to low, warp): first record, count
   std::vector<int32_t> out_enc;      // each output as row << 1 | negate (-1: not in set)
   std::vector<int32_t> col_row;      // tape row of each V column's INPUT node
   std::vector<int32_t> virt_base;    // folded node -> row of its operand (-1 otherwise)
