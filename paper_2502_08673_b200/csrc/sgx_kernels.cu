@@ -383,7 +383,7 @@ __device__ __forceinline__ void vload_nc(const float* p, float (&o)[V]) {
 #define SGX_REC_U 4  // records per chunk at 4 samples per lane (C2 backward: 4 -> 40.7, 6 -> 41.9, 8 -> 46.2 ms per 5 restarts)
 #endif
 template <int V, int U>
-__global__ void __launch_bounds__(32 * kWarps, 4)
+__global__ void __launch_bounds__(32 * kWarps, 16 / V)
 k_backward_rec(const int4* __restrict__ rec, const int2* __restrict__ lvl, int n_levels,
                const float* __restrict__ tape, float* adj, float* Vp, int ncols, int n_rows,
                const int* __restrict__ col_row, float* dv_out, float* dp_out, float lr,
@@ -467,7 +467,7 @@ k_backward_rec(const int4* __restrict__ rec, const int2* __restrict__ lvl, int n
       __syncthreads();
     }
     // V columns: dV = g p (1 - p) (autodiff.cpp:212-221), V -= lr dV (gd_step, :285-290).
-    constexpr int UC = SGX_REC_UC;
+    constexpr int UC = V == 4 ? SGX_REC_UC : 1;  // narrower tiles run at 16/V CTAs per SM: no room
     for (int j0 = warp * UC; j0 < ncols; j0 += kWarps * UC) {
       int rw[UC];
       float x[UC][V], gg[UC][V];
@@ -1087,17 +1087,27 @@ k_harvest_smem(const float* __restrict__ V, int ncpi, int nucpi, const int* __re
     if (lane == 0) bits[__ldg(ucpi_row + k) * WPC + wl] = word;
   }
   __syncthreads();
-  // eval_discrete (circuit.cpp:126-146), level by level
-  for (int l = 0; l < n_levels; ++l) {
-    const int b = __ldg(lvl_ptr + l), e = __ldg(lvl_ptr + l + 1);
-    for (int item = threadIdx.x; item < (e - b) * WPC; item += kThreads) {
-      const int i = b + item / WPC, wl = item % WPC;
-      const int4 op = __ldg(ops + i);
-      const uint32_t a = bits[(op.z >> 1) * WPC + wl] ^ neg_mask(op.z);
-      const uint32_t c = bits[(op.w >> 1) * WPC + wl] ^ neg_mask(op.w);
-      bits[op.y * WPC + wl] = bit_gate(op.x, a, c);
+  // eval_discrete (circuit.cpp:126-146), level by level.  The op record of a
+  // thread's first item of level l+1 is fetched before level l's barrier, so
+  // the L2 round trip overlaps the level instead of following it.
+  {
+    int b = __ldg(lvl_ptr), e = n_levels > 0 ? __ldg(lvl_ptr + 1) : b;
+    int4 nxt = threadIdx.x < (e - b) * WPC ? __ldg(ops + b + threadIdx.x / WPC) : make_int4(0, 0, 0, 0);
+    for (int l = 0; l < n_levels; ++l) {
+      const int4 cur = nxt;
+      const int nb = e, ne = l + 2 <= n_levels ? __ldg(lvl_ptr + l + 2) : e;
+      if (threadIdx.x < (ne - nb) * WPC) nxt = __ldg(ops + nb + threadIdx.x / WPC);
+      for (int item = threadIdx.x; item < (e - b) * WPC; item += kThreads) {
+        const int wl = item % WPC;
+        const int4 op = item == static_cast<int>(threadIdx.x) ? cur : __ldg(ops + b + item / WPC);
+        const uint32_t a = bits[(op.z >> 1) * WPC + wl] ^ neg_mask(op.z);
+        const uint32_t c = bits[(op.w >> 1) * WPC + wl] ^ neg_mask(op.w);
+        bits[op.y * WPC + wl] = bit_gate(op.x, a, c);
+      }
+      b = nb;
+      e = ne;
+      __syncthreads();
     }
-    __syncthreads();
   }
   // PO check (sampler.cpp:140-146) + eval_cnf (cnf.cpp:136-145).  Each
   // thread owns whole clauses as int4 literal records stored transposed, so a
@@ -1115,8 +1125,10 @@ k_harvest_smem(const float* __restrict__ V, int ncpi, int nucpi, const int* __re
 #pragma unroll
       for (int wl = 0; wl < WPC; ++wl) ok[wl] &= bits[(e >> 1) * WPC + wl] ^ neg_mask(e) ^ t;
     }
+    int4 nrec = cnf_steps > 0 ? __ldg(cnf4 + threadIdx.x) : make_int4(-1, -1, -1, -1);
     for (int j = 0; j < cnf_steps; ++j) {
-      const int4 rec = __ldg(cnf4 + static_cast<size_t>(j) * kThreads + threadIdx.x);
+      const int4 rec = nrec;  // next step's record is in flight while this one runs
+      if (j + 1 < cnf_steps) nrec = __ldg(cnf4 + static_cast<size_t>(j + 1) * kThreads + threadIdx.x);
       const int lit[4] = {rec.x, rec.y, rec.z, rec.w};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -1505,12 +1517,12 @@ void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* 
                                                                  n_out, row_loss, exp_tab, tiles);
       break;
     case 2:
-      k_backward_rec<2, 8><<<grid, 32 * kWarps, 0, st>>>(rec, lvl, n_levels, tape, adj, V, ncols, n_rows, col_row,
+      k_backward_rec<2, 4><<<grid, 32 * kWarps, 0, st>>>(rec, lvl, n_levels, tape, adj, V, ncols, n_rows, col_row,
                                                          dv_out, dp_out, lr, out_enc, out_tgt, n_out, row_loss,
                                                          exp_tab, tiles);
       break;
     default:
-      k_backward_rec<1, 8><<<grid, 32 * kWarps, 0, st>>>(rec, lvl, n_levels, tape, adj, V, ncols, n_rows, col_row,
+      k_backward_rec<1, 4><<<grid, 32 * kWarps, 0, st>>>(rec, lvl, n_levels, tape, adj, V, ncols, n_rows, col_row,
                                                          dv_out, dp_out, lr, out_enc, out_tgt, n_out, row_loss,
                                                          exp_tab, tiles);
   }

@@ -2,7 +2,9 @@
 
 #include <algorithm>
 #include <numeric>
+#include <cstdlib>
 #include <stdexcept>
+#include <string>
 
 namespace sgx {
 
@@ -98,6 +100,19 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
     if (oc >= 1) lev[i] = lev[base_of(L.a[i])] + 1;
     if (oc == 2) lev[i] = std::max(lev[i], lev[base_of(L.b[i])] + 1);
     max_level = std::max(max_level, lev[i]);
+  }
+  if (!(getenv("SGX_SCHED") && std::string(getenv("SGX_SCHED")) == "asap")) {
+    // ALAP: every node one level below its earliest consumer, so adjoint and
+    // value rows are re-read soon after they are written (L2 reuse distance).
+    std::vector<int32_t> alap(n, max_level);
+    for (int j = n - 1; j >= 0; --j) {
+      if (!in_set[j] || virt[j]) continue;
+      const int oc = operand_count(L.kind[j]);
+      if (oc >= 1) alap[base_of(L.a[j])] = std::min(alap[base_of(L.a[j])], alap[j] - 1);
+      if (oc == 2) alap[base_of(L.b[j])] = std::min(alap[base_of(L.b[j])], alap[j] - 1);
+    }
+    for (int i = 0; i < n; ++i)
+      if (in_set[i] && !virt[i]) lev[i] = alap[i];
   }
   P.n_levels = max_level + 1;
   std::vector<std::vector<int32_t>> by_level(P.n_levels);
