@@ -191,7 +191,7 @@ struct sgx_circuit {
   int n_bit_levels = 0;
   // folded bit program (shared-memory harvest)
   DBuf<int4> fb_ops;
-  DBuf<int> fb_lvl_ptr, fb_cpi_row, fb_ucpi_row, fb_out_enc, fb_clause_enc, fb_key_enc;
+  DBuf<int> fb_lvl_ptr, fb_cpi_row, fb_ucpi_row, fb_out_enc, fb_key_enc;
   DBuf<int4> fb_cnf4;
   int fb_levels = 0;
 };
@@ -630,7 +630,6 @@ int sgx_circuit_upload(sgx_ctx* ctx, const sgx_circuit_desc* d, sgx_circuit** ou
       c->fb_cpi_row.upload(L.fb_cpi_row, st);
       c->fb_ucpi_row.upload(L.fb_ucpi_row, st);
       c->fb_out_enc.upload(L.fb_out_enc, st);
-      c->fb_clause_enc.upload(L.fb_clause_enc, st);
       c->fb_key_enc.upload(L.fb_key_enc, st);
       c->fb_cnf4.upload(to_int4(L.fb_cnf4), st);
       CK(cudaStreamSynchronize(st));
@@ -686,7 +685,7 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       // Shared-memory harvest: the widest word block whose folded bit tape
       // fits ~100 KB (two CTAs per SM) while leaving >= 2 CTAs per SM of work;
       // one word (up to 200 KB) for deep circuits; else the global path.
-      const size_t row_bytes = static_cast<size_t>(L.fb_rows) * sizeof(uint32_t);
+      const size_t row_bytes = static_cast<size_t>(L.fb_rows + 1) * sizeof(uint32_t);
       s->hwpc = 0;
       // (<= 8 words: the CNF check keeps one accumulator pair per word in
       // registers)

@@ -1039,7 +1039,7 @@ __device__ __forceinline__ uint32_t neg_mask(int enc) { return (enc & 1) ? kFull
 
 template <int WPC>
 __global__ void __launch_bounds__(kThreads)
-k_harvest_smem(const float* __restrict__ V, int ncpi, int nucpi, const int* __restrict__ cpi_row,
+k_harvest_smem(int n_rows, const float* __restrict__ V, int ncpi, int nucpi, const int* __restrict__ cpi_row,
                const int* __restrict__ ucpi_row, int tile_rows, uint64_t free_prefix, long long row_offset,
                const int4* __restrict__ ops, const int* __restrict__ lvl_ptr, int n_levels,
                const int* __restrict__ out_enc, const uint8_t* __restrict__ out_tgt, int n_out,
@@ -1047,12 +1047,13 @@ k_harvest_smem(const float* __restrict__ V, int ncpi, int nucpi, const int* __re
                const int* __restrict__ key_enc, int key_words, int batch, int Bp,
                uint32_t* __restrict__ valid_out, uint64_t* __restrict__ K, int* __restrict__ slot_of_row,
                unsigned long long* tkeys, unsigned long long* tmeta, uint64_t tmask, uint64_t epoch) {
-  extern __shared__ uint32_t bits[];  // [row][WPC]
+  extern __shared__ uint32_t bits[];  // [row][WPC], row n_rows = 0 (CNF padding)
   __shared__ uint32_t red[kThreads];
   __shared__ uint32_t vw[WPC];
   constexpr int NW = kThreads / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int w0 = blockIdx.x * WPC;
+  if (threadIdx.x < WPC) bits[n_rows * WPC + threadIdx.x] = 0u;
   // harden (autodiff.cpp:292-297): 8 independent V loads in flight per warp,
   // then one ballot each
   constexpr int HU = 8;
@@ -1125,27 +1126,27 @@ k_harvest_smem(const float* __restrict__ V, int ncpi, int nucpi, const int* __re
 #pragma unroll
       for (int wl = 0; wl < WPC; ++wl) ok[wl] &= bits[(e >> 1) * WPC + wl] ^ neg_mask(e) ^ t;
     }
-    int4 nrec = cnf_steps > 0 ? __ldg(cnf4 + threadIdx.x) : make_int4(-1, -1, -1, -1);
+    // Branch-free: a literal is row or ~row (negated), s = e >> 31 recovers
+    // both the row (e ^ s) and the word mask (x ^ s); padding reads the zero
+    // row; a record closes its clause unless .w is kCnfOpen.
+    int4 nrec = cnf_steps > 0 ? __ldg(cnf4 + threadIdx.x) : make_int4(0, 0, 0, kCnfOpen);
     for (int j = 0; j < cnf_steps; ++j) {
       const int4 rec = nrec;  // next step's record is in flight while this one runs
       if (j + 1 < cnf_steps) nrec = __ldg(cnf4 + static_cast<size_t>(j + 1) * kThreads + threadIdx.x);
-      const int lit[4] = {rec.x, rec.y, rec.z, rec.w};
+      const bool open = rec.w == kCnfOpen;
+      const uint32_t keep = open ? kFull : 0u;
+      const int lit[4] = {rec.x, rec.y, rec.z, open ? n_rows : rec.w};
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int e = lit[u];
-        if (e < 0) continue;
+      for (int wl = 0; wl < WPC; ++wl) {
+        uint32_t a = 0u;
 #pragma unroll
-        for (int wl = 0; wl < WPC; ++wl) {
-          const uint32_t x = bits[(e >> 2) * WPC + wl];
-          any[wl] |= (e & 1) ? ~x : x;
+        for (int u = 0; u < 4; ++u) {
+          const int sgn = lit[u] >> 31;
+          a |= bits[(lit[u] ^ sgn) * WPC + wl] ^ static_cast<uint32_t>(sgn);
         }
-        if (e & 2) {
-#pragma unroll
-          for (int wl = 0; wl < WPC; ++wl) {
-            ok[wl] &= any[wl];
-            any[wl] = 0u;
-          }
-        }
+        any[wl] |= a;
+        ok[wl] &= any[wl] | keep;
+        any[wl] &= keep;
       }
     }
 #pragma unroll
@@ -1586,7 +1587,7 @@ void launch_append(cudaStream_t st, const uint32_t* newmask, const int* block_of
 }
 
 template <int WPC>
-static void harvest_smem_t(cudaStream_t st, int grid, size_t smem, const HarvestSmemArgs& a) {
+static void harvest_smem_t(cudaStream_t st, int grid, int n_rows, size_t smem, const HarvestSmemArgs& a) {
   // Opt in whenever static (~10 KB) + dynamic could pass the 48 KB default.
   static size_t opted = 0;  // dynamic bytes this instantiation may use
   if (smem > opted) {
@@ -1594,21 +1595,21 @@ static void harvest_smem_t(cudaStream_t st, int grid, size_t smem, const Harvest
     opted = smem;
   }
   k_harvest_smem<WPC><<<grid, kThreads, smem, st>>>(
-      a.V, a.ncpi, a.nucpi, a.cpi_row, a.ucpi_row, a.tile_rows, a.free_prefix, a.row_offset, a.ops, a.lvl_ptr,
+      n_rows, a.V, a.ncpi, a.nucpi, a.cpi_row, a.ucpi_row, a.tile_rows, a.free_prefix, a.row_offset, a.ops, a.lvl_ptr,
       a.n_levels, a.out_enc, a.out_tgt, a.n_out, a.cnf4, a.cnf_steps, a.key_enc, a.key_words,
       a.batch, a.Bp, a.valid, a.K, a.slot_of_row, a.tkeys, a.tmeta, a.tmask, a.epoch);
 }
 
 void launch_harvest_smem(cudaStream_t st, int wpc, int n_rows, int W, const HarvestSmemArgs& a) {
-  const size_t smem = static_cast<size_t>(n_rows) * wpc * sizeof(uint32_t);
+  const size_t smem = static_cast<size_t>(n_rows + 1) * wpc * sizeof(uint32_t);  // + the zero row
   const int grid = W / wpc;
   switch (wpc) {
-    case 32: harvest_smem_t<32>(st, grid, smem, a); break;
-    case 16: harvest_smem_t<16>(st, grid, smem, a); break;
-    case 8: harvest_smem_t<8>(st, grid, smem, a); break;
-    case 4: harvest_smem_t<4>(st, grid, smem, a); break;
-    case 2: harvest_smem_t<2>(st, grid, smem, a); break;
-    default: harvest_smem_t<1>(st, grid, smem, a); break;
+    case 32: harvest_smem_t<32>(st, grid, n_rows, smem, a); break;
+    case 16: harvest_smem_t<16>(st, grid, n_rows, smem, a); break;
+    case 8: harvest_smem_t<8>(st, grid, n_rows, smem, a); break;
+    case 4: harvest_smem_t<4>(st, grid, n_rows, smem, a); break;
+    case 2: harvest_smem_t<2>(st, grid, n_rows, smem, a); break;
+    default: harvest_smem_t<1>(st, grid, n_rows, smem, a); break;
   }
 }
 

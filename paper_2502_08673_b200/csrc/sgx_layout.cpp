@@ -339,27 +339,31 @@ void build_folded_bits(Layout& L) {
   for (int v : L.ucpi) L.fb_ucpi_row.push_back(row[L.node_of_var[v]]);
   L.fb_out_enc.clear();
   for (int o : L.out_node) L.fb_out_enc.push_back(enc(o));
-  L.fb_clause_enc.clear();
-  for (int64_t c = 0; c + 1 < static_cast<int64_t>(L.clause_ptr.size()); ++c)
-    for (int64_t l = L.clause_ptr[c]; l < L.clause_ptr[c + 1]; ++l) {
-      const int32_t lit = L.clause_lit[l];
-      const int e = enc(L.node_of_var[lit < 0 ? -lit : lit]);
-      const bool last = l + 1 == L.clause_ptr[c + 1];
-      L.fb_clause_enc.push_back(((e >> 1) << 2) | (last ? 2 : 0) | ((e & 1) ^ (lit < 0 ? 1 : 0)));
-    }
   L.fb_key_enc.assign(static_cast<size_t>(L.key_words) * 64, -1);
   for (int v = 1; v <= L.num_vars; ++v) L.fb_key_enc[v - 1] = enc(L.node_of_var[v]);
 
-  // CNF records: each clause as ceil(len/4) int4 records (the last literal
-  // carries the clause-end flag); whole clauses dealt to kCnfThreads threads,
-  // longest-first to the least loaded, then padded and transposed.
+  // CNF records (kCnfOpen): a literal is its row, bit-inverted when negated
+  // (row = e ^ (e >> 31)); a clause of <= 4 literals is one record padded with
+  // the always-zero row fb_rows; a longer one is a chain of open records of 3
+  // literals + kCnfOpen, then a closing record.  Whole clauses dealt to
+  // kCnfThreads threads, longest-first to the least loaded, then padded with
+  // open all-zero records and transposed.
   const int64_t n_clauses = static_cast<int64_t>(L.clause_ptr.size()) - 1;
+  const int32_t zero_row = L.fb_rows;
   std::vector<std::vector<I4>> recs(n_clauses);
   for (int64_t c = 0; c < n_clauses; ++c) {
-    std::vector<int32_t> lits(L.fb_clause_enc.begin() + L.clause_ptr[c],
-                              L.fb_clause_enc.begin() + L.clause_ptr[c + 1]);
-    while (lits.size() % 4) lits.push_back(-1);
-    for (size_t k = 0; k < lits.size(); k += 4) recs[c].push_back({lits[k], lits[k + 1], lits[k + 2], lits[k + 3]});
+    std::vector<int32_t> lits;
+    for (int64_t l = L.clause_ptr[c]; l < L.clause_ptr[c + 1]; ++l) {
+      const int32_t lit = L.clause_lit[l];
+      const int e = enc(L.node_of_var[lit < 0 ? -lit : lit]);
+      const bool neg = ((e & 1) ^ (lit < 0 ? 1 : 0)) != 0;
+      lits.push_back(neg ? ~(e >> 1) : (e >> 1));
+    }
+    size_t k = 0;
+    for (; lits.size() - k > 4; k += 3) recs[c].push_back({lits[k], lits[k + 1], lits[k + 2], kCnfOpen});
+    int32_t t[4] = {zero_row, zero_row, zero_row, zero_row};
+    for (size_t u = 0; k + u < lits.size(); ++u) t[u] = lits[k + u];
+    recs[c].push_back({t[0], t[1], t[2], t[3]});
   }
   std::vector<int64_t> order(n_clauses);
   std::iota(order.begin(), order.end(), 0);
@@ -377,7 +381,7 @@ void build_folded_bits(Layout& L) {
   size_t steps = 0;
   for (const auto& p : per) steps = std::max(steps, p.size());
   L.fb_cnf_steps = static_cast<int32_t>(steps);
-  L.fb_cnf4.assign(steps * kCnfThreads, I4{-1, -1, -1, -1});
+  L.fb_cnf4.assign(steps * kCnfThreads, I4{zero_row, zero_row, zero_row, kCnfOpen});
   for (int t = 0; t < kCnfThreads; ++t)
     for (size_t j = 0; j < per[t].size(); ++j) L.fb_cnf4[j * kCnfThreads + t] = per[t][j];
 }

@@ -69,6 +69,7 @@ constexpr int32_t kRInSub = 1 << 4, kRNegOther = 1 << 5, kRFirst = 1 << 6, kRSub
                   kRSubLast = 1 << 8, kRSubNot = 1 << 9, kRSeed = 1 << 10, kRTarget = 1 << 11,
                   kRSubSeed = 1 << 12, kRSubTarget = 1 << 13, kRNegSelf = 1 << 14, kRLast = 1 << 15;
 constexpr int kCnfThreads = 256;               // threads of the shared-memory harvest CTA
+constexpr int32_t kCnfOpen = INT32_MIN;        // CNF record continues (see fb_cnf4)
 constexpr int kGroup = 4;                      // ops per forward group
 constexpr int kGroupRecs = 1 + kGroup / 2;     // int4 records per group
 
@@ -125,17 +126,18 @@ struct Layout {
 
   // Folded bit program for the shared-memory harvest: NOT/BUF nodes whose
   // operand is materialized own no row (read as row ^ mask); every reference
-  // is row << 1 | negate (clause literals: row << 2 | last << 1 | negate).
+  // is row << 1 | negate.
   int32_t fb_rows = 0;
   std::vector<I4> fb_ops;            // {kind, out_row, a_enc, b_enc}, level-sorted
   std::vector<int32_t> fb_lvl_ptr;
   std::vector<int32_t> fb_cpi_row, fb_ucpi_row;
   std::vector<int32_t> fb_out_enc;
-  std::vector<int32_t> fb_clause_enc;
   std::vector<int32_t> fb_key_enc;   // key_words * 64, -1 = padding
-  // CNF as int4 records of up to 4 literals (-1 = none), clauses kept whole
-  // per thread and stored transposed [step][kCnfThreads] so that at every
-  // step the CTA's threads read consecutive records.
+  // CNF as int4 records of up to 4 literals (row, or ~row when negated;
+  // padding = the zero row fb_rows; .w == kCnfOpen: the clause continues in
+  // the thread's next record), clauses kept whole per thread and stored
+  // transposed [step][kCnfThreads] so that at every step the CTA's threads
+  // read consecutive records.  Shared-memory tapes hold fb_rows + 1 rows.
   int32_t fb_cnf_steps = 0;
   std::vector<I4> fb_cnf4;
 
