@@ -132,44 +132,28 @@ std::vector<int2> to_int2(const std::vector<int32_t>& v) {
 }
 
 struct DevSoft {
-  DBuf<int4> fwd, bwd, rec;
-  DBuf<int2> fwd_lvl, bwd_lvl, rec_lvl;
+  DBuf<int4> fwd, rec;
+  DBuf<int2> fwd_lvl, rec_lvl;
   DBuf<int> out_enc, col_row;
   int n_fwd_levels = 0, n_bwd_levels = 0, n_rows = 0;
   void upload(const sgx::SoftProgram& P, cudaStream_t st) {
     fwd.upload(to_int4(P.fwd), st);
-    bwd.upload(to_int4(P.bwd), st);
     rec.upload(to_int4(P.rec), st);
     fwd_lvl.upload(to_int2(P.fwd_lvl), st);
-    bwd_lvl.upload(to_int2(P.bwd_lvl), st);
     rec_lvl.upload(to_int2(P.rec_lvl), st);
     out_enc.upload(P.out_enc, st);
     col_row.upload(P.col_row, st);
     n_fwd_levels = static_cast<int>(P.fwd_lvl.size() / (2 * sgx::kWarps));
-    n_bwd_levels = static_cast<int>(P.bwd_lvl.size() / (2 * sgx::kWarps));
+    n_bwd_levels = static_cast<int>(P.rec_lvl.size() / (2 * sgx::kWarps));
     n_rows = P.n_rows;
   }
 };
 
-// Backward form: edge records (default) or the micro-op interpreter
-// (SGX_BWD=ops, kept for A/B measurement).
-bool bwd_records() {
-  static const bool r = [] {
-    const char* e = std::getenv("SGX_BWD");
-    return !(e && std::string(e) == "ops");
-  }();
-  return r;
-}
-
 void backward(cudaStream_t st, int vec, const DevSoft& P, const float* tape, float* adj, float* V, int ncols,
               float* dv_out, float* dp_out, int Bp, float lr, const uint8_t* out_tgt, int n_out, float* row_loss,
-              const uint64_t* tab) {
-  if (bwd_records())
-    sgx::launch_backward_rec(st, vec, P.rec.p, P.rec_lvl.p, P.n_bwd_levels, tape, adj, V, ncols, P.n_rows,
-                             P.col_row.p, dv_out, dp_out, Bp, lr, P.out_enc.p, out_tgt, n_out, row_loss, tab);
-  else
-    sgx::launch_backward(st, vec, P.bwd.p, P.bwd_lvl.p, P.n_bwd_levels, tape, adj, V, ncols, P.n_rows, dv_out,
-                         dp_out, Bp, lr, P.out_enc.p, out_tgt, n_out, row_loss, tab);
+              const uint64_t* tab, uint32_t* hb) {
+  sgx::launch_backward_rec(st, vec, P.rec.p, P.rec_lvl.p, P.n_bwd_levels, tape, adj, V, ncols, P.n_rows,
+                           P.col_row.p, dv_out, dp_out, Bp, lr, P.out_enc.p, out_tgt, n_out, row_loss, tab, hb);
 }
 
 }  // namespace
@@ -205,6 +189,7 @@ struct sgx_sampler {
   DBuf<float> V, tape, adj, row_loss;
   DBuf<double> partial;
   DBuf<uint32_t> BT, valid, newmask;
+  DBuf<uint32_t> HB;  // hardened V columns [word][ncpi] (shared-memory harvest input)
   DBuf<int> slot_of_row, block_count;
   DBuf<uint64_t> K, store;
   DBuf<unsigned long long> fps_local;  // multi-GPU: this harvest's new fingerprints
@@ -268,7 +253,7 @@ void sampler_init(sgx_sampler* s, int restart) {
   uint64_t prefix = sgx::fold(sgx::fold(sgx::fold(sgx::kPi, s->cfg.seed), sgx::kInitTag),
                               static_cast<uint64_t>(static_cast<int64_t>(restart)));
   sgx::launch_init_v(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, 32 * s->vec, prefix,
-                     s->cfg.row_offset);
+                     s->cfg.row_offset, s->HB.p);
   s->launches += L.cpi.empty() ? 0 : 1;
   CK(cudaGetLastError());
 }
@@ -283,7 +268,7 @@ void sampler_step(sgx_sampler* s) {
   CK(cudaEventRecord(s->ev[1], s->st));
   backward(s->st, s->vec, c->cone, s->tape.p, s->adj.p, s->V.p, ncpi, nullptr, nullptr, s->Bp,
            static_cast<float>(s->cfg.learning_rate), c->out_tgt.p, static_cast<int>(c->L.out_node.size()),
-           s->row_loss.p, tab);
+           s->row_loss.p, tab, s->HB.p);
   sgx::launch_loss(s->st, s->row_loss.p, s->cfg.batch, s->partial.p, s->n_partial, s->hout.p);
   s->launches += 4;
   CK(cudaEventRecord(s->ev[2], s->st));
@@ -349,12 +334,11 @@ void harvest_front(sgx_sampler* s, int restart, int iter, long long quota_left) 
   s->epoch += 1;
   if (s->hwpc > 0) {
     sgx::HarvestSmemArgs a{};
-    a.V = s->V.p;
+    a.hb = s->HB.p;
     a.ncpi = static_cast<int>(L.cpi.size());
     a.nucpi = static_cast<int>(L.ucpi.size());
     a.cpi_row = c->fb_cpi_row.p;
     a.ucpi_row = c->fb_ucpi_row.p;
-    a.tile_rows = 32 * s->vec;
     a.free_prefix = fprefix;
     a.row_offset = s->cfg.row_offset;
     a.ops = c->fb_ops.p;
@@ -703,6 +687,7 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       const size_t Bp = static_cast<size_t>(s->Bp);
       cudaStream_t st = s->st;
       s->V.alloc_async(L.cpi.size() * Bp, st);
+      s->HB.alloc_async(L.cpi.size() * s->W, st);
       s->tape.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
       s->adj.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
       s->row_loss.alloc_async(Bp, st);
@@ -720,6 +705,7 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       s->store_cap = cfg->solution_capacity > 0 ? cfg->solution_capacity : want_rows;
       s->store.alloc_async(static_cast<size_t>(s->store_cap) * L.key_words, st);
       CK(cudaMemsetAsync(s->V.p, 0, s->V.n * sizeof(float), s->st));
+      CK(cudaMemsetAsync(s->HB.p, 0xff, s->HB.n * sizeof(uint32_t), s->st));  // harden(0) = 1
       ensure_table(s.get());
       CK(cudaStreamSynchronize(s->st));
     }
@@ -735,7 +721,7 @@ int sgx_sampler_free(sgx_sampler* s) {
     if (st) {  // hand the big buffers back to the pool in stream order
       for (auto* b : {&s->V, &s->tape, &s->adj, &s->row_loss}) b->reset_async(st);
       s->partial.reset_async(st);
-      for (auto* b : {&s->BT, &s->valid, &s->newmask}) b->reset_async(st);
+      for (auto* b : {&s->BT, &s->valid, &s->newmask, &s->HB}) b->reset_async(st);
       s->slot_of_row.reset_async(st);
       s->block_count.reset_async(st);
       s->K.reset_async(st);
@@ -1035,7 +1021,7 @@ int sgx_backward(sgx_circuit* c, const float* tape, int32_t batch, const float* 
     CK(cudaMemsetAsync(ddv.p, 0, ddv.n * sizeof(float), st));
     CK(cudaMemsetAsync(ddp.p, 0, ddp.n * sizeof(float), st));
     backward(st, kTapVec, c->full, dt.p, dadj.p, dV.p, static_cast<int>(ncpi), ddv.p, ddp.p, Bp, 0.0f,
-             c->out_tgt.p, static_cast<int>(L.out_node.size()), nullptr, c->ctx->exp_tab.p);
+             c->out_tgt.p, static_cast<int>(L.out_node.size()), nullptr, c->ctx->exp_tab.p, nullptr);
     CK(cudaGetLastError());
     std::vector<float> hdv(ddv.n), hdp(ddp.n);
     CK(cudaMemcpyAsync(hdv.data(), ddv.p, hdv.size() * sizeof(float), cudaMemcpyDeviceToHost, st));

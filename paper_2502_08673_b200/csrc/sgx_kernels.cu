@@ -11,8 +11,13 @@ namespace sgx {
 // ---------------------------------------------------------------------------
 // V is tile-major like the tape: [tile][col][tile_rows]; i walks it in
 // memory order.
+// The harvest's hardened input words hb[word][col] (bit = V >= 0,
+// autodiff.cpp:292-297) come out of the same pass: a warp covers 32
+// consecutive rows of one column (ncols * Bp and the stride are multiples of
+// 32, so every warp stays converged).
 __global__ void __launch_bounds__(kThreads)
-k_init_v(float* __restrict__ V, int ncols, int Bp, int tile_rows, uint64_t prefix, long long row_offset) {
+k_init_v(float* __restrict__ V, int ncols, int Bp, int tile_rows, uint64_t prefix, long long row_offset,
+         uint32_t* __restrict__ hb) {
   const long long total = static_cast<long long>(ncols) * Bp;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -22,7 +27,10 @@ k_init_v(float* __restrict__ V, int ncols, int Bp, int tile_rows, uint64_t prefi
     const int r = static_cast<int>(tile * tile_rows) + within % tile_rows;
     uint64_t h = fold(fold(prefix, static_cast<uint64_t>(row_offset + r)), static_cast<uint64_t>(c));
     double u = static_cast<double>(h >> 11) * 0x1.0p-53;  // u01, rng.hpp:28-30
-    V[i] = __double2float_rn(__dsub_rn(__dmul_rn(2.0, u), 1.0));
+    const float v = __double2float_rn(__dsub_rn(__dmul_rn(2.0, u), 1.0));
+    V[i] = v;
+    const uint32_t word = __ballot_sync(kFull, v >= 0.0f);
+    if ((threadIdx.x & 31) == 0) hb[static_cast<size_t>(r >> 5) * ncols + c] = word;
   }
 }
 
@@ -196,8 +204,8 @@ k_forward(const int4* __restrict__ grp, const int2* __restrict__ lvl, int n_leve
 template <int V>
 __device__ __forceinline__ void input_end(const float (&x)[V], const float (&acc)[V], float lr,
                                           const uint64_t* __restrict__ exp_tab, size_t at, float* Vp,
-                                          float* dv_out, float* dp_out) {
-  float dv[V], nv[V];
+                                          float* dv_out, float* dp_out, float (&nv)[V]) {
+  float dv[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const float p = sigmoid_ref(x[v], exp_tab);
@@ -212,120 +220,32 @@ __device__ __forceinline__ void input_end(const float (&x)[V], const float (&acc
   }
 }
 
-// ---------------------------------------------------------------------------
-// K3+K4: per-row loss, pull-style backward and the fused GD step.  Same tile
-// and level split as the forward, levels high to low.  Each warp runs its
-// own micro-op stream in chunks of U records (all loads of a chunk issued
-// first): BEGIN (seed) / EDGE* (fan-out slots, consumers in descending
-// reference id) / SUB_BEGIN EDGE* SUB_END (a folded NOT/BUF consumer's
-// adjoint, summed in its own order, then subtracted/added) / END (store the
-// adjoint; for a V column: dV and V -= lr * dV).  No atomics: every adjoint
-// is produced once, by the warp that owns the node.
-// ---------------------------------------------------------------------------
-template <int V, int U>
-__global__ void __launch_bounds__(32 * kWarps)
-k_backward(const int4* __restrict__ ops, const int2* __restrict__ lvl, int n_levels,
-           const float* tape, float* adj, float* Vp, int ncols, int n_rows, float* dv_out,
-           float* dp_out, float lr, const int* __restrict__ out_enc,
-           const uint8_t* __restrict__ out_tgt, int n_out, float* __restrict__ row_loss,
-           const uint64_t* __restrict__ exp_tab, int n_tiles) {
-  constexpr int TILE = 32 * V;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // Persistent over tiles when the grid is smaller than the tile count.
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-  const size_t tbase = static_cast<size_t>(tile) * n_rows * TILE + lane * V;
-  const float* T = tape + tbase;
-  float* A = adj + tbase;
-  const size_t vbase = static_cast<size_t>(tile) * ncols * TILE + lane * V;
-  if (row_loss && warp == 0) {  // loss (autodiff.cpp:160-166): outputs in order
-    float l[V];
+// Hardened input words from a tile's ballots: b[v] bit l = sample V*l + v of
+// the tile; word k of the tile (rows 32k .. 32k+31) interleaves the k-th
+// 32/V-bit slice of every b[v] with stride V.
+__device__ __forceinline__ uint32_t spread4(uint32_t x) {  // bit m -> bit 4m (8 bits)
+  x = (x | (x << 12)) & 0x000F000Fu;
+  x = (x | (x << 6)) & 0x03030303u;
+  return (x | (x << 3)) & 0x11111111u;
+}
+__device__ __forceinline__ uint32_t spread2(uint32_t x) {  // bit m -> bit 2m (16 bits)
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  return (x | (x << 1)) & 0x55555555u;
+}
+template <int V>
+__device__ __forceinline__ uint32_t pack_word(const uint32_t (&b)[V], int k) {
+  if constexpr (V == 1) {
+    return b[0];
+  } else if constexpr (V == 2) {
+    return spread2((b[0] >> (16 * k)) & 0xffffu) | (spread2((b[1] >> (16 * k)) & 0xffffu) << 1);
+  } else {
+    uint32_t w = 0u;
 #pragma unroll
-    for (int v = 0; v < V; ++v) l[v] = 0.0f;
-    for (int m = 0; m < n_out; ++m) {
-      float yv[V];
-      load_operand<V>(T, __ldg(out_enc + m), yv);
-      const float t = __ldg(out_tgt + m) ? 1.0f : 0.0f;
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const float d = __fsub_rn(yv[v], t);
-        l[v] = __fadd_rn(l[v], __fmul_rn(d, d));
-      }
-    }
-    vstore<V>(row_loss + static_cast<size_t>(tile) * TILE + lane * V, l);
+    for (int v = 0; v < 4; ++v) w |= spread4((b[v] >> (8 * k)) & 0xffu) << v;
+    return w;
   }
-  float acc[V], acc2[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) acc[v] = acc2[v] = 0.0f;
-  for (int li = 0; li < n_levels; ++li) {
-    const int2 L = __ldg(lvl + li * kWarps + warp);
-    for (int c = 0; c < L.y; c += U) {
-      int4 op[U];
-#pragma unroll
-      for (int k = 0; k < U; ++k)
-        op[k] = c + k < L.y ? __ldg(ops + L.x + c + k) : make_int4(kNop, -1, -1, 0);
-      float x[U][V], y[U][V];
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int code = op[k].x & 0xff;
-        if (code == kEdge) {
-          vload<V>(A + static_cast<size_t>(op[k].y) * TILE, x[k]);
-          if (op[k].z >= 0) vload<V>(T + static_cast<size_t>(op[k].z) * TILE, y[k]);
-        } else if (code == kBegin || code == kSubBegin) {
-          if (op[k].x & kSeedBit) vload<V>(T + static_cast<size_t>(op[k].y) * TILE, x[k]);
-        } else if (code == kEnd) {
-          if (op[k].z >= 0) vload<V>(Vp + vbase + static_cast<size_t>(op[k].z) * TILE, x[k]);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int f = op[k].x;
-        const int code = f & 0xff;
-        if (code == kEdge) {
-          const int ck = (f >> kKindShift) & 0xf;
-          const float c0 = kPullC0[ck], c1 = kPullC1[ck];
-          const bool neg = f & kNegOtherBit;
-          const float ns = neg ? -1.0f : 1.0f, no = neg ? 1.0f : 0.0f;
-          float p[V];
-#pragma unroll
-          for (int v = 0; v < V; ++v) {  // BUF/NOT consumers have no other operand (c1 = 0)
-            const float vo = op[k].z >= 0 ? __fmaf_rn(ns, y[k][v], no) : 0.0f;
-            p[v] = __fmul_rn(x[k][v], __fmaf_rn(c1, vo, c0));
-          }
-          if (f & kInSubBit) {
-#pragma unroll
-            for (int v = 0; v < V; ++v) acc2[v] = __fadd_rn(acc2[v], p[v]);
-          } else {
-#pragma unroll
-            for (int v = 0; v < V; ++v) acc[v] = __fadd_rn(acc[v], p[v]);
-          }
-        } else if (code == kBegin || code == kSubBegin) {
-          const float t = (f & kTargetBit) ? 1.0f : 0.0f;
-#pragma unroll
-          for (int v = 0; v < V; ++v) {
-            float yv = x[k][v];
-            if (f & kNegSelfBit) yv = __fsub_rn(1.0f, yv);
-            // adj[out] += 2 (y - t) on a zero adjoint (autodiff.cpp:206)
-            const float sd = (f & kSeedBit) ? __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(yv, t))) : 0.0f;
-            if (code == kBegin)
-              acc[v] = sd;
-            else
-              acc2[v] = sd;
-          }
-        } else if (code == kSubEnd) {
-          const bool is_not = ((f >> kKindShift) & 0xf) == SGX_NOT;
-#pragma unroll
-          for (int v = 0; v < V; ++v) acc[v] = is_not ? __fsub_rn(acc[v], acc2[v]) : __fadd_rn(acc[v], acc2[v]);
-        } else if (code == kEnd) {
-          if (op[k].y >= 0) vstore<V>(A + static_cast<size_t>(op[k].y) * TILE, acc);
-          if (op[k].z >= 0)  // autodiff.cpp:212-221 then gd_step :285-290
-            input_end<V>(x[k], acc, lr, exp_tab, vbase + static_cast<size_t>(op[k].z) * TILE, Vp, dv_out,
-                         dp_out);
-        }
-      }
-    }
-    __syncthreads();
-  }
-  }  // tile loop
 }
 
 // Edge-record decode tables (sgx_layout.hpp kR* flags).  kRecC[ck | in_sub<<4]
@@ -361,9 +281,14 @@ __device__ __forceinline__ void vload_nc(const float* p, float (&o)[V]) {
 }
 
 // ---------------------------------------------------------------------------
-// K3+K4, edge-record form: the same pull-CSR backward as k_backward, but the
-// micro-op control (BEGIN / SUB_BEGIN / SUB_END / END) rides as flag bits on
-// the edges, so every record runs the same branch-free arithmetic:
+// K3+K4+K5a: per-row loss, pull-CSR backward, fused GD step and harden.
+// Same tile and level split as the forward, levels high to low; no atomics:
+// every adjoint is produced once, by the warp that owns the node, summing
+// its fan-out in the reference's order (seed, then consumers in descending
+// id, a-slot first, a folded NOT/BUF consumer's own sum nested as a SUB
+// run).  The micro-op control (BEGIN / SUB_BEGIN / SUB_END / END) rides as
+// flag bits on the edge records, so every record runs the same branch-free
+// arithmetic:
 //   acc  = acc  * k  + seed        (k = 0 on a node's first record)
 //   acc2 = acc2 * k2 + seed2       (k2 = 0 on a SUB run's first record)
 //   vo = ns * T[other] + no;  acc += g * (c0a + c1a vo);  acc2 += g * (c0b + c1b vo)
@@ -374,7 +299,8 @@ __device__ __forceinline__ void vload_nc(const float* p, float (&o)[V]) {
 // accumulator is never -0 (it starts at +0 and RN sums only give -0 from
 // -0 + -0).  Seeds (output nodes, autodiff.cpp:206) take a rare uniform
 // branch.  Column-input adjoints are stored like any other and the V update
-// (dV = g p (1 - p), V -= lr dV) runs as an epilogue over the tile's columns.
+// (dV = g p (1 - p), V -= lr dV) runs as an epilogue over the tile's columns,
+// which also hardens the new V into the harvest's input words (hb).
 // ---------------------------------------------------------------------------
 #ifndef SGX_REC_UC
 #define SGX_REC_UC 2
@@ -388,7 +314,8 @@ k_backward_rec(const int4* __restrict__ rec, const int2* __restrict__ lvl, int n
                const float* __restrict__ tape, float* adj, float* Vp, int ncols, int n_rows,
                const int* __restrict__ col_row, float* dv_out, float* dp_out, float lr,
                const int* __restrict__ out_enc, const uint8_t* __restrict__ out_tgt, int n_out,
-               float* __restrict__ row_loss, const uint64_t* __restrict__ exp_tab, int n_tiles) {
+               float* __restrict__ row_loss, const uint64_t* __restrict__ exp_tab, uint32_t* __restrict__ hb,
+               int n_tiles) {
   constexpr int TILE = 32 * V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -481,40 +408,36 @@ k_backward_rec(const int4* __restrict__ rec, const int2* __restrict__ lvl, int n
       }
 #pragma unroll
       for (int q = 0; q < UC; ++q)
-        if (rw[q] >= 0)
-          input_end<V>(x[q], gg[q], lr, exp_tab, vbase + static_cast<size_t>(j0 + q) * TILE, Vp, dv_out, dp_out);
+        if (rw[q] >= 0) {  // warp-uniform
+          float nv[V];
+          input_end<V>(x[q], gg[q], lr, exp_tab, vbase + static_cast<size_t>(j0 + q) * TILE, Vp, dv_out, dp_out,
+                       nv);
+          if (hb) {  // harden (autodiff.cpp:292-297): bit = V >= 0, NaN -> 0
+            uint32_t b[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) b[v] = __ballot_sync(kFull, nv[v] >= 0.0f);
+            if (lane < V) hb[(static_cast<size_t>(tile) * V + lane) * ncols + j0 + q] = pack_word<V>(b, lane);
+          }
+        }
     }
     if (n_tiles > static_cast<int>(gridDim.x)) __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------------------
-// v4: the same forward / backward, with every operand row staged through
-// shared memory by cp.async (LDGSTS, 16 B per lane = the lane's 4 samples).
-// Each warp keeps kStages groups (forward) or kU-op chunks (backward) in
-// flight without spending registers on them, so the loads of the next three
-// groups overlap the arithmetic of the current one.  Lanes only ever read
-// their own staged bytes, so per-thread cp.async.wait_group is the only
+// The forward with every operand row staged through shared memory by cp.async
+// (LDGSTS, 16 B per lane = the lane's 4 samples).  Each warp keeps kStages
+// groups in flight without spending registers on them, so the loads of the
+// next groups overlap the arithmetic of the current one.  Lanes only ever
+// read their own staged bytes, so per-thread cp.async.wait_group is the only
 // synchronisation inside a level.
 // ---------------------------------------------------------------------------
-#ifndef SGX_BWD_U
-#define SGX_BWD_U 8  // backward micro-ops per chunk at 4 samples per lane (measured: 4 -> 3.34 ms,
-                     // 8 -> 2.94 ms, 16 -> 5.2 ms per C2 launch)
-#endif
 #ifndef SGX_STAGES
 #define SGX_STAGES 3
 #endif
-constexpr int kStages = SGX_STAGES;      // groups / chunks in flight per warp
-constexpr int kSlots = 2 * kGroup;       // staged rows per stage (= 2 * kAsyncU)
-constexpr int kAsyncU = 4;               // backward micro-ops per chunk
+constexpr int kStages = SGX_STAGES;      // groups in flight per warp
+constexpr int kSlots = 2 * kGroup;       // staged rows per stage
 constexpr int kAsyncSmem = kWarps * kStages * kSlots * 32 * 16;  // bytes per CTA
-#ifndef SGX_ABWD_U
-#define SGX_ABWD_U 4
-#endif
-#ifndef SGX_ABWD_STAGES
-#define SGX_ABWD_STAGES 3
-#endif
-constexpr int kAsyncSmemBwd = kWarps * SGX_ABWD_STAGES * 2 * SGX_ABWD_U * 32 * 16;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -670,137 +593,6 @@ k_forward_async(const int4* __restrict__ grp, const int2* __restrict__ lvl, int 
   }  // tile loop
 }
 
-__global__ void __launch_bounds__(32 * kWarps)
-k_backward_async(const int4* __restrict__ ops, const int2* __restrict__ lvl, int n_levels,
-                 const float* tape, float* adj, float* Vp, int ncols, int n_rows, float* dv_out,
-                 float* dp_out, float lr, const int* __restrict__ out_enc,
-                 const uint8_t* __restrict__ out_tgt, int n_out, float* __restrict__ row_loss,
-                 const uint64_t* __restrict__ exp_tab) {
-  constexpr int TILE = 128, U = SGX_ABWD_U;
-  constexpr int kStages = SGX_ABWD_STAGES, kSlots = 2 * SGX_ABWD_U;  // shadow the forward's
-  extern __shared__ float4 stage_mem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t tbase = static_cast<size_t>(blockIdx.x) * n_rows * TILE + lane * 4;
-  const float* T = tape + tbase;
-  float* A = adj + tbase;
-  const size_t vbase = static_cast<size_t>(blockIdx.x) * ncols * TILE + lane * 4;
-  float4* my = stage_mem + warp * kStages * kSlots * 32 + lane;
-  if (row_loss && warp == 0) {  // loss (autodiff.cpp:160-166): outputs in order
-    float l[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    for (int m = 0; m < n_out; ++m) {
-      float yv[4];
-      load_operand<4>(T, __ldg(out_enc + m), yv);
-      const float t = __ldg(out_tgt + m) ? 1.0f : 0.0f;
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const float d = __fsub_rn(yv[v], t);
-        l[v] = __fadd_rn(l[v], __fmul_rn(d, d));
-      }
-    }
-    vstore<4>(row_loss + static_cast<size_t>(blockIdx.x) * TILE + lane * 4, l);
-  }
-  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f}, acc2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-  for (int li = 0; li < n_levels; ++li) {
-    const int2 L = __ldg(lvl + li * kWarps + warp);
-    const int nch = (L.y + U - 1) / U;
-    auto issue = [&](int c, int d) {
-      float4* base = my + d * kSlots * 32;
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        if (c * U + k >= L.y) break;
-        const int4 op = __ldg(ops + L.x + c * U + k);
-        const int code = op.x & 0xff;
-        if (code == kEdge) {
-          cp_async16(base + (2 * k) * 32, A + static_cast<size_t>(op.y) * TILE);
-          if (op.z >= 0) cp_async16(base + (2 * k + 1) * 32, T + static_cast<size_t>(op.z) * TILE);
-        } else if (code == kBegin || code == kSubBegin) {
-          if (op.x & kSeedBit) cp_async16(base + (2 * k) * 32, T + static_cast<size_t>(op.y) * TILE);
-        } else if (code == kEnd) {
-          if (op.z >= 0) cp_async16(base + (2 * k) * 32, Vp + vbase + static_cast<size_t>(op.z) * TILE);
-        }
-      }
-      cp_async_commit();
-    };
-#pragma unroll
-    for (int i = 0; i < kStages - 1; ++i) {
-      if (i < nch)
-        issue(i, i);
-      else
-        cp_async_commit();
-    }
-    for (int c = 0; c < nch; ++c) {
-      const int nxt = c + kStages - 1;
-      if (nxt < nch)
-        issue(nxt, nxt % kStages);
-      else
-        cp_async_commit();
-      cp_async_wait<kStages - 1>();
-      const float4* base = my + (c % kStages) * kSlots * 32;
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        if (c * U + k >= L.y) break;
-        const int4 op = __ldg(ops + L.x + c * U + k);
-        const int f = op.x;
-        const int code = f & 0xff;
-        if (code == kEdge) {
-          const int ck = (f >> kKindShift) & 0xf;
-          const float c0 = kPullC0[ck], c1 = kPullC1[ck];
-          float g[4], y[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-          f4(base[(2 * k) * 32], g);
-          if (op.z >= 0) f4(base[(2 * k + 1) * 32], y);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            float vo = y[v];
-            if (f & kNegOtherBit) vo = __fsub_rn(1.0f, vo);
-            const float p = __fmul_rn(g[v], __fmaf_rn(c1, vo, c0));
-            if (f & kInSubBit)
-              acc2[v] = __fadd_rn(acc2[v], p);
-            else
-              acc[v] = __fadd_rn(acc[v], p);
-          }
-        } else if (code == kBegin || code == kSubBegin) {
-          const float t = (f & kTargetBit) ? 1.0f : 0.0f;
-          float x[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-          if (f & kSeedBit) f4(base[(2 * k) * 32], x);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            float yv = x[v];
-            if (f & kNegSelfBit) yv = __fsub_rn(1.0f, yv);
-            const float sd = (f & kSeedBit) ? __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(yv, t))) : 0.0f;
-            if (code == kBegin)
-              acc[v] = sd;
-            else
-              acc2[v] = sd;
-          }
-        } else if (code == kSubEnd) {
-          const bool is_not = ((f >> kKindShift) & 0xf) == SGX_NOT;
-#pragma unroll
-          for (int v = 0; v < 4; ++v) acc[v] = is_not ? __fsub_rn(acc[v], acc2[v]) : __fadd_rn(acc[v], acc2[v]);
-        } else if (code == kEnd) {
-          if (op.y >= 0) vstore<4>(A + static_cast<size_t>(op.y) * TILE, acc);
-          if (op.z >= 0) {  // autodiff.cpp:212-221 then gd_step :285-290
-            float x[4], dv[4], nv[4];
-            f4(base[(2 * k) * 32], x);
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const float p = sigmoid_ref(x[v], exp_tab);
-              dv[v] = __fmul_rn(__fmul_rn(acc[v], p), __fsub_rn(1.0f, p));
-              nv[v] = __fsub_rn(x[v], __fmul_rn(lr, dv[v]));
-            }
-            const size_t at = vbase + static_cast<size_t>(op.z) * TILE;
-            if (dv_out) {
-              vstore<4>(dv_out + at, dv);
-              vstore<4>(dp_out + at, acc);
-            } else {
-              vstore<4>(Vp + at, nv);
-            }
-          }
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
 
 // Deterministic loss total: fixed per-block partial sums in double, then one
 // block folds the partials in block order.
@@ -1039,8 +831,8 @@ __device__ __forceinline__ uint32_t neg_mask(int enc) { return (enc & 1) ? kFull
 
 template <int WPC>
 __global__ void __launch_bounds__(kThreads)
-k_harvest_smem(int n_rows, const float* __restrict__ V, int ncpi, int nucpi, const int* __restrict__ cpi_row,
-               const int* __restrict__ ucpi_row, int tile_rows, uint64_t free_prefix, long long row_offset,
+k_harvest_smem(int n_rows, const uint32_t* __restrict__ hb, int ncpi, int nucpi, const int* __restrict__ cpi_row,
+               const int* __restrict__ ucpi_row, uint64_t free_prefix, long long row_offset,
                const int4* __restrict__ ops, const int* __restrict__ lvl_ptr, int n_levels,
                const int* __restrict__ out_enc, const uint8_t* __restrict__ out_tgt, int n_out,
                const int4* __restrict__ cnf4, int cnf_steps,
@@ -1054,30 +846,12 @@ k_harvest_smem(int n_rows, const float* __restrict__ V, int ncpi, int nucpi, con
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int w0 = blockIdx.x * WPC;
   if (threadIdx.x < WPC) bits[n_rows * WPC + threadIdx.x] = 0u;
-  // harden (autodiff.cpp:292-297): 8 independent V loads in flight per warp,
-  // then one ballot each
-  constexpr int HU = 8;
-  for (int item0 = warp * HU; item0 < ncpi * WPC; item0 += NW * HU) {
-    float x[HU];
-#pragma unroll
-    for (int u = 0; u < HU; ++u) {
-      const int item = item0 + u;
-      x[u] = -1.0f;
-      if (item < ncpi * WPC) {
-        const int input = item / WPC, wl = item - input * WPC;
-        const int r = (w0 + wl) * 32 + lane;
-        const size_t tile = static_cast<size_t>(r / tile_rows);
-        x[u] = V[(tile * ncpi + input) * tile_rows + r % tile_rows];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < HU; ++u) {
-      const int item = item0 + u;
-      if (item >= ncpi * WPC) break;  // warp-uniform
-      const uint32_t word = __ballot_sync(kFull, x[u] >= 0.0f);
-      const int input = item / WPC, wl = item - input * WPC;
-      if (lane == 0) bits[__ldg(cpi_row + input) * WPC + wl] = word;
-    }
+  // hardened inputs (autodiff.cpp:292-297), produced by k_init_v / the
+  // backward epilogue as hb[word][col]: consecutive threads, consecutive
+  // columns of one word
+  for (int item = threadIdx.x; item < ncpi * WPC; item += kThreads) {
+    const int wl = item / ncpi, input = item - wl * ncpi;
+    bits[__ldg(cpi_row + input) * WPC + wl] = __ldg(hb + static_cast<size_t>(w0 + wl) * ncpi + input);
   }
   // free bits (sampler.cpp:132-137)
   for (int item = warp; item < nucpi * WPC; item += NW) {
@@ -1413,26 +1187,22 @@ static int grid_for(long long n, int per_block, int cap) {
 }
 
 void launch_init_v(cudaStream_t st, float* V, int ncols, int Bp, int tile_rows, uint64_t prefix,
-                   long long row_offset) {
+                   long long row_offset, uint32_t* hb) {
   if (ncols == 0) return;
   k_init_v<<<grid_for(static_cast<long long>(ncols) * Bp, kThreads, 148 * 64), kThreads, 0, st>>>(
-      V, ncols, Bp, tile_rows, prefix, row_offset);
+      V, ncols, Bp, tile_rows, prefix, row_offset, hb);
 }
 
-// Kernel variant per pass (measured on B200, c2_iscas @ 64k rows): the
-// cp.async-staged forward beats the register one (1.41 vs 1.78 ms), the
-// register backward beats the staged one (3.35 vs 4.27 ms).  SGX_SOFT=3
-// forces register kernels for both passes, SGX_SOFT=4 staged for both.
-static int soft_mode() {
-  static int m = -1;
-  if (m < 0) {
+// Forward variant (measured on B200, c2_iscas @ 64k rows): the
+// cp.async-staged forward beats the register one (1.41 vs 1.78 ms);
+// SGX_SOFT=3 forces the register kernel.
+static bool async_enabled_fwd() {
+  static const bool on = [] {
     const char* e = std::getenv("SGX_SOFT");
-    m = (e && (e[0] == '3' || e[0] == '4')) ? e[0] - '0' : 0;
-  }
-  return m;
+    return !(e && e[0] == '3');
+  }();
+  return on;
 }
-static bool async_enabled_fwd() { return soft_mode() != 3; }
-static bool async_enabled_bwd() { return soft_mode() == 4; }
 
 // Grid for the tile-looped soft kernels: default one CTA per tile; SGX_GRID_FWD /
 // SGX_GRID_BWD cap it (a persistent grid walks tiles with a stride).
@@ -1470,44 +1240,12 @@ void launch_forward(cudaStream_t st, int vec, const int4* grp, const int2* lvl, 
   }
 }
 
-void launch_backward(cudaStream_t st, int vec, const int4* ops, const int2* lvl, int n_levels,
-                     const float* tape, float* adj, float* V, int ncols, int n_rows, float* dv_out,
-                     float* dp_out, int Bp, float lr, const int* out_enc, const uint8_t* out_tgt,
-                     int n_out, float* row_loss, const uint64_t* exp_tab) {
-  const int tiles = Bp / (32 * vec);
-  if (vec == 4 && async_enabled_bwd()) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_backward_async, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsyncSmemBwd);
-      attr = true;
-    }
-    k_backward_async<<<tiles, 32 * kWarps, kAsyncSmemBwd, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows,
-                                                            dv_out, dp_out, lr, out_enc, out_tgt, n_out,
-                                                            row_loss, exp_tab);
-    return;
-  }
-  static const int gcap = tile_grid("SGX_GRID_BWD", 1 << 30);
-  const int grid = gcap < tiles ? gcap : tiles;
-  switch (vec) {
-    case 4:
-      k_backward<4, SGX_BWD_U><<<grid, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows,
-                                                             dv_out, dp_out, lr, out_enc, out_tgt, n_out, row_loss,
-                                                             exp_tab, tiles);
-      break;
-    case 2:
-      k_backward<2, 8><<<grid, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows, dv_out,
-                                                     dp_out, lr, out_enc, out_tgt, n_out, row_loss, exp_tab, tiles);
-      break;
-    default:
-      k_backward<1, 8><<<grid, 32 * kWarps, 0, st>>>(ops, lvl, n_levels, tape, adj, V, ncols, n_rows, dv_out,
-                                                     dp_out, lr, out_enc, out_tgt, n_out, row_loss, exp_tab, tiles);
-  }
-}
 
 void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* lvl, int n_levels,
                          const float* tape, float* adj, float* V, int ncols, int n_rows, const int* col_row,
                          float* dv_out, float* dp_out, int Bp, float lr, const int* out_enc,
-                         const uint8_t* out_tgt, int n_out, float* row_loss, const uint64_t* exp_tab) {
+                         const uint8_t* out_tgt, int n_out, float* row_loss, const uint64_t* exp_tab,
+                         uint32_t* hb) {
   const int tiles = Bp / (32 * vec);
   static const int gcap = tile_grid("SGX_GRID_BWD", 1 << 30);
   const int grid = gcap < tiles ? gcap : tiles;
@@ -1515,17 +1253,17 @@ void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* 
     case 4:
       k_backward_rec<4, SGX_REC_U><<<grid, 32 * kWarps, 0, st>>>(rec, lvl, n_levels, tape, adj, V, ncols, n_rows,
                                                                  col_row, dv_out, dp_out, lr, out_enc, out_tgt,
-                                                                 n_out, row_loss, exp_tab, tiles);
+                                                                 n_out, row_loss, exp_tab, hb, tiles);
       break;
     case 2:
       k_backward_rec<2, 4><<<grid, 32 * kWarps, 0, st>>>(rec, lvl, n_levels, tape, adj, V, ncols, n_rows, col_row,
                                                          dv_out, dp_out, lr, out_enc, out_tgt, n_out, row_loss,
-                                                         exp_tab, tiles);
+                                                         exp_tab, hb, tiles);
       break;
     default:
       k_backward_rec<1, 4><<<grid, 32 * kWarps, 0, st>>>(rec, lvl, n_levels, tape, adj, V, ncols, n_rows, col_row,
                                                          dv_out, dp_out, lr, out_enc, out_tgt, n_out, row_loss,
-                                                         exp_tab, tiles);
+                                                         exp_tab, hb, tiles);
   }
 }
 
@@ -1595,7 +1333,7 @@ static void harvest_smem_t(cudaStream_t st, int grid, int n_rows, size_t smem, c
     opted = smem;
   }
   k_harvest_smem<WPC><<<grid, kThreads, smem, st>>>(
-      n_rows, a.V, a.ncpi, a.nucpi, a.cpi_row, a.ucpi_row, a.tile_rows, a.free_prefix, a.row_offset, a.ops, a.lvl_ptr,
+      n_rows, a.hb, a.ncpi, a.nucpi, a.cpi_row, a.ucpi_row, a.free_prefix, a.row_offset, a.ops, a.lvl_ptr,
       a.n_levels, a.out_enc, a.out_tgt, a.n_out, a.cnf4, a.cnf_steps, a.key_enc, a.key_words,
       a.batch, a.Bp, a.valid, a.K, a.slot_of_row, a.tkeys, a.tmeta, a.tmask, a.epoch);
 }

@@ -10,20 +10,18 @@ namespace sgx {
 struct HarvestOut;
 
 void launch_init_v(cudaStream_t st, float* V, int ncols, int Bp, int tile_rows, uint64_t prefix,
-                   long long row_offset);
+                   long long row_offset, uint32_t* hb);
 void launch_forward(cudaStream_t st, int vec, const int4* grp, const int2* lvl, int n_levels,
                     const float* src, int ncols, float* tape, int n_rows, int Bp, int src_is_prob,
                     const uint64_t* exp_tab);
-void launch_backward(cudaStream_t st, int vec, const int4* ops, const int2* lvl, int n_levels,
-                     const float* tape, float* adj, float* V, int ncols, int n_rows, float* dv_out,
-                     float* dp_out, int Bp, float lr, const int* out_enc, const uint8_t* out_tgt,
-                     int n_out, float* row_loss, const uint64_t* exp_tab);
 // Edge-record backward (sgx_layout.hpp kR* records); col_row[ncols] = tape row
-// of each V column's INPUT node (-1: outside the program).
+// of each V column's INPUT node (-1: outside the program).  With hb, the new V
+// is also hardened into hb[word][col] for the shared-memory harvest.
 void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* lvl, int n_levels,
                          const float* tape, float* adj, float* V, int ncols, int n_rows, const int* col_row,
                          float* dv_out, float* dp_out, int Bp, float lr, const int* out_enc,
-                         const uint8_t* out_tgt, int n_out, float* row_loss, const uint64_t* exp_tab);
+                         const uint8_t* out_tgt, int n_out, float* row_loss, const uint64_t* exp_tab,
+                         uint32_t* hb);
 void launch_loss(cudaStream_t st, const float* row_loss, int batch, double* partial, int n_partial,
                  HarvestOut* out);
 void launch_harden(cudaStream_t st, const float* V, int ncpi, int nucpi, const int* cpi_row,
@@ -43,10 +41,9 @@ void launch_append(cudaStream_t st, const uint32_t* newmask, const int* block_of
                    int key_words, int Bp, uint64_t* store, long long base, long long cap,
                    HarvestOut* out);
 struct HarvestSmemArgs {
-  const float* V;
+  const uint32_t* hb;  // hardened V columns [word][ncpi]
   int ncpi, nucpi;
   const int *cpi_row, *ucpi_row;
-  int tile_rows;
   uint64_t free_prefix;
   long long row_offset;
   const int4* ops;

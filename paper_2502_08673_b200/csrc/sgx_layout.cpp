@@ -223,10 +223,11 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
     run.push_back({x, P.row_of_node[e.consumer], other, 0});
   };
 
-  // Backward micro-op runs, levels high to low; a run is kept whole inside
-  // one warp's stream, runs go longest-first to the least loaded warp.
+  // Backward, levels high to low: each node's micro-op run (the reference's
+  // summation order) becomes edge records; a node's records stay whole
+  // inside one warp's stream, nodes go longest-first to the least loaded warp.
   for (int l = P.n_levels - 1; l >= 0; --l) {
-    std::vector<std::vector<I4>> runs;
+    std::vector<std::vector<I4>> recs;
     for (int i : by_level[l]) {
       int32_t k = L.kind[i];
       bool is_col_input = k == SGX_INPUT && col_of_node[i] >= 0;
@@ -248,28 +249,9 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
         run.push_back({kSubEnd | (L.kind[j] << kKindShift), 0, 0, 0});
       }
       run.push_back({kEnd, has_operands ? r : -1, is_col_input ? col_of_node[i] : -1, 0});
-      runs.push_back(std::move(run));
-    }
-    std::stable_sort(runs.begin(), runs.end(),
-                     [](const auto& x, const auto& y) { return x.size() > y.size(); });
-    std::vector<std::vector<I4>> per(kWarps);
-    for (auto& run : runs) {
-      int best = 0;
-      for (int w = 1; w < kWarps; ++w)
-        if (per[w].size() < per[best].size()) best = w;
-      per[best].insert(per[best].end(), run.begin(), run.end());
-    }
-    for (int w = 0; w < kWarps; ++w) {
-      P.bwd_lvl.push_back(static_cast<int32_t>(P.bwd.size()));
-      P.bwd_lvl.push_back(static_cast<int32_t>(per[w].size()));
-      P.bwd.insert(P.bwd.end(), per[w].begin(), per[w].end());
-    }
-    // The same runs as edge records, balanced by record count.
-    std::vector<std::vector<I4>> recs;
-    for (const auto& run : runs) {
-      std::vector<I4> r;
-      run_records(run, r);
-      recs.push_back(std::move(r));
+      std::vector<I4> rr;
+      run_records(run, rr);
+      recs.push_back(std::move(rr));
     }
     std::stable_sort(recs.begin(), recs.end(),
                      [](const auto& x, const auto& y) { return x.size() > y.size(); });
@@ -286,8 +268,7 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
       P.rec.insert(P.rec.end(), rper[w].begin(), rper[w].end());
     }
   }
-  // Slack so a chunk of kU records may read past the last op.
-  for (int k = 0; k < kU; ++k) P.bwd.push_back({kNop, -1, -1, 0});
+  // Slack so a chunk of records may read past the last one.
   for (int k = 0; k < kU; ++k) P.rec.push_back({0, -1, -1, 0});
   return P;
 }
@@ -547,7 +528,7 @@ void layout_info(const Layout& L, int64_t* info) {
   info[3] = L.cone.n_levels;
   info[4] = static_cast<int64_t>(L.bit_lvl_ptr.size()) - 1;
   info[5] = L.cone.n_rows;  // materialized (tape) rows after NOT/BUF folding
-  info[6] = static_cast<int64_t>(L.cone.bwd.size());
+  info[6] = static_cast<int64_t>(L.cone.rec.size());  // backward edge records
   info[7] = static_cast<int64_t>(L.bit_ops.size());
   info[8] = static_cast<int64_t>(L.clause_ptr.size()) - 1;
   info[9] = L.n_lits();

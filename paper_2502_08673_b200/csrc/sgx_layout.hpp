@@ -40,7 +40,8 @@ constexpr int kWarps = SGX_WARPS;  // warps per CTA sharing one sample tile (nod
 // then kGroup operand pairs (a, b) packed two per int4; an operand is
 // row << 1 | negate (negate = read through a folded NOT).  INPUT: a = V
 // column or -1 (= 0.5).  The group's outputs are rows first_out_row + [0, n).
-// Backward micro-op (int4), opcode in the low byte:
+// Backward micro-op (int4, host-side intermediate of the edge records), opcode
+// in the low byte:
 //   BEGIN     {kBegin | seed | target, row, 0, 0}
 //   EDGE      {kEdge | consumer_kind << 12 | neg_other | in_sub,
 //              adj_row_of_consumer, other_row (-1), 0}
@@ -85,10 +86,8 @@ struct SoftProgram {
   std::vector<int32_t> row_of_node;  // -1 if the node is not in the program
   std::vector<int32_t> node_of_row;
   std::vector<I4> fwd;               // groups, kGroupRecs records each
-  std::vector<I4> bwd;               // micro-ops
   std::vector<int32_t> fwd_lvl;      // per (level, warp): first group, group count
-  std::vector<int32_t> bwd_lvl;      // per (level high to low, warp): first op, op count
-  std::vector<I4> rec;               // edge records (same runs as bwd)
+  std::vector<I4> rec;               // backward edge records
   std::vector<int32_t> rec_lvl;      // per (level high to low, warp): first record, count
   std::vector<int32_t> out_enc;      // each output as row << 1 | negate (-1: not in set)
   std::vector<int32_t> col_row;      // tape row of each V column's INPUT node
