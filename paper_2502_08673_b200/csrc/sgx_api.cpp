@@ -133,8 +133,8 @@ std::vector<int2> to_int2(const std::vector<int32_t>& v) {
 
 struct DevSoft {
   DBuf<int4> fwd, rec;
-  DBuf<int2> fwd_lvl, rec_lvl;
-  DBuf<int> out_enc, col_row;
+  DBuf<int2> fwd_lvl, rec_lvl, dead_lvl;
+  DBuf<int> out_enc, col_row, dead;
   int n_fwd_levels = 0, n_bwd_levels = 0, n_rows = 0;
   void upload(const sgx::SoftProgram& P, cudaStream_t st) {
     fwd.upload(to_int4(P.fwd), st);
@@ -143,6 +143,8 @@ struct DevSoft {
     rec_lvl.upload(to_int2(P.rec_lvl), st);
     out_enc.upload(P.out_enc, st);
     col_row.upload(P.col_row, st);
+    dead.upload(P.dead.empty() ? std::vector<int32_t>{-1} : P.dead, st);
+    dead_lvl.upload(to_int2(P.dead_lvl), st);
     n_fwd_levels = static_cast<int>(P.fwd_lvl.size() / (2 * sgx::kWarps));
     n_bwd_levels = static_cast<int>(P.rec_lvl.size() / (2 * sgx::kWarps));
     n_rows = P.n_rows;
@@ -153,7 +155,8 @@ void backward(cudaStream_t st, int vec, const DevSoft& P, const float* tape, flo
               float* dv_out, float* dp_out, int Bp, float lr, const uint8_t* out_tgt, int n_out, float* row_loss,
               const uint64_t* tab, uint32_t* hb) {
   sgx::launch_backward_rec(st, vec, P.rec.p, P.rec_lvl.p, P.n_bwd_levels, tape, adj, V, ncols, P.n_rows,
-                           P.col_row.p, dv_out, dp_out, Bp, lr, P.out_enc.p, out_tgt, n_out, row_loss, tab, hb);
+                           P.col_row.p, dv_out, dp_out, Bp, lr, P.out_enc.p, out_tgt, n_out, row_loss, tab, hb,
+                           P.dead.p, P.dead_lvl.p);
 }
 
 }  // namespace

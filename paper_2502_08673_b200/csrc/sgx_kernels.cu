@@ -280,6 +280,41 @@ __device__ __forceinline__ void vload_nc(const float* p, float (&o)[V]) {
   }
 }
 
+// Column epilogue of the backward, shared by the register and the staged
+// kernels: dV = g p (1 - p) (autodiff.cpp:212-221), V -= lr dV (gd_step,
+// :285-290), and the hardened new V into hb[word][col].
+template <int V, int UC>
+__device__ __forceinline__ void backward_columns(int warp, int lane, int tile, const float* A, float* Vp, size_t vbase,
+                                                 int ncols, const int* __restrict__ col_row, float* dv_out,
+                                                 float* dp_out, float lr, const uint64_t* __restrict__ exp_tab,
+                                                 uint32_t* __restrict__ hb) {
+  constexpr int TILE = 32 * V;
+  for (int j0 = warp * UC; j0 < ncols; j0 += kWarps * UC) {
+    int rw[UC];
+    float x[UC][V], gg[UC][V];
+#pragma unroll
+    for (int q = 0; q < UC; ++q) {
+      rw[q] = j0 + q < ncols ? __ldg(col_row + j0 + q) : -1;
+      if (rw[q] >= 0) {
+        vload<V>(A + static_cast<size_t>(rw[q]) * TILE, gg[q]);
+        vload<V>(Vp + vbase + static_cast<size_t>(j0 + q) * TILE, x[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < UC; ++q)
+      if (rw[q] >= 0) {  // warp-uniform
+        float nv[V];
+        input_end<V>(x[q], gg[q], lr, exp_tab, vbase + static_cast<size_t>(j0 + q) * TILE, Vp, dv_out, dp_out, nv);
+        if (hb) {  // harden (autodiff.cpp:292-297): bit = V >= 0, NaN -> 0
+          uint32_t b[V];
+#pragma unroll
+          for (int v = 0; v < V; ++v) b[v] = __ballot_sync(kFull, nv[v] >= 0.0f);
+          if (lane < V) hb[(static_cast<size_t>(tile) * V + lane) * ncols + j0 + q] = pack_word<V>(b, lane);
+        }
+      }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K3+K4+K5a: per-row loss, pull-CSR backward, fused GD step and harden.
 // Same tile and level split as the forward, levels high to low; no atomics:
@@ -309,7 +344,7 @@ __device__ __forceinline__ void vload_nc(const float* p, float (&o)[V]) {
 #define SGX_REC_U 4  // records per chunk at 4 samples per lane (C2 backward: 4 -> 40.7, 6 -> 41.9, 8 -> 46.2 ms per 5 restarts)
 #endif
 template <int V, int U>
-__global__ void __launch_bounds__(32 * kWarps, 16 / V)
+__global__ void __launch_bounds__(32 * kWarps, (64 / (V * kWarps)) > 0 ? 64 / (V * kWarps) : 1)
 k_backward_rec(const int4* __restrict__ rec, const int2* __restrict__ lvl, int n_levels,
                const float* __restrict__ tape, float* adj, float* Vp, int ncols, int n_rows,
                const int* __restrict__ col_row, float* dv_out, float* dp_out, float lr,
@@ -395,31 +430,7 @@ k_backward_rec(const int4* __restrict__ rec, const int2* __restrict__ lvl, int n
     }
     // V columns: dV = g p (1 - p) (autodiff.cpp:212-221), V -= lr dV (gd_step, :285-290).
     constexpr int UC = V == 4 ? SGX_REC_UC : 1;  // narrower tiles run at 16/V CTAs per SM: no room
-    for (int j0 = warp * UC; j0 < ncols; j0 += kWarps * UC) {
-      int rw[UC];
-      float x[UC][V], gg[UC][V];
-#pragma unroll
-      for (int q = 0; q < UC; ++q) {
-        rw[q] = j0 + q < ncols ? __ldg(col_row + j0 + q) : -1;
-        if (rw[q] >= 0) {
-          vload<V>(A + static_cast<size_t>(rw[q]) * TILE, gg[q]);
-          vload<V>(Vp + vbase + static_cast<size_t>(j0 + q) * TILE, x[q]);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < UC; ++q)
-        if (rw[q] >= 0) {  // warp-uniform
-          float nv[V];
-          input_end<V>(x[q], gg[q], lr, exp_tab, vbase + static_cast<size_t>(j0 + q) * TILE, Vp, dv_out, dp_out,
-                       nv);
-          if (hb) {  // harden (autodiff.cpp:292-297): bit = V >= 0, NaN -> 0
-            uint32_t b[V];
-#pragma unroll
-            for (int v = 0; v < V; ++v) b[v] = __ballot_sync(kFull, nv[v] >= 0.0f);
-            if (lane < V) hb[(static_cast<size_t>(tile) * V + lane) * ncols + j0 + q] = pack_word<V>(b, lane);
-          }
-        }
-    }
+    backward_columns<V, UC>(warp, lane, tile, A, Vp, vbase, ncols, col_row, dv_out, dp_out, lr, exp_tab, hb);
     if (n_tiles > static_cast<int>(gridDim.x)) __syncthreads();
   }
 }
@@ -442,6 +453,32 @@ constexpr int kAsyncSmem = kWarps * kStages * kSlots * 32 * 16;  // bytes per CT
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+// L2 eviction-priority policies (createpolicy): tape rows the backward
+// streams are read evict_first, adjoint rows it will re-read soon are stored
+// evict_last, so the L2 keeps adjoints rather than tape.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, uint64_t pol) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_hint(float* p, const float (&o)[4], uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;\n" ::"l"(p), "f"(o[0]), "f"(o[1]),
+               "f"(o[2]), "f"(o[3]), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(p) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -591,6 +628,200 @@ k_forward_async(const int4* __restrict__ grp, const int2* __restrict__ lvl, int 
     __syncthreads();
   }
   }  // tile loop
+}
+
+// ---------------------------------------------------------------------------
+// The backward with its edge operands staged through shared memory by
+// cp.async.  Same records, order and arithmetic as k_backward_rec (so the
+// same bits); what changes is the memory pipeline.  Per warp, a ring of BS
+// stages of BU records each: the adjoint row of the consumer (g) and the
+// value row of the other operand (y) of every record land in the lane's own
+// 16-byte slots while the warp computes BS-1 chunks behind, so a level's
+// loads are all in flight instead of one chunk's.  The records of the chunk
+// after the next issue are prefetched into registers, so issuing never waits
+// on a record load either.  Only the level barrier drains the ring: the next
+// level's adjoint reads depend on this level's stores.
+// ---------------------------------------------------------------------------
+#ifndef SGX_BU
+#define SGX_BU 4
+#endif
+#ifndef SGX_BS
+#define SGX_BS 3
+#endif
+#ifndef SGX_HINT_Y
+#define SGX_HINT_Y 1
+#endif
+#ifndef SGX_HINT_ADJ
+#define SGX_HINT_ADJ 1
+#endif
+constexpr int kBU = SGX_BU, kBS = SGX_BS;
+constexpr int kBwdSmem = kWarps * kBS * kBU * 2 * 32 * 16;  // bytes per CTA
+
+__global__ void __launch_bounds__(32 * kWarps)
+k_backward_async(const int4* __restrict__ rec, const int2* __restrict__ lvl, int n_levels,
+                 const float* __restrict__ tape, float* adj, float* Vp, int ncols, int n_rows,
+                 const int* __restrict__ col_row, float* dv_out, float* dp_out, float lr,
+                 const int* __restrict__ out_enc, const uint8_t* __restrict__ out_tgt, int n_out,
+                 float* __restrict__ row_loss, const uint64_t* __restrict__ exp_tab, uint32_t* __restrict__ hb,
+                 int n_tiles, const int* __restrict__ dead, const int2* __restrict__ dead_lvl) {
+  constexpr int V = 4, TILE = 128;
+  extern __shared__ float4 bstage[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float4* my = bstage + warp * kBS * kBU * 2 * 32 + lane;  // slot (d, k, j): my[((d * kBU + k) * 2 + j) * 32]
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const size_t tbase = static_cast<size_t>(tile) * n_rows * TILE + lane * V;
+    const float* T = tape + tbase;
+    float* A = adj + tbase;
+    float* Abase = adj + static_cast<size_t>(tile) * n_rows * TILE;
+    const size_t vbase = static_cast<size_t>(tile) * ncols * TILE + lane * V;
+    if (row_loss && warp == 0) {  // loss (autodiff.cpp:160-166): outputs in order
+      float l[V] = {0.0f, 0.0f, 0.0f, 0.0f};
+      for (int m = 0; m < n_out; ++m) {
+        float yv[V];
+        load_operand<V>(T, __ldg(out_enc + m), yv);
+        const float t = __ldg(out_tgt + m) ? 1.0f : 0.0f;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const float d = __fsub_rn(yv[v], t);
+          l[v] = __fadd_rn(l[v], __fmul_rn(d, d));
+        }
+      }
+      vstore<V>(row_loss + static_cast<size_t>(tile) * TILE + lane * V, l);
+    }
+    float acc[V], acc2[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = acc2[v] = 0.0f;
+    for (int li = 0; li < n_levels; ++li) {
+      const int2 L = __ldg(lvl + li * kWarps + warp);
+      const int nch = (L.y + kBU - 1) / kBU;
+      const int4* R = rec + L.x;
+      int4 pre[kBU];  // records of the next chunk to issue
+      auto fetch = [&](int ch) {
+#pragma unroll
+        for (int k = 0; k < kBU; ++k)
+          pre[k] = ch * kBU + k < L.y ? __ldg(R + ch * kBU + k) : make_int4(0, -1, -1, 0);
+      };
+      auto issue = [&](int d) {
+        float4* base = my + d * kBU * 2 * 32;
+#pragma unroll
+        for (int k = 0; k < kBU; ++k) {
+          if (pre[k].y >= 0) cp_async16(base + (2 * k) * 32, A + static_cast<size_t>(pre[k].y) * TILE);
+          if (pre[k].z >= 0) {
+            if (SGX_HINT_Y)
+              cp_async16_hint(base + (2 * k + 1) * 32, T + static_cast<size_t>(pre[k].z) * TILE, pol_first);
+            else
+              cp_async16(base + (2 * k + 1) * 32, T + static_cast<size_t>(pre[k].z) * TILE);
+          } else {
+            base[(2 * k + 1) * 32] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);  // unary consumer: c1 * 0
+          }
+        }
+        cp_async_commit();
+      };
+      fetch(0);
+#pragma unroll
+      for (int i = 0; i < kBS - 1; ++i) {
+        if (i < nch) {
+          issue(i);
+          fetch(i + 1);
+        } else {
+          cp_async_commit();
+        }
+      }
+      for (int ch = 0; ch < nch; ++ch) {
+        const int nxt = ch + kBS - 1;
+        if (nxt < nch) {
+          issue(nxt % kBS);
+          fetch(nxt + 1);
+        } else {
+          cp_async_commit();
+        }
+        cp_async_wait<kBS - 1>();
+        const float4* base = my + (ch % kBS) * kBU * 2 * 32;
+#pragma unroll
+        for (int k = 0; k < kBU; ++k) {
+          const int4 r = ch * kBU + k < L.y ? __ldg(R + ch * kBU + k) : make_int4(0, -1, -1, 0);
+          const int f = r.x;
+          float g[V], y[V];
+          f4(base[(2 * k) * 32], g);
+          f4(base[(2 * k + 1) * 32], y);
+          // Pull factor c0 + c1*vo of the consumer kind, vo = y or 1 - y
+          // (other operand read through a folded NOT): both fmas round
+          // exactly as the reference's (1 - v), (1 - 2v), ... (c1*vo exact).
+          const float4 C = kRecC[f & 0xf];  // {c0, c1} of the consumer kind (the a-side half)
+          const float ns = (f & kRNegOther) ? -1.0f : 1.0f, no = (f & kRNegOther) ? 1.0f : 0.0f;
+          if (!(f & kRSlow)) {  // plain edge into this node's adjoint (most records)
+            if (f & kRFirst) {
+#pragma unroll
+              for (int v = 0; v < V; ++v) acc[v] = 0.0f;
+            }
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              const float fa = __fmaf_rn(C.y, __fmaf_rn(ns, y[v], no), C.x);
+              acc[v] = __fadd_rn(acc[v], __fmul_rn(g[v], fa));
+            }
+          } else {  // seeds, SUB runs (folded NOT/BUF consumers), empty nodes
+            if (f & (kRFirst | kRSubFirst)) {
+              float sd[V] = {0.0f, 0.0f, 0.0f, 0.0f}, sd2[V] = {0.0f, 0.0f, 0.0f, 0.0f};
+              if (f & (kRSeed | kRSubSeed)) {  // adj[out] += 2 (y - t) on a zero adjoint (autodiff.cpp:206)
+                float yw[V];
+                vload_nc<V>(T + static_cast<size_t>(r.w) * TILE, yw);
+                const float t = (f & kRTarget) ? 1.0f : 0.0f, t2 = (f & kRSubTarget) ? 1.0f : 0.0f;
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                  if (f & kRSeed) sd[v] = __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(yw[v], t)));
+                  if (f & kRSubSeed) {
+                    const float ys = (f & kRNegSelf) ? __fsub_rn(1.0f, yw[v]) : yw[v];
+                    sd2[v] = __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(ys, t2)));
+                  }
+                }
+              }
+#pragma unroll
+              for (int v = 0; v < V; ++v) {
+                if (f & kRFirst) acc[v] = sd[v];
+                if (f & kRSubFirst) acc2[v] = sd2[v];
+              }
+            }
+            if (r.y >= 0) {
+#pragma unroll
+              for (int v = 0; v < V; ++v) {
+                const float t = __fmul_rn(g[v], __fmaf_rn(C.y, __fmaf_rn(ns, y[v], no), C.x));
+                if (f & kRInSub)
+                  acc2[v] = __fadd_rn(acc2[v], t);
+                else
+                  acc[v] = __fadd_rn(acc[v], t);
+              }
+            }
+            if (f & kRSubLast) {  // adj[i] += -adj[j] (NOT) / +adj[j] (BUF), autodiff.cpp:225-233
+#pragma unroll
+              for (int v = 0; v < V; ++v)
+                acc[v] = (f & kRSubNot) ? __fsub_rn(acc[v], acc2[v]) : __fadd_rn(acc[v], acc2[v]);
+            }
+          }
+          if (f & kRLast) {
+            if (SGX_HINT_ADJ)
+              st_hint(A + static_cast<size_t>(r.w) * TILE, acc, pol_last);
+            else
+              vstore<V>(A + static_cast<size_t>(r.w) * TILE, acc);
+          }
+        }
+      }
+      __syncthreads();
+      if (dead) {  // adjoints whose last reader ran in this pass: drop from L2, no write-back
+        const int2 D = __ldg(dead_lvl + li);
+        for (int i = threadIdx.x; i < 4 * D.y; i += 32 * kWarps)
+          discard_l2(Abase + static_cast<size_t>(__ldg(dead + D.x + (i >> 2))) * TILE + (i & 3) * 32);
+      }
+    }
+    backward_columns<V, SGX_REC_UC>(warp, lane, tile, A, Vp, vbase, ncols, col_row, dv_out, dp_out, lr, exp_tab, hb);
+    __syncthreads();
+    if (dead) {
+      for (int i = threadIdx.x; i < 4 * ncols; i += 32 * kWarps) {
+        const int rw = __ldg(col_row + (i >> 2));
+        if (rw >= 0) discard_l2(Abase + static_cast<size_t>(rw) * TILE + (i & 3) * 32);
+      }
+    }
+  }
 }
 
 
@@ -1241,14 +1472,39 @@ void launch_forward(cudaStream_t st, int vec, const int4* grp, const int2* lvl, 
 }
 
 
+// SGX_DISCARD=0 keeps dead adjoints in L2 (A/B of the discard lists).
+static bool discard_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SGX_DISCARD");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* lvl, int n_levels,
                          const float* tape, float* adj, float* V, int ncols, int n_rows, const int* col_row,
                          float* dv_out, float* dp_out, int Bp, float lr, const int* out_enc,
                          const uint8_t* out_tgt, int n_out, float* row_loss, const uint64_t* exp_tab,
-                         uint32_t* hb) {
+                         uint32_t* hb, const int* dead, const int2* dead_lvl) {
   const int tiles = Bp / (32 * vec);
   static const int gcap = tile_grid("SGX_GRID_BWD", 1 << 30);
   const int grid = gcap < tiles ? gcap : tiles;
+  static const bool staged = [] {  // SGX_BWD=reg forces the register-pipelined kernel
+    const char* e = std::getenv("SGX_BWD");
+    return !(e && e[0] == 'r');
+  }();
+  if (vec == 4 && staged) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_backward_async, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
+      attr = true;
+    }
+    k_backward_async<<<grid, 32 * kWarps, kBwdSmem, st>>>(rec, lvl, n_levels, tape, adj, V, ncols, n_rows, col_row,
+                                                          dv_out, dp_out, lr, out_enc, out_tgt, n_out, row_loss,
+                                                          exp_tab, hb, tiles, discard_enabled() ? dead : nullptr,
+                                                          dead_lvl);
+    return;
+  }
   switch (vec) {
     case 4:
       k_backward_rec<4, SGX_REC_U><<<grid, 32 * kWarps, 0, st>>>(rec, lvl, n_levels, tape, adj, V, ncols, n_rows,

@@ -21,7 +21,7 @@ void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* 
                          const float* tape, float* adj, float* V, int ncols, int n_rows, const int* col_row,
                          float* dv_out, float* dp_out, int Bp, float lr, const int* out_enc,
                          const uint8_t* out_tgt, int n_out, float* row_loss, const uint64_t* exp_tab,
-                         uint32_t* hb);
+                         uint32_t* hb, const int* dead, const int2* dead_lvl);
 void launch_loss(cudaStream_t st, const float* row_loss, int batch, double* partial, int n_partial,
                  HarvestOut* out);
 void launch_harden(cudaStream_t st, const float* V, int ncpi, int nucpi, const int* cpi_row,

@@ -67,6 +67,8 @@ void run_records(const std::vector<I4>& run, std::vector<I4>& out) {
       if (o.y >= 0 || o.z >= 0) out.back().x |= kRLast;
     }
   }
+  for (size_t k = start; k < out.size(); ++k)
+    if ((out[k].x & (kRInSub | kRSubFirst | kRSubLast | kRSeed | kRSubSeed)) || out[k].y < 0) out[k].x |= kRSlow;
 }
 
 // Soft program over the nodes with in_set[i] != 0 (closed under operands).
@@ -266,6 +268,29 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
       P.rec_lvl.push_back(static_cast<int32_t>(P.rec.size()));
       P.rec_lvl.push_back(static_cast<int32_t>(rper[w].size()));
       P.rec.insert(P.rec.end(), rper[w].begin(), rper[w].end());
+    }
+  }
+  // Dead-adjoint lists: the last pass reading each adjoint row (a record's
+  // .y), passes numbered in backward order.
+  {
+    const int nl = P.n_levels;
+    std::vector<int32_t> last(P.n_rows, -1);
+    for (int li = 0; li < nl; ++li)
+      for (int w = 0; w < kWarps; ++w) {
+        const int32_t first = P.rec_lvl[2 * (li * kWarps + w)], cnt = P.rec_lvl[2 * (li * kWarps + w) + 1];
+        for (int32_t k = first; k < first + cnt; ++k)
+          if (P.rec[k].y >= 0) last[P.rec[k].y] = li;
+      }
+    std::vector<uint8_t> is_col(P.n_rows, 0);
+    for (int32_t r : P.col_row)
+      if (r >= 0) is_col[r] = 1;
+    std::vector<std::vector<int32_t>> by(nl);
+    for (int32_t r = 0; r < P.n_rows; ++r)
+      if (last[r] >= 0 && !is_col[r]) by[last[r]].push_back(r);
+    for (int li = 0; li < nl; ++li) {
+      P.dead_lvl.push_back(static_cast<int32_t>(P.dead.size()));
+      P.dead_lvl.push_back(static_cast<int32_t>(by[li].size()));
+      P.dead.insert(P.dead.end(), by[li].begin(), by[li].end());
     }
   }
   // Slack so a chunk of records may read past the last one.

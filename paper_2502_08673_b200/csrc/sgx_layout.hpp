@@ -69,6 +69,10 @@ constexpr int32_t kSeedBit = 1 << 8, kTargetBit = 1 << 9, kNegOtherBit = 1 << 10
 constexpr int32_t kRInSub = 1 << 4, kRNegOther = 1 << 5, kRFirst = 1 << 6, kRSubFirst = 1 << 7,
                   kRSubLast = 1 << 8, kRSubNot = 1 << 9, kRSeed = 1 << 10, kRTarget = 1 << 11,
                   kRSubSeed = 1 << 12, kRSubTarget = 1 << 13, kRNegSelf = 1 << 14, kRLast = 1 << 15;
+// kRSlow: anything but a plain edge into the node's own accumulator (seeds,
+// SUB-run records, records without an edge) -- the staged kernel's fast path
+// is taken only without it.
+constexpr int32_t kRSlow = 1 << 16;
 constexpr int kCnfThreads = 256;               // threads of the shared-memory harvest CTA
 constexpr int32_t kCnfOpen = INT32_MIN;        // CNF record continues (see fb_cnf4)
 constexpr int kGroup = 4;                      // ops per forward group
@@ -89,6 +93,12 @@ struct SoftProgram {
   std::vector<int32_t> fwd_lvl;      // per (level, warp): first group, group count
   std::vector<I4> rec;               // backward edge records
   std::vector<int32_t> rec_lvl;      // per (level high to low, warp): first record, count
+  // Adjoint rows whose last reader runs in backward pass li (levels high to
+  // low): after that pass's barrier the rows are dead and are discarded from
+  // L2 without write-back (discard.global.L2).  Column-input rows are read by
+  // the V epilogue and discarded after it.
+  std::vector<int32_t> dead;         // rows, grouped by pass
+  std::vector<int32_t> dead_lvl;     // per pass: first index into dead, count
   std::vector<int32_t> out_enc;      // each output as row << 1 | negate (-1: not in set)
   std::vector<int32_t> col_row;      // tape row of each V column's INPUT node
   std::vector<int32_t> virt_base;    // folded node -> row of its operand (-1 otherwise)
