@@ -134,7 +134,9 @@ std::vector<int2> to_int2(const std::vector<int32_t>& v) {
 struct DevSoft {
   DBuf<int4> fwd, rec;
   DBuf<int2> fwd_lvl, rec_lvl, dead_lvl;
-  DBuf<int> out_enc, col_row, dead;
+  DBuf<int> out_enc, col_row, dead, tail_dead;
+  DBuf<int4> sblk;
+  sgx::BwdBlocks bb;
   int n_fwd_levels = 0, n_bwd_levels = 0, n_rows = 0;
   void upload(const sgx::SoftProgram& P, cudaStream_t st) {
     fwd.upload(to_int4(P.fwd), st);
@@ -145,6 +147,16 @@ struct DevSoft {
     col_row.upload(P.col_row, st);
     dead.upload(P.dead.empty() ? std::vector<int32_t>{-1} : P.dead, st);
     dead_lvl.upload(to_int2(P.dead_lvl), st);
+    sblk.upload(to_int4(P.sblk), st);
+    tail_dead.upload(P.tail_dead.empty() ? std::vector<int32_t>{-1} : P.tail_dead, st);
+    bb = sgx::BwdBlocks{};
+    if (!P.sblk.empty()) {
+      bb.sblk = sblk.p;
+      bb.blk0_n4 = P.sblk_lvl[1];
+      bb.blk_max = P.sblk_max;
+      bb.tail_dead = tail_dead.p;
+      bb.n_tail_dead = static_cast<int>(P.tail_dead.size());
+    }
     n_fwd_levels = static_cast<int>(P.fwd_lvl.size() / (2 * sgx::kWarps));
     n_bwd_levels = static_cast<int>(P.rec_lvl.size() / (2 * sgx::kWarps));
     n_rows = P.n_rows;
@@ -156,7 +168,7 @@ void backward(cudaStream_t st, int vec, const DevSoft& P, const float* tape, flo
               const uint64_t* tab, uint32_t* hb) {
   sgx::launch_backward_rec(st, vec, P.rec.p, P.rec_lvl.p, P.n_bwd_levels, tape, adj, V, ncols, P.n_rows,
                            P.col_row.p, dv_out, dp_out, Bp, lr, P.out_enc.p, out_tgt, n_out, row_loss, tab, hb,
-                           P.dead.p, P.dead_lvl.p);
+                           P.dead.p, P.dead_lvl.p, &P.bb);
 }
 
 }  // namespace

@@ -657,6 +657,79 @@ k_forward_async(const int4* __restrict__ grp, const int2* __restrict__ lvl, int 
 constexpr int kBU = SGX_BU, kBS = SGX_BS;
 constexpr int kBwdSmem = kWarps * kBS * kBU * 2 * 32 * 16;  // bytes per CTA
 
+// One backward edge record (sgx_layout.hpp kR* flags) on a lane's 4 samples,
+// g = adjoint row of the consumer, y = value row of the other operand (both
+// staged on chip).  Plain edges take a 4-op path; seeds, SUB runs and
+// edge-less records branch (warp-uniform) and follow the reference's
+// operations exactly.
+__device__ __forceinline__ void backward_record(const int4 r, const float4 gs, const float4 ys, float (&acc)[4],
+                                                float (&acc2)[4], const float* T, float* A, uint64_t pol_last) {
+  constexpr int V = 4, TILE = 128;
+  const int f = r.x;
+  float g[V], y[V];
+  f4(gs, g);
+  f4(ys, y);
+          // Pull factor c0 + c1*vo of the consumer kind, vo = y or 1 - y
+          // (other operand read through a folded NOT): both fmas round
+          // exactly as the reference's (1 - v), (1 - 2v), ... (c1*vo exact).
+          const float4 C = kRecC[f & 0xf];  // {c0, c1} of the consumer kind (the a-side half)
+          const float ns = (f & kRNegOther) ? -1.0f : 1.0f, no = (f & kRNegOther) ? 1.0f : 0.0f;
+          if (!(f & kRSlow)) {  // plain edge into this node's adjoint (most records)
+            if (f & kRFirst) {
+#pragma unroll
+              for (int v = 0; v < V; ++v) acc[v] = 0.0f;
+            }
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              const float fa = __fmaf_rn(C.y, __fmaf_rn(ns, y[v], no), C.x);
+              acc[v] = __fadd_rn(acc[v], __fmul_rn(g[v], fa));
+            }
+          } else {  // seeds, SUB runs (folded NOT/BUF consumers), empty nodes
+            if (f & (kRFirst | kRSubFirst)) {
+              float sd[V] = {0.0f, 0.0f, 0.0f, 0.0f}, sd2[V] = {0.0f, 0.0f, 0.0f, 0.0f};
+              if (f & (kRSeed | kRSubSeed)) {  // adj[out] += 2 (y - t) on a zero adjoint (autodiff.cpp:206)
+                float yw[V];
+                vload_nc<V>(T + static_cast<size_t>(r.w) * TILE, yw);
+                const float t = (f & kRTarget) ? 1.0f : 0.0f, t2 = (f & kRSubTarget) ? 1.0f : 0.0f;
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                  if (f & kRSeed) sd[v] = __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(yw[v], t)));
+                  if (f & kRSubSeed) {
+                    const float ys = (f & kRNegSelf) ? __fsub_rn(1.0f, yw[v]) : yw[v];
+                    sd2[v] = __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(ys, t2)));
+                  }
+                }
+              }
+#pragma unroll
+              for (int v = 0; v < V; ++v) {
+                if (f & kRFirst) acc[v] = sd[v];
+                if (f & kRSubFirst) acc2[v] = sd2[v];
+              }
+            }
+            if (r.y >= 0) {
+#pragma unroll
+              for (int v = 0; v < V; ++v) {
+                const float t = __fmul_rn(g[v], __fmaf_rn(C.y, __fmaf_rn(ns, y[v], no), C.x));
+                if (f & kRInSub)
+                  acc2[v] = __fadd_rn(acc2[v], t);
+                else
+                  acc[v] = __fadd_rn(acc[v], t);
+              }
+            }
+            if (f & kRSubLast) {  // adj[i] += -adj[j] (NOT) / +adj[j] (BUF), autodiff.cpp:225-233
+#pragma unroll
+              for (int v = 0; v < V; ++v)
+                acc[v] = (f & kRSubNot) ? __fsub_rn(acc[v], acc2[v]) : __fadd_rn(acc[v], acc2[v]);
+            }
+          }
+          if (f & kRLast) {
+            if (SGX_HINT_ADJ)
+              st_hint(A + static_cast<size_t>(r.w) * TILE, acc, pol_last);
+            else
+              vstore<V>(A + static_cast<size_t>(r.w) * TILE, acc);
+          }
+}
+
 __global__ void __launch_bounds__(32 * kWarps)
 k_backward_async(const int4* __restrict__ rec, const int2* __restrict__ lvl, int n_levels,
                  const float* __restrict__ tape, float* adj, float* Vp, int ncols, int n_rows,
@@ -741,69 +814,7 @@ k_backward_async(const int4* __restrict__ rec, const int2* __restrict__ lvl, int
 #pragma unroll
         for (int k = 0; k < kBU; ++k) {
           const int4 r = ch * kBU + k < L.y ? __ldg(R + ch * kBU + k) : make_int4(0, -1, -1, 0);
-          const int f = r.x;
-          float g[V], y[V];
-          f4(base[(2 * k) * 32], g);
-          f4(base[(2 * k + 1) * 32], y);
-          // Pull factor c0 + c1*vo of the consumer kind, vo = y or 1 - y
-          // (other operand read through a folded NOT): both fmas round
-          // exactly as the reference's (1 - v), (1 - 2v), ... (c1*vo exact).
-          const float4 C = kRecC[f & 0xf];  // {c0, c1} of the consumer kind (the a-side half)
-          const float ns = (f & kRNegOther) ? -1.0f : 1.0f, no = (f & kRNegOther) ? 1.0f : 0.0f;
-          if (!(f & kRSlow)) {  // plain edge into this node's adjoint (most records)
-            if (f & kRFirst) {
-#pragma unroll
-              for (int v = 0; v < V; ++v) acc[v] = 0.0f;
-            }
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-              const float fa = __fmaf_rn(C.y, __fmaf_rn(ns, y[v], no), C.x);
-              acc[v] = __fadd_rn(acc[v], __fmul_rn(g[v], fa));
-            }
-          } else {  // seeds, SUB runs (folded NOT/BUF consumers), empty nodes
-            if (f & (kRFirst | kRSubFirst)) {
-              float sd[V] = {0.0f, 0.0f, 0.0f, 0.0f}, sd2[V] = {0.0f, 0.0f, 0.0f, 0.0f};
-              if (f & (kRSeed | kRSubSeed)) {  // adj[out] += 2 (y - t) on a zero adjoint (autodiff.cpp:206)
-                float yw[V];
-                vload_nc<V>(T + static_cast<size_t>(r.w) * TILE, yw);
-                const float t = (f & kRTarget) ? 1.0f : 0.0f, t2 = (f & kRSubTarget) ? 1.0f : 0.0f;
-#pragma unroll
-                for (int v = 0; v < V; ++v) {
-                  if (f & kRSeed) sd[v] = __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(yw[v], t)));
-                  if (f & kRSubSeed) {
-                    const float ys = (f & kRNegSelf) ? __fsub_rn(1.0f, yw[v]) : yw[v];
-                    sd2[v] = __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(ys, t2)));
-                  }
-                }
-              }
-#pragma unroll
-              for (int v = 0; v < V; ++v) {
-                if (f & kRFirst) acc[v] = sd[v];
-                if (f & kRSubFirst) acc2[v] = sd2[v];
-              }
-            }
-            if (r.y >= 0) {
-#pragma unroll
-              for (int v = 0; v < V; ++v) {
-                const float t = __fmul_rn(g[v], __fmaf_rn(C.y, __fmaf_rn(ns, y[v], no), C.x));
-                if (f & kRInSub)
-                  acc2[v] = __fadd_rn(acc2[v], t);
-                else
-                  acc[v] = __fadd_rn(acc[v], t);
-              }
-            }
-            if (f & kRSubLast) {  // adj[i] += -adj[j] (NOT) / +adj[j] (BUF), autodiff.cpp:225-233
-#pragma unroll
-              for (int v = 0; v < V; ++v)
-                acc[v] = (f & kRSubNot) ? __fsub_rn(acc[v], acc2[v]) : __fadd_rn(acc[v], acc2[v]);
-            }
-          }
-          if (f & kRLast) {
-            if (SGX_HINT_ADJ)
-              st_hint(A + static_cast<size_t>(r.w) * TILE, acc, pol_last);
-            else
-              vstore<V>(A + static_cast<size_t>(r.w) * TILE, acc);
-          }
+          backward_record(r, base[(2 * k) * 32], base[(2 * k + 1) * 32], acc, acc2, T, A, pol_last);
         }
       }
       __syncthreads();
@@ -824,6 +835,152 @@ k_backward_async(const int4* __restrict__ rec, const int2* __restrict__ lvl, int
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// TMA-fed backward.  Like k_backward_async, but the control stream is on
+// chip too: each pass's block (sgx_layout.hpp sblk: header, per-warp record
+// ranges, records, the previous pass's dead adjoint rows) arrives by one
+// cp.async.bulk into a double buffer, completion on an mbarrier, issued one
+// pass ahead by thread 0.  Record reads (issue side and compute side) and
+// the dead-row list are shared-memory broadcasts, so no load in the loop
+// waits on L2 except the staged data rows themselves.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned phase) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(m)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+// Thread-0 only: bring n4 int4s at src into dst, completing on m.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned n4, uint64_t* m) {
+  const unsigned bytes = n4 * 16u;
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(m))
+               : "memory");
+}
+
+template <int BS>
+__global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
+k_backward_tma(const int4* __restrict__ sblk, int blk0_n4, int blk_max, int n_levels, const float* __restrict__ tape,
+               float* adj, float* Vp, int ncols, int n_rows, const int* __restrict__ col_row, float* dv_out,
+               float* dp_out, float lr, const int* __restrict__ out_enc, const uint8_t* __restrict__ out_tgt,
+               int n_out, float* __restrict__ row_loss, const uint64_t* __restrict__ exp_tab,
+               uint32_t* __restrict__ hb, int n_tiles, const int* __restrict__ tail_dead, int n_tail_dead,
+               int discard) {
+  constexpr int V = 4, TILE = 128;
+  extern __shared__ __align__(128) float4 tstage[];
+  __shared__ __align__(8) uint64_t mbar[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float4* my = tstage + warp * BS * kBU * 2 * 32 + lane;  // slot (d, k, j): my[((d * kBU + k) * 2 + j) * 32]
+  int4* const blk0 = reinterpret_cast<int4*>(tstage + kWarps * BS * kBU * 2 * 32);  // buffer b: blk0 + b * blk_max
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  unsigned phase = 0u;  // bit b: parity of buffer b's next completion
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    if (threadIdx.x == 0) bulk_load(blk0, sblk, blk0_n4, &mbar[0]);
+    const size_t tbase = static_cast<size_t>(tile) * n_rows * TILE + lane * V;
+    const float* T = tape + tbase;
+    float* A = adj + tbase;
+    float* Abase = adj + static_cast<size_t>(tile) * n_rows * TILE;
+    const size_t vbase = static_cast<size_t>(tile) * ncols * TILE + lane * V;
+    if (row_loss && warp == 0) {  // loss (autodiff.cpp:160-166): outputs in order
+      float l[V] = {0.0f, 0.0f, 0.0f, 0.0f};
+      for (int m = 0; m < n_out; ++m) {
+        float yv[V];
+        load_operand<V>(T, __ldg(out_enc + m), yv);
+        const float t = __ldg(out_tgt + m) ? 1.0f : 0.0f;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const float d = __fsub_rn(yv[v], t);
+          l[v] = __fadd_rn(l[v], __fmul_rn(d, d));
+        }
+      }
+      vstore<V>(row_loss + static_cast<size_t>(tile) * TILE + lane * V, l);
+    }
+    float acc[V], acc2[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = acc2[v] = 0.0f;
+    for (int li = 0; li < n_levels; ++li) {
+      const int b = li & 1;
+      mbar_wait(mbar + b, (phase >> b) & 1u);
+      phase ^= 1u << b;
+      const int4* B = blk0 + b * blk_max;
+      const int4 H = B[0];  // {dead_rel, n_dead, next_start, next_n4}
+      if (threadIdx.x == 0 && li + 1 < n_levels) bulk_load(blk0 + (b ^ 1) * blk_max, sblk + H.z, H.w, mbar + (b ^ 1));
+      if (discard) {  // rows whose last reader ran in the previous pass (barrier passed): no write-back
+        const int* D = reinterpret_cast<const int*>(B + H.x);
+        for (int i = threadIdx.x; i < 4 * H.y; i += 32 * kWarps)
+          discard_l2(Abase + static_cast<size_t>(D[i >> 2]) * TILE + (i & 3) * 32);
+      }
+      const int2 W = reinterpret_cast<const int2*>(B + 1)[warp];  // {first_rel, count}
+      const int4* R = B + W.x;
+      const int nch = (W.y + kBU - 1) / kBU;
+      auto issue = [&](int ch, int d) {
+        float4* base = my + d * kBU * 2 * 32;
+#pragma unroll
+        for (int k = 0; k < kBU; ++k) {
+          const int4 q = ch * kBU + k < W.y ? R[ch * kBU + k] : make_int4(0, -1, -1, 0);
+          if (q.y >= 0) cp_async16(base + (2 * k) * 32, A + static_cast<size_t>(q.y) * TILE);
+          if (q.z >= 0)
+            cp_async16_hint(base + (2 * k + 1) * 32, T + static_cast<size_t>(q.z) * TILE, pol_first);
+          else
+            base[(2 * k + 1) * 32] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);  // unary consumer: c1 * 0
+        }
+        cp_async_commit();
+      };
+#pragma unroll
+      for (int i = 0; i < BS - 1; ++i) {
+        if (i < nch)
+          issue(i, i);
+        else
+          cp_async_commit();
+      }
+      for (int ch = 0; ch < nch; ++ch) {
+        const int nxt = ch + BS - 1;
+        if (nxt < nch)
+          issue(nxt, nxt % BS);
+        else
+          cp_async_commit();
+        cp_async_wait<BS - 1>();
+        const float4* base = my + (ch % BS) * kBU * 2 * 32;
+#pragma unroll
+        for (int k = 0; k < kBU; ++k) {
+          const int4 r = ch * kBU + k < W.y ? R[ch * kBU + k] : make_int4(0, -1, -1, 0);
+          backward_record(r, base[(2 * k) * 32], base[(2 * k + 1) * 32], acc, acc2, T, A, pol_last);
+        }
+      }
+      __syncthreads();
+    }
+    backward_columns<V, SGX_REC_UC>(warp, lane, tile, A, Vp, vbase, ncols, col_row, dv_out, dp_out, lr, exp_tab, hb);
+    __syncthreads();
+    if (discard) {  // the last pass's dead rows and the column inputs (read by the epilogue)
+      for (int i = threadIdx.x; i < 4 * n_tail_dead; i += 32 * kWarps)
+        discard_l2(Abase + static_cast<size_t>(__ldg(tail_dead + (i >> 2))) * TILE + (i & 3) * 32);
+      for (int i = threadIdx.x; i < 4 * ncols; i += 32 * kWarps) {
+        const int rw = __ldg(col_row + (i >> 2));
+        if (rw >= 0) discard_l2(Abase + static_cast<size_t>(rw) * TILE + (i & 3) * 32);
+      }
+    }
+  }
+}
 
 // Deterministic loss total: fixed per-block partial sums in double, then one
 // block folds the partials in block order.
@@ -1485,7 +1642,7 @@ void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* 
                          const float* tape, float* adj, float* V, int ncols, int n_rows, const int* col_row,
                          float* dv_out, float* dp_out, int Bp, float lr, const int* out_enc,
                          const uint8_t* out_tgt, int n_out, float* row_loss, const uint64_t* exp_tab,
-                         uint32_t* hb, const int* dead, const int2* dead_lvl) {
+                         uint32_t* hb, const int* dead, const int2* dead_lvl, const BwdBlocks* bb) {
   const int tiles = Bp / (32 * vec);
   static const int gcap = tile_grid("SGX_GRID_BWD", 1 << 30);
   const int grid = gcap < tiles ? gcap : tiles;
@@ -1493,6 +1650,42 @@ void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* 
     const char* e = std::getenv("SGX_BWD");
     return !(e && e[0] == 'r');
   }();
+  static const bool tma = [] {  // SGX_BWD=async: staged data, records from L2 (no TMA control stream)
+    const char* e = std::getenv("SGX_BWD");
+    return !(e && e[0] == 'a');
+  }();
+  if (!tma) bb = nullptr;
+  if (vec == 4 && staged && bb && bb->sblk) {
+    // TMA-fed kernel: 3-stage data ring when 4 CTAs still fit per SM, else 2.
+    const size_t blk = 2 * static_cast<size_t>(bb->blk_max) * 16;
+    const size_t s3 = static_cast<size_t>(kWarps) * 3 * kBU * 2 * 32 * 16 + blk;
+    const size_t s2 = static_cast<size_t>(kWarps) * 2 * kBU * 2 * 32 * 16 + blk;
+    const int disc = discard_enabled() ? 1 : 0;
+    if (s3 <= 54 * 1024) {
+      static size_t opted = 0;
+      if (s3 > opted) {
+        cudaFuncSetAttribute(k_backward_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s3));
+        opted = s3;
+      }
+      k_backward_tma<3><<<grid, 32 * kWarps, s3, st>>>(bb->sblk, bb->blk0_n4, bb->blk_max, n_levels, tape, adj, V,
+                                                     ncols, n_rows, col_row, dv_out, dp_out, lr, out_enc, out_tgt,
+                                                     n_out, row_loss, exp_tab, hb, tiles, bb->tail_dead,
+                                                     bb->n_tail_dead, disc);
+      return;
+    }
+    if (s2 <= 200 * 1024) {
+      static size_t opted = 0;
+      if (s2 > opted) {
+        cudaFuncSetAttribute(k_backward_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s2));
+        opted = s2;
+      }
+      k_backward_tma<2><<<grid, 32 * kWarps, s2, st>>>(bb->sblk, bb->blk0_n4, bb->blk_max, n_levels, tape, adj, V,
+                                                     ncols, n_rows, col_row, dv_out, dp_out, lr, out_enc, out_tgt,
+                                                     n_out, row_loss, exp_tab, hb, tiles, bb->tail_dead,
+                                                     bb->n_tail_dead, disc);
+      return;
+    }
+  }
   if (vec == 4 && staged) {
     static bool attr = false;
     if (!attr) {

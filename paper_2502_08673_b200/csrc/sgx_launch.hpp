@@ -17,11 +17,18 @@ void launch_forward(cudaStream_t st, int vec, const int4* grp, const int2* lvl, 
 // Edge-record backward (sgx_layout.hpp kR* records); col_row[ncols] = tape row
 // of each V column's INPUT node (-1: outside the program).  With hb, the new V
 // is also hardened into hb[word][col] for the shared-memory harvest.
+// The TMA-fed backward's control stream (sgx_layout.hpp SoftProgram::sblk).
+struct BwdBlocks {
+  const int4* sblk = nullptr;
+  int blk0_n4 = 0, blk_max = 0;
+  const int* tail_dead = nullptr;
+  int n_tail_dead = 0;
+};
 void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* lvl, int n_levels,
                          const float* tape, float* adj, float* V, int ncols, int n_rows, const int* col_row,
                          float* dv_out, float* dp_out, int Bp, float lr, const int* out_enc,
                          const uint8_t* out_tgt, int n_out, float* row_loss, const uint64_t* exp_tab,
-                         uint32_t* hb, const int* dead, const int2* dead_lvl);
+                         uint32_t* hb, const int* dead, const int2* dead_lvl, const BwdBlocks* bb);
 void launch_loss(cudaStream_t st, const float* row_loss, int batch, double* partial, int n_partial,
                  HarvestOut* out);
 void launch_harden(cudaStream_t st, const float* V, int ncpi, int nucpi, const int* cpi_row,

@@ -1,6 +1,8 @@
 #include "sgx_layout.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 #include <cstdlib>
 #include <stdexcept>
@@ -292,6 +294,46 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
       P.dead_lvl.push_back(static_cast<int32_t>(by[li].size()));
       P.dead.insert(P.dead.end(), by[li].begin(), by[li].end());
     }
+    // Block li: header {dead_rel, n_dead, next_start, next_n4}, then per warp
+    // {first_rel, count} (two warps per int4), the records, the dead rows.
+    const int nhdr = 1 + (kWarps + 1) / 2;
+    std::vector<int32_t> starts;
+    for (int li = 0; li < nl; ++li) {
+      const int32_t start = static_cast<int32_t>(P.sblk.size());
+      starts.push_back(start);
+      P.sblk.resize(P.sblk.size() + nhdr, I4{0, 0, 0, 0});
+      for (int w = 0; w < kWarps; ++w) {
+        const int32_t first = P.rec_lvl[2 * (li * kWarps + w)], cnt = P.rec_lvl[2 * (li * kWarps + w) + 1];
+        int32_t* h = &P.sblk[start + 1 + w / 2].x + 2 * (w & 1);
+        h[0] = static_cast<int32_t>(P.sblk.size()) - start;
+        h[1] = cnt;
+        P.srec_lvl.push_back(h[0]);
+        P.srec_lvl.push_back(cnt);
+        P.sblk.insert(P.sblk.end(), P.rec.begin() + first, P.rec.begin() + first + cnt);
+      }
+      const int32_t dstart = static_cast<int32_t>(P.sblk.size()) - start;
+      const std::vector<int32_t> none;
+      const std::vector<int32_t>& d = li > 0 ? by[li - 1] : none;
+      for (size_t k = 0; k < d.size(); k += 4) {
+        I4 q{-1, -1, -1, -1};
+        int32_t* qq = &q.x;
+        for (size_t j = 0; j < 4 && k + j < d.size(); ++j) qq[j] = d[k + j];
+        P.sblk.push_back(q);
+      }
+      const int32_t n4 = static_cast<int32_t>(P.sblk.size()) - start;
+      P.sblk[start].x = dstart;
+      P.sblk[start].y = static_cast<int32_t>(d.size());
+      P.sblk_lvl.insert(P.sblk_lvl.end(), {start, n4, dstart, static_cast<int32_t>(d.size())});
+      P.sblk_max = std::max(P.sblk_max, n4);
+    }
+    for (int li = 0; li + 1 < nl; ++li) {
+      P.sblk[starts[li]].z = P.sblk_lvl[4 * (li + 1)];
+      P.sblk[starts[li]].w = P.sblk_lvl[4 * (li + 1) + 1];
+    }
+    if (nl > 0) P.tail_dead = by[nl - 1];
+    if (getenv("SGX_TRACE"))
+      fprintf(stderr, "[sgx] staged backward blocks: %d passes, max %d int4 (%d B), total %zu int4\n", nl,
+              P.sblk_max, P.sblk_max * 16, P.sblk.size());
   }
   // Slack so a chunk of records may read past the last one.
   for (int k = 0; k < kU; ++k) P.rec.push_back({0, -1, -1, 0});

@@ -99,6 +99,17 @@ struct SoftProgram {
   // the V epilogue and discarded after it.
   std::vector<int32_t> dead;         // rows, grouped by pass
   std::vector<int32_t> dead_lvl;     // per pass: first index into dead, count
+  // Staged blocks for the TMA-fed backward: per pass li one contiguous block
+  // of int4s = a header {dead_rel, n_dead, next_start, next_n4}, per warp
+  // {first_rel, count} (two warps per int4), the pass's records (all warps,
+  // warp order), then the rows that died in pass li-1, packed four per int4
+  // (-1 padding).  One bulk copy brings a pass's whole control stream on
+  // chip, and the header says where the next one is.
+  std::vector<I4> sblk;
+  std::vector<int32_t> sblk_lvl;     // per pass: start, n_int4, dead start (relative), n_dead
+  std::vector<int32_t> srec_lvl;     // per (pass, warp): first record (relative to the block), count
+  std::vector<int32_t> tail_dead;    // rows that died in the last pass (+ none) -> discarded after it
+  int32_t sblk_max = 0;              // largest block, int4s
   std::vector<int32_t> out_enc;      // each output as row << 1 | negate (-1: not in set)
   std::vector<int32_t> col_row;      // tape row of each V column's INPUT node
   std::vector<int32_t> virt_base;    // folded node -> row of its operand (-1 otherwise)
