@@ -171,6 +171,16 @@ int sgx_run_traces(sgx_sampler* s, double* loss_trace, int64_t* new_unique);
 int64_t sgx_solution_count(const sgx_sampler* s);
 int32_t sgx_key_words(const sgx_sampler* s);
 int sgx_fetch_solutions(sgx_sampler* s, int64_t first, int64_t count, uint64_t* keys);
+/* Host streaming of the result (satgrad::run returns every solution,
+ * sampler.hpp:79-81): with it on, each harvest's new keys are copied to host
+ * memory by a worker thread while sampling continues.  Enable before sgx_run. */
+int sgx_set_host_stream(sgx_sampler* s, int32_t on);
+/* Move all solution keys ([rows][key_words], insertion order) to the caller
+ * without a copy when host streaming had them already, else copy them now.
+ * The memory belongs to the caller: release it with sgx_host_free(keys,
+ * map_bytes).  keys = NULL when there are no solutions. */
+int sgx_solutions_take(sgx_sampler* s, uint64_t** keys, int64_t* rows, int64_t* map_bytes);
+int sgx_host_free(uint64_t* keys, int64_t map_bytes);
 /* The sampler's current logits V as [batch][n_cpi] row-major (the reference's
  * Mat<float> v of run_impl, sampler.cpp:157-173): trajectory parity tap. */
 int sgx_read_logits(sgx_sampler* s, float* v);

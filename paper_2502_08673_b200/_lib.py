@@ -23,6 +23,7 @@ EXPORTS = [
     "sgx_solution_count", "sgx_key_words", "sgx_fetch_solutions", "sgx_phase_times",
     "sgx_forward", "sgx_backward", "sgx_embed", "sgx_expf", "sgx_fingerprint_stride",
     "sgx_harvest_local", "sgx_harvest_merge", "sgx_harvest_commit", "sgx_read_logits",
+    "sgx_set_host_stream", "sgx_solutions_take", "sgx_host_free",
 ]
 
 
@@ -112,6 +113,9 @@ def load() -> C.CDLL:
         "sgx_harvest_merge": (C.c_int, [vp, C.c_void_p, i64p, i32, i32, i64, i64p]),
         "sgx_harvest_commit": (C.c_int, [vp, i64, i64p, i64p]),
         "sgx_read_logits": (C.c_int, [vp, f32p]),
+        "sgx_set_host_stream": (C.c_int, [vp, i32]),
+        "sgx_solutions_take": (C.c_int, [vp, C.POINTER(C.c_void_p), i64p, i64p]),
+        "sgx_host_free": (C.c_int, [C.c_void_p, i64]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

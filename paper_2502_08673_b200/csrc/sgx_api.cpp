@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../include/satgrad_b200.h"
+#include "sgx_drain.hpp"
 #include "sgx_kernels.cuh"
 #include "sgx_launch.hpp"
 #include "sgx_layout.hpp"
@@ -214,6 +215,7 @@ struct sgx_sampler {
   uint64_t tcap = 0;
   long long table_count = 0;
   long long store_cap = 0, n_solutions = 0;
+  std::unique_ptr<sgx::HostDrain> drain;  // host streaming of new solutions (sgx_set_host_stream)
   uint64_t epoch = 0;
   long long launches = 0;
   DBuf<sgx::HarvestOut> hout;
@@ -320,6 +322,7 @@ void ensure_table(sgx_sampler* s) {
 void grow_store(sgx_sampler* s, long long need_rows) {
   long long ncap = std::max<long long>(need_rows, s->store_cap * 2);
   const size_t kw = static_cast<size_t>(s->c->L.key_words);
+  if (s->drain) s->drain->wait_idle();  // no host copy may still read the old store
   DBuf<uint64_t> ns;
   ns.alloc_async(static_cast<size_t>(ncap) * kw, s->st);
   if (s->n_solutions)
@@ -421,6 +424,7 @@ void harvest_back(sgx_sampler* s, long long quota_left, long long* attempts, lon
   }
   const sgx::HarvestOut& h = *s->hpin;
   s->table_count += h.new_rows;
+  if (s->drain && h.accepted > 0) s->drain->push(s->store.p, s->n_solutions, h.accepted, s->st);
   s->n_solutions += h.accepted;
   *added = h.accepted;
   // Grow ahead of need, in stream order, so the next harvest never overflows.
@@ -532,6 +536,7 @@ void sampler_run(sgx_sampler* s) {
 
 void reset_solutions(sgx_sampler* s) {
   s->n_solutions = 0;
+  if (s->drain) s->drain->reset();
   s->table_count = 0;
   s->epoch = 0;
   if (s->tcap) {
@@ -745,6 +750,7 @@ int sgx_sampler_free(sgx_sampler* s) {
       s->tmeta.reset_async(st);
       cudaStreamSynchronize(st);
     }
+    s->drain.reset();
     for (auto& e : s->ev)
       if (e) cudaEventDestroy(e);
     if (s->hpin) cudaFreeHost(s->hpin);
@@ -799,8 +805,12 @@ int sgx_run(sgx_sampler* s, sgx_run_stats* stats) {
   return guard([&] {
     need(s, "sampler");
     CK(cudaSetDevice(s->c->ctx->device));
-    if (s->c->layout_ok && !s->c->L.unsat) reset_solutions(s);
-    else s->n_solutions = 0;
+    if (s->c->layout_ok && !s->c->L.unsat) {
+      reset_solutions(s);
+    } else {
+      s->n_solutions = 0;
+      if (s->drain) s->drain->reset();
+    }
     sampler_run(s);
     if (stats) *stats = s->stats;
   });
@@ -833,6 +843,60 @@ int sgx_fetch_solutions(sgx_sampler* s, int64_t first, int64_t count, uint64_t* 
                        static_cast<size_t>(count) * kw * sizeof(uint64_t), cudaMemcpyDeviceToHost, s->st));
     CK(cudaStreamSynchronize(s->st));
   });
+}
+
+int sgx_set_host_stream(sgx_sampler* s, int32_t on) {
+  return guard([&] {
+    need(s, "sampler");
+    CK(cudaSetDevice(s->c->ctx->device));
+    if (!on) {
+      s->drain.reset();
+    } else if (!s->drain) {
+      if (s->n_solutions) throw StateError("sgx_set_host_stream: enable before the run");
+      s->drain = std::make_unique<sgx::HostDrain>(s->c->ctx->device, s->c->L.key_words);
+    }
+  });
+}
+
+int sgx_solutions_take(sgx_sampler* s, uint64_t** keys, int64_t* rows, int64_t* map_bytes) {
+  return guard([&] {
+    need(s, "sampler");
+    need(keys, "keys");
+    CK(cudaSetDevice(s->c->ctx->device));
+    const size_t kw = static_cast<size_t>(s->c->L.key_words);
+    *keys = nullptr;
+    *rows = 0;
+    *map_bytes = 0;
+    if (s->n_solutions == 0) return;
+    if (s->drain && s->drain->queued() == s->n_solutions) {
+      int64_t r = 0;
+      size_t b = 0;
+      uint64_t* p = s->drain->take(&r, &b);
+      if (r != s->n_solutions) {
+        sgx::host_free(p, b);
+        throw CudaError("host drain lost rows");
+      }
+      *keys = p;
+      *rows = r;
+      *map_bytes = static_cast<int64_t>(b);
+      return;
+    }
+    const size_t bytes = static_cast<size_t>(s->n_solutions) * kw * sizeof(uint64_t);
+    void* p = sgx::host_map(bytes);
+    const cudaError_t e = cudaMemcpyAsync(p, s->store.p, bytes, cudaMemcpyDeviceToHost, s->st);
+    const cudaError_t e2 = e == cudaSuccess ? cudaStreamSynchronize(s->st) : e;
+    if (e2 != cudaSuccess) {
+      sgx::host_free(p, bytes);
+      CK(e2);
+    }
+    *keys = static_cast<uint64_t*>(p);
+    *rows = s->n_solutions;
+    *map_bytes = static_cast<int64_t>(bytes);
+  });
+}
+
+int sgx_host_free(uint64_t* keys, int64_t map_bytes) {
+  return guard([&] { sgx::host_free(keys, static_cast<size_t>(map_bytes)); });
 }
 
 int sgx_phase_times(const sgx_sampler* s, double* ms8) {

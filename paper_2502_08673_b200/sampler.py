@@ -11,6 +11,7 @@ The device implements the reference's single-precision instantiation
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 import enum
 from dataclasses import dataclass, field
 
@@ -231,6 +232,21 @@ class Sampler:
                                               _lib.ptr(out, C.c_uint64) if count else None))
         return out
 
+    def set_host_stream(self, on: bool = True):
+        """Copy each harvest's new solutions to host memory while sampling runs."""
+        _lib.check(self.L.sgx_set_host_stream(self.h, 1 if on else 0))
+
+    def take(self) -> np.ndarray:
+        """Every solution key, [n][key_words] uint64 in insertion order, as an
+        array that owns the library's host result memory (no copy when host
+        streaming already landed it; released when the array is collected)."""
+        words = int(self.L.sgx_key_words(self.h))
+        p, rows, nbytes = C.c_void_p(), C.c_int64(), C.c_int64()
+        _lib.check(self.L.sgx_solutions_take(self.h, C.byref(p), C.byref(rows), C.byref(nbytes)))
+        if not p.value or rows.value == 0:
+            return np.zeros((0, words), np.uint64)
+        return _owned_keys(p.value, rows.value, words, nbytes.value)
+
     # building blocks ----------------------------------------------------------
     def logits(self) -> np.ndarray:
         """Current V, [batch][n_cpi] (trajectory parity tap)."""
@@ -265,6 +281,14 @@ class Sampler:
             pass
 
 
+def _owned_keys(addr: int, rows: int, words: int, map_bytes: int) -> np.ndarray:
+    """A numpy view of library host memory that frees it (sgx_host_free) when
+    the last view is collected."""
+    buf = (C.c_uint64 * (rows * words)).from_address(addr)
+    weakref.finalize(buf, _lib.load().sgx_host_free, C.c_void_p(addr), map_bytes)
+    return np.frombuffer(buf, dtype=np.uint64).reshape(rows, words)
+
+
 def run(cnf: CnfFormula, circuit: Circuit, paths: PathClassification, cfg: SamplerConfig,
         unsat: bool = False, unsat_note: str = "", device: int = 0) -> RunResult:
     """satgrad::run (sampler.hpp:79-81): upload, sample, fetch every solution."""
@@ -272,8 +296,9 @@ def run(cnf: CnfFormula, circuit: Circuit, paths: PathClassification, cfg: Sampl
     dc.unsat_note = unsat_note
     s = Sampler(dc, cfg)
     try:
+        s.set_host_stream(True)  # the result streams to the host while sampling runs
         stats = s.run()
-        keys = s.fetch()
+        keys = s.take()
     finally:
         s.close()
         dc.close()

@@ -251,3 +251,29 @@ def test_sampler_building_blocks(gpu):
     want = PortLib().run(i, batch=5000, seed=9, iterations=3)
     assert total == want.new_unique
     assert np.array_equal(keys, want.keys)
+
+
+@pytest.mark.parametrize("name,batch,restarts", [("c3a_or50", 1 << 16, 6), ("c2_iscas", 8192, 3)])
+def test_host_stream_take_equals_device_store(gpu, name, batch, restarts):
+    """Host streaming (a worker copies each harvest's new keys while sampling
+    continues; the store grows mid-run at library-default sizing) hands over
+    exactly the device store, in insertion order, run after run."""
+    i = inst(name)
+    cfg = SamplerConfig(batch=batch, iterations=5, seed=3, restart=RestartPolicy.REINIT_ON_EXHAUST,
+                        max_restarts=restarts)
+    dc = DeviceCircuit.from_instance(i)
+    a, b = Sampler(dc, cfg), Sampler(dc, cfg)
+    try:
+        a.set_host_stream(True)
+        sa, sb = a.run(), b.run()
+        ka, kb = a.take(), b.fetch()
+        assert sa.unique_count == sb.unique_count == len(ka) > 0
+        assert np.array_equal(ka, kb)
+        sa2 = a.run()  # the next run starts a fresh host buffer
+        assert sa2.unique_count == sa.unique_count
+        assert np.array_equal(a.take(), kb)
+        del ka
+    finally:
+        a.close()
+        b.close()
+        dc.close()

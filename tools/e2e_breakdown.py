@@ -11,9 +11,9 @@ for name, cfg in [("c3a_or50", SamplerConfig(batch=1 << 20, seed=1, max_solution
     for rep in range(3):
         t = [time.perf_counter()]
         dc = DeviceCircuit.from_instance(inst); t.append(time.perf_counter())
-        s = Sampler(dc, cfg); t.append(time.perf_counter())
+        s = Sampler(dc, cfg); s.set_host_stream(True); t.append(time.perf_counter())
         st = s.run(); t.append(time.perf_counter())
-        k = s.fetch(); t.append(time.perf_counter())
+        k = s.take(); t.append(time.perf_counter())
         s.close(); dc.close(); t.append(time.perf_counter())
         d = [1000 * (b - a) for a, b in zip(t, t[1:])]
         print(name, rep, "upload %.1f create %.1f run %.1f (device %.1f) fetch %.1f free %.1f ms; unique %d" % (*d[:3], st.device_ms, d[3], d[4], st.unique_count))

@@ -149,3 +149,44 @@ if __name__ == "__main__":
             rd, wr = simulate(P, t, args.l2, bool(yf), bool(dc), bool(ie))
             print(f"tiles {t:4d} y_first {yf} discard {dc} inline_end {ie}: rd {rd:.2f} wr {wr:.2f} "
                   f"total {rd + wr:.2f} GB")
+
+
+def simulate_forward(P, tiles, l2_mb=110.0, total_tiles=512, store_first=False):
+    """Forward: per level read operand rows (V columns for inputs), write rows."""
+    blk = tiles * 512
+    cap = int(l2_mb * 1e6 // blk)
+    lru = OrderedDict()
+    st = dict(rd=0, wr=0)
+
+    def touch(k, dirty, cold=False):
+        if k in lru:
+            lru[k] = lru[k] or dirty
+            lru.move_to_end(k)
+        else:
+            if not dirty:
+                st["rd"] += 1
+            lru[k] = dirty
+            if cold:
+                lru.move_to_end(k, last=False)
+        while len(lru) > cap:
+            _, d = lru.popitem(last=False)
+            if d:
+                st["wr"] += 1
+
+    real, lv = P["real"], P["lv"]
+    a, b, base, kind = P["a"], P["b"], P["base"], P["kind"]
+    by = {}
+    for n in range(P["N"]):
+        if real[n]:
+            by.setdefault(lv[n], []).append(n)
+    for l in range(P["L"] + 1):
+        for n in by.get(l, []):
+            if kind[n] == 0:
+                touch(("v", n), False)
+            for o in (a[n], b[n]):
+                if o >= 0:
+                    touch(("t", base[o]), False)
+            touch(("t", n), True, cold=store_first)
+    st["wr"] += sum(1 for d in lru.values() if d)
+    waves = total_tiles / tiles
+    return st["rd"] * blk * waves / 1e9, st["wr"] * blk * waves / 1e9
