@@ -136,8 +136,9 @@ struct DevSoft {
   DBuf<int4> fwd, rec;
   DBuf<int2> fwd_lvl, rec_lvl, dead_lvl;
   DBuf<int> out_enc, col_row, dead, tail_dead;
-  DBuf<int4> sblk;
+  DBuf<int4> sblk, fblk;
   sgx::BwdBlocks bb;
+  sgx::FwdBlocks fb;
   int n_fwd_levels = 0, n_bwd_levels = 0, n_rows = 0;
   void upload(const sgx::SoftProgram& P, cudaStream_t st) {
     fwd.upload(to_int4(P.fwd), st);
@@ -150,6 +151,13 @@ struct DevSoft {
     dead_lvl.upload(to_int2(P.dead_lvl), st);
     sblk.upload(to_int4(P.sblk), st);
     tail_dead.upload(P.tail_dead.empty() ? std::vector<int32_t>{-1} : P.tail_dead, st);
+    fblk.upload(to_int4(P.fblk), st);
+    fb = sgx::FwdBlocks{};
+    if (!P.fblk.empty()) {
+      fb.fblk = fblk.p;
+      fb.blk0_n4 = P.fblk_lvl[1];
+      fb.blk_max = P.fblk_max;
+    }
     bb = sgx::BwdBlocks{};
     if (!P.sblk.empty()) {
       bb.sblk = sblk.p;
@@ -281,7 +289,7 @@ void sampler_step(sgx_sampler* s) {
   CK(cudaEventRecord(s->ev[0], s->st));
   const int ncpi = static_cast<int>(c->L.cpi.size());
   sgx::launch_forward(s->st, s->vec, c->cone.fwd.p, c->cone.fwd_lvl.p, c->cone.n_fwd_levels, s->V.p, ncpi,
-                      s->tape.p, c->cone.n_rows, s->Bp, 0, tab);
+                      s->tape.p, c->cone.n_rows, s->Bp, 0, tab, &c->cone.fb);
   CK(cudaEventRecord(s->ev[1], s->st));
   backward(s->st, s->vec, c->cone, s->tape.p, s->adj.p, s->V.p, ncpi, nullptr, nullptr, s->Bp,
            static_cast<float>(s->cfg.learning_rate), c->out_tgt.p, static_cast<int>(c->L.out_node.size()),
@@ -1036,7 +1044,7 @@ int sgx_forward(sgx_circuit* c, const float* p, int32_t batch, float* tape, floa
     dsrc.upload(src, st);
     dtape.alloc(nr * Bp);
     sgx::launch_forward(st, kTapVec, c->full.fwd.p, c->full.fwd_lvl.p, c->full.n_fwd_levels, dsrc.p,
-                        static_cast<int>(ncpi), dtape.p, L.full.n_rows, Bp, 1, c->ctx->exp_tab.p);
+                        static_cast<int>(ncpi), dtape.p, L.full.n_rows, Bp, 1, c->ctx->exp_tab.p, &c->full.fb);
     CK(cudaGetLastError());
     std::vector<float> h(nr * Bp);
     CK(cudaMemcpyAsync(h.data(), dtape.p, h.size() * sizeof(float), cudaMemcpyDeviceToHost, st));

@@ -982,6 +982,117 @@ k_backward_tma(const int4* __restrict__ sblk, int blk0_n4, int blk_max, int n_le
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-fed forward: k_forward_async's staged operand pipeline with the group
+// records on chip -- each level's block (sgx_layout.hpp fblk: header, warp
+// ranges, groups) arrives by cp.async.bulk one level ahead, so neither the
+// issue side nor the compute side waits on a record load.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(32 * kWarps)
+k_forward_tma(const int4* __restrict__ fblk, int blk0_n4, int blk_max, int n_levels, const float* __restrict__ src,
+              int ncols, float* tape, int n_rows, int src_is_prob, const uint64_t* __restrict__ exp_tab,
+              int n_tiles) {
+  constexpr int TILE = 128;
+  extern __shared__ __align__(128) float4 fstage[];
+  __shared__ __align__(8) uint64_t mbar[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float4* my = fstage + warp * kStages * kSlots * 32 + lane;  // slot (d, j): my[(d*kSlots + j) * 32]
+  int4* const blk0 = reinterpret_cast<int4*>(fstage + kWarps * kStages * kSlots * 32);
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  unsigned phase = 0u;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    if (threadIdx.x == 0) bulk_load(blk0, fblk, blk0_n4, &mbar[0]);
+    float* T = tape + static_cast<size_t>(tile) * n_rows * TILE + lane * 4;
+    const float* S = src + static_cast<size_t>(tile) * ncols * TILE + lane * 4;
+    for (int l = 0; l < n_levels; ++l) {
+      const int b = l & 1;
+      mbar_wait(mbar + b, (phase >> b) & 1u);
+      phase ^= 1u << b;
+      const int4* B = blk0 + b * blk_max;
+      const int4 H = B[0];  // {next_start, next_n4}
+      if (threadIdx.x == 0 && l + 1 < n_levels) bulk_load(blk0 + (b ^ 1) * blk_max, fblk + H.x, H.y, mbar + (b ^ 1));
+      const int2 Wr = reinterpret_cast<const int2*>(B + 1)[warp];  // {first_rel, groups}
+      const int4* G = B + Wr.x;
+      auto issue = [&](int g, int d) {
+        const int4* rec = G + g * kGroupRecs;
+        const int4 h = rec[0], o0 = rec[1], o1 = rec[2];
+        const int opd[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+        const int kind = h.x, n = h.y;
+        float4* base = my + d * kSlots * 32;
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k) {
+          if (k >= n) break;
+          if (kind >= SGX_AND2) {
+            cp_async16(base + (2 * k) * 32, T + static_cast<size_t>(opd[2 * k] >> 1) * TILE);
+            cp_async16(base + (2 * k + 1) * 32, T + static_cast<size_t>(opd[2 * k + 1] >> 1) * TILE);
+          } else if (kind == SGX_NOT || kind == SGX_BUF) {
+            cp_async16(base + (2 * k) * 32, T + static_cast<size_t>(opd[2 * k] >> 1) * TILE);
+          } else if (kind == SGX_INPUT && opd[2 * k] >= 0) {
+            cp_async16(base + (2 * k) * 32, S + static_cast<size_t>(opd[2 * k]) * TILE);
+          }
+        }
+        cp_async_commit();
+      };
+#pragma unroll
+      for (int i = 0; i < kStages - 1; ++i) {
+        if (i < Wr.y)
+          issue(i, i);
+        else
+          cp_async_commit();
+      }
+      for (int i = 0; i < Wr.y; ++i) {
+        const int nxt = i + kStages - 1;
+        if (nxt < Wr.y)
+          issue(nxt, nxt % kStages);
+        else
+          cp_async_commit();
+        cp_async_wait<kStages - 1>();
+        const int4* rec = G + i * kGroupRecs;
+        const int4 h = rec[0], o0 = rec[1], o1 = rec[2];
+        const int opd[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+        const int kind = h.x, n = h.y;
+        const float4* base = my + (i % kStages) * kSlots * 32;
+        float* out = T + static_cast<size_t>(h.z) * TILE;
+        switch (kind) {
+          case SGX_AND2: group_binary<SGX_AND2>(base, opd, n, out); break;
+          case SGX_OR2: group_binary<SGX_OR2>(base, opd, n, out); break;
+          case SGX_XOR2: group_binary<SGX_XOR2>(base, opd, n, out); break;
+          case SGX_XNOR2: group_binary<SGX_XNOR2>(base, opd, n, out); break;
+          case SGX_NOT: group_unary<true>(base, opd, n, out); break;
+          case SGX_BUF: group_unary<false>(base, opd, n, out); break;
+          case SGX_INPUT:
+#pragma unroll
+            for (int k = 0; k < kGroup; ++k) {
+              if (k >= n) break;
+              float a[4] = {0.0f, 0.0f, 0.0f, 0.0f}, r[4];
+              if (opd[2 * k] >= 0) f4(base[(2 * k) * 32], a);
+#pragma unroll
+              for (int v = 0; v < 4; ++v)
+                r[v] = opd[2 * k] < 0 ? 0.5f : (src_is_prob ? a[v] : sigmoid_ref(a[v], exp_tab));
+              vstore<4>(out + k * TILE, r);
+            }
+            break;
+          default: {
+            const float c = kind == SGX_CONST1 ? 1.0f : 0.0f;
+            const float r[4] = {c, c, c, c};
+#pragma unroll
+            for (int k = 0; k < kGroup; ++k) {
+              if (k >= n) break;
+              vstore<4>(out + k * TILE, r);
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // Deterministic loss total: fixed per-block partial sums in double, then one
 // block folds the partials in block order.
 __global__ void __launch_bounds__(kThreads)
@@ -1602,8 +1713,27 @@ static int tile_grid(const char* env, int tiles) {
 
 void launch_forward(cudaStream_t st, int vec, const int4* grp, const int2* lvl, int n_levels,
                     const float* src, int ncols, float* tape, int n_rows, int Bp, int src_is_prob,
-                    const uint64_t* exp_tab) {
+                    const uint64_t* exp_tab, const FwdBlocks* fb) {
   const int tiles = Bp / (32 * vec);
+  static const bool tma = [] {  // SGX_FWD=async: staged operands, records from L2
+    const char* e = std::getenv("SGX_FWD");
+    return !(e && e[0] == 'a');
+  }();
+  if (vec == 4 && async_enabled_fwd() && tma && fb && fb->fblk) {
+    const size_t smem = static_cast<size_t>(kAsyncSmem) + 2 * static_cast<size_t>(fb->blk_max) * 16;
+    if (smem <= 200 * 1024) {
+      static size_t opted = 0;
+      if (smem > opted) {
+        cudaFuncSetAttribute(k_forward_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        opted = smem;
+      }
+      static const int gcap = tile_grid("SGX_GRID_FWD", 1 << 30);
+      const int grid = gcap < tiles ? gcap : tiles;
+      k_forward_tma<<<grid, 32 * kWarps, smem, st>>>(fb->fblk, fb->blk0_n4, fb->blk_max, n_levels, src, ncols, tape,
+                                                    n_rows, src_is_prob, exp_tab, tiles);
+      return;
+    }
+  }
   if (vec == 4 && async_enabled_fwd()) {
     static bool attr = false;
     if (!attr) {

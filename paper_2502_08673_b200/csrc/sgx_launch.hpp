@@ -11,9 +11,14 @@ struct HarvestOut;
 
 void launch_init_v(cudaStream_t st, float* V, int ncols, int Bp, int tile_rows, uint64_t prefix,
                    long long row_offset, uint32_t* hb);
+// The TMA-fed forward's control stream (sgx_layout.hpp SoftProgram::fblk).
+struct FwdBlocks {
+  const int4* fblk = nullptr;
+  int blk0_n4 = 0, blk_max = 0;
+};
 void launch_forward(cudaStream_t st, int vec, const int4* grp, const int2* lvl, int n_levels,
                     const float* src, int ncols, float* tape, int n_rows, int Bp, int src_is_prob,
-                    const uint64_t* exp_tab);
+                    const uint64_t* exp_tab, const FwdBlocks* fb);
 // Edge-record backward (sgx_layout.hpp kR* records); col_row[ncols] = tape row
 // of each V column's INPUT node (-1: outside the program).  With hb, the new V
 // is also hardened into hb[word][col] for the shared-memory harvest.

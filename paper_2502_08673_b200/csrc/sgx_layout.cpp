@@ -175,6 +175,31 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
   }
   P.n_rows = next_row;
   for (int i = 0; i < n; ++i) P.n_set += in_set[i] ? 1 : 0;
+  {  // staged forward blocks (see SoftProgram::fblk)
+    const int nhdr = 1 + (kWarps + 1) / 2;
+    std::vector<int32_t> starts;
+    for (int l = 0; l < P.n_levels; ++l) {
+      const int32_t start = static_cast<int32_t>(P.fblk.size());
+      starts.push_back(start);
+      P.fblk.resize(P.fblk.size() + nhdr, I4{0, 0, 0, 0});
+      for (int w = 0; w < kWarps; ++w) {
+        const int32_t first = P.fwd_lvl[2 * (l * kWarps + w)], cnt = P.fwd_lvl[2 * (l * kWarps + w) + 1];
+        int32_t* h = &P.fblk[start + 1 + w / 2].x + 2 * (w & 1);
+        h[0] = static_cast<int32_t>(P.fblk.size()) - start;
+        h[1] = cnt;
+        P.fblk.insert(P.fblk.end(), P.fwd.begin() + static_cast<size_t>(first) * kGroupRecs,
+                      P.fwd.begin() + static_cast<size_t>(first + cnt) * kGroupRecs);
+      }
+      const int32_t n4 = static_cast<int32_t>(P.fblk.size()) - start;
+      P.fblk_lvl.push_back(start);
+      P.fblk_lvl.push_back(n4);
+      P.fblk_max = std::max(P.fblk_max, n4);
+    }
+    for (int l = 0; l + 1 < P.n_levels; ++l) {
+      P.fblk[starts[l]].x = P.fblk_lvl[2 * (l + 1)];
+      P.fblk[starts[l]].y = P.fblk_lvl[2 * (l + 1) + 1];
+    }
+  }
   // Virtual nodes read as their base row (for the taps / outputs).
   P.virt_base.assign(n, -1);
   P.virt_neg.assign(n, 0);
@@ -332,8 +357,8 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
     }
     if (nl > 0) P.tail_dead = by[nl - 1];
     if (getenv("SGX_TRACE"))
-      fprintf(stderr, "[sgx] staged backward blocks: %d passes, max %d int4 (%d B), total %zu int4\n", nl,
-              P.sblk_max, P.sblk_max * 16, P.sblk.size());
+      fprintf(stderr, "[sgx] staged blocks: backward %d passes, max %d int4 (%d B); forward max %d int4 (%d B)\n",
+              nl, P.sblk_max, P.sblk_max * 16, P.fblk_max, P.fblk_max * 16);
   }
   // Slack so a chunk of records may read past the last one.
   for (int k = 0; k < kU; ++k) P.rec.push_back({0, -1, -1, 0});

@@ -109,6 +109,12 @@ struct SoftProgram {
   std::vector<int32_t> sblk_lvl;     // per pass: start, n_int4, dead start (relative), n_dead
   std::vector<int32_t> srec_lvl;     // per (pass, warp): first record (relative to the block), count
   std::vector<int32_t> tail_dead;    // rows that died in the last pass (+ none) -> discarded after it
+  // Staged forward blocks: per level a header {next_start, next_n4, 0, 0},
+  // per warp {first_rel, groups} (two warps per int4), then the level's
+  // groups (kGroupRecs int4s each, warp order).
+  std::vector<I4> fblk;
+  std::vector<int32_t> fblk_lvl;     // per level: start, n_int4
+  int32_t fblk_max = 0;
   int32_t sblk_max = 0;              // largest block, int4s
   std::vector<int32_t> out_enc;      // each output as row << 1 | negate (-1: not in set)
   std::vector<int32_t> col_row;      // tape row of each V column's INPUT node
