@@ -144,3 +144,71 @@ def test_two_ranks_equal_one_process(cfg):
         assert restarts == want.restarts
     if cfg.max_solutions:
         assert res[0][1] == cfg.max_solutions
+
+
+# ---------------------------------------------------------------------------
+# C5 sweep driver (paper_2502_08673_b200/sweep.py) at world size 2: every
+# suite instance goes through run_sharded; both ranks must report the same
+# per-instance global counts as one process over the union, and the same
+# family summary.
+
+SUITE = ["c5/or50_01", "c5/q_17", "c5/s15850_33", "c5/prod_45", "c5/blasted200_55"]
+
+
+def _suite_runner(solo):
+    from paper_2502_08673_b200.sweep import family
+
+    def run_one(name, batch, rank, world):
+        b = 24 + 7 * SUITE.index(name)  # small stand-in batch per instance
+        cfg = SamplerConfig(batch=b, iterations=2, seed=1)
+        if solo:
+            st = _single(cfg, world)
+        else:
+            shard = FakeShard(b, rank * b)
+            st = run_sharded(shard, ListExchange(TorchExchange()), cfg, rank, world, b)
+        return st.unique_count, 0.5 + rank + len(family(name))
+
+    return run_one
+
+
+def _suite_worker(rank, world, port, q):
+    from paper_2502_08673_b200.sweep import run_suite, summarize
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+
+        def sync(x):
+            t = torch.tensor([x], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        res = run_suite(SUITE, _suite_runner(False), rank, world, sync)
+        q.put((rank, [(r.name, r.unique, r.seconds) for r in res], summarize(res, world)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_c5_suite_two_ranks_equal_one_process():
+    from paper_2502_08673_b200.sweep import FAMILY_BATCH, run_suite, summarize
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_suite_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = run_suite(SUITE, _suite_runner(True), 0, world)
+    for rank, rows, summ in got:
+        assert [(n, u) for n, u, _ in rows] == [(r.name, r.unique) for r in want]
+        # device time is the max over ranks (rank 1's stand-in time here)
+        assert [s for _, _, s in rows] == [r.seconds + 1 for r in want]
+        assert summ == got[0][2]
+        assert summ["unique"] == sum(r.unique for r in want)
+        assert set(summ["families"]) == {"or", "q", "s15850", "prod", "blasted"}
+        assert all(f["batch_per_gpu"] == FAMILY_BATCH[k] for k, f in summ["families"].items())
+    assert summarize(want, 1)["unique"] == got[0][2]["unique"]

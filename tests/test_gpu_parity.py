@@ -277,3 +277,30 @@ def test_host_stream_take_equals_device_store(gpu, name, batch, restarts):
         a.close()
         b.close()
         dc.close()
+
+
+def _c5_runs():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "c5_runs.json")) as f:
+        return json.load(f)
+
+
+def test_c5_suite_matches_reference(gpu):
+    """C5 (BASELINE configs[4]): all 60 suite instances -- or-chain, q, s15850,
+    Prod and deep blasted shapes -- reproduce the reference's satgrad::run
+    exactly at batch 256: unique count, attempts, per-harvest new-unique trace,
+    insertion-ordered keys; every key re-verifies against its CNF."""
+    bad = []
+    for rec in _c5_runs():
+        i = load_instance(rec["instance"])
+        res = run_instance(i, SamplerConfig(**rec["config"]))
+        st = res.stats
+        got = (st.unique_count, st.attempts, st.new_unique, sha(res.solutions.keys))
+        want = (rec["unique"], rec["attempts"], rec["new_unique"], rec["keys_sha256"])
+        if got != want:
+            bad.append((rec["instance"], got[:2], want[:2]))
+            continue
+        np.testing.assert_allclose(st.loss_trace, rec["loss_trace"], rtol=LOSS_RTOL, atol=0)
+        assert verify_keys(i.cnf, res.solutions.keys).all()
+    assert not bad, bad
