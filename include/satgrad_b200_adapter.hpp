@@ -118,6 +118,8 @@ inline satgrad::RunResult run(const satgrad::CnfFormula& cnf, const satgrad::Cir
   sgx_sampler* s = nullptr;
   check(sgx_sampler_create(circ, &sc, &s));
   std::unique_ptr<sgx_sampler, int (*)(sgx_sampler*)> s_guard(s, sgx_sampler_free);
+  // The result streams to host memory while the run samples (sgx_drain).
+  check(sgx_set_host_stream(s, 1));
   sgx_run_stats st{};
   check(sgx_run(s, &st));
 
@@ -135,11 +137,18 @@ inline satgrad::RunResult run(const satgrad::CnfFormula& cnf, const satgrad::Cir
   check(sgx_run_traces(s, out.stats.loss_trace.data(), nu.data()));
   out.stats.new_unique.assign(nu.begin(), nu.end());
 
-  // Solutions in insertion order -> SolutionSet (dedupe_key layout).
-  const int64_t n = sgx_solution_count(s);
+  // Solutions in insertion order -> SolutionSet (dedupe_key layout).  The
+  // keys are already on the host: take them without a copy.
   const int32_t words = sgx_key_words(s);
-  std::vector<uint64_t> keys(static_cast<size_t>(n) * words);
-  if (n) check(sgx_fetch_solutions(s, 0, n, keys.data()));
+  uint64_t* kp = nullptr;
+  int64_t n = 0, map_bytes = 0;
+  check(sgx_solutions_take(s, &kp, &n, &map_bytes));
+  struct HostKeys {
+    uint64_t* p;
+    int64_t bytes;
+    ~HostKeys() { sgx_host_free(p, bytes); }
+  } hold{kp, map_bytes};
+  const uint64_t* keys = kp;
   satgrad::Assignment a(cnf.num_vars + 1, 0);
   for (int64_t i = 0; i < n; ++i) {
     for (int v = 1; v <= cnf.num_vars; ++v)
