@@ -224,6 +224,15 @@ struct sgx_sampler {
   long long table_count = 0;
   long long store_cap = 0, n_solutions = 0;
   std::unique_ptr<sgx::HostDrain> drain;  // host streaming of new solutions (sgx_set_host_stream)
+  // The harvest runs on its own stream, overlapping the next step's forward:
+  // ev_soft (st: init / step done) orders a harvest after the soft pass that
+  // produced its inputs; ev_front (sh: the harvest's reads of V / HB done)
+  // orders the next backward / init, which rewrite them, after it.
+  cudaStream_t sh = nullptr;
+  cudaEvent_t ev_soft = nullptr, ev_front = nullptr, ev_join = nullptr;
+  cudaEvent_t sev[2][4] = {};  // per step parity: fwd begin / end, bwd begin / end
+  DBuf<double> dloss;          // per step parity: loss total (sum over rows)
+  long long steps = 0;         // steps launched (parity of the next)
   uint64_t epoch = 0;
   long long launches = 0;
   DBuf<sgx::HarvestOut> hout;
@@ -275,29 +284,38 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 // ---------------------------------------------------------------- sampler ops
 void sampler_init(sgx_sampler* s, int restart) {
   const auto& L = s->c->L;
+  CK(cudaStreamWaitEvent(s->st, s->ev_front, 0));  // the last harvest is done reading V / HB
   uint64_t prefix = sgx::fold(sgx::fold(sgx::fold(sgx::kPi, s->cfg.seed), sgx::kInitTag),
                               static_cast<uint64_t>(static_cast<int64_t>(restart)));
   sgx::launch_init_v(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, 32 * s->vec, prefix,
                      s->cfg.row_offset, s->HB.p);
   s->launches += L.cpi.empty() ? 0 : 1;
+  CK(cudaEventRecord(s->ev_soft, s->st));
   CK(cudaGetLastError());
 }
 
-void sampler_step(sgx_sampler* s) {
+// One GD step; returns its parity slot (loss total in dloss[slot], timing in sev[slot]).
+int sampler_step(sgx_sampler* s) {
   sgx_circuit* c = s->c;
   const uint64_t* tab = c->ctx->exp_tab.p;
-  CK(cudaEventRecord(s->ev[0], s->st));
+  const int slot = static_cast<int>(s->steps++ & 1);
+  cudaEvent_t* ev = s->sev[slot];
+  CK(cudaEventRecord(ev[0], s->st));
   const int ncpi = static_cast<int>(c->L.cpi.size());
   sgx::launch_forward(s->st, s->vec, c->cone.fwd.p, c->cone.fwd_lvl.p, c->cone.n_fwd_levels, s->V.p, ncpi,
                       s->tape.p, c->cone.n_rows, s->Bp, 0, tab, &c->cone.fb);
-  CK(cudaEventRecord(s->ev[1], s->st));
+  CK(cudaEventRecord(ev[1], s->st));
+  CK(cudaStreamWaitEvent(s->st, s->ev_front, 0));  // the running harvest still reads V / HB
+  CK(cudaEventRecord(ev[2], s->st));
   backward(s->st, s->vec, c->cone, s->tape.p, s->adj.p, s->V.p, ncpi, nullptr, nullptr, s->Bp,
            static_cast<float>(s->cfg.learning_rate), c->out_tgt.p, static_cast<int>(c->L.out_node.size()),
            s->row_loss.p, tab, s->HB.p);
-  sgx::launch_loss(s->st, s->row_loss.p, s->cfg.batch, s->partial.p, s->n_partial, s->hout.p);
+  sgx::launch_loss(s->st, s->row_loss.p, s->cfg.batch, s->partial.p, s->n_partial, s->dloss.p + slot);
   s->launches += 4;
-  CK(cudaEventRecord(s->ev[2], s->st));
+  CK(cudaEventRecord(ev[3], s->st));
+  CK(cudaEventRecord(s->ev_soft, s->st));
   CK(cudaGetLastError());
+  return slot;
 }
 
 void ensure_table(sgx_sampler* s) {
@@ -310,19 +328,19 @@ void ensure_table(sgx_sampler* s) {
   if (s->cfg.solution_capacity > 0) first = std::max<uint64_t>(first, 2ull * s->cfg.solution_capacity);
   uint64_t ncap = next_pow2(std::max<uint64_t>(std::max<uint64_t>(want * 2, first), 1u << 16));
   DBuf<unsigned long long> nk, nm;
-  nk.alloc_async(ncap, s->st);
-  nm.alloc_async(ncap, s->st);
-  CK(cudaMemsetAsync(nk.p, 0, ncap * sizeof(unsigned long long), s->st));
-  CK(cudaMemsetAsync(nm.p, 0xff, ncap * sizeof(unsigned long long), s->st));
+  nk.alloc_async(ncap, s->sh);
+  nm.alloc_async(ncap, s->sh);
+  CK(cudaMemsetAsync(nk.p, 0, ncap * sizeof(unsigned long long), s->sh));
+  CK(cudaMemsetAsync(nm.p, 0xff, ncap * sizeof(unsigned long long), s->sh));
   if (s->tcap) {
-    sgx::launch_rehash(s->st, s->tkeys.p, s->tmeta.p, s->tcap, nk.p, nm.p, ncap - 1);
+    sgx::launch_rehash(s->sh, s->tkeys.p, s->tmeta.p, s->tcap, nk.p, nm.p, ncap - 1);
     s->launches += 1;
   }
   CK(cudaGetLastError());
   s->tkeys.swap(nk);
   s->tmeta.swap(nm);
-  nk.reset_async(s->st);  // the old table, after the rehash in stream order
-  nm.reset_async(s->st);
+  nk.reset_async(s->sh);  // the old table, after the rehash in stream order
+  nm.reset_async(s->sh);
   s->tcap = ncap;
 }
 
@@ -332,12 +350,12 @@ void grow_store(sgx_sampler* s, long long need_rows) {
   const size_t kw = static_cast<size_t>(s->c->L.key_words);
   if (s->drain) s->drain->wait_idle();  // no host copy may still read the old store
   DBuf<uint64_t> ns;
-  ns.alloc_async(static_cast<size_t>(ncap) * kw, s->st);
+  ns.alloc_async(static_cast<size_t>(ncap) * kw, s->sh);
   if (s->n_solutions)
     CK(cudaMemcpyAsync(ns.p, s->store.p, static_cast<size_t>(s->n_solutions) * kw * sizeof(uint64_t),
-                       cudaMemcpyDeviceToDevice, s->st));
+                       cudaMemcpyDeviceToDevice, s->sh));
   s->store.swap(ns);
-  ns.reset_async(s->st);
+  ns.reset_async(s->sh);
   s->store_cap = ncap;
 }
 
@@ -353,7 +371,8 @@ void harvest_front(sgx_sampler* s, int restart, int iter, long long quota_left) 
     ensure_table(s);
     s->host_ms[1] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
-  CK(cudaEventRecord(s->ev[3], s->st));
+  CK(cudaStreamWaitEvent(s->sh, s->ev_soft, 0));  // the soft pass that produced V / HB
+  CK(cudaEventRecord(s->ev[3], s->sh));
   uint64_t fprefix = sgx::fold(
       sgx::fold(sgx::fold(sgx::fold(sgx::kPi, s->cfg.seed), sgx::kFreeTag), static_cast<uint64_t>(static_cast<int64_t>(restart))),
       static_cast<uint64_t>(static_cast<int64_t>(iter)));
@@ -386,53 +405,69 @@ void harvest_front(sgx_sampler* s, int restart, int iter, long long quota_left) 
     a.tmeta = s->tmeta.p;
     a.tmask = s->tcap - 1;
     a.epoch = s->epoch;
-    sgx::launch_harvest_smem(s->st, s->hwpc, L.fb_rows, s->W, a);
-    CK(cudaEventRecord(s->ev[4], s->st));
-    CK(cudaEventRecord(s->ev[5], s->st));
+    sgx::launch_harvest_smem(s->sh, s->hwpc, L.fb_rows, s->W, a);
+    CK(cudaEventRecord(s->ev[4], s->sh));
+    CK(cudaEventRecord(s->ev[5], s->sh));
     s->launches += 1;
   } else {
-    sgx::launch_harden(s->st, s->V.p, static_cast<int>(L.cpi.size()), static_cast<int>(L.ucpi.size()),
+    sgx::launch_harden(s->sh, s->V.p, static_cast<int>(L.cpi.size()), static_cast<int>(L.ucpi.size()),
                        c->cpi_bit_row.p, c->ucpi_bit_row.p, s->BT.p, s->W, 32 * s->vec, fprefix,
                        s->cfg.row_offset);
-    sgx::launch_bit_eval(s->st, s->wpc, c->bit_ops.p, c->bit_lvl_ptr.p, c->n_bit_levels, s->BT.p, s->W,
+    sgx::launch_bit_eval(s->sh, s->wpc, c->bit_ops.p, c->bit_lvl_ptr.p, c->n_bit_levels, s->BT.p, s->W,
                          c->out_bit_row.p, c->out_tgt.p, static_cast<int>(L.out_node.size()), c->clause_ptr.p,
                          c->clause_enc.p, static_cast<int>(L.clause_ptr.size()) - 1, s->valid.p, s->cfg.batch);
-    CK(cudaEventRecord(s->ev[4], s->st));
-    sgx::launch_keys(s->st, s->BT.p, s->W, c->key_bit_row.p, L.key_words, s->valid.p, s->Bp, s->K.p,
+    CK(cudaEventRecord(s->ev[4], s->sh));
+    sgx::launch_keys(s->sh, s->BT.p, s->W, c->key_bit_row.p, L.key_words, s->valid.p, s->Bp, s->K.p,
                      s->slot_of_row.p, s->tkeys.p, s->tmeta.p, s->tcap - 1, s->epoch);
-    CK(cudaEventRecord(s->ev[5], s->st));
+    CK(cudaEventRecord(s->ev[5], s->sh));
     s->launches += (L.cpi.size() + L.ucpi.size() ? 1 : 0) + 2;
   }
-  sgx::launch_commit(s->st, s->valid.p, s->slot_of_row.p, s->tmeta.p, s->epoch, s->Bp, s->newmask.p,
+  CK(cudaEventRecord(s->ev_front, s->sh));
+  sgx::launch_commit(s->sh, s->valid.p, s->slot_of_row.p, s->tmeta.p, s->epoch, s->Bp, s->newmask.p,
                      s->block_count.p, quota_left, s->hout.p);
   s->launches += 2;
 }
 
-// Back half: append the accepted rows (hout->accepted) in row order, one sync.
-void harvest_back(sgx_sampler* s, long long quota_left, long long* attempts, long long* added) {
+// Back half, launch: append the accepted rows (hout->accepted) in row order
+// and queue the counters (and the loss of step `loss_slot`, if any) for the
+// host; no sync.
+void harvest_back_launch(sgx_sampler* s, int loss_slot) {
   const auto& L = s->c->L;
-  sgx::launch_append(s->st, s->newmask.p, s->block_count.p, s->K.p, L.key_words, s->Bp, s->store.p,
+  sgx::launch_append(s->sh, s->newmask.p, s->block_count.p, s->K.p, L.key_words, s->Bp, s->store.p,
                      s->n_solutions, s->store_cap, s->hout.p);
   s->launches += 1;
-  CK(cudaEventRecord(s->ev[6], s->st));
+  CK(cudaEventRecord(s->ev[6], s->sh));
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->st));
-  CK(cudaStreamSynchronize(s->st));
+  CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->sh));
+  if (loss_slot >= 0)
+    CK(cudaMemcpyAsync(&s->hpin->loss_total, s->dloss.p + loss_slot, sizeof(double), cudaMemcpyDeviceToHost,
+                       s->sh));
+}
+
+// Back half, finish: the one host sync of the harvest, store overflow
+// handling, counters.  Device time of the harvest (and of the step it
+// followed, slot `step_slot`) is accumulated here, once its events are done.
+void harvest_back_finish(sgx_sampler* s, long long quota_left, long long* attempts, long long* added,
+                         int step_slot) {
+  const auto& L = s->c->L;
+  CK(cudaStreamSynchronize(s->sh));
   if (s->hpin->overflow) {
+    const double loss = s->hpin->loss_total;
     const auto t0 = std::chrono::steady_clock::now();
     grow_store(s, s->n_solutions + s->hpin->accepted);
     s->host_ms[2] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    CK(cudaMemsetAsync(&s->hout.p->overflow, 0, sizeof(long long), s->st));
-    sgx::launch_append(s->st, s->newmask.p, s->block_count.p, s->K.p, L.key_words, s->Bp, s->store.p,
+    CK(cudaMemsetAsync(&s->hout.p->overflow, 0, sizeof(long long), s->sh));
+    sgx::launch_append(s->sh, s->newmask.p, s->block_count.p, s->K.p, L.key_words, s->Bp, s->store.p,
                        s->n_solutions, s->store_cap, s->hout.p);
     s->launches += 1;
-    CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->st));
-    CK(cudaStreamSynchronize(s->st));
+    CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->sh));
+    CK(cudaStreamSynchronize(s->sh));
+    s->hpin->loss_total = loss;
     if (s->hpin->overflow) throw CudaError("solution store overflow after growth");
   }
   const sgx::HarvestOut& h = *s->hpin;
   s->table_count += h.new_rows;
-  if (s->drain && h.accepted > 0) s->drain->push(s->store.p, s->n_solutions, h.accepted, s->st);
+  if (s->drain && h.accepted > 0) s->drain->push(s->store.p, s->n_solutions, h.accepted, s->sh);
   s->n_solutions += h.accepted;
   *added = h.accepted;
   // Grow ahead of need, in stream order, so the next harvest never overflows.
@@ -447,14 +482,22 @@ void harvest_back(sgx_sampler* s, long long quota_left, long long* attempts, lon
   s->phase_ms[5] += elapsed(s->ev[3], s->ev[4]);
   s->phase_ms[6] += elapsed(s->ev[4], s->ev[5]);
   s->phase_ms[7] += elapsed(s->ev[5], s->ev[6]);
+  if (step_slot >= 0) {
+    cudaEvent_t* ev = s->sev[step_slot];
+    s->phase_ms[1] += elapsed(ev[0], ev[3]);
+    s->phase_ms[3] += elapsed(ev[0], ev[1]);
+    s->phase_ms[4] += elapsed(ev[2], ev[3]);
+  }
 }
 
 // The harvest lambda of sampler.cpp:124-153 for one (restart, iter), single
-// device: quota applied in the scan, one host sync.
+// device: quota applied in the scan, one host sync.  `step_slot` = parity
+// slot of the step this harvest follows (-1 after init).
 void sampler_harvest(sgx_sampler* s, int restart, int iter, long long quota_left, long long* attempts,
-                     long long* added) {
+                     long long* added, int step_slot) {
   harvest_front(s, restart, iter, quota_left);
-  harvest_back(s, quota_left, attempts, added);
+  harvest_back_launch(s, step_slot);
+  harvest_back_finish(s, quota_left, attempts, added, step_slot);
 }
 
 // run_impl<float> (sampler.cpp:89-194).
@@ -477,14 +520,18 @@ void sampler_run(sgx_sampler* s) {
   const bool quota = cfg.max_solutions > 0;
   auto quota_met = [&] { return quota && s->n_solutions >= cfg.max_solutions; };
   auto out_of_time = [&] { return cfg.timeout_s > 0.0 && now_s() >= cfg.timeout_s; };
-  auto harvest = [&](int restart, int iter) {
+  // Harvest `iter` finishes on the host; its counters feed the reference's
+  // bookkeeping (attempts, per-harvest new-unique, loss trace).
+  auto finish = [&](int iter, long long quota_left, int step_slot) {
     long long att = 0, add = 0;
     const auto h0 = clock::now();
-    sampler_harvest(s, restart, iter, quota ? cfg.max_solutions - s->n_solutions : -1, &att, &add);
+    harvest_back_finish(s, quota_left, &att, &add, step_slot);
     s->host_ms[0] += std::chrono::duration<double, std::milli>(clock::now() - h0).count();
     s->stats.attempts += att;
     s->new_unique.push_back(add);
+    if (iter > 0) s->loss_trace.push_back(s->hpin->loss_total / cfg.batch);
   };
+  auto quota_left = [&] { return quota ? cfg.max_solutions - s->n_solutions : -1LL; };
   const int max_restarts = cfg.max_restarts > 0 ? cfg.max_restarts : 1000;
   bool timed_out = false;
   cudaEvent_t e0, e1, r0, r1;
@@ -498,19 +545,34 @@ void sampler_run(sgx_sampler* s) {
     sampler_init(s, restart);
     CK(cudaEventRecord(e1, s->st));
     const long long before = s->n_solutions;
-    harvest(restart, 0);
-    s->phase_ms[0] += elapsed(e0, e1);
-    for (int iter = 1; iter <= cfg.iterations && !quota_met(); ++iter) {
-      if (out_of_time()) {
+    // Harvest `h_iter` (stream sh) runs while the step of iteration h_iter + 1
+    // (stream st) already samples: the step needs only V, the harvest only
+    // the hardened words, and the backward waits for the harvest's reads
+    // (ev_front) before rewriting them.  Without a quota the next step is
+    // launched before the host waits on the harvest (it is discarded if the
+    // run stops there); with a quota it follows the harvest, as the reference
+    // decides per row whether to continue (sampler.cpp:129, :163).
+    long long h_quota = quota_left();
+    harvest_front(s, restart, 0, h_quota);
+    harvest_back_launch(s, -1);
+    int h_iter = 0, h_slot = -1;
+    for (;;) {
+      const int it = h_iter + 1;
+      int slot = -1;
+      if (!quota && it <= cfg.iterations && !out_of_time()) slot = sampler_step(s);
+      finish(h_iter, h_quota, h_slot);
+      if (h_iter == 0) s->phase_ms[0] += elapsed(e0, e1);
+      if (it > cfg.iterations || quota_met()) break;
+      if (out_of_time()) {  // sampler.cpp:164: checked before every step
         timed_out = true;
         break;
       }
-      sampler_step(s);
-      harvest(restart, iter);
-      s->loss_trace.push_back(s->hpin->loss_total / cfg.batch);
-      s->phase_ms[1] += elapsed(s->ev[0], s->ev[2]);
-      s->phase_ms[3] += elapsed(s->ev[0], s->ev[1]);
-      s->phase_ms[4] += elapsed(s->ev[1], s->ev[2]);
+      if (slot < 0) slot = sampler_step(s);
+      h_quota = quota_left();
+      harvest_front(s, restart, it, h_quota);
+      harvest_back_launch(s, slot);
+      h_iter = it;
+      h_slot = slot;
     }
     if (quota_met() || timed_out) break;
     if (cfg.restart_policy != SGX_RESTART_REINIT_ON_EXHAUST) break;
@@ -522,6 +584,8 @@ void sampler_run(sgx_sampler* s) {
     }
     s->stats.restarts = restart + 1;
   }
+  CK(cudaEventRecord(s->ev_join, s->sh));
+  CK(cudaStreamWaitEvent(s->st, s->ev_join, 0));
   CK(cudaEventRecord(r1, s->st));
   CK(cudaEventSynchronize(r1));
   s->stats.device_ms = elapsed(r0, r1);
@@ -548,8 +612,8 @@ void reset_solutions(sgx_sampler* s) {
   s->table_count = 0;
   s->epoch = 0;
   if (s->tcap) {
-    CK(cudaMemsetAsync(s->tkeys.p, 0, s->tcap * sizeof(unsigned long long), s->st));
-    CK(cudaMemsetAsync(s->tmeta.p, 0xff, s->tcap * sizeof(unsigned long long), s->st));
+    CK(cudaMemsetAsync(s->tkeys.p, 0, s->tcap * sizeof(unsigned long long), s->sh));
+    CK(cudaMemsetAsync(s->tmeta.p, 0xff, s->tcap * sizeof(unsigned long long), s->sh));
   }
 }
 
@@ -678,7 +742,13 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
     s->c = c;
     s->cfg = *cfg;
     CK(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s->sh, cudaStreamNonBlocking));
     for (auto& e : s->ev) CK(cudaEventCreate(&e));
+    for (auto& row : s->sev)
+      for (auto& e : row) CK(cudaEventCreate(&e));
+    for (auto* e : {&s->ev_soft, &s->ev_front, &s->ev_join}) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    // Nothing recorded yet: a wait on a never-recorded event is a no-op.
+    s->dloss.alloc(2);
     CK(cudaMallocHost(&s->hpin, sizeof(sgx::HarvestOut)));
     std::memset(s->hpin, 0, sizeof(sgx::HarvestOut));
     s->hout.alloc(1);
@@ -710,6 +780,10 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       if (const char* e = std::getenv("SGX_HARVEST")) {
         if (e[0] == 'g') s->hwpc = 0;  // force the global-memory harvest
       }
+      if (const char* e = std::getenv("SGX_HWPC")) {  // A/B: words per harvest CTA
+        const int w = std::atoi(e);
+        if ((w == 1 || w == 2 || w == 4 || w == 8) && row_bytes * w <= 220 * 1024) s->hwpc = w;
+      }
       // Stream-ordered pool allocations: a sampler created after another one
       // reuses its memory without cudaMalloc / cudaFree round trips.
       const size_t Bp = static_cast<size_t>(s->Bp);
@@ -736,6 +810,7 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       CK(cudaMemsetAsync(s->HB.p, 0xff, s->HB.n * sizeof(uint32_t), s->st));  // harden(0) = 1
       ensure_table(s.get());
       CK(cudaStreamSynchronize(s->st));
+      CK(cudaStreamSynchronize(s->sh));
     }
     *out = s.release();
   });
@@ -746,6 +821,8 @@ int sgx_sampler_free(sgx_sampler* s) {
     if (!s) return;
     cudaSetDevice(s->c->ctx->device);
     cudaStream_t st = s->st;
+    if (s->sh) cudaStreamSynchronize(s->sh);  // no harvest work left
+    s->drain.reset();                          // no host copy left reading the store
     if (st) {  // hand the big buffers back to the pool in stream order
       for (auto* b : {&s->V, &s->tape, &s->adj, &s->row_loss}) b->reset_async(st);
       s->partial.reset_async(st);
@@ -758,12 +835,18 @@ int sgx_sampler_free(sgx_sampler* s) {
       s->tmeta.reset_async(st);
       cudaStreamSynchronize(st);
     }
-    s->drain.reset();
     for (auto& e : s->ev)
       if (e) cudaEventDestroy(e);
+    for (auto& row : s->sev)
+      for (auto& e : row)
+        if (e) cudaEventDestroy(e);
+    for (auto e : {s->ev_soft, s->ev_front, s->ev_join})
+      if (e) cudaEventDestroy(e);
     if (s->hpin) cudaFreeHost(s->hpin);
+    cudaStream_t sh = s->sh;
     delete s;
     if (st) cudaStreamDestroy(st);
+    if (sh) cudaStreamDestroy(sh);
   });
 }
 
@@ -785,10 +868,11 @@ int sgx_step(sgx_sampler* s, double* loss_total) {
   return guard([&] {
     need_ready(s);
     CK(cudaSetDevice(s->c->ctx->device));
-    sampler_step(s);
-    CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->st));
+    const int slot = sampler_step(s);
+    double loss = 0.0;
+    CK(cudaMemcpyAsync(&loss, s->dloss.p + slot, sizeof(double), cudaMemcpyDeviceToHost, s->st));
     CK(cudaStreamSynchronize(s->st));
-    if (loss_total) *loss_total = s->hpin->loss_total;
+    if (loss_total) *loss_total = loss;
   });
 }
 
@@ -803,7 +887,7 @@ int sgx_harvest(sgx_sampler* s, int32_t restart, int32_t iter, int64_t* attempts
       return;
     }
     long long att = 0, add = 0;
-    sampler_harvest(s, restart, iter, quota_left, &att, &add);
+    sampler_harvest(s, restart, iter, quota_left, &att, &add, -1);
     if (attempts) *attempts = att;
     if (added) *added = add;
   });
@@ -848,8 +932,8 @@ int sgx_fetch_solutions(sgx_sampler* s, int64_t first, int64_t count, uint64_t* 
     CK(cudaSetDevice(s->c->ctx->device));
     const size_t kw = static_cast<size_t>(s->c->L.key_words);
     CK(cudaMemcpyAsync(keys, s->store.p + static_cast<size_t>(first) * kw,
-                       static_cast<size_t>(count) * kw * sizeof(uint64_t), cudaMemcpyDeviceToHost, s->st));
-    CK(cudaStreamSynchronize(s->st));
+                       static_cast<size_t>(count) * kw * sizeof(uint64_t), cudaMemcpyDeviceToHost, s->sh));
+    CK(cudaStreamSynchronize(s->sh));
   });
 }
 
@@ -891,8 +975,8 @@ int sgx_solutions_take(sgx_sampler* s, uint64_t** keys, int64_t* rows, int64_t* 
     }
     const size_t bytes = static_cast<size_t>(s->n_solutions) * kw * sizeof(uint64_t);
     void* p = sgx::host_map(bytes);
-    const cudaError_t e = cudaMemcpyAsync(p, s->store.p, bytes, cudaMemcpyDeviceToHost, s->st);
-    const cudaError_t e2 = e == cudaSuccess ? cudaStreamSynchronize(s->st) : e;
+    const cudaError_t e = cudaMemcpyAsync(p, s->store.p, bytes, cudaMemcpyDeviceToHost, s->sh);
+    const cudaError_t e2 = e == cudaSuccess ? cudaStreamSynchronize(s->sh) : e;
     if (e2 != cudaSuccess) {
       sgx::host_free(p, bytes);
       CK(e2);
@@ -942,12 +1026,12 @@ int sgx_harvest_local(sgx_sampler* s, int32_t restart, int32_t iter, int64_t* n_
     CK(cudaSetDevice(s->c->ctx->device));
     if (!s->fps_local.p) s->fps_local.alloc(s->Bp);
     harvest_front(s, restart, iter, -1);
-    sgx::launch_compact_new(s->st, s->newmask.p, s->block_count.p, s->slot_of_row.p, s->tkeys.p, s->Bp,
+    sgx::launch_compact_new(s->sh, s->newmask.p, s->block_count.p, s->slot_of_row.p, s->tkeys.p, s->Bp,
                             s->fps_local.p);
     s->launches += 1;
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->st));
-    CK(cudaStreamSynchronize(s->st));
+    CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->sh));
+    CK(cudaStreamSynchronize(s->sh));
     if (n_new) *n_new = s->hpin->new_rows;
     if (fps) *fps = reinterpret_cast<uint64_t*>(s->fps_local.p);
     s->dist_stage = 1;
@@ -977,14 +1061,14 @@ int sgx_harvest_merge(sgx_sampler* s, const uint64_t* all_fps, const int64_t* co
     s->table_count += remote;
     ensure_table(s);
     if (!s->n_of.p || static_cast<int>(s->n_of.n) < nranks) s->n_of.alloc(std::max(nranks, 64));
-    CK(cudaMemcpyAsync(s->n_of.p, cnt.data(), nranks * sizeof(long long), cudaMemcpyHostToDevice, s->st));
-    sgx::launch_merge_remote(s->st, reinterpret_cast<const unsigned long long*>(all_fps), s->n_of.p,
+    CK(cudaMemcpyAsync(s->n_of.p, cnt.data(), nranks * sizeof(long long), cudaMemcpyHostToDevice, s->sh));
+    sgx::launch_merge_remote(s->sh, reinterpret_cast<const unsigned long long*>(all_fps), s->n_of.p,
                              nranks > 1 ? nranks : 0, rank, stride, s->tkeys.p, s->tmeta.p, s->tcap - 1,
                              s->epoch, s->newmask.p, s->Bp, s->block_count.p, s->hout.p);
     s->launches += nranks > 1 ? 3 : 2;
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->st));
-    CK(cudaStreamSynchronize(s->st));
+    CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->sh));
+    CK(cudaStreamSynchronize(s->sh));
     // Locally-new rows another rank claimed still occupy table slots.
     s->table_count += n_local - s->hpin->new_rows;
     if (n_won) *n_won = s->hpin->new_rows;
@@ -1002,9 +1086,10 @@ int sgx_harvest_commit(sgx_sampler* s, int64_t quota_left, int64_t* attempts, in
     h.last_row = -1;
     h.overflow = 0;
     *s->hpin = h;
-    CK(cudaMemcpyAsync(s->hout.p, s->hpin, sizeof(sgx::HarvestOut), cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->hout.p, s->hpin, sizeof(sgx::HarvestOut), cudaMemcpyHostToDevice, s->sh));
     long long att = 0, add = 0;
-    harvest_back(s, quota_left, &att, &add);  // counts the winners into table_count
+    harvest_back_launch(s, -1);
+    harvest_back_finish(s, quota_left, &att, &add, -1);  // counts the winners into table_count
     if (attempts) *attempts = att;
     if (added) *added = add;
     s->dist_stage = 0;

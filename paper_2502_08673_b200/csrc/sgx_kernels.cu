@@ -1110,11 +1110,11 @@ k_loss_partial(const float* __restrict__ row_loss, int batch, double* __restrict
   if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
 }
 
-__global__ void k_loss_final(const double* __restrict__ partial, int n, HarvestOut* out) {
+__global__ void k_loss_final(const double* __restrict__ partial, int n, double* out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double t = 0.0;
     for (int i = 0; i < n; ++i) t += partial[i];
-    out->loss_total = t;
+    *out = t;
   }
 }
 
@@ -1847,7 +1847,7 @@ void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* 
 }
 
 void launch_loss(cudaStream_t st, const float* row_loss, int batch, double* partial, int n_partial,
-                 HarvestOut* out) {
+                 double* out) {
   k_loss_partial<<<n_partial, kThreads, 0, st>>>(row_loss, batch, partial);
   k_loss_final<<<1, 32, 0, st>>>(partial, n_partial, out);
 }

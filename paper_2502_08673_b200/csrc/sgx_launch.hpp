@@ -35,7 +35,7 @@ void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* 
                          const uint8_t* out_tgt, int n_out, float* row_loss, const uint64_t* exp_tab,
                          uint32_t* hb, const int* dead, const int2* dead_lvl, const BwdBlocks* bb);
 void launch_loss(cudaStream_t st, const float* row_loss, int batch, double* partial, int n_partial,
-                 HarvestOut* out);
+                 double* out);
 void launch_harden(cudaStream_t st, const float* V, int ncpi, int nucpi, const int* cpi_row,
                    const int* ucpi_row, uint32_t* BT, int W, int tile_rows, uint64_t free_prefix,
                    long long row_offset);
