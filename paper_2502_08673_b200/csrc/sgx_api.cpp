@@ -819,10 +819,14 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
 int sgx_sampler_free(sgx_sampler* s) {
   return guard([&] {
     if (!s) return;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
     cudaSetDevice(s->c->ctx->device);
     cudaStream_t st = s->st;
     if (s->sh) cudaStreamSynchronize(s->sh);  // no harvest work left
+    const double t_sync = ms();
     s->drain.reset();                          // no host copy left reading the store
+    const double t_drain = ms();
     if (st) {  // hand the big buffers back to the pool in stream order
       for (auto* b : {&s->V, &s->tape, &s->adj, &s->row_loss}) b->reset_async(st);
       s->partial.reset_async(st);
@@ -847,6 +851,9 @@ int sgx_sampler_free(sgx_sampler* s) {
     delete s;
     if (st) cudaStreamDestroy(st);
     if (sh) cudaStreamDestroy(sh);
+    if (std::getenv("SGX_TRACE"))
+      std::fprintf(stderr, "[sgx] sampler free: harvest sync %.2f, drain %.2f, total %.2f ms\n", t_sync, t_drain,
+                   ms());
   });
 }
 

@@ -1,9 +1,11 @@
 #include "sgx_layout.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <numeric>
+#include <queue>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -27,6 +29,18 @@ int operand_count(int32_t k) {
 }
 
 std::string xv(int v) { return "x" + std::to_string(v); }
+
+// SGX_TRACE stage timer for the layout compiler.
+struct Lap {
+  bool on = getenv("SGX_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void operator()(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[sgx] layout   %-14s %.2f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
 
 // One node's micro-op run (BEGIN ... END) as edge records (kR* flags): the
 // BEGIN / SUB_BEGIN / SUB_END / END control rides on the neighbouring edge.
@@ -84,6 +98,7 @@ void run_records(const std::vector<I4>& run, std::vector<I4>& out) {
 // (autodiff.cpp:225-233 pushed in descending id order).  A NOT/BUF whose
 // operand is itself virtual stays materialized, so nesting depth is one.
 SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
+  Lap lap;
   SoftProgram P;
   const int n = L.n_nodes;
   P.row_of_node.assign(n, -1);
@@ -214,6 +229,7 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
   P.col_row.assign(L.cpi.size(), -1);
   for (size_t j = 0; j < L.cpi.size(); ++j) P.col_row[j] = P.row_of_node[L.node_of_var[L.cpi[j]]];
 
+  lap("fwd");
   // Fan-out lists inside the set: consumers in descending id, a-slot first.
   std::vector<int32_t> fo_cnt(n + 1, 0);
   for (int j = 0; j < n; ++j) {
@@ -297,6 +313,7 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
       P.rec.insert(P.rec.end(), rper[w].begin(), rper[w].end());
     }
   }
+  lap("bwd records");
   // Dead-adjoint lists: the last pass reading each adjoint row (a record's
   // .y), passes numbered in backward order.
   {
@@ -369,6 +386,7 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
 // ~x and x are free on a 32-row word, so NOT/BUF nodes with a materialized
 // operand become a mask on the reference instead of a row.
 void build_folded_bits(Layout& L) {
+  Lap lap;
   const int n = L.n_nodes;
   std::vector<uint8_t> virt(n, 0);
   for (int i = 0; i < n; ++i)
@@ -414,6 +432,7 @@ void build_folded_bits(Layout& L) {
   for (int o : L.out_node) L.fb_out_enc.push_back(enc(o));
   L.fb_key_enc.assign(static_cast<size_t>(L.key_words) * 64, -1);
   for (int v = 1; v <= L.num_vars; ++v) L.fb_key_enc[v - 1] = enc(L.node_of_var[v]);
+  lap("fb ops");
 
   // CNF records (kCnfOpen): a literal is its row, bit-inverted when negated
   // (row = e ^ (e >> 31)); a clause of <= 4 literals is one record padded with
@@ -423,9 +442,11 @@ void build_folded_bits(Layout& L) {
   // open all-zero records and transposed.
   const int64_t n_clauses = static_cast<int64_t>(L.clause_ptr.size()) - 1;
   const int32_t zero_row = L.fb_rows;
-  std::vector<std::vector<I4>> recs(n_clauses);
+  std::vector<I4> recs;                 // all clauses' records, flat
+  std::vector<int64_t> rec_ptr(n_clauses + 1, 0);
+  std::vector<int32_t> lits;
   for (int64_t c = 0; c < n_clauses; ++c) {
-    std::vector<int32_t> lits;
+    lits.clear();
     for (int64_t l = L.clause_ptr[c]; l < L.clause_ptr[c + 1]; ++l) {
       const int32_t lit = L.clause_lit[l];
       const int e = enc(L.node_of_var[lit < 0 ? -lit : lit]);
@@ -433,24 +454,33 @@ void build_folded_bits(Layout& L) {
       lits.push_back(neg ? ~(e >> 1) : (e >> 1));
     }
     size_t k = 0;
-    for (; lits.size() - k > 4; k += 3) recs[c].push_back({lits[k], lits[k + 1], lits[k + 2], kCnfOpen});
+    for (; lits.size() - k > 4; k += 3) recs.push_back({lits[k], lits[k + 1], lits[k + 2], kCnfOpen});
     int32_t t[4] = {zero_row, zero_row, zero_row, zero_row};
     for (size_t u = 0; k + u < lits.size(); ++u) t[u] = lits[k + u];
-    recs[c].push_back({t[0], t[1], t[2], t[3]});
+    recs.push_back({t[0], t[1], t[2], t[3]});
+    rec_ptr[c + 1] = static_cast<int64_t>(recs.size());
   }
+  auto nrec = [&](int64_t c) { return rec_ptr[c + 1] - rec_ptr[c]; };
+  lap("cnf recs");
+  // Longest first, stable (a bucket sort on the record count).
+  int64_t maxr = 0;
+  for (int64_t c = 0; c < n_clauses; ++c) maxr = std::max(maxr, nrec(c));
+  std::vector<int64_t> bstart(maxr + 2, 0);
+  for (int64_t c = 0; c < n_clauses; ++c) ++bstart[maxr - nrec(c) + 1];
+  for (int64_t r = 1; r <= maxr + 1; ++r) bstart[r] += bstart[r - 1];
   std::vector<int64_t> order(n_clauses);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int64_t x, int64_t y) { return recs[x].size() > recs[y].size(); });
+  for (int64_t c = 0; c < n_clauses; ++c) order[bstart[maxr - nrec(c)]++] = c;
+  // Least-loaded thread, lowest index on ties (a min-heap of (load, thread)).
   std::vector<std::vector<I4>> per(kCnfThreads);
-  std::vector<size_t> load(kCnfThreads, 0);
+  std::priority_queue<std::pair<int64_t, int>, std::vector<std::pair<int64_t, int>>, std::greater<>> heap;
+  for (int t = 0; t < kCnfThreads; ++t) heap.push({0, t});
   for (int64_t c : order) {
-    int best = 0;
-    for (int t = 1; t < kCnfThreads; ++t)
-      if (load[t] < load[best]) best = t;
-    per[best].insert(per[best].end(), recs[c].begin(), recs[c].end());
-    load[best] += recs[c].size();
+    auto [ld, best] = heap.top();
+    heap.pop();
+    per[best].insert(per[best].end(), recs.begin() + rec_ptr[c], recs.begin() + rec_ptr[c + 1]);
+    heap.push({ld + nrec(c), best});
   }
+  lap("cnf deal");
   size_t steps = 0;
   for (const auto& p : per) steps = std::max(steps, p.size());
   L.fb_cnf_steps = static_cast<int32_t>(steps);
@@ -463,6 +493,14 @@ void build_folded_bits(Layout& L) {
 
 Layout build_layout(const sgx_circuit_desc& d) {
   Layout L;
+  const bool trace = getenv("SGX_TRACE") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[sgx] layout %-12s %.2f ms\n", what, std::chrono::duration<double, std::milli>(t - tp).count());
+    tp = t;
+  };
   if (d.n_nodes < 0 || d.num_vars < 0 || d.n_outputs < 0 || d.n_cpi < 0 || d.n_ucpi < 0 ||
       d.n_clauses < 0)
     throw std::invalid_argument("negative size in circuit descriptor");
@@ -543,6 +581,7 @@ Layout build_layout(const sgx_circuit_desc& d) {
     if (v == 0 || v > L.num_vars) throw std::invalid_argument("variable " + std::to_string(v) + " is unassigned");
   }
 
+  lap("validate");
   // ASAP levels.
   L.level.assign(n, 0);
   for (int i = 0; i < n; ++i) {
@@ -561,6 +600,7 @@ Layout build_layout(const sgx_circuit_desc& d) {
     if (oc == 2) cone[L.b[i]] = 1;
   }
   L.cone = build_soft(L, cone);
+  lap("soft");
   (void)all;  // the all-node program for the parity taps is built on demand
 
   // Bit program: every node, level-sorted; INPUT rows come from the harden
@@ -604,7 +644,9 @@ Layout build_layout(const sgx_circuit_desc& d) {
   L.key_words = (L.num_vars + 63) / 64;
   L.key_bit_row.assign(static_cast<size_t>(L.key_words) * 64, -1);
   for (int v = 1; v <= L.num_vars; ++v) L.key_bit_row[v - 1] = L.bit_row_of_node[L.node_of_var[v]];
+  lap("bits");
   build_folded_bits(L);
+  lap("folded");
   return L;
 }
 
