@@ -202,6 +202,10 @@ struct sgx_circuit {
   DBuf<int> fb_lvl_ptr, fb_cpi_row, fb_ucpi_row, fb_out_enc, fb_key_enc;
   DBuf<int4> fb_cnf4;
   int fb_levels = 0;
+  // liveness-allocated harvest (Layout::lb_*)
+  DBuf<int4> lb_ops, lb_chk;
+  DBuf<int> lb_op_ptr, lb_chk_ptr, lb_big, lb_key_enc;
+  DBuf<int2> lb_cpi, lb_ucpi;
 };
 
 struct sgx_sampler {
@@ -210,6 +214,8 @@ struct sgx_sampler {
   cudaStream_t st = nullptr;
   int Bp = 0, W = 0, wpc = 8, vec = 2, n_partial = 148;
   int hwpc = 0;  // words per CTA of the shared-memory harvest (0: global-memory path)
+  int hlive = 0;  // words per CTA of the liveness-allocated harvest (0: not used)
+  DBuf<uint32_t> SP;  // its spill tape of CNF-variable rows [n_spill][W]
   DBuf<float> V, tape, adj, row_loss;
   DBuf<double> partial;
   DBuf<uint32_t> BT, valid, newmask;
@@ -377,7 +383,40 @@ void harvest_front(sgx_sampler* s, int restart, int iter, long long quota_left) 
       sgx::fold(sgx::fold(sgx::fold(sgx::kPi, s->cfg.seed), sgx::kFreeTag), static_cast<uint64_t>(static_cast<int64_t>(restart))),
       static_cast<uint64_t>(static_cast<int64_t>(iter)));
   s->epoch += 1;
-  if (s->hwpc > 0) {
+  if (s->hlive > 0) {
+    sgx::HarvestLiveArgs a{};
+    a.hb = s->HB.p;
+    a.ncpi = static_cast<int>(L.cpi.size());
+    a.nucpi = static_cast<int>(L.ucpi.size());
+    a.cpi = c->lb_cpi.p;
+    a.ucpi = c->lb_ucpi.p;
+    a.free_prefix = fprefix;
+    a.row_offset = s->cfg.row_offset;
+    a.ops = c->lb_ops.p;
+    a.op_ptr = c->lb_op_ptr.p;
+    a.chk = c->lb_chk.p;
+    a.chk_ptr = c->lb_chk_ptr.p;
+    a.big_lits = c->lb_big.p;
+    a.n_phases = L.lb_levels;
+    a.slots = L.lb_slots;
+    a.spill = s->SP.p;
+    a.W = s->W;
+    a.key_enc = c->lb_key_enc.p;
+    a.key_words = L.key_words;
+    a.batch = s->cfg.batch;
+    a.Bp = s->Bp;
+    a.valid = s->valid.p;
+    a.K = s->K.p;
+    a.slot_of_row = s->slot_of_row.p;
+    a.tkeys = s->tkeys.p;
+    a.tmeta = s->tmeta.p;
+    a.tmask = s->tcap - 1;
+    a.epoch = s->epoch;
+    if (!sgx::launch_harvest_live(s->sh, s->hlive, a)) throw CudaError("live harvest does not fit shared memory");
+    CK(cudaEventRecord(s->ev[4], s->sh));
+    CK(cudaEventRecord(s->ev[5], s->sh));
+    s->launches += 1;
+  } else if (s->hwpc > 0) {
     sgx::HarvestSmemArgs a{};
     a.hb = s->HB.p;
     a.ncpi = static_cast<int>(L.cpi.size());
@@ -708,6 +747,14 @@ int sgx_circuit_upload(sgx_ctx* ctx, const sgx_circuit_desc* d, sgx_circuit** ou
       c->fb_out_enc.upload(L.fb_out_enc, st);
       c->fb_key_enc.upload(L.fb_key_enc, st);
       c->fb_cnf4.upload(to_int4(L.fb_cnf4), st);
+      c->lb_ops.upload(to_int4(L.lb_ops), st);
+      c->lb_chk.upload(to_int4(L.lb_chk), st);
+      c->lb_op_ptr.upload(L.lb_op_ptr, st);
+      c->lb_chk_ptr.upload(L.lb_chk_ptr, st);
+      c->lb_big.upload(L.lb_big_lits.empty() ? std::vector<int32_t>{0} : L.lb_big_lits, st);
+      c->lb_key_enc.upload(L.lb_key_enc, st);
+      c->lb_cpi.upload(to_int2(L.lb_cpi), st);
+      c->lb_ucpi.upload(to_int2(L.lb_ucpi), st);
       CK(cudaStreamSynchronize(st));
     }
     *out = c.release();
@@ -784,6 +831,33 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
         const int w = std::atoi(e);
         if ((w == 1 || w == 2 || w == 4 || w == 8) && row_bytes * w <= 220 * 1024) s->hwpc = w;
       }
+      // Liveness-allocated harvest (default): the words per CTA that keep the
+      // most words resident per SM (8 CTAs of 256 threads at most, ~227 KB of
+      // shared memory) with at least one CTA per SM; ties go to more words per
+      // CTA (per-level overhead amortised).  SGX_HARVEST=smem / g force the
+      // full-tape shared-memory / global-memory harvests.
+      s->hlive = 0;
+      {
+        const char* e = std::getenv("SGX_HARVEST");
+        const bool live_ok = !(e && (e[0] == 'g' || e[0] == 's'));
+        int best_words = 0;
+        for (int w = 1; w <= 8 && live_ok; w *= 2) {
+          const size_t smem = static_cast<size_t>(L.lb_slots) * w * sizeof(uint32_t) + 3 * 1024;
+          if (smem > 200 * 1024 || s->W / w < 148) continue;
+          const int ctas = std::min<int>(8, static_cast<int>((227 * 1024) / (smem + 1024)));
+          if (ctas * w >= best_words) {
+            best_words = ctas * w;
+            s->hlive = w;
+          }
+        }
+        if (const char* v = std::getenv("SGX_LWPC")) {  // A/B: words per live-harvest CTA
+          const int w = std::atoi(v);
+          if ((w == 1 || w == 2 || w == 4 || w == 8) && live_ok &&
+              static_cast<size_t>(L.lb_slots) * w * 4 <= 200 * 1024)
+            s->hlive = w;
+        }
+        if (s->hlive) s->hwpc = 0;
+      }
       // Stream-ordered pool allocations: a sampler created after another one
       // reuses its memory without cudaMalloc / cudaFree round trips.
       const size_t Bp = static_cast<size_t>(s->Bp);
@@ -794,7 +868,8 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       s->adj.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
       s->row_loss.alloc_async(Bp, st);
       s->partial.alloc_async(s->n_partial, st);
-      if (!s->hwpc) s->BT.alloc_async(static_cast<size_t>(L.n_bit_rows) * s->W, st);
+      if (!s->hwpc && !s->hlive) s->BT.alloc_async(static_cast<size_t>(L.n_bit_rows) * s->W, st);
+      if (s->hlive) s->SP.alloc_async(static_cast<size_t>(std::max(L.lb_n_spill, 1)) * s->W, st);
       s->valid.alloc_async(s->W, st);
       s->newmask.alloc_async(s->W, st);
       s->slot_of_row.alloc_async(Bp, st);
@@ -830,7 +905,7 @@ int sgx_sampler_free(sgx_sampler* s) {
     if (st) {  // hand the big buffers back to the pool in stream order
       for (auto* b : {&s->V, &s->tape, &s->adj, &s->row_loss}) b->reset_async(st);
       s->partial.reset_async(st);
-      for (auto* b : {&s->BT, &s->valid, &s->newmask, &s->HB}) b->reset_async(st);
+      for (auto* b : {&s->BT, &s->valid, &s->newmask, &s->HB, &s->SP}) b->reset_async(st);
       s->slot_of_row.reset_async(st);
       s->block_count.reset_async(st);
       s->K.reset_async(st);

@@ -1482,6 +1482,222 @@ k_harvest_smem(int n_rows, const uint32_t* __restrict__ hb, int ncpi, int nucpi,
   }
 }
 
+// ---------------------------------------------------------------------------
+// K5+K6+K7 fused with a liveness-allocated bit tape: a CTA owns WPC words
+// (32*WPC rows); its shared memory holds only the LIVE rows of the folded
+// bit program, in host-assigned slots (sgx_layout.cpp build_live_bits), so
+// deep and wide circuits (C4: 8,072 slots instead of 54,234 rows) stay on chip
+// and shallow ones fit several CTAs per SM.  Per phase: that level's gate ops
+// (eval_discrete, circuit.cpp:126-146), then the output checks and CNF
+// clauses whose latest literal was defined one phase earlier (sampler.cpp:
+// 140-147, cnf.cpp:136-145); one barrier.  Rows of CNF variables are also
+// written to a global spill tape, which the key phase (dedupe_key,
+// sampler.cpp:18-26) reads back after the last phase.
+// ---------------------------------------------------------------------------
+template <int WPC>
+__device__ __forceinline__ void load_words(const uint32_t* p, uint32_t (&x)[WPC]) {
+  if constexpr (WPC == 4) {
+    const uint4 t = *reinterpret_cast<const uint4*>(p);
+    x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
+  } else if constexpr (WPC == 8) {
+    const uint4 t = reinterpret_cast<const uint4*>(p)[0], u = reinterpret_cast<const uint4*>(p)[1];
+    x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w; x[4] = u.x; x[5] = u.y; x[6] = u.z; x[7] = u.w;
+  } else if constexpr (WPC == 2) {
+    const uint2 t = *reinterpret_cast<const uint2*>(p);
+    x[0] = t.x; x[1] = t.y;
+  } else {
+    x[0] = *p;
+  }
+}
+
+template <int WPC>
+__global__ void __launch_bounds__(kThreads)
+k_harvest_live(const HarvestLiveArgs a) {
+  extern __shared__ uint32_t bits[];  // [slot][WPC]; slot 0 = 0
+  __shared__ uint32_t red[kThreads];
+  __shared__ uint32_t vw[WPC];
+  __shared__ unsigned long long hsum[WPC * 32];
+  constexpr int NW = kThreads / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w0 = blockIdx.x * WPC;
+  const size_t Wz = static_cast<size_t>(a.W);
+  if (threadIdx.x < WPC) bits[threadIdx.x] = 0u;
+  for (int t = threadIdx.x; t < WPC * 32; t += kThreads) hsum[t] = 0ull;
+  // phase 0 inputs: hardened V (autodiff.cpp:292-297) and free bits (sampler.cpp:132-137)
+  for (int item = threadIdx.x; item < a.ncpi * WPC; item += kThreads) {
+    const int wl = item / a.ncpi, j = item - wl * a.ncpi;
+    const int2 cs = __ldg(a.cpi + j);
+    const uint32_t word = __ldg(a.hb + static_cast<size_t>(w0 + wl) * a.ncpi + j);
+    bits[cs.x * WPC + wl] = word;
+    if (cs.y >= 0) a.spill[cs.y * Wz + w0 + wl] = word;
+  }
+  for (int item = warp; item < a.nucpi * WPC; item += NW) {
+    const int k = item / WPC, wl = item - k * WPC;
+    const int r = (w0 + wl) * 32 + lane;
+    const bool bit = fold(fold(a.free_prefix, static_cast<uint64_t>(a.row_offset + r)), static_cast<uint64_t>(k)) & 1;
+    const uint32_t word = __ballot_sync(kFull, bit);
+    if (lane == 0) {
+      const int2 cs = __ldg(a.ucpi + k);
+      bits[cs.x * WPC + wl] = word;
+      if (cs.y >= 0) a.spill[cs.y * Wz + w0 + wl] = word;
+    }
+  }
+  __syncthreads();
+  uint32_t ok[WPC];
+#pragma unroll
+  for (int wl = 0; wl < WPC; ++wl) ok[wl] = kFull;
+  // Each thread's first op and first check of the next phase are loaded
+  // before this phase's barrier (and the phase bounds one phase further
+  // ahead), so a phase starts on records already in registers instead of an
+  // L2 round trip (C4: 635 phases).
+  int ob = __ldg(a.op_ptr), oe = __ldg(a.op_ptr + 1), cb = __ldg(a.chk_ptr), ce = __ldg(a.chk_ptr + 1);
+  int4 nop = threadIdx.x < (oe - ob) * WPC ? __ldg(a.ops + ob + threadIdx.x / WPC) : make_int4(0, 0, 0, -1);
+  int4 nchk = threadIdx.x < ce - cb ? __ldg(a.chk + cb + threadIdx.x) : make_int4(0, 0, 0, 0);
+  int oe2 = a.n_phases > 1 ? __ldg(a.op_ptr + 2) : oe, ce2 = a.n_phases > 1 ? __ldg(a.chk_ptr + 2) : ce;
+  for (int ph = 0; ph < a.n_phases; ++ph) {
+    const int4 cop = nop, cchk = nchk;
+    const int nob = oe, noe = oe2, ncb = ce, nce = ce2;  // phase ph + 1
+    if (ph + 1 < a.n_phases) {
+      nop = threadIdx.x < (noe - nob) * WPC ? __ldg(a.ops + nob + threadIdx.x / WPC) : make_int4(0, 0, 0, -1);
+      nchk = threadIdx.x < nce - ncb ? __ldg(a.chk + ncb + threadIdx.x) : make_int4(0, 0, 0, 0);
+      oe2 = ph + 3 <= a.n_phases ? __ldg(a.op_ptr + ph + 3) : noe;
+      ce2 = ph + 3 <= a.n_phases ? __ldg(a.chk_ptr + ph + 3) : nce;
+    }
+    for (int item = threadIdx.x; item < (oe - ob) * WPC; item += kThreads) {
+      const int wl = item % WPC;
+      const int4 op = item == static_cast<int>(threadIdx.x) ? cop : __ldg(a.ops + ob + item / WPC);
+      const uint32_t x = bits[(op.y >> 1) * WPC + wl] ^ neg_mask(op.y);
+      const uint32_t y = bits[(op.z >> 1) * WPC + wl] ^ neg_mask(op.z);
+      const uint32_t v = bit_gate(op.x & 0xf, x, y);
+      bits[(op.x >> 4) * WPC + wl] = v;
+      if (op.w >= 0) a.spill[op.w * Wz + w0 + wl] = v;
+    }
+    for (int i = cb + threadIdx.x; i < ce; i += kThreads) {
+      const int4 rec = i == cb + static_cast<int>(threadIdx.x) ? cchk : __ldg(a.chk + i);
+      if (rec.w == kLbBig) {  // a long clause, literal by literal
+        uint32_t any[WPC];
+#pragma unroll
+        for (int wl = 0; wl < WPC; ++wl) any[wl] = 0u;
+        for (int l = rec.x; l < rec.x + rec.y; ++l) {
+          const int lit = __ldg(a.big_lits + l), sgn = lit >> 31;
+#pragma unroll
+          for (int wl = 0; wl < WPC; ++wl) any[wl] |= bits[(lit ^ sgn) * WPC + wl] ^ static_cast<uint32_t>(sgn);
+        }
+#pragma unroll
+        for (int wl = 0; wl < WPC; ++wl) ok[wl] &= any[wl];
+      } else {
+        const int lit[4] = {rec.x, rec.y, rec.z, rec.w};
+#pragma unroll
+        for (int wl = 0; wl < WPC; ++wl) {
+          uint32_t any = 0u;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int sgn = lit[u] >> 31;
+            any |= bits[(lit[u] ^ sgn) * WPC + wl] ^ static_cast<uint32_t>(sgn);
+          }
+          ok[wl] &= any;
+        }
+      }
+    }
+    ob = nob;
+    oe = noe;
+    cb = ncb;
+    ce = nce;
+    __syncthreads();
+  }
+#pragma unroll
+  for (int wl = 0; wl < WPC; ++wl) {
+    const uint32_t v = __reduce_and_sync(kFull, ok[wl]);
+    if (lane == 0) red[warp * WPC + wl] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < WPC) {
+    const int wl = threadIdx.x;
+    uint32_t v = kFull;
+#pragma unroll
+    for (int j = 0; j < NW; ++j) v &= red[j * WPC + wl];
+    const int r0 = (w0 + wl) * 32;
+    const uint32_t mask = r0 + 32 <= a.batch ? kFull : (r0 >= a.batch ? 0u : ((1u << (a.batch - r0)) - 1u));
+    vw[wl] = v & mask;
+    a.valid[w0 + wl] = v & mask;
+  }
+  __syncthreads();
+  // dedupe keys (sampler.cpp:18-26) from the spill tape: one warp per key
+  // word, all WPC words of a variable row in one vector load
+  uint32_t anyv = 0u;
+#pragma unroll
+  for (int wl = 0; wl < WPC; ++wl) anyv |= vw[wl];
+  if (anyv) {
+    for (int q = warp; q < a.key_words; q += NW) {
+      uint32_t half[2][WPC];
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        const int e = __ldg(a.key_enc + (2 * q + hf) * 32 + lane);
+        uint32_t x[WPC];
+        if (e >= 0) {
+          load_words<WPC>(a.spill + (e >> 1) * Wz + w0, x);
+#pragma unroll
+          for (int wl = 0; wl < WPC; ++wl) x[wl] ^= neg_mask(e);
+        } else {
+#pragma unroll
+          for (int wl = 0; wl < WPC; ++wl) x[wl] = 0u;
+        }
+#pragma unroll
+        for (int wl = 0; wl < WPC; ++wl) half[hf][wl] = transpose32(x[wl], lane);
+      }
+#pragma unroll
+      for (int wl = 0; wl < WPC; ++wl) {
+        if (!vw[wl]) continue;  // block-uniform
+        const uint64_t kw = static_cast<uint64_t>(half[0][wl]) | (static_cast<uint64_t>(half[1][wl]) << 32);
+        atomicAdd(hsum + wl * 32 + lane, static_cast<unsigned long long>(key_term(kw, q)));
+        if ((vw[wl] >> lane) & 1u) a.K[static_cast<size_t>(q) * a.Bp + (w0 + wl) * 32 + lane] = kw;
+      }
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < WPC * 32; t += kThreads) {
+    const int wl = t >> 5, ln = t & 31;
+    if (!((vw[wl] >> ln) & 1u)) continue;
+    const int r = (w0 + wl) * 32 + ln;
+    const uint64_t h = mix64(hsum[t]);
+    const unsigned long long fp = h ? h : 1ull;
+    uint64_t idx = (fp ^ (fp >> 29)) & a.tmask;
+    for (;;) {
+      unsigned long long cur = a.tkeys[idx];
+      if (cur == fp) break;
+      if (cur == 0ull) {
+        cur = atomicCAS(a.tkeys + idx, 0ull, fp);
+        if (cur == 0ull || cur == fp) break;
+      }
+      idx = (idx + 1) & a.tmask;
+    }
+    atomicMin(a.tmeta + idx, static_cast<unsigned long long>((a.epoch << 32) | static_cast<uint32_t>(r)));
+    a.slot_of_row[r] = static_cast<int>(idx);
+  }
+}
+
+template <int WPC>
+static bool harvest_live_t(cudaStream_t st, const HarvestLiveArgs& a) {
+  const size_t smem = static_cast<size_t>(a.slots) * WPC * sizeof(uint32_t);
+  if (smem > 200 * 1024) return false;
+  static size_t opted = 0;
+  if (smem > opted) {
+    cudaFuncSetAttribute(k_harvest_live<WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    opted = smem;
+  }
+  k_harvest_live<WPC><<<a.W / WPC, kThreads, smem, st>>>(a);
+  return true;
+}
+
+bool launch_harvest_live(cudaStream_t st, int wpc, const HarvestLiveArgs& a) {
+  switch (wpc) {
+    case 8: return harvest_live_t<8>(st, a);
+    case 4: return harvest_live_t<4>(st, a);
+    case 2: return harvest_live_t<2>(st, a);
+    default: return harvest_live_t<1>(st, a);
+  }
+}
+
 // new[w] bit r: valid row whose fingerprint this epoch first saw at this row.
 // Per-block counts for the row-order scan.
 __global__ void __launch_bounds__(kThreads)

@@ -77,6 +77,33 @@ struct HarvestSmemArgs {
 // Fused shared-memory harvest (harden + eval + PO/CNF + keys + insert); the
 // folded bit tape of wpc words must fit in shared memory.
 void launch_harvest_smem(cudaStream_t st, int wpc, int n_rows, int W, const HarvestSmemArgs& a);
+// Liveness-allocated harvest (sgx_layout.hpp Layout::lb_*): bit tape in
+// `slots` shared-memory rows per word, CNF-variable rows spilled to a global
+// tape [n_spill][W] for the key phase.
+struct HarvestLiveArgs {
+  const uint32_t* hb;  // hardened V columns [word][ncpi]
+  int ncpi, nucpi;
+  const int2 *cpi, *ucpi;  // {slot, spill}
+  uint64_t free_prefix;
+  long long row_offset;
+  const int4* ops;
+  const int* op_ptr;
+  const int4* chk;
+  const int* chk_ptr;
+  const int* big_lits;
+  int n_phases, slots;
+  uint32_t* spill;  // [n_spill][W]
+  int W;
+  const int* key_enc;
+  int key_words, batch, Bp;
+  uint32_t* valid;
+  uint64_t* K;
+  int* slot_of_row;
+  unsigned long long *tkeys, *tmeta;
+  uint64_t tmask, epoch;
+};
+// wpc words per CTA; returns false if the slots do not fit shared memory.
+bool launch_harvest_live(cudaStream_t st, int wpc, const HarvestLiveArgs& a);
 void launch_compact_new(cudaStream_t st, const uint32_t* newmask, const int* block_off, const int* slot_of_row,
                         const unsigned long long* tkeys, int Bp, unsigned long long* out);
 void launch_merge_remote(cudaStream_t st, const unsigned long long* all_fps, const long long* n_of, int nranks,

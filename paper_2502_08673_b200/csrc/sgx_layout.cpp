@@ -491,6 +491,147 @@ void build_folded_bits(Layout& L) {
 
 }  // namespace
 
+// Liveness-allocated harvest program (Layout::lb_*; k_harvest_live).
+void build_live_bits(Layout& L) {
+  const int n = L.n_nodes;
+  std::vector<uint8_t> virt(n, 0);
+  for (int i = 0; i < n; ++i)
+    if ((L.kind[i] == SGX_NOT || L.kind[i] == SGX_BUF) && !virt[L.a[i]]) virt[i] = 1;
+  auto base = [&](int x) { return virt[x] ? L.a[x] : x; };
+  auto negv = [&](int x) { return virt[x] && L.kind[x] == SGX_NOT; };
+  std::vector<int32_t> lev(n, 0);
+  int max_level = 0;
+  for (int i = 0; i < n; ++i) {
+    if (virt[i]) continue;
+    const int oc = operand_count(L.kind[i]);
+    if (oc >= 1) lev[i] = lev[base(L.a[i])] + 1;
+    if (oc == 2) lev[i] = std::max(lev[i], lev[base(L.b[i])] + 1);
+    max_level = std::max(max_level, lev[i]);
+  }
+  const int P = max_level + 2;  // checks of the last level run in the extra phase
+  // last phase reading each row
+  std::vector<int32_t> last(n, -1);
+  for (int i = 0; i < n; ++i) {
+    if (virt[i]) continue;
+    last[i] = std::max(last[i], lev[i]);
+    const int oc = operand_count(L.kind[i]);
+    if (oc >= 1) last[base(L.a[i])] = std::max(last[base(L.a[i])], lev[i]);
+    if (oc == 2) last[base(L.b[i])] = std::max(last[base(L.b[i])], lev[i]);
+  }
+  const int64_t n_clauses = static_cast<int64_t>(L.clause_ptr.size()) - 1;
+  std::vector<int32_t> cl_phase(n_clauses);
+  for (int64_t c = 0; c < n_clauses; ++c) {
+    int m = 0;
+    for (int64_t l = L.clause_ptr[c]; l < L.clause_ptr[c + 1]; ++l) {
+      const int32_t lit = L.clause_lit[l];
+      m = std::max(m, lev[base(L.node_of_var[lit < 0 ? -lit : lit])]);
+    }
+    cl_phase[c] = m + 1;
+    for (int64_t l = L.clause_ptr[c]; l < L.clause_ptr[c + 1]; ++l) {
+      const int32_t lit = L.clause_lit[l];
+      const int r = base(L.node_of_var[lit < 0 ? -lit : lit]);
+      last[r] = std::max(last[r], m + 1);
+    }
+  }
+  for (int o : L.out_node) last[base(o)] = std::max(last[base(o)], lev[base(o)] + 1);
+  // linear-scan slot allocation (slot 0 is the always-zero row)
+  std::vector<std::vector<int32_t>> def_at(P), free_at(P + 1);
+  for (int i = 0; i < n; ++i)
+    if (!virt[i]) {
+      def_at[lev[i]].push_back(i);
+      free_at[last[i] + 1].push_back(i);
+    }
+  std::vector<int32_t> slot(n, -1);
+  std::priority_queue<int32_t, std::vector<int32_t>, std::greater<>> freeq;
+  int32_t nslots = 1;
+  for (int ph = 0; ph < P; ++ph) {
+    for (int r : free_at[ph]) freeq.push(slot[r]);
+    for (int r : def_at[ph]) {
+      if (freeq.empty()) {
+        slot[r] = nslots++;
+      } else {
+        slot[r] = freeq.top();
+        freeq.pop();
+      }
+    }
+  }
+  L.lb_slots = nslots;
+  L.lb_levels = P;
+  // spill rows: bases of CNF-variable nodes
+  std::vector<int32_t> spill(n, -1);
+  int32_t nsp = 0;
+  for (int v = 1; v <= L.num_vars; ++v) {
+    const int r = base(L.node_of_var[v]);
+    if (spill[r] < 0) spill[r] = nsp++;
+  }
+  L.lb_n_spill = nsp;
+  auto enc = [&](int x) { return (slot[base(x)] << 1) | (negv(x) ? 1 : 0); };
+  L.lb_ops.clear();
+  L.lb_op_ptr.clear();
+  for (int ph = 0; ph < P; ++ph) {
+    L.lb_op_ptr.push_back(static_cast<int32_t>(L.lb_ops.size()));
+    for (int i : def_at[ph]) {
+      if (L.kind[i] == SGX_INPUT) continue;
+      const int oc = operand_count(L.kind[i]);
+      L.lb_ops.push_back({L.kind[i] | (slot[i] << 4), oc >= 1 ? enc(L.a[i]) : 0, oc == 2 ? enc(L.b[i]) : 0,
+                          spill[i]});
+    }
+  }
+  L.lb_op_ptr.push_back(static_cast<int32_t>(L.lb_ops.size()));
+  // checks by phase: output targets (one-literal checks), then clauses
+  std::vector<std::vector<I4>> chk(P);
+  auto lit_of = [&](int x, bool negate) {  // slot, or ~slot when the value is complemented
+    const int32_t sl = slot[base(x)];
+    return (negv(x) != negate) ? ~sl : sl;
+  };
+  for (size_t m = 0; m < L.out_node.size(); ++m) {
+    const int o = L.out_node[m];
+    chk[lev[base(o)] + 1].push_back({lit_of(o, L.out_tgt[m] == 0), 0, 0, 0});
+  }
+  L.lb_big_lits.clear();
+  for (int64_t c = 0; c < n_clauses; ++c) {
+    const int64_t k = L.clause_ptr[c + 1] - L.clause_ptr[c];
+    std::vector<int32_t> lits;
+    for (int64_t l = L.clause_ptr[c]; l < L.clause_ptr[c + 1]; ++l) {
+      const int32_t lit = L.clause_lit[l];
+      lits.push_back(lit_of(L.node_of_var[lit < 0 ? -lit : lit], lit < 0));
+    }
+    if (k <= 4) {
+      int32_t t[4] = {0, 0, 0, 0};
+      for (int64_t u = 0; u < k; ++u) t[u] = lits[u];
+      chk[cl_phase[c]].push_back({t[0], t[1], t[2], t[3]});
+    } else {
+      chk[cl_phase[c]].push_back({static_cast<int32_t>(L.lb_big_lits.size()), static_cast<int32_t>(k), 0, kLbBig});
+      L.lb_big_lits.insert(L.lb_big_lits.end(), lits.begin(), lits.end());
+    }
+  }
+  L.lb_chk.clear();
+  L.lb_chk_ptr.clear();
+  for (int ph = 0; ph < P; ++ph) {
+    L.lb_chk_ptr.push_back(static_cast<int32_t>(L.lb_chk.size()));
+    L.lb_chk.insert(L.lb_chk.end(), chk[ph].begin(), chk[ph].end());
+  }
+  L.lb_chk_ptr.push_back(static_cast<int32_t>(L.lb_chk.size()));
+  L.lb_cpi.clear();
+  L.lb_ucpi.clear();
+  for (int v : L.cpi) {
+    const int r = L.node_of_var[v];
+    L.lb_cpi.insert(L.lb_cpi.end(), {slot[r], spill[r]});
+  }
+  for (int v : L.ucpi) {
+    const int r = L.node_of_var[v];
+    L.lb_ucpi.insert(L.lb_ucpi.end(), {slot[r], spill[r]});
+  }
+  L.lb_key_enc.assign(static_cast<size_t>(L.key_words) * 64, -1);
+  for (int v = 1; v <= L.num_vars; ++v) {
+    const int x = L.node_of_var[v];
+    L.lb_key_enc[v - 1] = (spill[base(x)] << 1) | (negv(x) ? 1 : 0);
+  }
+  if (getenv("SGX_TRACE"))
+    fprintf(stderr, "[sgx] live harvest: %d phases, %d slots (of %d rows), %d spill rows, %zu ops, %zu checks\n",
+            P, nslots, L.fb_rows, nsp, L.lb_ops.size(), L.lb_chk.size());
+}
+
 Layout build_layout(const sgx_circuit_desc& d) {
   Layout L;
   const bool trace = getenv("SGX_TRACE") != nullptr;
@@ -647,6 +788,8 @@ Layout build_layout(const sgx_circuit_desc& d) {
   lap("bits");
   build_folded_bits(L);
   lap("folded");
+  build_live_bits(L);
+  lap("live");
   return L;
 }
 

@@ -75,6 +75,7 @@ constexpr int32_t kRInSub = 1 << 4, kRNegOther = 1 << 5, kRFirst = 1 << 6, kRSub
 constexpr int32_t kRSlow = 1 << 16;
 constexpr int kCnfThreads = 256;               // threads of the shared-memory harvest CTA
 constexpr int32_t kCnfOpen = INT32_MIN;        // CNF record continues (see fb_cnf4)
+constexpr int32_t kLbBig = INT32_MIN;          // lb_chk: long clause, literals in lb_big_lits
 constexpr int kGroup = 4;                      // ops per forward group
 constexpr int kGroupRecs = 1 + kGroup / 2;     // int4 records per group
 
@@ -166,6 +167,29 @@ struct Layout {
   // read consecutive records.  Shared-memory tapes hold fb_rows + 1 rows.
   int32_t fb_cnf_steps = 0;
   std::vector<I4> fb_cnf4;
+
+  // Liveness-allocated harvest (k_harvest_live): the folded bit program with
+  // rows mapped to shared-memory SLOTS by a linear scan over the levels (a
+  // slot is reused once its row's last reader -- gate operand, clause or
+  // output check -- has run), so only the live set is on chip.  Every check
+  // runs one level after its latest literal is defined (one barrier per
+  // level).  Rows whose node carries a CNF variable are also written to a
+  // global spill tape [lb_n_spill][words], read back by the key phase.
+  //   op record:      {kind | out_slot << 4, a_enc, b_enc, spill (-1)}, enc = slot << 1 | negate
+  //   check record:   up to 4 literals, slot or ~slot (negated), padding = slot 0
+  //                   (always zero); a longer clause is {lit offset, count, 0, kLbBig}
+  //                   with its literals in lb_big_lits
+  //   input:          {slot, spill} per constrained / free input (int2)
+  int32_t lb_slots = 0;              // slots incl. the zero slot 0
+  int32_t lb_levels = 0;             // phases (levels + one trailing check phase)
+  int32_t lb_n_spill = 0;
+  std::vector<I4> lb_ops;
+  std::vector<int32_t> lb_op_ptr;    // per phase
+  std::vector<I4> lb_chk;
+  std::vector<int32_t> lb_chk_ptr;   // per phase
+  std::vector<int32_t> lb_big_lits;
+  std::vector<int32_t> lb_cpi, lb_ucpi;  // {slot, spill} pairs
+  std::vector<int32_t> lb_key_enc;   // key_words * 64: spill << 1 | negate (-1 padding)
 
   int64_t n_lits() const { return static_cast<int64_t>(clause_lit.size()); }
 };
