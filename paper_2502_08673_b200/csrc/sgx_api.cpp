@@ -248,7 +248,7 @@ struct sgx_sampler {
   std::vector<int64_t> new_unique;
   sgx_run_stats stats{};
   double phase_ms[8] = {0};
-  double host_ms[4] = {0};  // harvest wall, table growth, store growth, (spare)
+  double host_ms[8] = {0};  // harvest wall, table growth, store growth, (spare)
   cudaEvent_t ev[8] = {nullptr};
 };
 
@@ -489,7 +489,14 @@ void harvest_back_launch(sgx_sampler* s, int loss_slot) {
 void harvest_back_finish(sgx_sampler* s, long long quota_left, long long* attempts, long long* added,
                          int step_slot) {
   const auto& L = s->c->L;
+  static const bool trace2 = std::getenv("SGX_TRACE2") != nullptr;
+  const auto tw = std::chrono::steady_clock::now();
   CK(cudaStreamSynchronize(s->sh));
+  if (trace2) {
+    const double w = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tw).count();
+    std::fprintf(stderr, "[sgx] harvest sync wait %.3f ms, harvest gpu %.3f ms, step gpu %.3f ms\n", w,
+                 elapsed(s->ev[3], s->ev[6]), step_slot >= 0 ? elapsed(s->sev[step_slot][0], s->sev[step_slot][3]) : 0.0);
+  }
   if (s->hpin->overflow) {
     const double loss = s->hpin->loss_total;
     const auto t0 = std::chrono::steady_clock::now();
@@ -510,7 +517,11 @@ void harvest_back_finish(sgx_sampler* s, long long quota_left, long long* attemp
   s->n_solutions += h.accepted;
   *added = h.accepted;
   // Grow ahead of need, in stream order, so the next harvest never overflows.
-  if (s->store_cap - s->n_solutions < s->Bp) grow_store(s, s->n_solutions + 2LL * s->Bp);
+  if (s->store_cap - s->n_solutions < s->Bp) {
+    const auto t0 = std::chrono::steady_clock::now();
+    grow_store(s, s->n_solutions + 2LL * s->Bp);
+    s->host_ms[2] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
   // Quota met inside this harvest: the reference stops at the row after the
   // one that filled it (sampler.cpp:129).
   if (quota_left >= 0 && h.accepted == quota_left && h.accepted > 0)
@@ -549,7 +560,7 @@ void sampler_run(sgx_sampler* s) {
   s->new_unique.clear();
   s->stats = sgx_run_stats{};
   std::fill(s->phase_ms, s->phase_ms + 8, 0.0);
-  std::fill(s->host_ms, s->host_ms + 4, 0.0);
+  std::fill(s->host_ms, s->host_ms + 8, 0.0);
   s->launches = 0;
   if (s->c->L.unsat) {
     s->stats.unsat = 1;
@@ -571,6 +582,10 @@ void sampler_run(sgx_sampler* s) {
     if (iter > 0) s->loss_trace.push_back(s->hpin->loss_total / cfg.batch);
   };
   auto quota_left = [&] { return quota ? cfg.max_solutions - s->n_solutions : -1LL; };
+  static const bool overlap = [] {  // SGX_OVERLAP=0: the next step waits for the harvest (A/B)
+    const char* e = std::getenv("SGX_OVERLAP");
+    return !(e && e[0] == '0');
+  }();
   const int max_restarts = cfg.max_restarts > 0 ? cfg.max_restarts : 1000;
   bool timed_out = false;
   cudaEvent_t e0, e1, r0, r1;
@@ -592,15 +607,24 @@ void sampler_run(sgx_sampler* s) {
     // run stops there); with a quota it follows the harvest, as the reference
     // decides per row whether to continue (sampler.cpp:129, :163).
     long long h_quota = quota_left();
+    auto hclk = clock::now();
+    auto hlap = [&](int k) {
+      const auto n = clock::now();
+      s->host_ms[k] += std::chrono::duration<double, std::milli>(n - hclk).count();
+      hclk = n;
+    };
     harvest_front(s, restart, 0, h_quota);
     harvest_back_launch(s, -1);
+    hlap(3);
     int h_iter = 0, h_slot = -1;
     for (;;) {
       const int it = h_iter + 1;
       int slot = -1;
-      if (!quota && it <= cfg.iterations && !out_of_time()) slot = sampler_step(s);
+      if (overlap && !quota && it <= cfg.iterations && !out_of_time()) slot = sampler_step(s);
+      hlap(4);
       finish(h_iter, h_quota, h_slot);
       if (h_iter == 0) s->phase_ms[0] += elapsed(e0, e1);
+      hlap(5);
       if (it > cfg.iterations || quota_met()) break;
       if (out_of_time()) {  // sampler.cpp:164: checked before every step
         timed_out = true;
@@ -608,8 +632,10 @@ void sampler_run(sgx_sampler* s) {
       }
       if (slot < 0) slot = sampler_step(s);
       h_quota = quota_left();
+      hlap(4);
       harvest_front(s, restart, it, h_quota);
       harvest_back_launch(s, slot);
+      hlap(3);
       h_iter = it;
       h_slot = slot;
     }
@@ -631,8 +657,10 @@ void sampler_run(sgx_sampler* s) {
   s->stats.launches = s->launches;
   if (std::getenv("SGX_TRACE"))
     std::fprintf(stderr, "[sgx] device %.2f ms; harvest wall %.2f ms (table growth %.2f, store growth %.2f); "
-                 "phases init %.2f step %.2f harvest %.2f\n", s->stats.device_ms, s->host_ms[0], s->host_ms[1],
-                 s->host_ms[2], s->phase_ms[0], s->phase_ms[1], s->phase_ms[2]);
+                 "phases init %.2f step %.2f harvest %.2f; host: harvest launch %.2f step launch %.2f finish %.2f, "
+                 "run wall %.2f ms\n", s->stats.device_ms, s->host_ms[0], s->host_ms[1],
+                 s->host_ms[2], s->phase_ms[0], s->phase_ms[1], s->phase_ms[2], s->host_ms[3], s->host_ms[4],
+                 s->host_ms[5], 1000.0 * now_s());
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaEventDestroy(r0);

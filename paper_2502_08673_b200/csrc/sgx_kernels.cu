@@ -1510,6 +1510,25 @@ __device__ __forceinline__ void load_words(const uint32_t* p, uint32_t (&x)[WPC]
   }
 }
 
+// WPC consecutive words of one shared-memory slot as one vector access.
+template <int WPC>
+__device__ __forceinline__ void lds_words(const uint32_t* p, uint32_t (&x)[WPC]) {
+  load_words<WPC>(p, x);
+}
+template <int WPC>
+__device__ __forceinline__ void sts_words(uint32_t* p, const uint32_t (&x)[WPC]) {
+  if constexpr (WPC == 4) {
+    *reinterpret_cast<uint4*>(p) = make_uint4(x[0], x[1], x[2], x[3]);
+  } else if constexpr (WPC == 8) {
+    reinterpret_cast<uint4*>(p)[0] = make_uint4(x[0], x[1], x[2], x[3]);
+    reinterpret_cast<uint4*>(p)[1] = make_uint4(x[4], x[5], x[6], x[7]);
+  } else if constexpr (WPC == 2) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(x[0], x[1]);
+  } else {
+    *p = x[0];
+  }
+}
+
 template <int WPC>
 __global__ void __launch_bounds__(kThreads)
 k_harvest_live(const HarvestLiveArgs a) {
@@ -1551,26 +1570,43 @@ k_harvest_live(const HarvestLiveArgs a) {
   // ahead), so a phase starts on records already in registers instead of an
   // L2 round trip (C4: 635 phases).
   int ob = __ldg(a.op_ptr), oe = __ldg(a.op_ptr + 1), cb = __ldg(a.chk_ptr), ce = __ldg(a.chk_ptr + 1);
-  int4 nop = threadIdx.x < (oe - ob) * WPC ? __ldg(a.ops + ob + threadIdx.x / WPC) : make_int4(0, 0, 0, -1);
+  // Narrow CTAs (WPC <= 2) spread a phase's ops over (op, word) items for
+  // more threads per phase; wider ones process an op's WPC words as vectors.
+  constexpr int OW = WPC <= 2 ? WPC : 1;  // items per op
+  int4 nop = threadIdx.x < (oe - ob) * OW ? __ldg(a.ops + ob + threadIdx.x / OW) : make_int4(0, 0, 0, -1);
   int4 nchk = threadIdx.x < ce - cb ? __ldg(a.chk + cb + threadIdx.x) : make_int4(0, 0, 0, 0);
   int oe2 = a.n_phases > 1 ? __ldg(a.op_ptr + 2) : oe, ce2 = a.n_phases > 1 ? __ldg(a.chk_ptr + 2) : ce;
   for (int ph = 0; ph < a.n_phases; ++ph) {
     const int4 cop = nop, cchk = nchk;
     const int nob = oe, noe = oe2, ncb = ce, nce = ce2;  // phase ph + 1
     if (ph + 1 < a.n_phases) {
-      nop = threadIdx.x < (noe - nob) * WPC ? __ldg(a.ops + nob + threadIdx.x / WPC) : make_int4(0, 0, 0, -1);
+      nop = threadIdx.x < (noe - nob) * OW ? __ldg(a.ops + nob + threadIdx.x / OW) : make_int4(0, 0, 0, -1);
       nchk = threadIdx.x < nce - ncb ? __ldg(a.chk + ncb + threadIdx.x) : make_int4(0, 0, 0, 0);
       oe2 = ph + 3 <= a.n_phases ? __ldg(a.op_ptr + ph + 3) : noe;
       ce2 = ph + 3 <= a.n_phases ? __ldg(a.chk_ptr + ph + 3) : nce;
     }
-    for (int item = threadIdx.x; item < (oe - ob) * WPC; item += kThreads) {
-      const int wl = item % WPC;
-      const int4 op = item == static_cast<int>(threadIdx.x) ? cop : __ldg(a.ops + ob + item / WPC);
-      const uint32_t x = bits[(op.y >> 1) * WPC + wl] ^ neg_mask(op.y);
-      const uint32_t y = bits[(op.z >> 1) * WPC + wl] ^ neg_mask(op.z);
-      const uint32_t v = bit_gate(op.x & 0xf, x, y);
-      bits[(op.x >> 4) * WPC + wl] = v;
-      if (op.w >= 0) a.spill[op.w * Wz + w0 + wl] = v;
+    if constexpr (OW > 1) {
+      for (int item = threadIdx.x; item < (oe - ob) * OW; item += kThreads) {  // (op, word)
+        const int wl = item % OW;
+        const int4 op = item == static_cast<int>(threadIdx.x) ? cop : __ldg(a.ops + ob + item / OW);
+        const uint32_t x = bits[(op.y >> 1) * WPC + wl] ^ neg_mask(op.y);
+        const uint32_t y = bits[(op.z >> 1) * WPC + wl] ^ neg_mask(op.z);
+        const uint32_t v = bit_gate(op.x & 0xf, x, y);
+        bits[(op.x >> 4) * WPC + wl] = v;
+        if (op.w >= 0) a.spill[op.w * Wz + w0 + wl] = v;
+      }
+    } else {
+      for (int item = threadIdx.x; item < oe - ob; item += kThreads) {  // one op, all WPC words
+        const int4 op = item == static_cast<int>(threadIdx.x) ? cop : __ldg(a.ops + ob + item);
+        uint32_t x[WPC], y[WPC], v[WPC];
+        lds_words<WPC>(bits + (op.y >> 1) * WPC, x);
+        lds_words<WPC>(bits + (op.z >> 1) * WPC, y);
+        const uint32_t mx = neg_mask(op.y), my = neg_mask(op.z);
+#pragma unroll
+        for (int wl = 0; wl < WPC; ++wl) v[wl] = bit_gate(op.x & 0xf, x[wl] ^ mx, y[wl] ^ my);
+        sts_words<WPC>(bits + (op.x >> 4) * WPC, v);
+        if (op.w >= 0) sts_words<WPC>(a.spill + op.w * Wz + w0, v);
+      }
     }
     for (int i = cb + threadIdx.x; i < ce; i += kThreads) {
       const int4 rec = i == cb + static_cast<int>(threadIdx.x) ? cchk : __ldg(a.chk + i);
@@ -1587,16 +1623,19 @@ k_harvest_live(const HarvestLiveArgs a) {
         for (int wl = 0; wl < WPC; ++wl) ok[wl] &= any[wl];
       } else {
         const int lit[4] = {rec.x, rec.y, rec.z, rec.w};
+        uint32_t any[WPC];
 #pragma unroll
-        for (int wl = 0; wl < WPC; ++wl) {
-          uint32_t any = 0u;
+        for (int wl = 0; wl < WPC; ++wl) any[wl] = 0u;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int sgn = lit[u] >> 31;
-            any |= bits[(lit[u] ^ sgn) * WPC + wl] ^ static_cast<uint32_t>(sgn);
-          }
-          ok[wl] &= any;
+        for (int u = 0; u < 4; ++u) {
+          const int sgn = lit[u] >> 31;
+          uint32_t x[WPC];
+          lds_words<WPC>(bits + (lit[u] ^ sgn) * WPC, x);
+#pragma unroll
+          for (int wl = 0; wl < WPC; ++wl) any[wl] |= x[wl] ^ static_cast<uint32_t>(sgn);
         }
+#pragma unroll
+        for (int wl = 0; wl < WPC; ++wl) ok[wl] &= any[wl];
       }
     }
     ob = nob;
