@@ -159,6 +159,14 @@ int sgx_harvest(sgx_sampler* s, int32_t restart, int32_t iter, int64_t* attempts
  *   sgx_harvest_commit  append the first min(n_won, quota_left) of them
  *                       (quota_left < 0: no quota); attempts as sgx_harvest. */
 int sgx_fingerprint_stride(const sgx_sampler* s);
+/* The fingerprint buffer of sgx_harvest_local holds stride + 1 int64: the
+ * harvest's new fingerprints in row order, then their count at [stride], so
+ * one all-gather of stride + 1 values per rank carries both. */
+/* A GD step launched without waiting (the multi-GPU loop runs the next step
+ * while the harvest's exchange is in flight); *slot names it for
+ * sgx_step_loss, which waits for that step and returns its loss total. */
+int sgx_step_async(sgx_sampler* s, int32_t* slot);
+int sgx_step_loss(sgx_sampler* s, int32_t slot, double* loss_total);
 int sgx_harvest_local(sgx_sampler* s, int32_t restart, int32_t iter, int64_t* n_new, uint64_t** fps);
 int sgx_harvest_merge(sgx_sampler* s, const uint64_t* all_fps, const int64_t* counts, int32_t nranks,
                       int32_t rank, int64_t stride, int64_t* n_won);

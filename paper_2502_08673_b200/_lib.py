@@ -23,7 +23,7 @@ EXPORTS = [
     "sgx_solution_count", "sgx_key_words", "sgx_fetch_solutions", "sgx_phase_times",
     "sgx_forward", "sgx_backward", "sgx_embed", "sgx_expf", "sgx_fingerprint_stride",
     "sgx_harvest_local", "sgx_harvest_merge", "sgx_harvest_commit", "sgx_read_logits",
-    "sgx_set_host_stream", "sgx_solutions_take", "sgx_host_free",
+    "sgx_set_host_stream", "sgx_solutions_take", "sgx_host_free", "sgx_step_async", "sgx_step_loss",
 ]
 
 
@@ -116,6 +116,8 @@ def load() -> C.CDLL:
         "sgx_set_host_stream": (C.c_int, [vp, i32]),
         "sgx_solutions_take": (C.c_int, [vp, C.POINTER(C.c_void_p), i64p, i64p]),
         "sgx_host_free": (C.c_int, [C.c_void_p, i64]),
+        "sgx_step_async": (C.c_int, [vp, C.POINTER(i32)]),
+        "sgx_step_loss": (C.c_int, [vp, i32, f64p]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

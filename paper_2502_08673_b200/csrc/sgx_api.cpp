@@ -238,6 +238,7 @@ struct sgx_sampler {
   cudaEvent_t ev_soft = nullptr, ev_front = nullptr, ev_join = nullptr;
   cudaEvent_t sev[2][4] = {};  // per step parity: fwd begin / end, bwd begin / end
   DBuf<double> dloss;          // per step parity: loss total (sum over rows)
+  double* hloss = nullptr;     // pinned copies of dloss (sgx_step_async / sgx_step_loss)
   long long steps = 0;         // steps launched (parity of the next)
   uint64_t epoch = 0;
   long long launches = 0;
@@ -318,6 +319,8 @@ int sampler_step(sgx_sampler* s) {
            s->row_loss.p, tab, s->HB.p);
   sgx::launch_loss(s->st, s->row_loss.p, s->cfg.batch, s->partial.p, s->n_partial, s->dloss.p + slot);
   s->launches += 4;
+  if (s->hloss)
+    CK(cudaMemcpyAsync(s->hloss + slot, s->dloss.p + slot, sizeof(double), cudaMemcpyDeviceToHost, s->st));
   CK(cudaEventRecord(ev[3], s->st));
   CK(cudaEventRecord(s->ev_soft, s->st));
   CK(cudaGetLastError());
@@ -824,6 +827,7 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
     for (auto* e : {&s->ev_soft, &s->ev_front, &s->ev_join}) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     // Nothing recorded yet: a wait on a never-recorded event is a no-op.
     s->dloss.alloc(2);
+    CK(cudaMallocHost(&s->hloss, 2 * sizeof(double)));
     CK(cudaMallocHost(&s->hpin, sizeof(sgx::HarvestOut)));
     std::memset(s->hpin, 0, sizeof(sgx::HarvestOut));
     s->hout.alloc(1);
@@ -950,6 +954,7 @@ int sgx_sampler_free(sgx_sampler* s) {
     for (auto e : {s->ev_soft, s->ev_front, s->ev_join})
       if (e) cudaEventDestroy(e);
     if (s->hpin) cudaFreeHost(s->hpin);
+    if (s->hloss) cudaFreeHost(s->hloss);
     cudaStream_t sh = s->sh;
     delete s;
     if (st) cudaStreamDestroy(st);
@@ -983,6 +988,25 @@ int sgx_step(sgx_sampler* s, double* loss_total) {
     CK(cudaMemcpyAsync(&loss, s->dloss.p + slot, sizeof(double), cudaMemcpyDeviceToHost, s->st));
     CK(cudaStreamSynchronize(s->st));
     if (loss_total) *loss_total = loss;
+  });
+}
+
+int sgx_step_async(sgx_sampler* s, int32_t* slot) {
+  return guard([&] {
+    need_ready(s);
+    need(slot, "slot");
+    CK(cudaSetDevice(s->c->ctx->device));
+    *slot = sampler_step(s);
+  });
+}
+
+int sgx_step_loss(sgx_sampler* s, int32_t slot, double* loss_total) {
+  return guard([&] {
+    need_ready(s);
+    if (slot != 0 && slot != 1) throw std::invalid_argument("step slot must be 0 or 1");
+    CK(cudaSetDevice(s->c->ctx->device));
+    CK(cudaEventSynchronize(s->sev[slot][3]));
+    if (loss_total) *loss_total = s->hloss[slot];
   });
 }
 
@@ -1134,12 +1158,15 @@ int sgx_harvest_local(sgx_sampler* s, int32_t restart, int32_t iter, int64_t* n_
     need_ready(s);
     if (s->dist_stage != 0) throw StateError("sgx_harvest_local: previous harvest not committed");
     CK(cudaSetDevice(s->c->ctx->device));
-    if (!s->fps_local.p) s->fps_local.alloc(s->Bp);
+    if (!s->fps_local.p) s->fps_local.alloc(static_cast<size_t>(s->Bp) + 1);
     harvest_front(s, restart, iter, -1);
     sgx::launch_compact_new(s->sh, s->newmask.p, s->block_count.p, s->slot_of_row.p, s->tkeys.p, s->Bp,
                             s->fps_local.p);
     s->launches += 1;
     CK(cudaGetLastError());
+    // the count rides at [stride] so one all-gather carries fingerprints and counts
+    CK(cudaMemcpyAsync(s->fps_local.p + s->Bp, &s->hout.p->new_rows, sizeof(long long), cudaMemcpyDeviceToDevice,
+                       s->sh));
     CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->sh));
     CK(cudaStreamSynchronize(s->sh));
     if (n_new) *n_new = s->hpin->new_rows;

@@ -17,9 +17,14 @@ sampler.cpp:89-194, restated over the union).
 can be exercised on CPU (gloo) with a stand-in sampler:
   * a sampler with init(restart) / step() / harvest_local(restart, it) ->
     (n_new, fps) / harvest_merge(gathered, counts, world, rank) -> n_won /
-    harvest_commit(quota_left) -> (attempts, added);
+    harvest_commit(quota_left) -> (attempts, added); optionally
+    step_async() -> slot / step_loss(slot) (the next step then samples while
+    the harvest's exchange is in flight) and gather_stride / counts(gathered,
+    world) (the counts ride in the fingerprint all-gather);
   * an exchange with all_gather_int(x) -> list[int] and
     all_gather_fps(fps, stride) -> gathered.
+Per harvest on the device path: one all-gather of fingerprints + counts, one
+of the merged counts (plus one of attempts only under a quota).
 """
 from __future__ import annotations
 
@@ -45,6 +50,7 @@ class DeviceShard:
         self.s = sampler
         self.L = _lib.load()
         self.stride = int(self.L.sgx_fingerprint_stride(sampler.h))
+        self.gather_stride = self.stride + 1  # fingerprints, then their count
         self.device = sampler.dc.device
 
     def init(self, restart: int):
@@ -53,12 +59,25 @@ class DeviceShard:
     def step(self) -> float:
         return self.s.step()
 
+    def step_async(self) -> int:
+        slot = C.c_int32()
+        _lib.check(self.L.sgx_step_async(self.s.h, C.byref(slot)))
+        return slot.value
+
+    def step_loss(self, slot: int) -> float:
+        x = C.c_double()
+        _lib.check(self.L.sgx_step_loss(self.s.h, slot, C.byref(x)))
+        return x.value
+
+    def counts(self, gathered, world: int) -> list[int]:
+        return [int(v) for v in gathered.view(world, self.gather_stride)[:, self.stride].cpu()]
+
     def harvest_local(self, restart: int, it: int):
         import torch
         n = C.c_int64()
         ptr = C.c_void_p()
         _lib.check(self.L.sgx_harvest_local(self.s.h, restart, it, C.byref(n), C.byref(ptr)))
-        fps = torch.as_tensor(_DevArray(ptr.value, self.stride, self.device),
+        fps = torch.as_tensor(_DevArray(ptr.value, self.gather_stride, self.device),
                               device=f"cuda:{self.device}")
         return n.value, fps
 
@@ -67,7 +86,7 @@ class DeviceShard:
         won = C.c_int64()
         cnt = np.ascontiguousarray(counts, np.int64)
         _lib.check(self.L.sgx_harvest_merge(self.s.h, C.c_void_p(gathered.data_ptr()),
-                                            _lib.ptr(cnt, C.c_int64), world, rank, self.stride,
+                                            _lib.ptr(cnt, C.c_int64), world, rank, self.gather_stride,
                                             C.byref(won)))
         return won.value
 
@@ -129,10 +148,17 @@ def run_sharded(shard, ex, cfg, rank: int, world: int, stride: int) -> ShardStat
         late = cfg.timeout_s > 0 and time.perf_counter() - t0 >= cfg.timeout_s
         return max(ex.all_gather_int(1 if late else 0)) > 0 if cfg.timeout_s > 0 else False
 
-    def harvest(restart, it):
+    overlap = hasattr(shard, "step_async")
+    gstride = getattr(shard, "gather_stride", stride)
+
+    def harvest(restart, it, launch_next):
+        """One harvest over the union; with launch_next the next step is
+        launched as soon as the local harvest kernels are done (it only reads
+        V; the backward waits for the harvest's reads on the device)."""
         n_new, fps = shard.harvest_local(restart, it)
-        counts = ex.all_gather_int(n_new)
-        gathered = ex.all_gather_fps(fps, stride)
+        slot = shard.step_async() if launch_next else None
+        gathered = ex.all_gather_fps(fps, gstride)
+        counts = shard.counts(gathered, world) if hasattr(shard, "counts") else ex.all_gather_int(n_new)
         won = shard.harvest_merge(gathered, counts, world, rank)
         wons = ex.all_gather_int(won)
         left = cfg.max_solutions - st.unique_count if quota else None
@@ -148,22 +174,33 @@ def run_sharded(shard, ex, cfg, rank: int, world: int, stride: int) -> ShardStat
             acc += take
         st.unique_count += acc
         st.local_count += add
-        st.attempts += sum(ex.all_gather_int(att))
+        # without a quota every rank attempts its whole batch
+        st.attempts += sum(ex.all_gather_int(att)) if quota else att * world
         st.new_unique.append(acc)
+        return slot
+
+    def speculate(it):  # the reference runs step `it` unless quota or time stop it first
+        return overlap and not quota and cfg.timeout_s <= 0 and it <= cfg.iterations
 
     restart = 0
     while True:
         shard.init(restart)
         before = st.unique_count
-        harvest(restart, 0)
+        slot = harvest(restart, 0, speculate(1))
         for it in range(1, cfg.iterations + 1):
             if quota_met():
                 break
             if out_of_time():
                 st.timed_out = True
                 break
-            st.loss_trace.append(shard.step() / cfg.batch)
-            harvest(restart, it)
+            if overlap:
+                if slot is None:
+                    slot = shard.step_async()
+                loss = shard.step_loss(slot)
+            else:
+                loss = shard.step()
+            st.loss_trace.append(loss / cfg.batch)
+            slot = harvest(restart, it, speculate(it + 1))
         if quota_met() or st.timed_out:
             break
         if int(cfg.restart) != 1:
