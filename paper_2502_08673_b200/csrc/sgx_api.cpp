@@ -872,16 +872,25 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       {
         const char* e = std::getenv("SGX_HARVEST");
         const bool live_ok = !(e && (e[0] == 'g' || e[0] == 's'));
-        int best_words = 0;
-        for (int w = 1; w <= 8 && live_ok; w *= 2) {
-          const size_t smem = static_cast<size_t>(L.lb_slots) * w * sizeof(uint32_t) + 3 * 1024;
-          if (smem > 200 * 1024 || s->W / w < 148) continue;
-          const int ctas = std::min<int>(8, static_cast<int>((227 * 1024) / (smem + 1024)));
-          if (ctas * w >= best_words) {
-            best_words = ctas * w;
-            s->hlive = w;
+        // words resident per SM for a tape of `rows` rows per word
+        auto best = [&](long long rows, int* wpc) {
+          int words = 0;
+          for (int w = 1; w <= 8; w *= 2) {
+            const size_t smem = static_cast<size_t>(rows) * w * sizeof(uint32_t) + 3 * 1024;
+            if (smem > 200 * 1024 || s->W / w < 148) continue;
+            const int ctas = std::min<int>(8, static_cast<int>((227 * 1024) / (smem + 1024)));
+            if (ctas * w >= words) {
+              words = ctas * w;
+              *wpc = w;
+            }
           }
-        }
+          return words;
+        };
+        int wl = 0, wf = 0;
+        const int live_words = live_ok ? best(L.lb_slots, &wl) : 0;
+        const int full_words = best(L.fb_rows + 1, &wf);
+        // The full tape needs no spill round trip for the keys: it wins ties.
+        if (live_words > full_words) s->hlive = wl;
         if (const char* v = std::getenv("SGX_LWPC")) {  // A/B: words per live-harvest CTA
           const int w = std::atoi(v);
           if ((w == 1 || w == 2 || w == 4 || w == 8) && live_ok &&

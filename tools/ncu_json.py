@@ -23,7 +23,8 @@ def val(r, key):
     return x * scale
 
 
-fam = {"k_backward": "k_backward", "k_forward": "k_forward", "k_harvest_smem": "k_harvest_smem"}
+fam = {"k_backward": "k_backward", "k_forward": "k_forward", "k_harvest_smem": "k_harvest",
+       "k_harvest_live": "k_harvest"}
 res = {}
 for r in rows[2:]:
     kname = r[hdr.index("Kernel Name")]
