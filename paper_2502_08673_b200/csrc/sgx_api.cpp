@@ -139,6 +139,8 @@ struct DevSoft {
   DBuf<int4> sblk, fblk;
   sgx::BwdBlocks bb;
   sgx::FwdBlocks fb;
+  DBuf<int4> oc;  // on-chip program (sgx_launch.hpp OnchipArgs layout)
+  int oc_n4 = 0, oc_rec = 0, oc_lvl = 0, oc_col = 0, oc_out = 0, oc_slots = 0;
   int n_fwd_levels = 0, n_bwd_levels = 0, n_rows = 0;
   void upload(const sgx::SoftProgram& P, cudaStream_t st) {
     fwd.upload(to_int4(P.fwd), st);
@@ -152,6 +154,30 @@ struct DevSoft {
     sblk.upload(to_int4(P.sblk), st);
     tail_dead.upload(P.tail_dead.empty() ? std::vector<int32_t>{-1} : P.tail_dead, st);
     fblk.upload(to_int4(P.fblk), st);
+    oc_n4 = 0;
+    if (!P.oc_fwd_lvl.empty()) {  // [groups][records][per level: fwd first, count, rec first, count][col slots][out enc]
+      std::vector<int4> pg;
+      for (const auto& g : P.oc_fwd) pg.push_back(make_int4(g.x, g.y, g.z, g.w));
+      oc_rec = static_cast<int>(pg.size());
+      for (const auto& r : P.oc_rec) pg.push_back(make_int4(r.x, r.y, r.z, r.w));
+      oc_lvl = static_cast<int>(pg.size());
+      for (int l = 0; l < P.n_levels; ++l)
+        pg.push_back(make_int4(P.oc_fwd_lvl[2 * l], P.oc_fwd_lvl[2 * l + 1], P.oc_rec_lvl[2 * l], P.oc_rec_lvl[2 * l + 1]));
+      auto pack = [&](const std::vector<int32_t>& v) {
+        const int at = static_cast<int>(pg.size());
+        for (size_t i = 0; i < v.size(); i += 4) {
+          int q[4] = {-1, -1, -1, -1};
+          for (size_t j = 0; j < 4 && i + j < v.size(); ++j) q[j] = v[i + j];
+          pg.push_back(make_int4(q[0], q[1], q[2], q[3]));
+        }
+        return at;
+      };
+      oc_col = pack(P.oc_col_slot);
+      oc_out = pack(P.out_enc);
+      oc_n4 = static_cast<int>(pg.size());
+      oc_slots = P.oc_adj_slots;
+      oc.upload(pg, st);
+    }
     fb = sgx::FwdBlocks{};
     if (!P.fblk.empty()) {
       fb.fblk = fblk.p;
@@ -215,6 +241,8 @@ struct sgx_sampler {
   int Bp = 0, W = 0, wpc = 8, vec = 2, n_partial = 148;
   int hwpc = 0;  // words per CTA of the shared-memory harvest (0: global-memory path)
   int hlive = 0;  // words per CTA of the liveness-allocated harvest (0: not used)
+  bool onchip = false;  // small circuit: fused on-chip soft pass (k_soft_onchip)
+  int hb_cur = 0;       // HB holds two buffers; the last init / step wrote this one
   DBuf<uint32_t> SP;  // its spill tape of CNF-variable rows [n_spill][W]
   DBuf<float> V, tape, adj, row_loss;
   DBuf<double> partial;
@@ -282,6 +310,18 @@ void need(const void* p, const char* what) {
   if (!p) throw std::invalid_argument(std::string(what) + " is null");
 }
 
+// The harvest's input words (hardened V) are double-buffered: an init or a
+// step writes the buffer the running harvest is not reading.
+uint32_t* hb_write(sgx_sampler* s) {
+  s->hb_cur ^= 1;
+  return s->HB.p + static_cast<size_t>(s->hb_cur) * s->c->L.cpi.size() * s->W;
+}
+uint32_t* hb_read(sgx_sampler* s) {
+  return s->HB.p + static_cast<size_t>(s->hb_cur) * s->c->L.cpi.size() * s->W;
+}
+// Only the global-memory harvest reads V itself.
+bool harvest_reads_v(const sgx_sampler* s) { return s->hwpc == 0 && s->hlive == 0; }
+
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.0f;
   CK(cudaEventElapsedTime(&ms, a, b));
@@ -291,11 +331,11 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 // ---------------------------------------------------------------- sampler ops
 void sampler_init(sgx_sampler* s, int restart) {
   const auto& L = s->c->L;
-  CK(cudaStreamWaitEvent(s->st, s->ev_front, 0));  // the last harvest is done reading V / HB
+  CK(cudaStreamWaitEvent(s->st, s->ev_front, 0));  // the last harvest is done reading V
   uint64_t prefix = sgx::fold(sgx::fold(sgx::fold(sgx::kPi, s->cfg.seed), sgx::kInitTag),
                               static_cast<uint64_t>(static_cast<int64_t>(restart)));
   sgx::launch_init_v(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, 32 * s->vec, prefix,
-                     s->cfg.row_offset, s->HB.p);
+                     s->cfg.row_offset, hb_write(s));
   s->launches += L.cpi.empty() ? 0 : 1;
   CK(cudaEventRecord(s->ev_soft, s->st));
   CK(cudaGetLastError());
@@ -309,14 +349,43 @@ int sampler_step(sgx_sampler* s) {
   cudaEvent_t* ev = s->sev[slot];
   CK(cudaEventRecord(ev[0], s->st));
   const int ncpi = static_cast<int>(c->L.cpi.size());
-  sgx::launch_forward(s->st, s->vec, c->cone.fwd.p, c->cone.fwd_lvl.p, c->cone.n_fwd_levels, s->V.p, ncpi,
-                      s->tape.p, c->cone.n_rows, s->Bp, 0, tab, &c->cone.fb);
-  CK(cudaEventRecord(ev[1], s->st));
-  CK(cudaStreamWaitEvent(s->st, s->ev_front, 0));  // the running harvest still reads V / HB
-  CK(cudaEventRecord(ev[2], s->st));
-  backward(s->st, s->vec, c->cone, s->tape.p, s->adj.p, s->V.p, ncpi, nullptr, nullptr, s->Bp,
-           static_cast<float>(s->cfg.learning_rate), c->out_tgt.p, static_cast<int>(c->L.out_node.size()),
-           s->row_loss.p, tab, s->HB.p);
+  uint32_t* hb = hb_write(s);
+  if (s->onchip) {
+    // forward + loss rows + backward + GD + harden in one kernel
+    if (harvest_reads_v(s)) CK(cudaStreamWaitEvent(s->st, s->ev_front, 0));
+    CK(cudaEventRecord(ev[1], s->st));
+    CK(cudaEventRecord(ev[2], s->st));
+    const DevSoft& P = c->cone;
+    sgx::OnchipArgs a{};
+    a.prog = P.oc.p;
+    a.prog_n4 = P.oc_n4;
+    a.off_rec = P.oc_rec;
+    a.off_lvl = P.oc_lvl;
+    a.off_col = P.oc_col;
+    a.off_out = P.oc_out;
+    a.n_levels = P.n_fwd_levels;
+    a.n_rows = P.n_rows;
+    a.n_slots = P.oc_slots;
+    a.ncols = ncpi;
+    a.n_out = static_cast<int>(c->L.out_node.size());
+    a.V = s->V.p;
+    a.hb = hb;
+    a.row_loss = s->row_loss.p;
+    a.out_tgt = c->out_tgt.p;
+    a.exp_tab = tab;
+    a.lr = static_cast<float>(s->cfg.learning_rate);
+    a.n_tiles = s->Bp / 32;
+    if (!sgx::launch_soft_onchip(s->st, a)) throw CudaError("on-chip soft pass does not fit");
+  } else {
+    sgx::launch_forward(s->st, s->vec, c->cone.fwd.p, c->cone.fwd_lvl.p, c->cone.n_fwd_levels, s->V.p, ncpi,
+                        s->tape.p, c->cone.n_rows, s->Bp, 0, tab, &c->cone.fb);
+    CK(cudaEventRecord(ev[1], s->st));
+    if (harvest_reads_v(s)) CK(cudaStreamWaitEvent(s->st, s->ev_front, 0));  // the running harvest reads V
+    CK(cudaEventRecord(ev[2], s->st));
+    backward(s->st, s->vec, c->cone, s->tape.p, s->adj.p, s->V.p, ncpi, nullptr, nullptr, s->Bp,
+             static_cast<float>(s->cfg.learning_rate), c->out_tgt.p, static_cast<int>(c->L.out_node.size()),
+             s->row_loss.p, tab, hb);
+  }
   sgx::launch_loss(s->st, s->row_loss.p, s->cfg.batch, s->partial.p, s->n_partial, s->dloss.p + slot);
   s->launches += 4;
   if (s->hloss)
@@ -388,7 +457,7 @@ void harvest_front(sgx_sampler* s, int restart, int iter, long long quota_left) 
   s->epoch += 1;
   if (s->hlive > 0) {
     sgx::HarvestLiveArgs a{};
-    a.hb = s->HB.p;
+    a.hb = hb_read(s);
     a.ncpi = static_cast<int>(L.cpi.size());
     a.nucpi = static_cast<int>(L.ucpi.size());
     a.cpi = c->lb_cpi.p;
@@ -421,7 +490,7 @@ void harvest_front(sgx_sampler* s, int restart, int iter, long long quota_left) 
     s->launches += 1;
   } else if (s->hwpc > 0) {
     sgx::HarvestSmemArgs a{};
-    a.hb = s->HB.p;
+    a.hb = hb_read(s);
     a.ncpi = static_cast<int>(L.cpi.size());
     a.nucpi = static_cast<int>(L.ucpi.size());
     a.cpi_row = c->fb_cpi_row.p;
@@ -843,6 +912,17 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
         int v = std::atoi(e);
         if (v == 1 || v == 2 || v == 4) s->vec = v;
       }
+      // SGX_ONCHIP=1: small circuits (>= 2 tiles of tape + adjoint slots per
+      // SM) run the fused on-chip soft pass on 32-sample tiles.  Opt-in:
+      // measured on C3a it is 2.3x SLOWER than the HBM-tape kernels (one
+      // sample per lane spends ~23k warp instructions per 32-sample tile on
+      // record control, at 8 warps per SM).
+      {
+        const char* e = std::getenv("SGX_ONCHIP");
+        s->onchip = e && e[0] == '1' && c->cone.oc_n4 > 0 &&
+                    sgx::onchip_warps(c->cone.n_rows, c->cone.oc_slots, c->cone.oc_n4) >= 2;
+        if (s->onchip) s->vec = 1;
+      }
       // Shared-memory harvest: the widest word block whose folded bit tape
       // fits ~100 KB (two CTAs per SM) while leaving >= 2 CTAs per SM of work;
       // one word (up to 200 KB) for deep circuits; else the global path.
@@ -904,9 +984,11 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       const size_t Bp = static_cast<size_t>(s->Bp);
       cudaStream_t st = s->st;
       s->V.alloc_async(L.cpi.size() * Bp, st);
-      s->HB.alloc_async(L.cpi.size() * s->W, st);
-      s->tape.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
-      s->adj.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
+      s->HB.alloc_async(2 * L.cpi.size() * s->W, st);
+      if (!s->onchip) {  // the on-chip pass keeps tape and adjoints in shared memory
+        s->tape.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
+        s->adj.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
+      }
       s->row_loss.alloc_async(Bp, st);
       s->partial.alloc_async(s->n_partial, st);
       if (!s->hwpc && !s->hlive) s->BT.alloc_async(static_cast<size_t>(L.n_bit_rows) * s->W, st);

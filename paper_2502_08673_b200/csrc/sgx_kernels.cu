@@ -1,5 +1,7 @@
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "sgx_kernels.cuh"
 #include "sgx_launch.hpp"
 
@@ -1091,6 +1093,178 @@ k_forward_tma(const int4* __restrict__ fblk, int blk0_n4, int blk_max, int n_lev
       __syncthreads();
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// On-chip soft pass (small circuits): embed + forward + loss + backward + GD
+// + harden for a 32-sample tile in ONE warp, with the tape [row][32] and the
+// adjoint slots [slot][32] in that warp's shared memory and the program
+// (copied once per persistent CTA) read as shared-memory broadcasts.  Each
+// lane owns one sample and touches only its own column, so no barrier or
+// fence is needed anywhere: program order of one thread orders every
+// dependency.  Loads are hoisted only within a level, where records are
+// independent.  Arithmetic and order are those of the HBM kernels (so the
+// same bits); the only HBM traffic left is V and the harvest's input words.
+// ---------------------------------------------------------------------------
+constexpr int kOcMaxWarps = 8;
+
+__device__ __forceinline__ void onchip_record(const int4 r, float g, float y, float& acc, float& acc2, const float* T,
+                                              float* A, int lane) {
+  const int f = r.x;
+  const float4 C = kRecC[f & 0xf];
+  const float ns = (f & kRNegOther) ? -1.0f : 1.0f, no = (f & kRNegOther) ? 1.0f : 0.0f;
+  if (!(f & kRSlow)) {
+    if (f & kRFirst) acc = 0.0f;
+    acc = __fadd_rn(acc, __fmul_rn(g, __fmaf_rn(C.y, __fmaf_rn(ns, y, no), C.x)));
+  } else {
+    if (f & (kRFirst | kRSubFirst)) {
+      float sd = 0.0f, sd2 = 0.0f;
+      if (f & (kRSeed | kRSubSeed)) {  // adj[out] += 2 (y - t) on a zero adjoint (autodiff.cpp:206)
+        const float yw = T[r.w * 32 + lane];
+        const float t = (f & kRTarget) ? 1.0f : 0.0f, t2 = (f & kRSubTarget) ? 1.0f : 0.0f;
+        if (f & kRSeed) sd = __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(yw, t)));
+        if (f & kRSubSeed) {
+          const float ys = (f & kRNegSelf) ? __fsub_rn(1.0f, yw) : yw;
+          sd2 = __fadd_rn(0.0f, __fmul_rn(2.0f, __fsub_rn(ys, t2)));
+        }
+      }
+      if (f & kRFirst) acc = sd;
+      if (f & kRSubFirst) acc2 = sd2;
+    }
+    if (r.y >= 0) {
+      const float t = __fmul_rn(g, __fmaf_rn(C.y, __fmaf_rn(ns, y, no), C.x));
+      if (f & kRInSub)
+        acc2 = __fadd_rn(acc2, t);
+      else
+        acc = __fadd_rn(acc, t);
+    }
+    if (f & kRSubLast) acc = (f & kRSubNot) ? __fsub_rn(acc, acc2) : __fadd_rn(acc, acc2);
+  }
+  if (f & kRLast) A[(f >> kOcSlotShift) * 32 + lane] = acc;
+}
+
+__global__ void __launch_bounds__(32 * kOcMaxWarps)
+k_soft_onchip(const OnchipArgs a) {
+  extern __shared__ int4 osm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < a.prog_n4; i += blockDim.x) osm[i] = __ldg(a.prog + i);
+  __syncthreads();
+  const int4* G = osm;                      // groups
+  const int4* R = osm + a.off_rec;          // records
+  const int4* LV = osm + a.off_lvl;         // per level / pass ranges
+  const int* COL = reinterpret_cast<const int*>(osm + a.off_col);
+  const int* OUT = reinterpret_cast<const int*>(osm + a.off_out);
+  float* T = reinterpret_cast<float*>(osm + a.prog_n4) + static_cast<size_t>(warp) * (a.n_rows + a.n_slots) * 32;
+  float* A = T + static_cast<size_t>(a.n_rows) * 32;
+  for (int tile = blockIdx.x * nw + warp; tile < a.n_tiles; tile += gridDim.x * nw) {
+    float* Vt = a.V + static_cast<size_t>(tile) * a.ncols * 32 + lane;
+    // forward (autodiff.cpp:64-152), NOT/BUF folded into operand reads
+    for (int l = 0; l < a.n_levels; ++l) {
+      const int4 L = LV[l];
+      for (int gi = L.x; gi < L.x + L.y; ++gi) {
+        const int4* rec = G + gi * kGroupRecs;
+        const int4 h = rec[0], o0 = rec[1], o1 = rec[2];
+        const int opd[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+        const int kind = h.x, n = h.y;
+        float* out = T + h.z * 32 + lane;
+        float xa[kGroup], xb[kGroup];
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k) {
+          xa[k] = xb[k] = 0.0f;
+          if (k < n) {
+            if (kind >= SGX_AND2) {
+              xa[k] = fold_read(T[(opd[2 * k] >> 1) * 32 + lane], opd[2 * k]);
+              xb[k] = fold_read(T[(opd[2 * k + 1] >> 1) * 32 + lane], opd[2 * k + 1]);
+            } else if (kind == SGX_NOT || kind == SGX_BUF) {
+              xa[k] = fold_read(T[(opd[2 * k] >> 1) * 32 + lane], opd[2 * k]);
+            } else if (kind == SGX_INPUT && opd[2 * k] >= 0) {
+              xa[k] = Vt[opd[2 * k] * 32];
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k) {
+          if (k >= n) break;
+          float r;
+          if (kind == SGX_INPUT)
+            r = opd[2 * k] < 0 ? 0.5f : sigmoid_ref(xa[k], a.exp_tab);
+          else if (kind == SGX_CONST0 || kind == SGX_CONST1)
+            r = kind == SGX_CONST1 ? 1.0f : 0.0f;
+          else
+            r = gate_value(kind, xa[k], xb[k]);
+          out[k * 32] = r;
+        }
+      }
+    }
+    // loss (autodiff.cpp:160-166): outputs in order
+    if (a.row_loss) {
+      float l = 0.0f;
+      for (int m = 0; m < a.n_out; ++m) {
+        const int e = OUT[m];
+        const float yv = fold_read(T[(e >> 1) * 32 + lane], e);
+        const float t = __ldg(a.out_tgt + m) ? 1.0f : 0.0f;
+        const float d = __fsub_rn(yv, t);
+        l = __fadd_rn(l, __fmul_rn(d, d));
+      }
+      a.row_loss[static_cast<size_t>(tile) * 32 + lane] = l;
+    }
+    // backward (autodiff.cpp:172-283), pull records in the reference's order
+    float acc = 0.0f, acc2 = 0.0f;
+    for (int li = 0; li < a.n_levels; ++li) {
+      const int4 L = LV[li];
+      for (int k0 = L.z; k0 < L.z + L.w; k0 += 4) {
+        int4 r[4];
+        float g[4], y[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          r[k] = k0 + k < L.z + L.w ? R[k0 + k] : make_int4(0, -1, -1, 0);
+          g[k] = r[k].y >= 0 ? A[r[k].y * 32 + lane] : 0.0f;
+          y[k] = r[k].z >= 0 ? T[r[k].z * 32 + lane] : 0.0f;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k0 + k < L.z + L.w) onchip_record(r[k], g[k], y[k], acc, acc2, T, A, lane);
+      }
+    }
+    // V columns: dV = g p (1 - p) (autodiff.cpp:212-221), V -= lr dV
+    // (gd_step, :285-290), harden (:292-297) into the harvest's words
+    for (int j = 0; j < a.ncols; ++j) {
+      const int sl = COL[j];
+      if (sl < 0) continue;  // warp-uniform
+      const float x = Vt[j * 32], gg = A[sl * 32 + lane];
+      const float p = sigmoid_ref(x, a.exp_tab);
+      const float dv = __fmul_rn(__fmul_rn(gg, p), __fsub_rn(1.0f, p));
+      const float nv = __fsub_rn(x, __fmul_rn(a.lr, dv));
+      Vt[j * 32] = nv;
+      const uint32_t b = __ballot_sync(kFull, nv >= 0.0f);
+      if (lane == 0) a.hb[static_cast<size_t>(tile) * a.ncols + j] = b;
+    }
+  }
+}
+
+int onchip_warps(int n_rows, int n_slots, int prog_n4) {
+  const size_t per_warp = static_cast<size_t>(n_rows + n_slots) * 32 * sizeof(float);
+  const size_t prog = static_cast<size_t>(prog_n4) * 16;
+  const size_t budget = 200 * 1024;
+  if (prog + 2 * per_warp > budget) return 0;  // at least two warps per SM
+  return static_cast<int>(std::min<size_t>(kOcMaxWarps, (budget - prog) / per_warp));
+}
+
+bool launch_soft_onchip(cudaStream_t st, const OnchipArgs& a) {
+  const int nw = onchip_warps(a.n_rows, a.n_slots, a.prog_n4);
+  if (nw == 0) return false;
+  const size_t smem = static_cast<size_t>(a.prog_n4) * 16 +
+                      static_cast<size_t>(nw) * (a.n_rows + a.n_slots) * 32 * sizeof(float);
+  static size_t opted = 0;
+  if (smem > opted) {
+    cudaFuncSetAttribute(k_soft_onchip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    opted = smem;
+  }
+  int ctas = (a.n_tiles + nw - 1) / nw;
+  if (ctas > 148) ctas = 148;  // persistent: one CTA per SM (the program is copied once)
+  k_soft_onchip<<<ctas, 32 * nw, smem, st>>>(a);
+  return true;
 }
 
 // Deterministic loss total: fixed per-block partial sums in double, then one

@@ -77,6 +77,28 @@ struct HarvestSmemArgs {
 // Fused shared-memory harvest (harden + eval + PO/CNF + keys + insert); the
 // folded bit tape of wpc words must fit in shared memory.
 void launch_harvest_smem(cudaStream_t st, int wpc, int n_rows, int W, const HarvestSmemArgs& a);
+// On-chip soft pass for small circuits (sgx_layout.hpp SoftProgram::oc_*):
+// one warp per 32-sample tile runs forward, loss, backward, the V update and
+// the hardening with its tape and adjoints in shared memory.  prog is one
+// int4 buffer: [groups (kGroupRecs each)][records][per level / pass: fwd
+// first, fwd count, rec first, rec count][column adjoint slots, 4 per int4]
+// [output encodings, 4 per int4].
+struct OnchipArgs {
+  const int4* prog;
+  int prog_n4, off_rec, off_lvl, off_col, off_out;
+  int n_levels, n_rows, n_slots, ncols, n_out;
+  float* V;             // [tile][col][32]
+  uint32_t* hb;         // [word][col]
+  float* row_loss;      // [B]
+  const uint8_t* out_tgt;
+  const uint64_t* exp_tab;
+  float lr;
+  int n_tiles;
+};
+// Returns false when the tile does not fit (the caller keeps the HBM kernels).
+bool launch_soft_onchip(cudaStream_t st, const OnchipArgs& a);
+int onchip_warps(int n_rows, int n_slots, int prog_n4);  // 0 = not eligible
+
 // Liveness-allocated harvest (sgx_layout.hpp Layout::lb_*): bit tape in
 // `slots` shared-memory rows per word, CNF-variable rows spilled to a global
 // tape [n_spill][W] for the key phase.

@@ -377,6 +377,68 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
       fprintf(stderr, "[sgx] staged blocks: backward %d passes, max %d int4 (%d B); forward max %d int4 (%d B)\n",
               nl, P.sblk_max, P.sblk_max * 16, P.fblk_max, P.fblk_max * 16);
   }
+  if (P.n_rows <= 1024) {  // on-chip program (SoftProgram::oc_*); larger tapes cannot fit a warp's share
+    for (int l = 0; l < P.n_levels; ++l) {
+      P.oc_fwd_lvl.push_back(static_cast<int32_t>(P.oc_fwd.size() / kGroupRecs));
+      for (int w = 0; w < kWarps; ++w) {
+        const int32_t first = P.fwd_lvl[2 * (l * kWarps + w)], cnt = P.fwd_lvl[2 * (l * kWarps + w) + 1];
+        P.oc_fwd.insert(P.oc_fwd.end(), P.fwd.begin() + static_cast<size_t>(first) * kGroupRecs,
+                        P.fwd.begin() + static_cast<size_t>(first + cnt) * kGroupRecs);
+      }
+      P.oc_fwd_lvl.push_back(static_cast<int32_t>(P.oc_fwd.size() / kGroupRecs) - P.oc_fwd_lvl.back());
+    }
+    const int nl = P.n_levels;
+    for (int li = 0; li < nl; ++li) {
+      P.oc_rec_lvl.push_back(static_cast<int32_t>(P.oc_rec.size()));
+      for (int w = 0; w < kWarps; ++w) {
+        const int32_t first = P.rec_lvl[2 * (li * kWarps + w)], cnt = P.rec_lvl[2 * (li * kWarps + w) + 1];
+        P.oc_rec.insert(P.oc_rec.end(), P.rec.begin() + first, P.rec.begin() + first + cnt);
+      }
+      P.oc_rec_lvl.push_back(static_cast<int32_t>(P.oc_rec.size()) - P.oc_rec_lvl.back());
+    }
+    // adjoint live ranges over the record stream: defined at the node's
+    // kRLast record, dead after its last reader (.y); column inputs live on
+    // to the epilogue
+    const int64_t nr = static_cast<int64_t>(P.oc_rec.size());
+    std::vector<int64_t> last(P.n_rows, -1);
+    for (int64_t k = 0; k < nr; ++k)
+      if (P.oc_rec[k].y >= 0) last[P.oc_rec[k].y] = k;
+    for (int32_t r : P.col_row)
+      if (r >= 0) last[r] = nr;
+    std::vector<int32_t> slot(P.n_rows, -1);
+    std::vector<std::vector<int32_t>> free_after(nr + 1);
+    std::priority_queue<int32_t, std::vector<int32_t>, std::greater<>> freeq;
+    int32_t nslots = 0;
+    for (int64_t k = 0; k < nr; ++k) {
+      I4& r = P.oc_rec[k];
+      if (r.y >= 0) r.y = slot[r.y];  // the consumer's adjoint (defined earlier)
+      if (r.x & kRLast) {
+        const int32_t own = r.w;
+        int32_t sl;
+        if (freeq.empty()) {
+          sl = nslots++;
+        } else {
+          sl = freeq.top();
+          freeq.pop();
+        }
+        slot[own] = sl;
+        r.x |= sl << kOcSlotShift;
+        if (last[own] < 0) {
+          freeq.push(sl);  // never read: reusable at once
+        } else if (last[own] < nr) {
+          free_after[last[own]].push_back(sl);
+        }
+      }
+      for (int32_t sl : free_after[k]) freeq.push(sl);
+    }
+    P.oc_adj_slots = std::max(nslots, 1);
+    if (getenv("SGX_TRACE"))
+      fprintf(stderr, "[sgx] on-chip program: %d tape rows, %d adjoint slots, %zu groups, %lld records\n", P.n_rows,
+              P.oc_adj_slots, P.oc_fwd.size() / kGroupRecs, static_cast<long long>(nr));
+    P.oc_col_slot.assign(P.col_row.size(), -1);
+    for (size_t j = 0; j < P.col_row.size(); ++j)
+      if (P.col_row[j] >= 0) P.oc_col_slot[j] = slot[P.col_row[j]];
+  }
   // Slack so a chunk of records may read past the last one.
   for (int k = 0; k < kU; ++k) P.rec.push_back({0, -1, -1, 0});
   return P;

@@ -73,6 +73,7 @@ constexpr int32_t kRInSub = 1 << 4, kRNegOther = 1 << 5, kRFirst = 1 << 6, kRSub
 // SUB-run records, records without an edge) -- the staged kernel's fast path
 // is taken only without it.
 constexpr int32_t kRSlow = 1 << 16;
+constexpr int kOcSlotShift = 17;  // oc_rec: adjoint store slot in the flag word
 constexpr int kCnfThreads = 256;               // threads of the shared-memory harvest CTA
 constexpr int32_t kCnfOpen = INT32_MIN;        // CNF record continues (see fb_cnf4)
 constexpr int32_t kLbBig = INT32_MIN;          // lb_chk: long clause, literals in lb_big_lits
@@ -116,6 +117,20 @@ struct SoftProgram {
   std::vector<I4> fblk;
   std::vector<int32_t> fblk_lvl;     // per level: start, n_int4
   int32_t fblk_max = 0;
+  // On-chip program (k_soft_onchip, small circuits): one warp owns 32
+  // samples and runs the whole program alone, so levels need no barrier and
+  // the streams are linear: oc_fwd = the forward groups in level order,
+  // oc_rec = the backward records (levels high to low) with the adjoint
+  // rows renamed to live-range slots: .y = slot of the consumer's adjoint,
+  // flags bits 17+ = slot the node's adjoint is stored to (kRLast); .z / .w
+  // stay tape rows.  oc_col_slot = adjoint slot of each V column's input
+  // (live until the V epilogue).
+  std::vector<I4> oc_fwd;
+  std::vector<I4> oc_rec;
+  std::vector<int32_t> oc_fwd_lvl;   // per level: first group, count (records hoist loads only within a level)
+  std::vector<int32_t> oc_rec_lvl;   // per pass (high to low): first record, count
+  std::vector<int32_t> oc_col_slot;
+  int32_t oc_adj_slots = 0;
   int32_t sblk_max = 0;              // largest block, int4s
   std::vector<int32_t> out_enc;      // each output as row << 1 | negate (-1: not in set)
   std::vector<int32_t> col_row;      // tape row of each V column's INPUT node

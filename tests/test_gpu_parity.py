@@ -304,3 +304,16 @@ def test_c5_suite_matches_reference(gpu):
         np.testing.assert_allclose(st.loss_trace, rec["loss_trace"], rtol=LOSS_RTOL, atol=0)
         assert verify_keys(i.cnf, res.solutions.keys).all()
     assert not bad, bad
+
+
+@pytest.mark.parametrize("rec", [r for r in golden_runs()
+                                 if r["instance"] in ("mux_chain14", "c3a_or50", "c1b_random", "c3b_or100")],
+                         ids=lambda r: f"{r['instance']}-{r['config']}")
+def test_onchip_soft_pass_matches_reference(gpu, rec, monkeypatch):
+    """The opt-in fused on-chip soft pass (SGX_ONCHIP=1: tape and adjoint
+    slots in shared memory, one warp per 32-sample tile) reproduces the
+    reference's runs exactly, like the default HBM-tape kernels."""
+    monkeypatch.setenv("SGX_ONCHIP", "1")
+    i = inst(rec["instance"])
+    res = run_instance(i, SamplerConfig(**cfg_kwargs(rec["config"])))
+    check_run(res, rec, i)
