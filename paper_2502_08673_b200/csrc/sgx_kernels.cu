@@ -268,6 +268,22 @@ __constant__ float4 kRecS[8] = {{1.0f, 0.0f, 1.0f, 1.0f},  {-1.0f, 1.0f, 1.0f, 1
                                 {-1.0f, 1.0f, 0.0f, 1.0f}, {1.0f, 0.0f, 1.0f, 0.0f},  {-1.0f, 1.0f, 1.0f, 0.0f},
                                 {1.0f, 0.0f, 0.0f, 0.0f},  {-1.0f, 1.0f, 0.0f, 0.0f}};
 __constant__ float kRecE[4] = {0.0f, 1.0f, 0.0f, -1.0f};
+// Pull factor and operand sign in one entry, indexed by consumer kind |
+// kRNegOther >> 1: {c0, c1, ns, no} with vo = ns*y + no (y or 1 - y) and
+// factor c0 + c1*vo (autodiff.cpp:225-277).
+#define SGX_PULL4(c0, c1) {c0, c1, 1.0f, 0.0f}
+#define SGX_PULL4N(c0, c1) {c0, c1, -1.0f, 1.0f}
+__constant__ float4 kPull4[32] = {
+    SGX_PULL4(0.f, 0.f),  SGX_PULL4(0.f, 0.f),  SGX_PULL4(0.f, 0.f),   SGX_PULL4(1.f, 0.f),
+    SGX_PULL4(-1.f, 0.f), SGX_PULL4(0.f, 1.f),  SGX_PULL4(1.f, -1.f),  SGX_PULL4(1.f, -2.f),
+    SGX_PULL4(-1.f, 2.f), SGX_PULL4(0.f, 0.f),  SGX_PULL4(0.f, 0.f),   SGX_PULL4(0.f, 0.f),
+    SGX_PULL4(0.f, 0.f),  SGX_PULL4(0.f, 0.f),  SGX_PULL4(0.f, 0.f),   SGX_PULL4(0.f, 0.f),
+    SGX_PULL4N(0.f, 0.f), SGX_PULL4N(0.f, 0.f), SGX_PULL4N(0.f, 0.f),  SGX_PULL4N(1.f, 0.f),
+    SGX_PULL4N(-1.f, 0.f), SGX_PULL4N(0.f, 1.f), SGX_PULL4N(1.f, -1.f), SGX_PULL4N(1.f, -2.f),
+    SGX_PULL4N(-1.f, 2.f), SGX_PULL4N(0.f, 0.f), SGX_PULL4N(0.f, 0.f),  SGX_PULL4N(0.f, 0.f),
+    SGX_PULL4N(0.f, 0.f), SGX_PULL4N(0.f, 0.f), SGX_PULL4N(0.f, 0.f),  SGX_PULL4N(0.f, 0.f)};
+#undef SGX_PULL4
+#undef SGX_PULL4N
 
 template <int V>
 __device__ __forceinline__ void vload_nc(const float* p, float (&o)[V]) {
@@ -674,13 +690,10 @@ __device__ __forceinline__ void backward_record(const int4 r, const float4 gs, c
           // Pull factor c0 + c1*vo of the consumer kind, vo = y or 1 - y
           // (other operand read through a folded NOT): both fmas round
           // exactly as the reference's (1 - v), (1 - 2v), ... (c1*vo exact).
-          const float4 C = kRecC[f & 0xf];  // {c0, c1} of the consumer kind (the a-side half)
-          const float ns = (f & kRNegOther) ? -1.0f : 1.0f, no = (f & kRNegOther) ? 1.0f : 0.0f;
-          if (!(f & kRSlow)) {  // plain edge into this node's adjoint (most records)
-            if (f & kRFirst) {
-#pragma unroll
-              for (int v = 0; v < V; ++v) acc[v] = 0.0f;
-            }
+          const float4 C = kPull4[(f & 0xf) | ((f >> 1) & 0x10)];  // {c0, c1, ns, no}
+          const float ns = C.z, no = C.w;
+          if (!(f & kRSlow)) {  // plain edge into this node's adjoint (most records; the
+                                // accumulator is already +0 at a node's first record)
 #pragma unroll
             for (int v = 0; v < V; ++v) {
               const float fa = __fmaf_rn(C.y, __fmaf_rn(ns, y[v], no), C.x);
@@ -729,6 +742,13 @@ __device__ __forceinline__ void backward_record(const int4 r, const float4 gs, c
               st_hint(A + static_cast<size_t>(r.w) * TILE, acc, pol_last);
             else
               vstore<V>(A + static_cast<size_t>(r.w) * TILE, acc);
+            // the next node starts from +0: every emitted node run ends with
+            // kRLast, and a seed 0 + x is never -0, so this equals the
+            // reference's fresh zero adjoint (autodiff.cpp:191).  Chunk
+            // padding records are kRSlow without an edge, so they never
+            // touch the accumulator (a stale slot times zero could be NaN).
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[v] = 0.0f;
           }
 }
 
@@ -815,7 +835,7 @@ k_backward_async(const int4* __restrict__ rec, const int2* __restrict__ lvl, int
         const float4* base = my + (ch % kBS) * kBU * 2 * 32;
 #pragma unroll
         for (int k = 0; k < kBU; ++k) {
-          const int4 r = ch * kBU + k < L.y ? __ldg(R + ch * kBU + k) : make_int4(0, -1, -1, 0);
+          const int4 r = ch * kBU + k < L.y ? __ldg(R + ch * kBU + k) : make_int4(kRSlow, -1, -1, 0);  // inert pad
           backward_record(r, base[(2 * k) * 32], base[(2 * k + 1) * 32], acc, acc2, T, A, pol_last);
         }
       }
@@ -965,7 +985,7 @@ k_backward_tma(const int4* __restrict__ sblk, int blk0_n4, int blk_max, int n_le
         const float4* base = my + (ch % BS) * kBU * 2 * 32;
 #pragma unroll
         for (int k = 0; k < kBU; ++k) {
-          const int4 r = ch * kBU + k < W.y ? R[ch * kBU + k] : make_int4(0, -1, -1, 0);
+          const int4 r = ch * kBU + k < W.y ? R[ch * kBU + k] : make_int4(kRSlow, -1, -1, 0);  // inert pad
           backward_record(r, base[(2 * k) * 32], base[(2 * k + 1) * 32], acc, acc2, T, A, pol_last);
         }
       }
