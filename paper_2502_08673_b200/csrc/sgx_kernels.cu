@@ -669,6 +669,9 @@ k_forward_async(const int4* __restrict__ grp, const int2* __restrict__ lvl, int 
 #ifndef SGX_HINT_Y
 #define SGX_HINT_Y 1
 #endif
+#ifndef SGX_FWD_HINT
+#define SGX_FWD_HINT 1  // forward: last reads of a row evict_first
+#endif
 #ifndef SGX_HINT_ADJ
 #define SGX_HINT_ADJ 1
 #endif
@@ -1020,6 +1023,13 @@ k_forward_tma(const int4* __restrict__ fblk, int blk0_n4, int blk_max, int n_lev
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float4* my = fstage + warp * kStages * kSlots * 32 + lane;  // slot (d, j): my[(d*kSlots + j) * 32]
   int4* const blk0 = reinterpret_cast<int4*>(fstage + kWarps * kStages * kSlots * 32);
+  const uint64_t pol = policy_evict_first();
+  auto load_row = [](float4* dst, const float* src, int last, uint64_t p) {
+    if (SGX_FWD_HINT && last)
+      cp_async16_hint(dst, src, p);
+    else
+      cp_async16(dst, src);
+  };
   if (threadIdx.x == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
@@ -1049,13 +1059,16 @@ k_forward_tma(const int4* __restrict__ fblk, int blk0_n4, int blk_max, int n_lev
 #pragma unroll
         for (int k = 0; k < kGroup; ++k) {
           if (k >= n) break;
+          // a row's last forward read (header mask) and the V columns (read
+          // once) leave L2 first
           if (kind >= SGX_AND2) {
-            cp_async16(base + (2 * k) * 32, T + static_cast<size_t>(opd[2 * k] >> 1) * TILE);
-            cp_async16(base + (2 * k + 1) * 32, T + static_cast<size_t>(opd[2 * k + 1] >> 1) * TILE);
+            load_row(base + (2 * k) * 32, T + static_cast<size_t>(opd[2 * k] >> 1) * TILE, (h.w >> (2 * k)) & 1, pol);
+            load_row(base + (2 * k + 1) * 32, T + static_cast<size_t>(opd[2 * k + 1] >> 1) * TILE,
+                     (h.w >> (2 * k + 1)) & 1, pol);
           } else if (kind == SGX_NOT || kind == SGX_BUF) {
-            cp_async16(base + (2 * k) * 32, T + static_cast<size_t>(opd[2 * k] >> 1) * TILE);
+            load_row(base + (2 * k) * 32, T + static_cast<size_t>(opd[2 * k] >> 1) * TILE, (h.w >> (2 * k)) & 1, pol);
           } else if (kind == SGX_INPUT && opd[2 * k] >= 0) {
-            cp_async16(base + (2 * k) * 32, S + static_cast<size_t>(opd[2 * k]) * TILE);
+            load_row(base + (2 * k) * 32, S + static_cast<size_t>(opd[2 * k]) * TILE, 1, pol);
           }
         }
         cp_async_commit();

@@ -148,6 +148,15 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
   // sorting by kind), each warp's list cut into kind-homogeneous groups of at
   // most kGroup ops.  Rows are assigned in emission order, so a group's
   // outputs are consecutive rows.
+  // Last forward level reading each (materialized) node: operand loads at that
+  // level are the row's last forward use and go to L2 as evict_first.
+  std::vector<int32_t> last_fwd(n, -1);
+  for (int i = 0; i < n; ++i) {
+    if (!in_set[i] || virt[i]) continue;
+    const int oc = operand_count(L.kind[i]);
+    if (oc >= 1) last_fwd[base_of(L.a[i])] = std::max(last_fwd[base_of(L.a[i])], lev[i]);
+    if (oc == 2) last_fwd[base_of(L.b[i])] = std::max(last_fwd[base_of(L.b[i])], lev[i]);
+  }
   int32_t next_row = 0;
   auto enc = [&](int x) {  // operand encoding: row << 1 | negate
     int bse = base_of(x);
@@ -167,6 +176,7 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
         size_t e = t;
         while (e < lst.size() && L.kind[lst[e]] == k && e - t < static_cast<size_t>(kGroup)) ++e;
         const int32_t cnt = static_cast<int32_t>(e - t);
+        // header .w: bit 2k+j = operand j of op k is its row's last forward read
         I4 head{k, cnt, next_row, 0};
         std::vector<int32_t> operands(2 * kGroup, 0);
         for (size_t u = t; u < e; ++u) {
@@ -177,6 +187,8 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
           if (k == SGX_INPUT) operands[2 * (u - t)] = col_of_node[i];
           if (oc >= 1) operands[2 * (u - t)] = enc(L.a[i]);
           if (oc == 2) operands[2 * (u - t) + 1] = enc(L.b[i]);
+          if (oc >= 1 && last_fwd[base_of(L.a[i])] == lev[i]) head.w |= 1 << (2 * (u - t));
+          if (oc == 2 && last_fwd[base_of(L.b[i])] == lev[i]) head.w |= 1 << (2 * (u - t) + 1);
         }
         P.fwd.push_back(head);
         for (int q = 0; q < kGroup / 2; ++q)
