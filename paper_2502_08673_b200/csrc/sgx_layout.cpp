@@ -1,6 +1,8 @@
 #include "sgx_layout.hpp"
 
 #include <algorithm>
+#include <exception>
+#include <thread>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -702,8 +704,8 @@ void build_live_bits(Layout& L) {
     L.lb_key_enc[v - 1] = (spill[base(x)] << 1) | (negv(x) ? 1 : 0);
   }
   if (getenv("SGX_TRACE"))
-    fprintf(stderr, "[sgx] live harvest: %d phases, %d slots (of %d rows), %d spill rows, %zu ops, %zu checks\n",
-            P, nslots, L.fb_rows, nsp, L.lb_ops.size(), L.lb_chk.size());
+    fprintf(stderr, "[sgx] live harvest: %d phases, %d slots, %d spill rows, %zu ops, %zu checks\n", P, nslots, nsp,
+            L.lb_ops.size(), L.lb_chk.size());
 }
 
 Layout build_layout(const sgx_circuit_desc& d) {
@@ -814,8 +816,40 @@ Layout build_layout(const sgx_circuit_desc& d) {
     if (oc >= 1) cone[L.a[i]] = 1;
     if (oc == 2) cone[L.b[i]] = 1;
   }
-  L.cone = build_soft(L, cone);
-  lap("soft");
+  // The soft program, the live harvest program and the bit / folded bit
+  // programs below read the validated inputs only and write disjoint fields:
+  // the first two are compiled on their own threads.
+  L.key_words = (L.num_vars + 63) / 64;
+  std::exception_ptr err_soft, err_live;
+  std::thread t_soft([&] {
+    try {
+      L.cone = build_soft(L, cone);
+    } catch (...) {
+      err_soft = std::current_exception();
+    }
+  });
+  std::thread t_live([&] {
+    try {
+      build_live_bits(L);
+    } catch (...) {
+      err_live = std::current_exception();
+    }
+  });
+  std::exception_ptr err_fold;
+  std::thread t_fold([&] {
+    try {
+      build_folded_bits(L);
+    } catch (...) {
+      err_fold = std::current_exception();
+    }
+  });
+  struct Join {  // joined on every path out (exceptions included)
+    std::thread &a, &b, &c;
+    ~Join() {
+      for (std::thread* t : {&a, &b, &c})
+        if (t->joinable()) t->join();
+    }
+  } join{t_soft, t_live, t_fold};
   (void)all;  // the all-node program for the parity taps is built on demand
 
   // Bit program: every node, level-sorted; INPUT rows come from the harden
@@ -856,14 +890,16 @@ Layout build_layout(const sgx_circuit_desc& d) {
                              (lit < 0 ? 1 : 0));
     }
   }
-  L.key_words = (L.num_vars + 63) / 64;
   L.key_bit_row.assign(static_cast<size_t>(L.key_words) * 64, -1);
   for (int v = 1; v <= L.num_vars; ++v) L.key_bit_row[v - 1] = L.bit_row_of_node[L.node_of_var[v]];
   lap("bits");
-  build_folded_bits(L);
-  lap("folded");
-  build_live_bits(L);
-  lap("live");
+  t_soft.join();
+  t_live.join();
+  t_fold.join();
+  lap("threads join");
+  if (err_soft) std::rethrow_exception(err_soft);
+  if (err_live) std::rethrow_exception(err_live);
+  if (err_fold) std::rethrow_exception(err_fold);
   return L;
 }
 
