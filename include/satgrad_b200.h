@@ -189,6 +189,11 @@ int sgx_set_host_stream(sgx_sampler* s, int32_t on);
  * map_bytes).  keys = NULL when there are no solutions. */
 int sgx_solutions_take(sgx_sampler* s, uint64_t** keys, int64_t* rows, int64_t* map_bytes);
 int sgx_host_free(uint64_t* keys, int64_t map_bytes);
+/* format_solutions (include/satgrad/sampler.hpp:86, sampler.cpp:78-85) of
+ * solutions [first, first + count), rendered on the device: "v1 -v2 ... vn 0\n"
+ * per solution.  *len = text bytes; with out = NULL only the length is
+ * computed, else out must hold cap >= *len bytes (SGX_E_INVALID otherwise). */
+int sgx_format_solutions(sgx_sampler* s, int64_t first, int64_t count, char* out, int64_t cap, int64_t* len);
 /* The sampler's current logits V as [batch][n_cpi] row-major (the reference's
  * Mat<float> v of run_impl, sampler.cpp:157-173): trajectory parity tap. */
 int sgx_read_logits(sgx_sampler* s, float* v);

@@ -101,6 +101,8 @@ class RefLib:
             L.ref_run_note.restype = C.c_char_p
             L.ref_run_note.argtypes = [C.c_void_p]
             L.ref_run_keys.argtypes = [C.c_void_p, _u64p]
+            L.ref_format_keys.restype = C.c_longlong
+            L.ref_format_keys.argtypes = [_u64p, C.c_longlong, C.c_int, C.c_void_p, C.c_longlong]
             RefLib._lib = L
         self.L = RefLib._lib
 
@@ -109,6 +111,17 @@ class RefLib:
 
     def hash5(self, *xs) -> int:
         return int(self.L.ref_hash5(*[int(x) for x in xs]))
+
+    def format_keys(self, keys: np.ndarray, num_vars: int) -> bytes:
+        """satgrad::format_solutions (sampler.cpp:78-85) of keys inserted in order."""
+        keys = np.ascontiguousarray(keys, np.uint64).reshape(-1, (num_vars + 63) // 64 or 1)
+        n = len(keys) if num_vars else 0
+        ln = self.L.ref_format_keys(keys.ravel() if keys.size else np.zeros(1, np.uint64), n, num_vars, None, 0)
+        if ln < 0:
+            raise ValueError(self.error())
+        buf = C.create_string_buffer(max(1, ln))
+        self.L.ref_format_keys(keys.ravel() if keys.size else np.zeros(1, np.uint64), n, num_vars, buf, ln)
+        return buf.raw[:ln]
 
     def hash6(self, *xs) -> int:
         return int(self.L.ref_hash6(*[int(x) for x in xs]))

@@ -450,4 +450,22 @@ void ref_run_keys(void* hv, uint64_t* keys) {
   }
 }
 
+// format_solutions (sampler.cpp:78-85) of n keys [n][words] (dedupe_key
+// layout) inserted in order into a SolutionSet; returns the text length and
+// copies min(len, cap) bytes into out (out may be null to size it).
+long long ref_format_keys(const uint64_t* keys, long long n, int num_vars, char* out, long long cap) {
+  GUARD_BEGIN
+  SolutionSet s(num_vars);
+  const int words = (num_vars + 63) / 64;
+  Assignment a(num_vars + 1, 0);
+  for (long long i = 0; i < n; ++i) {
+    for (int v = 1; v <= num_vars; ++v) a[v] = (keys[i * words + (v - 1) / 64] >> ((v - 1) % 64)) & 1;
+    s.insert(a);
+  }
+  const std::string t = format_solutions(s);
+  if (out) std::memcpy(out, t.data(), std::min<long long>(cap, static_cast<long long>(t.size())));
+  return static_cast<long long>(t.size());
+  GUARD_END(-1)
+}
+
 }  // extern "C"

@@ -1216,6 +1216,55 @@ int sgx_host_free(uint64_t* keys, int64_t map_bytes) {
   return guard([&] { sgx::host_free(keys, static_cast<size_t>(map_bytes)); });
 }
 
+int sgx_format_solutions(sgx_sampler* s, int64_t first, int64_t count, char* out, int64_t cap, int64_t* len) {
+  return guard([&] {
+    need(s, "sampler");
+    need(len, "len");
+    if (first < 0 || count < 0 || first + count > s->n_solutions)
+      throw std::invalid_argument("solution range out of bounds");
+    *len = 0;
+    if (count == 0) return;
+    CK(cudaSetDevice(s->c->ctx->device));
+    const int kw = s->c->L.key_words, nv = s->c->L.num_vars;
+    cudaStream_t st = s->sh;  // the store belongs to the harvest stream
+    DBuf<long long> lo;
+    lo.alloc_async(static_cast<size_t>(count) + 1, st);
+    size_t scratch_bytes = 0;
+    sgx::launch_fmt_lengths(st, s->store.p, first, count, kw, nv, lo.p, nullptr, &scratch_bytes);
+    DBuf<unsigned char> scratch;
+    scratch.alloc_async(std::max<size_t>(scratch_bytes, 1), st);
+    sgx::launch_fmt_lengths(st, s->store.p, first, count, kw, nv, lo.p, scratch.p, &scratch_bytes);
+    std::vector<long long> off(static_cast<size_t>(count) + 1);
+    CK(cudaMemcpyAsync(off.data(), lo.p, off.size() * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *len = off[count];
+    if (!out) {
+      scratch.reset_async(st);
+      lo.reset_async(st);
+      return;
+    }
+    if (cap < off[count]) throw std::invalid_argument("format_solutions: output buffer too small");
+    // Render in chunks of at most 256 MB of text (a single longer line gets its own chunk).
+    const long long chunk = 256ll << 20;
+    long long longest = 0;
+    for (long long i = 0; i < count; ++i) longest = std::max(longest, off[i + 1] - off[i]);
+    DBuf<char> buf;
+    buf.alloc_async(static_cast<size_t>(std::max(std::min(chunk, off[count]), longest)), st);
+    for (long long i = 0; i < count;) {
+      long long j = i + 1;
+      while (j < count && off[j + 1] - off[i] <= static_cast<long long>(buf.n)) ++j;
+      sgx::launch_fmt_write(st, s->store.p, first + i, j - i, kw, nv, lo.p + i, off[i], buf.p);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(out + off[i], buf.p, static_cast<size_t>(off[j] - off[i]), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      i = j;
+    }
+    buf.reset_async(st);
+    scratch.reset_async(st);
+    lo.reset_async(st);
+  });
+}
+
 int sgx_phase_times(const sgx_sampler* s, double* ms8) {
   return guard([&] {
     need(s, "sampler");

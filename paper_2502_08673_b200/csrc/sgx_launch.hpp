@@ -77,6 +77,15 @@ struct HarvestSmemArgs {
 // Fused shared-memory harvest (harden + eval + PO/CNF + keys + insert); the
 // folded bit tape of wpc words must fit in shared memory.
 void launch_harvest_smem(cudaStream_t st, int wpc, int n_rows, int W, const HarvestSmemArgs& a);
+// Device-side format_solutions (sgx_format.cu).  len_off: n + 1 int64,
+// lengths then in-place exclusive offsets; call once with scratch = nullptr
+// to size the scan's scratch.
+long long fmt_base_len(int num_vars);
+void launch_fmt_lengths(cudaStream_t st, const uint64_t* store, long long first, long long n, int words,
+                        int num_vars, long long* len_off, void* scratch, size_t* scratch_bytes);
+void launch_fmt_write(cudaStream_t st, const uint64_t* store, long long first, long long n, int words,
+                      int num_vars, const long long* off, long long out_base, char* out);
+
 // On-chip soft pass for small circuits (sgx_layout.hpp SoftProgram::oc_*):
 // one warp per 32-sample tile runs forward, loss, backward, the V update and
 // the hardening with its tape and adjoints in shared memory.  prog is one

@@ -247,6 +247,19 @@ class Sampler:
             return np.zeros((0, words), np.uint64)
         return _owned_keys(p.value, rows.value, words, nbytes.value)
 
+    def format_solutions(self, first: int = 0, count: int | None = None) -> bytes:
+        """format_solutions (sampler.cpp:78-85) rendered on the device: one
+        "v1 -v2 ... vn 0" line per solution, insertion order."""
+        n = self.solution_count()
+        if count is None:
+            count = n - first
+        ln = C.c_int64()
+        _lib.check(self.L.sgx_format_solutions(self.h, first, count, None, 0, C.byref(ln)))
+        buf = np.empty(max(1, ln.value), np.uint8)
+        _lib.check(self.L.sgx_format_solutions(self.h, first, count, buf.ctypes.data_as(C.c_void_p),
+                                               ln.value, C.byref(ln)))
+        return buf[: ln.value].tobytes()
+
     # building blocks ----------------------------------------------------------
     def logits(self) -> np.ndarray:
         """Current V, [batch][n_cpi] (trajectory parity tap)."""

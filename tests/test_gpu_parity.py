@@ -317,3 +317,27 @@ def test_onchip_soft_pass_matches_reference(gpu, rec, monkeypatch):
     i = inst(rec["instance"])
     res = run_instance(i, SamplerConfig(**cfg_kwargs(rec["config"])))
     check_run(res, rec, i)
+
+
+@pytest.mark.skipif(not ref_available(), reason="reference library not built (oracle/_ref)")
+@pytest.mark.parametrize("name,batch,iters", [("mux_chain14", 64, 5), ("c3a_or50", 4096, 5),
+                                              ("c2_iscas", 256, 2), ("free_inputs", 8, 3)])
+def test_device_format_matches_reference(gpu, name, batch, iters):
+    """Device-side format_solutions == the reference's format_solutions
+    (sampler.cpp:78-85) byte for byte, whole store and a sub-range."""
+    from oracle.oracle import RefLib
+    i = inst(name)
+    dc = DeviceCircuit.from_instance(i)
+    s = Sampler(dc, SamplerConfig(batch=batch, iterations=iters, seed=2))
+    try:
+        s.run()
+        keys = s.fetch()
+        assert len(keys) > 0
+        nv = i.cnf.num_vars
+        text = s.format_solutions()
+        assert text == RefLib().format_keys(keys, nv)
+        a, b = len(keys) // 3, len(keys) // 3 + max(1, len(keys) // 4)
+        assert s.format_solutions(a, b - a) == RefLib().format_keys(keys[a:b], nv)
+    finally:
+        s.close()
+        dc.close()
