@@ -305,6 +305,8 @@ def run_b200_arm(args, world, rank, local, dist):
     # (H2D), the run, every solution key fetched to host memory (D2H).
     e2e_cfg = cfg_for(args.steps)
     e2e_cfg.solution_capacity = 0  # library defaults, as a user calling run() gets them
+    if world == 1:  # warm-up of the public path (host result mapping, pool)
+        del run_instance(inst, e2e_cfg, device=dev).solutions.keys
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)

@@ -56,14 +56,24 @@ template <typename T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  bool pooled = false;  // from the stream-ordered pool (freed without a device sync)
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { reset(); }
+  // Owners free quiescent buffers only (samplers sync their streams first; a
+  // circuit outlives its samplers), so a pooled buffer goes back to the pool
+  // in the legacy stream's order instead of through cudaFree's device sync.
   void reset() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (pooled)
+        cudaFreeAsync(p, 0);
+      else
+        cudaFree(p);
+    }
     p = nullptr;
     n = 0;
+    pooled = false;
   }
   void alloc(size_t count) {
     reset();
@@ -88,19 +98,24 @@ struct DBuf {
       throw NoMem("cudaMallocAsync(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e));
     }
     n = count;
+    pooled = true;
   }
   void reset_async(cudaStream_t st) {
     if (p) cudaFreeAsync(p, st);
     p = nullptr;
     n = 0;
+    pooled = false;
   }
+  // Stream-ordered upload (pool memory; the caller syncs `st` before use
+  // elsewhere).
   void upload(const std::vector<T>& v, cudaStream_t st) {
-    alloc(v.size());
+    alloc_async(v.size(), st);
     if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
   }
   void swap(DBuf& o) {
     std::swap(p, o.p);
     std::swap(n, o.n);
+    std::swap(pooled, o.pooled);
   }
 };
 
@@ -1198,9 +1213,10 @@ int sgx_solutions_take(sgx_sampler* s, uint64_t** keys, int64_t* rows, int64_t* 
       *map_bytes = static_cast<int64_t>(b);
       return;
     }
-    const size_t bytes = static_cast<size_t>(s->n_solutions) * kw * sizeof(uint64_t);
-    void* p = sgx::host_map(bytes);
-    const cudaError_t e = cudaMemcpyAsync(p, s->store.p, bytes, cudaMemcpyDeviceToHost, s->sh);
+    const size_t need_bytes = static_cast<size_t>(s->n_solutions) * kw * sizeof(uint64_t);
+    size_t bytes = 0;
+    void* p = sgx::host_map(need_bytes, &bytes);
+    const cudaError_t e = cudaMemcpyAsync(p, s->store.p, need_bytes, cudaMemcpyDeviceToHost, s->sh);
     const cudaError_t e2 = e == cudaSuccess ? cudaStreamSynchronize(s->sh) : e;
     if (e2 != cudaSuccess) {
       sgx::host_free(p, bytes);

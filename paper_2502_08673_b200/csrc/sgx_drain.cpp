@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <stdexcept>
 #include <vector>
 
@@ -19,14 +20,14 @@ void check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// First touch of [p, p + n) on up to 8 threads, one write per 4 KB page (a
-// huge page is zeroed once, by the first write into it).
-void touch(char* p, size_t n) {
+// memcpy on up to 8 threads (the destination's first touch -- page faults,
+// huge-page zeroing -- happens inside, in parallel).
+void par_copy(char* dst, const char* src, size_t n) {
   if (n == 0) return;
-  const int T = static_cast<int>(std::min<size_t>(8, std::max<size_t>(1, n / (8u << 20))));
-  auto work = [p, n, T](int t) {
+  const int T = static_cast<int>(std::min<size_t>(8, std::max<size_t>(1, n / (4u << 20))));
+  auto work = [dst, src, n, T](int t) {
     const size_t lo = n / T * t, hi = t + 1 == T ? n : n / T * (t + 1);
-    for (size_t o = lo; o < hi; o += 4096) p[o] = 0;
+    std::memcpy(dst + lo, src + lo, hi - lo);
   };
   if (T == 1) {
     work(0);
@@ -38,18 +39,88 @@ void touch(char* p, size_t n) {
   for (auto& x : th) x.join();
 }
 
+// Process-wide pinned staging per device: two 32 MB buffers, allocated once
+// (cudaHostAlloc is ~0.5 ms/MB; a per-run allocation would cost more than
+// the copies).  The D2H copies are then real DMA that return at once,
+// instead of pageable copies that hold the driver while they run.
+constexpr size_t kStage = size_t{32} << 20;
+struct Staging {
+  char* buf[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  std::mutex mu;  // one drain at a time per device
+};
+Staging& staging(int device) {
+  static std::mutex mu;
+  static std::vector<std::unique_ptr<Staging>> all;
+  std::lock_guard<std::mutex> lk(mu);
+  if (static_cast<int>(all.size()) <= device) all.resize(device + 1);
+  if (!all[device]) {
+    auto st = std::make_unique<Staging>();
+    for (int k = 0; k < 2; ++k) {
+      check(cudaHostAlloc(reinterpret_cast<void**>(&st->buf[k]), kStage, cudaHostAllocPortable), "drain staging");
+      check(cudaEventCreateWithFlags(&st->done[k], cudaEventDisableTiming), "drain staging event");
+    }
+    all[device] = std::move(st);
+  }
+  return *all[device];
+}
+
 }  // namespace
 
-void* host_map(size_t bytes) {
+// Released result mappings are parked (up to two, 16 GB in all) and handed
+// to the next run: their pages are already faulted in, so a run does not pay
+// the first touch -- or the kernel's huge-page compaction -- again.
+namespace {
+std::mutex g_cache_mu;
+std::vector<std::pair<void*, size_t>> g_cache;
+constexpr size_t kCacheEntries = 2, kCacheBytes = size_t{16} << 30;
+}  // namespace
+
+void* host_map(size_t bytes, size_t* actual) {
   const size_t b = round_huge(std::max<size_t>(bytes, 1));
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    size_t best = g_cache.size();
+    for (size_t i = 0; i < g_cache.size(); ++i)  // the largest parked mapping
+      if (best == g_cache.size() || g_cache[i].second > g_cache[best].second) best = i;
+    if (best < g_cache.size()) {
+      auto [p, n] = g_cache[best];
+      g_cache.erase(g_cache.begin() + static_cast<long>(best));
+      if (n < b) {
+        void* q = mremap(p, n, b, MREMAP_MAYMOVE);
+        if (q == MAP_FAILED) {
+          munmap(p, n);
+        } else {
+          madvise(q, b, MADV_HUGEPAGE);
+          *actual = b;
+          return q;
+        }
+      } else {
+        *actual = n;
+        return p;
+      }
+    }
+  }
   void* p = mmap(nullptr, b, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
   if (p == MAP_FAILED) throw std::runtime_error("host result mapping failed");
   madvise(p, b, MADV_HUGEPAGE);
+  *actual = b;
   return p;
 }
 
 void host_free(void* p, size_t bytes) {
-  if (p) munmap(p, round_huge(std::max<size_t>(bytes, 1)));
+  if (!p) return;
+  const size_t b = round_huge(std::max<size_t>(bytes, 1));
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    size_t held = 0;
+    for (auto& e : g_cache) held += e.second;
+    if (g_cache.size() < kCacheEntries && held + b <= kCacheBytes) {
+      g_cache.emplace_back(p, b);
+      return;
+    }
+  }
+  munmap(p, b);
 }
 
 HostDrain::HostDrain(int device, int key_words)
@@ -95,7 +166,7 @@ void HostDrain::reset() {
   wait_idle();
   host_free(buf_, cap_bytes_);
   buf_ = nullptr;
-  cap_bytes_ = touched_bytes_ = 0;
+  cap_bytes_ = 0;
   landed_ = queued_ = 0;
 }
 
@@ -105,7 +176,7 @@ uint64_t* HostDrain::take(int64_t* rows, size_t* bytes) {
   *rows = landed_;
   *bytes = cap_bytes_;
   buf_ = nullptr;
-  cap_bytes_ = touched_bytes_ = 0;
+  cap_bytes_ = 0;
   landed_ = queued_ = 0;
   return p;
 }
@@ -115,7 +186,10 @@ void HostDrain::ensure(int64_t rows) {
   if (need > cap_bytes_) {
     const size_t ncap = round_huge(std::max<size_t>({need + need / 2, 2 * cap_bytes_, size_t{64} << 20}));
     if (!buf_) {
-      buf_ = static_cast<char*>(host_map(ncap));
+      size_t got = 0;
+      buf_ = static_cast<char*>(host_map(ncap, &got));
+      cap_bytes_ = got;
+      return;
     } else {
       void* p = mremap(buf_, cap_bytes_, ncap, MREMAP_MAYMOVE);
       if (p == MAP_FAILED) throw std::runtime_error("host result mapping could not grow");
@@ -123,10 +197,6 @@ void HostDrain::ensure(int64_t rows) {
       madvise(buf_, ncap, MADV_HUGEPAGE);
     }
     cap_bytes_ = ncap;
-  }
-  if (need > touched_bytes_) {
-    touch(buf_ + touched_bytes_, need - touched_bytes_);
-    touched_bytes_ = need;
   }
 }
 
@@ -147,11 +217,26 @@ void HostDrain::loop() {
       if (err_.empty()) {
         ensure(j.first + j.count);
         check(cudaStreamWaitEvent(cst_, j.ev, 0), "drain wait");
-        check(cudaMemcpyAsync(buf_ + static_cast<size_t>(j.first) * row_bytes_,
-                              j.src + static_cast<size_t>(j.first) * (row_bytes_ / sizeof(uint64_t)),
-                              static_cast<size_t>(j.count) * row_bytes_, cudaMemcpyDeviceToHost, cst_),
-              "drain copy");
-        check(cudaStreamSynchronize(cst_), "drain sync");
+        // D2H through the pinned double buffer: chunk c lands in buf[c % 2]
+        // while chunk c - 1 is copied out of the other one.
+        Staging& sg = staging(device_);
+        std::lock_guard<std::mutex> lk(sg.mu);
+        const char* src = reinterpret_cast<const char*>(j.src + static_cast<size_t>(j.first) * (row_bytes_ / sizeof(uint64_t)));
+        char* dst = buf_ + static_cast<size_t>(j.first) * row_bytes_;
+        const size_t total = static_cast<size_t>(j.count) * row_bytes_;
+        const size_t nchunk = (total + kStage - 1) / kStage;
+        for (size_t c = 0; c <= nchunk; ++c) {
+          if (c < nchunk) {
+            const size_t n = std::min(kStage, total - c * kStage);
+            check(cudaMemcpyAsync(sg.buf[c & 1], src + c * kStage, n, cudaMemcpyDeviceToHost, cst_), "drain copy");
+            check(cudaEventRecord(sg.done[c & 1], cst_), "drain copy event");
+          }
+          if (c > 0) {
+            const size_t p = c - 1;
+            check(cudaEventSynchronize(sg.done[p & 1]), "drain copy wait");
+            par_copy(dst + p * kStage, sg.buf[p & 1], std::min(kStage, total - p * kStage));
+          }
+        }
         landed_ = j.first + j.count;
       }
     } catch (const std::exception& x) {

@@ -5,10 +5,12 @@
 // no copy at the end of the run.
 //
 // Host memory is one anonymous mapping with transparent huge pages, grown by
-// mremap and first-touched by several threads ahead of each copy (measured on
-// the B200 host: a 400 MB first touch costs ~200 ms on one thread with 4 KB
-// pages, ~16 ms on 8 threads with huge pages; pinning 400 MB with
-// cudaHostAlloc costs ~220 ms, more than the copy it would speed up).
+// mremap.  Keys arrive by DMA into a process-wide pinned double buffer (2 x
+// 32 MB, allocated once) and are copied out on up to 8 threads, which also
+// spreads the first touch (measured on the B200 host: a 400 MB first touch
+// costs ~200 ms on one thread with 4 KB pages, ~16 ms on 8 threads with huge
+// pages; pinning 400 MB with cudaHostAlloc costs ~220 ms, more than the copy
+// it would speed up; pageable copies hold the driver while they run).
 // Ownership of the mapping moves to the caller with take(); host_free()
 // unmaps it.
 #pragma once
@@ -51,7 +53,7 @@ class HostDrain {
     cudaEvent_t ev;
   };
   void loop();
-  void ensure(int64_t rows);  // capacity + parallel first touch up to `rows`
+  void ensure(int64_t rows);  // capacity up to `rows` (first touch happens in the copy)
 
   int device_;
   size_t row_bytes_;
@@ -64,13 +66,14 @@ class HostDrain {
   std::string err_;
   // worker-owned while busy
   char* buf_ = nullptr;
-  size_t cap_bytes_ = 0, touched_bytes_ = 0;
+  size_t cap_bytes_ = 0;
   int64_t landed_ = 0;
   int64_t queued_ = 0;  // main thread
 };
 
-// Allocate / release host result memory of the drain's kind.
-void* host_map(size_t bytes);
+// Allocate / release host result memory of the drain's kind (a released
+// mapping is parked for reuse; *actual = the mapping's size).
+void* host_map(size_t bytes, size_t* actual);
 void host_free(void* p, size_t bytes);
 
 }  // namespace sgx
