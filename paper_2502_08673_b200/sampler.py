@@ -305,16 +305,29 @@ def _owned_keys(addr: int, rows: int, words: int, map_bytes: int) -> np.ndarray:
 def run(cnf: CnfFormula, circuit: Circuit, paths: PathClassification, cfg: SamplerConfig,
         unsat: bool = False, unsat_note: str = "", device: int = 0) -> RunResult:
     """satgrad::run (sampler.hpp:79-81): upload, sample, fetch every solution."""
+    import os
+    import time
+    trace = os.environ.get("SGX_E2E_TRACE")
+    t = [time.perf_counter()]
     dc = DeviceCircuit(cnf, circuit, paths, unsat, device)
     dc.unsat_note = unsat_note
+    t.append(time.perf_counter())
     s = Sampler(dc, cfg)
     try:
         s.set_host_stream(True)  # the result streams to the host while sampling runs
+        t.append(time.perf_counter())
         stats = s.run()
+        t.append(time.perf_counter())
         keys = s.take()
+        t.append(time.perf_counter())
     finally:
         s.close()
         dc.close()
+    t.append(time.perf_counter())
+    if trace:
+        d = [1000 * (b - a) for a, b in zip(t, t[1:])]
+        print("[run] circuit %.1f sampler %.1f run %.1f (device %.1f) take %.1f close %.1f ms" %
+              (d[0], d[1], d[2], stats.device_ms, d[3], d[4]), flush=True)
     return RunResult(SolutionSet(cnf.num_vars, keys), stats)
 
 
