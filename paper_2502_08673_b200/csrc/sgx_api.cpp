@@ -903,8 +903,15 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
     auto s = std::make_unique<sgx_sampler>();
     s->c = c;
     s->cfg = *cfg;
-    CK(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&s->sh, cudaStreamNonBlocking));
+    // SGX_PRIO=1: the soft passes (st) outrank the harvest (sh) at the block
+    // scheduler.  Measured: C2 even, C4 +4.7 %, C3a -1.8 %, and the in-run
+    // backward launch 1.43 -> 1.47 ms; equal priorities by default.
+    int prio_lo = 0, prio_hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    const char* pe = std::getenv("SGX_PRIO");
+    const bool prio = pe && pe[0] == '1';
+    CK(cudaStreamCreateWithPriority(&s->st, cudaStreamNonBlocking, prio ? prio_hi : prio_lo));
+    CK(cudaStreamCreateWithPriority(&s->sh, cudaStreamNonBlocking, prio_lo));
     for (auto& e : s->ev) CK(cudaEventCreate(&e));
     for (auto& row : s->sev)
       for (auto& e : row) CK(cudaEventCreate(&e));
