@@ -140,8 +140,13 @@ def dist_setup(args):
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl" if args.impl != "reference" else "gloo")
+        # BENCH_DIST_BACKEND=gloo: a test set-up running several ranks on fewer
+        # GPUs (payloads staged through the host); the bench itself uses NCCL.
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if args.impl != "reference":
+            local = local % max(1, torch.cuda.device_count())
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend if args.impl != "reference" else "gloo")
         pg = dist
     return world, rank, local, pg
 
@@ -244,6 +249,8 @@ def run_b200_arm(args, world, rank, local, dist):
     batch = args.batch or batch
     dev = local
     torch.cuda.set_device(dev)
+    # max-over-ranks reductions: on the device over NCCL, on the host over gloo
+    coll_dev = "cpu" if (dist and dist.get_backend() == "gloo") else f"cuda:{dev}"
     inst = load_instance(name)
     dc = DeviceCircuit.from_instance(inst, device=dev)
     info = dc.info()
@@ -292,11 +299,13 @@ def run_b200_arm(args, world, rank, local, dist):
             sst = run_sharded(shard, ex, cfg_for(args.steps), rank, world, shard.stride)
             torch.cuda.synchronize(dev)
             wall = time.perf_counter() - t0
-        t_dev = torch.tensor([wall], dtype=torch.float64, device=f"cuda:{dev}")
+        t_dev = torch.tensor([wall], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
         device_s = float(t_dev.item())
         global_unique = sst.unique_count
-        restarts_done, attempts, launches, ph = sst.restarts + 1, sst.attempts, None, None
+        # this rank's kernels and device phase times (rank 0 reports)
+        restarts_done, attempts = sst.restarts + 1, sst.attempts
+        launches, ph = sampler.launch_count(), sampler.phase_times()
     if dist:
         dist.barrier()
     sampler.close()
@@ -326,7 +335,7 @@ def run_b200_arm(args, world, rank, local, dist):
         dc2.close()
     e2e_wall = time.perf_counter() - t0
     if dist:
-        t_e = torch.tensor([e2e_wall], dtype=torch.float64, device=f"cuda:{dev}")
+        t_e = torch.tensor([e2e_wall], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
         e2e_wall = float(t_e.item())
     h2d = sum(x.nbytes for x in (inst.kind, inst.a, inst.b, inst.var, inst.out_var, inst.out_tgt,

@@ -167,6 +167,8 @@ int sgx_fingerprint_stride(const sgx_sampler* s);
  * sgx_step_loss, which waits for that step and returns its loss total. */
 int sgx_step_async(sgx_sampler* s, int32_t* slot);
 int sgx_step_loss(sgx_sampler* s, int32_t slot, double* loss_total);
+/* Kernels this sampler launched (since its last sgx_run, or since creation). */
+int64_t sgx_launch_count(const sgx_sampler* s);
 int sgx_harvest_local(sgx_sampler* s, int32_t restart, int32_t iter, int64_t* n_new, uint64_t** fps);
 int sgx_harvest_merge(sgx_sampler* s, const uint64_t* all_fps, const int64_t* counts, int32_t nranks,
                       int32_t rank, int64_t stride, int64_t* n_won);

@@ -24,7 +24,7 @@ EXPORTS = [
     "sgx_forward", "sgx_backward", "sgx_embed", "sgx_expf", "sgx_fingerprint_stride",
     "sgx_harvest_local", "sgx_harvest_merge", "sgx_harvest_commit", "sgx_read_logits",
     "sgx_set_host_stream", "sgx_solutions_take", "sgx_host_free", "sgx_step_async", "sgx_step_loss",
-    "sgx_format_solutions",
+    "sgx_format_solutions", "sgx_launch_count",
 ]
 
 
@@ -120,6 +120,7 @@ def load() -> C.CDLL:
         "sgx_step_async": (C.c_int, [vp, C.POINTER(i32)]),
         "sgx_step_loss": (C.c_int, [vp, i32, f64p]),
         "sgx_format_solutions": (C.c_int, [vp, i64, i64, C.c_void_p, i64, i64p]),
+        "sgx_launch_count": (i64, [vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -1120,8 +1120,14 @@ int sgx_step_loss(sgx_sampler* s, int32_t slot, double* loss_total) {
     CK(cudaSetDevice(s->c->ctx->device));
     CK(cudaEventSynchronize(s->sev[slot][3]));
     if (loss_total) *loss_total = s->hloss[slot];
+    cudaEvent_t* ev = s->sev[slot];  // device time of the step (sgx_phase_times)
+    s->phase_ms[1] += elapsed(ev[0], ev[3]);
+    s->phase_ms[3] += elapsed(ev[0], ev[1]);
+    s->phase_ms[4] += elapsed(ev[2], ev[3]);
   });
 }
+
+int64_t sgx_launch_count(const sgx_sampler* s) { return s ? s->launches : -1; }
 
 int sgx_harvest(sgx_sampler* s, int32_t restart, int32_t iter, int64_t* attempts, int64_t* added) {
   return guard([&] {

@@ -107,16 +107,25 @@ class TorchExchange:
         self.world = dist.get_world_size(group)
         self.device = torch.device(device) if device is not None else torch.device("cpu")
         self.torch = torch
+        # gloo moves host tensors only: device payloads are staged through the
+        # host (a test set-up: several ranks on one GPU, where NCCL refuses)
+        self.host_staged = dist.get_backend(group) == "gloo"
+        self.coll_device = torch.device("cpu") if self.host_staged else self.device
 
     def all_gather_int(self, x: int) -> list[int]:
-        t = self.torch.tensor([int(x)], dtype=self.torch.int64, device=self.device)
-        out = self.torch.zeros(self.world, dtype=self.torch.int64, device=self.device)
+        t = self.torch.tensor([int(x)], dtype=self.torch.int64, device=self.coll_device)
+        out = self.torch.zeros(self.world, dtype=self.torch.int64, device=self.coll_device)
         self.dist.all_gather_into_tensor(out, t, group=self.group)
         return [int(v) for v in out.cpu()]
 
     def all_gather_fps(self, fps, stride: int):
-        out = self.torch.empty(self.world * stride, dtype=self.torch.int64, device=fps.device)
-        self.dist.all_gather_into_tensor(out, fps[:stride].contiguous(), group=self.group)
+        src = fps[:stride].contiguous()
+        if self.host_staged:
+            src = src.cpu()
+        out = self.torch.empty(self.world * stride, dtype=self.torch.int64, device=src.device)
+        self.dist.all_gather_into_tensor(out, src, group=self.group)
+        if self.host_staged and fps.is_cuda:
+            out = out.to(fps.device)
         if out.is_cuda:
             self.torch.cuda.current_stream(out.device).synchronize()
         return out

@@ -219,6 +219,16 @@ class Sampler:
                         phase_ms=dict(zip(names, (float(x) for x in ph))),
                         device_ms=st.device_ms, launches=st.launches)
 
+    def launch_count(self) -> int:
+        """Kernels launched since the last run() (or creation)."""
+        return int(self.L.sgx_launch_count(self.h))
+
+    def phase_times(self) -> dict:
+        ph = np.zeros(8, np.float64)
+        _lib.check(self.L.sgx_phase_times(self.h, _lib.ptr(ph, C.c_double)))
+        names = ["init", "step", "harvest", "forward", "backward", "eval", "keys", "commit"]
+        return dict(zip(names, (float(x) for x in ph)))
+
     def solution_count(self) -> int:
         return int(self.L.sgx_solution_count(self.h))
 
