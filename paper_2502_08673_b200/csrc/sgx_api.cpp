@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -120,6 +121,31 @@ struct DBuf {
 };
 
 int round_up(long long x, int m) { return static_cast<int>((x + m - 1) / m * m); }
+
+// Small pinned host slots (a sampler's harvest counters and loss copies) from
+// one process-wide pinned slab: cudaMallocHost / cudaFreeHost per sampler cost
+// milliseconds (and the free synchronises), more than a quota run itself.
+constexpr size_t kPinSlot = 64;
+std::mutex g_pin_mu;
+std::vector<void*> g_pin_free;
+void* pin_slot() {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  if (g_pin_free.empty()) {
+    constexpr size_t kSlab = 64 * 1024;
+    char* slab = nullptr;
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&slab), kSlab, cudaHostAllocPortable));
+    for (size_t o = 0; o < kSlab; o += kPinSlot) g_pin_free.push_back(slab + o);
+  }
+  void* p = g_pin_free.back();
+  g_pin_free.pop_back();
+  std::memset(p, 0, kPinSlot);
+  return p;
+}
+void pin_release(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.push_back(p);
+}
 
 // Parity taps run the sampler's kernels with 128-sample tiles (4 per lane).
 constexpr int kTapVec = 4, kTapTile = 32 * kTapVec;
@@ -918,8 +944,9 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
     for (auto* e : {&s->ev_soft, &s->ev_front, &s->ev_join}) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     // Nothing recorded yet: a wait on a never-recorded event is a no-op.
     s->dloss.alloc(2);
-    CK(cudaMallocHost(&s->hloss, 2 * sizeof(double)));
-    CK(cudaMallocHost(&s->hpin, sizeof(sgx::HarvestOut)));
+    static_assert(sizeof(sgx::HarvestOut) <= kPinSlot, "pinned slot too small");
+    s->hloss = static_cast<double*>(pin_slot());
+    s->hpin = static_cast<sgx::HarvestOut*>(pin_slot());
     std::memset(s->hpin, 0, sizeof(sgx::HarvestOut));
     s->hout.alloc(1);
     if (c->layout_ok && !c->L.unsat) {
@@ -1066,8 +1093,8 @@ int sgx_sampler_free(sgx_sampler* s) {
         if (e) cudaEventDestroy(e);
     for (auto e : {s->ev_soft, s->ev_front, s->ev_join})
       if (e) cudaEventDestroy(e);
-    if (s->hpin) cudaFreeHost(s->hpin);
-    if (s->hloss) cudaFreeHost(s->hloss);
+    pin_release(s->hpin);  // (the streams were synchronised above)
+    pin_release(s->hloss);
     cudaStream_t sh = s->sh;
     delete s;
     if (st) cudaStreamDestroy(st);
