@@ -943,12 +943,13 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       for (auto& e : row) CK(cudaEventCreate(&e));
     for (auto* e : {&s->ev_soft, &s->ev_front, &s->ev_join}) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     // Nothing recorded yet: a wait on a never-recorded event is a no-op.
-    s->dloss.alloc(2);
+    s->dloss.alloc_async(2, s->st);  // pool memory: freed without cudaFree's device sync
     static_assert(sizeof(sgx::HarvestOut) <= kPinSlot, "pinned slot too small");
     s->hloss = static_cast<double*>(pin_slot());
     s->hpin = static_cast<sgx::HarvestOut*>(pin_slot());
     std::memset(s->hpin, 0, sizeof(sgx::HarvestOut));
-    s->hout.alloc(1);
+    s->hout.alloc_async(1, s->st);
+    CK(cudaStreamSynchronize(s->st));
     if (c->layout_ok && !c->L.unsat) {
       const auto& L = c->L;
       s->Bp = round_up(cfg->batch, 1024);
@@ -1084,8 +1085,10 @@ int sgx_sampler_free(sgx_sampler* s) {
       s->store.reset_async(st);
       s->tkeys.reset_async(st);
       s->tmeta.reset_async(st);
-      cudaStreamSynchronize(st);
     }
+    const double t_reset = ms();
+    if (st) cudaStreamSynchronize(st);
+    const double t_sync2 = ms();
     for (auto& e : s->ev)
       if (e) cudaEventDestroy(e);
     for (auto& row : s->sev)
@@ -1100,8 +1103,8 @@ int sgx_sampler_free(sgx_sampler* s) {
     if (st) cudaStreamDestroy(st);
     if (sh) cudaStreamDestroy(sh);
     if (std::getenv("SGX_TRACE"))
-      std::fprintf(stderr, "[sgx] sampler free: harvest sync %.2f, drain %.2f, total %.2f ms\n", t_sync, t_drain,
-                   ms());
+      std::fprintf(stderr, "[sgx] sampler free: harvest sync %.2f, drain %.2f, frees %.2f, stream sync %.2f, total %.2f ms\n",
+                   t_sync, t_drain, t_reset, t_sync2, ms());
   });
 }
 
@@ -1354,7 +1357,7 @@ int sgx_harvest_local(sgx_sampler* s, int32_t restart, int32_t iter, int64_t* n_
     need_ready(s);
     if (s->dist_stage != 0) throw StateError("sgx_harvest_local: previous harvest not committed");
     CK(cudaSetDevice(s->c->ctx->device));
-    if (!s->fps_local.p) s->fps_local.alloc(static_cast<size_t>(s->Bp) + 1);
+    if (!s->fps_local.p) s->fps_local.alloc_async(static_cast<size_t>(s->Bp) + 1, s->sh);
     harvest_front(s, restart, iter, -1);
     sgx::launch_compact_new(s->sh, s->newmask.p, s->block_count.p, s->slot_of_row.p, s->tkeys.p, s->Bp,
                             s->fps_local.p);
@@ -1393,7 +1396,7 @@ int sgx_harvest_merge(sgx_sampler* s, const uint64_t* all_fps, const int64_t* co
     // Room for every remote fingerprint at load factor <= 1/2.
     s->table_count += remote;
     ensure_table(s);
-    if (!s->n_of.p || static_cast<int>(s->n_of.n) < nranks) s->n_of.alloc(std::max(nranks, 64));
+    if (!s->n_of.p || static_cast<int>(s->n_of.n) < nranks) s->n_of.alloc_async(std::max(nranks, 64), s->sh);
     CK(cudaMemcpyAsync(s->n_of.p, cnt.data(), nranks * sizeof(long long), cudaMemcpyHostToDevice, s->sh));
     sgx::launch_merge_remote(s->sh, reinterpret_cast<const unsigned long long*>(all_fps), s->n_of.p,
                              nranks > 1 ? nranks : 0, rank, stride, s->tkeys.p, s->tmeta.p, s->tcap - 1,
