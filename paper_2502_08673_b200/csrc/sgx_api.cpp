@@ -443,7 +443,7 @@ void ensure_table(sgx_sampler* s) {
   if (want <= s->tcap) return;
   // Geometric growth with a first size covering several restarts.
   // quota runs stay small; a declared solution capacity presizes the table
-  uint64_t first = s->cfg.max_solutions > 0 ? 0 : 16ull * s->Bp;
+  uint64_t first = s->cfg.max_solutions > 0 ? 0 : 32ull * s->Bp;
   if (s->cfg.solution_capacity > 0) first = std::max<uint64_t>(first, 2ull * s->cfg.solution_capacity);
   uint64_t ncap = next_pow2(std::max<uint64_t>(std::max<uint64_t>(want * 2, first), 1u << 16));
   DBuf<unsigned long long> nk, nm;
@@ -1048,9 +1048,12 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       s->slot_of_row.alloc_async(Bp, st);
       s->block_count.alloc_async(Bp / sgx::kThreads, st);
       s->K.alloc_async(static_cast<size_t>(L.key_words) * Bp, st);
-      // Room for about a restart's worth of solutions (6 harvests of unique
-      // rows) before the first growth; a quota caps it.
-      long long want_rows = 6 * static_cast<long long>(Bp);
+      // Room for a few restarts' worth of solutions (16 harvests of unique
+      // rows, at most 4 GB of keys) before the first growth -- a growth waits
+      // for the host drain and copies the store; a quota caps it.
+      long long want_rows = 16 * static_cast<long long>(Bp);
+      const long long cap_4g = (4ll << 30) / (static_cast<long long>(L.key_words) * 8);
+      want_rows = std::max<long long>(std::min(want_rows, cap_4g), 2 * static_cast<long long>(Bp));
       if (cfg->max_solutions > 0) want_rows = std::min<long long>(want_rows, cfg->max_solutions + Bp);
       s->store_cap = cfg->solution_capacity > 0 ? cfg->solution_capacity : want_rows;
       s->store.alloc_async(static_cast<size_t>(s->store_cap) * L.key_words, st);
