@@ -216,6 +216,25 @@ int sgx_embed(sgx_ctx* ctx, const float* v, int64_t n, float* p);
  * expf restatement used by embed/backward). */
 int sgx_expf(sgx_ctx* ctx, const float* x, int64_t n, float* out);
 
+/* ---- Circuit extraction (host) -------------------------
+ * extract + build (src/extract.cpp:43-172, src/boolexpr.cpp, src/circuit.cpp:
+ * 60-122; include/satgrad/extract.hpp:53, circuit.hpp:42): the CNF (CSR
+ * clause_ptr[n_clauses + 1] over DIMACS literals) to the reference's
+ * ExtractionResult and gate-level Circuit, node for node.  Caps are
+ * ExtractorConfig (extract.hpp:14-17: complement_cap 16, minimize_cap 12). */
+typedef struct sgx_extraction sgx_extraction;
+int sgx_extract(int32_t num_vars, const int32_t* clause_ptr, const int32_t* clause_lit, int64_t n_clauses,
+                int32_t complement_cap, int32_t minimize_cap, sgx_extraction** out);
+/* out[7] = {n_nodes, |pi|, |po|, |iv|, |aux|, |be|, unsat} */
+int sgx_extraction_sizes(const sgx_extraction* x, int64_t* out);
+/* Node arrays [n_nodes] (GateKind codes, operand ids or -1, var or 0), pi,
+ * po (var, target), iv, aux in the reference's orders; any pointer may be NULL. */
+int sgx_extraction_export(const sgx_extraction* x, int32_t* kind, int32_t* a, int32_t* b, int32_t* var,
+                          int32_t* inputs, int32_t* out_var, uint8_t* out_tgt, int32_t* iv, int32_t* aux);
+/* ExtractionResult::unsat_note ("" when satisfiable so far). */
+const char* sgx_extraction_note(const sgx_extraction* x);
+void sgx_extraction_free(sgx_extraction* x);
+
 #ifdef __cplusplus
 }
 #endif

@@ -103,8 +103,17 @@ class RefLib:
             L.ref_run_keys.argtypes = [C.c_void_p, _u64p]
             L.ref_format_keys.restype = C.c_longlong
             L.ref_format_keys.argtypes = [_u64p, C.c_longlong, C.c_int, C.c_void_p, C.c_longlong]
+            L.ref_extract_seconds.argtypes = [C.c_char_p, C.c_int, _f64p]
+            L.ref_extraction_lists.argtypes = [C.c_void_p, _i64p, _i32p, _i32p]
             RefLib._lib = L
         self.L = RefLib._lib
+
+    def extract_seconds(self, dimacs: str, repeats: int = 1) -> tuple[float, float]:
+        """Reference extract / build wall time on this host (one thread)."""
+        out = np.zeros(2, np.float64)
+        if self.L.ref_extract_seconds(dimacs.encode(), repeats, out) != 0:
+            raise ValueError(self.error())
+        return float(out[0]), float(out[1])
 
     def error(self) -> str:
         return self.L.ref_last_error().decode()
@@ -226,6 +235,15 @@ class RefInstance:
         if getattr(self, "h", None):
             self.lib.L.ref_free(self.h)
             self.h = None
+
+    def extraction_lists(self):
+        """ExtractionResult sizes {pi, po, iv, aux, be} and the iv / aux lists."""
+        sz = np.zeros(5, np.int64)
+        n = self.num_vars + self.n_clauses + 1  # bounds |iv| (<= vars) and |aux| (<= clauses)
+        iv = np.zeros(n, np.int32)
+        aux = np.zeros(n, np.int32)
+        self.lib.L.ref_extraction_lists(self.h, sz, iv, aux)
+        return [int(x) for x in sz], iv[: sz[2]], aux[: sz[3]]
 
     def dimacs(self) -> str:
         n = C.c_int64()

@@ -468,4 +468,37 @@ long long ref_format_keys(const uint64_t* keys, long long n, int num_vars, char*
   GUARD_END(-1)
 }
 
+// Extraction timing and lists: parse once, then time
+// satgrad::extract and satgrad::build separately; out_s = {extract, build}.
+int ref_extract_seconds(const char* text, int repeats, double* out_s) {
+  GUARD_BEGIN
+  CnfFormula cnf = parse_dimacs(text);
+  double te = 0, tb = 0;
+  for (int r = 0; r < std::max(1, repeats); ++r) {
+    auto t0 = std::chrono::steady_clock::now();
+    ExtractionResult res = extract(cnf);
+    auto t1 = std::chrono::steady_clock::now();
+    Circuit c = build(res);
+    auto t2 = std::chrono::steady_clock::now();
+    te += std::chrono::duration<double>(t1 - t0).count();
+    tb += std::chrono::duration<double>(t2 - t1).count();
+  }
+  out_s[0] = te / std::max(1, repeats);
+  out_s[1] = tb / std::max(1, repeats);
+  return 0;
+  GUARD_END(-1)
+}
+
+// ExtractionResult list sizes {pi, po, iv, aux, be} and the iv / aux lists.
+void ref_extraction_lists(void* hv, int64_t* sizes, int32_t* iv, int32_t* aux) {
+  const ExtractionResult& r = static_cast<RefInst*>(hv)->res;
+  sizes[0] = static_cast<int64_t>(r.pi.size());
+  sizes[1] = static_cast<int64_t>(r.po.size());
+  sizes[2] = static_cast<int64_t>(r.iv.size());
+  sizes[3] = static_cast<int64_t>(r.aux.size());
+  sizes[4] = static_cast<int64_t>(r.be.size());
+  if (iv) std::copy(r.iv.begin(), r.iv.end(), iv);
+  if (aux) std::copy(r.aux.begin(), r.aux.end(), aux);
+}
+
 }  // extern "C"

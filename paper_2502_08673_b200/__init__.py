@@ -8,6 +8,7 @@ sampler.hpp, autodiff.hpp); the sampling loop itself runs in
 from .cnf import CnfFormula, ParseError, eval_cnf, parse_dimacs, verify_keys, write_dimacs
 from .circuit import (Circuit, Instance, PathClassification, SchemaError, classify_paths,
                       export_json, import_json, load_instance)
+from .extract import ExtractionResult, extract_circuit, instance_from_cnf
 from .sampler import (DeviceCircuit, RestartPolicy, RunResult, RunStats, Sampler, SamplerConfig,
                       SolutionSet, layout_stats, run, run_instance)
 
@@ -16,4 +17,5 @@ __all__ = [
     "Circuit", "Instance", "PathClassification", "SchemaError", "classify_paths", "export_json",
     "import_json", "load_instance", "DeviceCircuit", "RestartPolicy", "RunResult", "RunStats",
     "Sampler", "SamplerConfig", "SolutionSet", "layout_stats", "run", "run_instance",
+    "ExtractionResult", "extract_circuit", "instance_from_cnf",
 ]

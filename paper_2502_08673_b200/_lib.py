@@ -24,7 +24,8 @@ EXPORTS = [
     "sgx_forward", "sgx_backward", "sgx_embed", "sgx_expf", "sgx_fingerprint_stride",
     "sgx_harvest_local", "sgx_harvest_merge", "sgx_harvest_commit", "sgx_read_logits",
     "sgx_set_host_stream", "sgx_solutions_take", "sgx_host_free", "sgx_step_async", "sgx_step_loss",
-    "sgx_format_solutions", "sgx_launch_count",
+    "sgx_format_solutions", "sgx_launch_count", "sgx_extract", "sgx_extraction_sizes",
+    "sgx_extraction_export", "sgx_extraction_note", "sgx_extraction_free",
 ]
 
 
@@ -121,6 +122,12 @@ def load() -> C.CDLL:
         "sgx_step_loss": (C.c_int, [vp, i32, f64p]),
         "sgx_format_solutions": (C.c_int, [vp, i64, i64, C.c_void_p, i64, i64p]),
         "sgx_launch_count": (i64, [vp]),
+        "sgx_extract": (C.c_int, [i32, C.POINTER(i32), C.POINTER(i32), i64, i32, i32, pvp]),
+        "sgx_extraction_sizes": (C.c_int, [vp, i64p]),
+        "sgx_extraction_export": (C.c_int, [vp] + [C.POINTER(i32)] * 6 + [C.POINTER(C.c_uint8)]
+                                  + [C.POINTER(i32)] * 2),
+        "sgx_extraction_note": (C.c_char_p, [vp]),
+        "sgx_extraction_free": (None, [vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -16,6 +16,7 @@
 
 #include "../../include/satgrad_b200.h"
 #include "sgx_drain.hpp"
+#include "sgx_extract.hpp"
 #include "sgx_kernels.cuh"
 #include "sgx_launch.hpp"
 #include "sgx_layout.hpp"
@@ -1569,5 +1570,71 @@ static int device_unary(sgx_ctx* ctx, const float* x, int64_t n, float* out, int
 int sgx_embed(sgx_ctx* ctx, const float* v, int64_t n, float* p) { return device_unary(ctx, v, n, p, 1); }
 
 int sgx_expf(sgx_ctx* ctx, const float* x, int64_t n, float* out) { return device_unary(ctx, x, n, out, 0); }
+
+struct sgx_extraction {
+  sgx::ext::Result r;
+};
+
+int sgx_extract(int32_t num_vars, const int32_t* clause_ptr, const int32_t* clause_lit, int64_t n_clauses,
+                int32_t complement_cap, int32_t minimize_cap, sgx_extraction** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = nullptr;
+    if (num_vars < 0 || n_clauses < 0) throw std::invalid_argument("negative CNF size");
+    if (n_clauses > 0) {
+      need(clause_ptr, "clause_ptr");
+      need(clause_lit, "clause_lit");
+      if (clause_ptr[0] != 0) throw std::invalid_argument("clause_ptr[0] must be 0");
+      for (int64_t c = 0; c < n_clauses; ++c)
+        if (clause_ptr[c + 1] < clause_ptr[c]) throw std::invalid_argument("clause_ptr not monotone");
+    }
+    if (complement_cap < 0 || minimize_cap < 0 || minimize_cap > 16)
+      throw std::invalid_argument("caps must be >= 0 (minimize_cap <= 16, the truth-table limit)");
+    auto h = std::make_unique<sgx_extraction>();
+    sgx::ext::extract_build(num_vars, clause_ptr, clause_lit, n_clauses, complement_cap, minimize_cap, h->r);
+    *out = h.release();
+  });
+}
+
+int sgx_extraction_sizes(const sgx_extraction* x, int64_t* out) {
+  return guard([&] {
+    need(x, "extraction");
+    need(out, "out");
+    const auto& r = x->r;
+    out[0] = static_cast<int64_t>(r.kind.size());
+    out[1] = static_cast<int64_t>(r.pi.size());
+    out[2] = static_cast<int64_t>(r.po.size());
+    out[3] = static_cast<int64_t>(r.iv.size());
+    out[4] = static_cast<int64_t>(r.aux.size());
+    out[5] = r.n_defs;
+    out[6] = r.unsat ? 1 : 0;
+  });
+}
+
+int sgx_extraction_export(const sgx_extraction* x, int32_t* kind, int32_t* a, int32_t* b, int32_t* var,
+                          int32_t* inputs, int32_t* out_var, uint8_t* out_tgt, int32_t* iv, int32_t* aux) {
+  return guard([&] {
+    need(x, "extraction");
+    const auto& r = x->r;
+    auto put = [](int32_t* dst, const std::vector<int>& src) {
+      if (dst) std::copy(src.begin(), src.end(), dst);
+    };
+    put(kind, r.kind);
+    put(a, r.a);
+    put(b, r.b);
+    put(var, r.var);
+    put(inputs, r.pi);
+    put(iv, r.iv);
+    put(aux, r.aux);
+    for (size_t i = 0; i < r.po.size(); ++i) {
+      if (out_var) out_var[i] = r.po[i].first;
+      if (out_tgt) out_tgt[i] = r.po[i].second ? 1 : 0;
+    }
+  });
+}
+
+const char* sgx_extraction_note(const sgx_extraction* x) { return x ? x->r.unsat_note.c_str() : ""; }
+
+void sgx_extraction_free(sgx_extraction* x) { delete x; }
 
 }  // extern "C"

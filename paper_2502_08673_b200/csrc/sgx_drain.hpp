@@ -6,7 +6,7 @@
 //
 // Host memory is one anonymous mapping with transparent huge pages, grown by
 // mremap.  Keys arrive by DMA into a process-wide pinned double buffer (2 x
-// 32 MB, allocated once) and are copied out on up to 8 threads, which also
+// 32 MB, allocated once) and are copied out on drain_threads() threads (2), which also
 // spreads the first touch (measured on the B200 host: a 400 MB first touch
 // costs ~200 ms on one thread with 4 KB pages, ~16 ms on 8 threads with huge
 // pages; pinning 400 MB with cudaHostAlloc costs ~220 ms, more than the copy

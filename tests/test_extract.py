@@ -1,0 +1,142 @@
+"""Native circuit extraction (csrc/sgx_extract.cpp) against
+the reference's extract + build (src/extract.cpp:43-172, src/circuit.cpp:
+60-122).
+
+1. Golden: every committed instance (data/instances, the 60-instance C5 suite,
+   the 155-instance acceptance corpus) carries the circuit the reference built
+   for its CNF; the native extractor must rebuild it node for node, with the
+   same PI / PO orders and the same unsat verdict and note.
+2. Live: random CNFs (unit clauses, tautologies, repeated literals, gate
+   encodings mixed with noise, contradictions) through the reference library
+   (oracle/_ref) and the native path; circuits and ExtractionResult lists
+   (iv, aux) must be identical.
+
+Host-only: no GPU needed (the library loads without one).
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from helpers import golden_corpus
+from paper_2502_08673_b200 import (CnfFormula, extract_circuit, instance_from_cnf, load_instance,
+                                   parse_dimacs, write_dimacs)
+from paper_2502_08673_b200.circuit import DATA_DIR
+
+FIELDS = ("kind", "a", "b", "var", "inputs", "out_var", "out_tgt")
+
+
+def _names():
+    out = [os.path.basename(p)[:-7] for p in sorted(glob.glob(DATA_DIR + "/*.cnf.gz"))]
+    out += ["c5/" + os.path.basename(p)[:-7] for p in sorted(glob.glob(DATA_DIR + "/c5/*.cnf.gz"))]
+    return out
+
+
+def _same(c, ref):
+    for f in FIELDS:
+        x, y = np.asarray(getattr(c, f)), np.asarray(getattr(ref, f))
+        assert x.shape == y.shape and np.array_equal(x, y), f
+
+
+@pytest.mark.parametrize("name", _names())
+def test_extract_matches_golden_instances(name):
+    inst = load_instance(name)
+    r = extract_circuit(inst.cnf)
+    _same(r.circuit, inst.circuit)
+    assert r.unsat == inst.unsat
+    if inst.unsat:
+        assert r.unsat_note == inst.unsat_note
+
+
+def test_extract_matches_golden_corpus():
+    from helpers import instance_from_corpus
+    corpus = golden_corpus()
+    entries = corpus["instances"] if isinstance(corpus, dict) and "instances" in corpus else corpus
+    n = 0
+    for e in entries:
+        inst = instance_from_corpus(e)
+        r = extract_circuit(inst.cnf)
+        _same(r.circuit, inst.circuit)
+        assert r.unsat == inst.unsat, e["name"]
+        n += 1
+    assert n >= 100
+
+
+def _random_cnf(rng, nv, nc):
+    clauses = []
+    for _ in range(nc):
+        r = rng.random()
+        if r < 0.08:  # unit
+            clauses.append([int(rng.integers(1, nv + 1)) * int(rng.choice([-1, 1]))])
+        elif r < 0.45:  # a gate encoding: z = AND/OR/XOR of two vars
+            z, x, y = (int(v) for v in rng.choice(np.arange(1, nv + 1), 3, replace=False))
+            g = rng.integers(0, 3)
+            if g == 0:
+                clauses += [[-z, x], [-z, y], [z, -x, -y]]
+            elif g == 1:
+                clauses += [[z, -x], [z, -y], [-z, x, y]]
+            else:
+                clauses += [[-z, x, y], [-z, -x, -y], [z, -x, y], [z, x, -y]]
+        else:
+            k = int(rng.integers(1, 6))
+            vs = rng.integers(1, nv + 1, k)  # repeats and tautologies allowed
+            clauses.append([int(v) * int(rng.choice([-1, 1])) for v in vs])
+    return CnfFormula.from_clauses(nv, clauses)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_extract_matches_reference_random(seed):
+    from oracle.oracle import RefInstance, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(seed)
+    nv = int(rng.integers(3, 40))
+    cnf = _random_cnf(rng, nv, int(rng.integers(1, 4 * nv)))
+    text = write_dimacs(cnf)
+    ref = RefInstance.from_dimacs(text)
+    r = extract_circuit(parse_dimacs(text))
+    _same(r.circuit, ref)
+    assert r.unsat == ref.unsat
+    assert r.unsat_note == ref.unsat_note
+    sizes, iv, aux = ref.extraction_lists()
+    assert [len(r.pi), len(r.po_var), len(r.iv), len(r.aux), r.n_defs] == sizes
+    assert np.array_equal(r.iv, iv) and np.array_equal(r.aux, aux)
+
+
+def test_extract_matches_reference_generated():
+    """Generator-built CNFs (random circuits, or-chains, every gate signature)."""
+    from oracle.oracle import RefInstance, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    refs = [RefInstance.random_circuit(s, 12, 6, 8, 3) for s in range(6)]
+    refs += [RefInstance.or_chain(s, 20, 4, 6, 3, 2) for s in range(4)]
+    refs += [RefInstance.gate_signature(t, a) for t in range(6) for a in (2, 3, 4)]
+    for ref in refs:
+        r = extract_circuit(parse_dimacs(ref.dimacs()))
+        _same(r.circuit, ref)
+        assert r.unsat == ref.unsat
+
+
+def test_instance_from_cnf_equals_cached_instance():
+    inst = load_instance("c3a_or50")
+    path = os.path.join(DATA_DIR, "c3a_or50.cnf.gz")
+    got = instance_from_cnf(path)
+    _same(got.circuit, inst.circuit)
+    assert np.array_equal(got.paths.constrained_pi, inst.paths.constrained_pi)
+    assert np.array_equal(got.paths.unconstrained_pi, inst.paths.unconstrained_pi)
+
+
+def test_extract_rejects_bad_input():
+    bad = CnfFormula(2, np.array([0, 2], np.int64), np.array([1, 3], np.int32))
+    with pytest.raises(ValueError):
+        extract_circuit(bad)
+    with pytest.raises(ValueError):
+        extract_circuit(CnfFormula.from_clauses(3, [[1, 2]]), minimize_cap=17)
+
+
+def test_extract_empty_and_trivial():
+    r = extract_circuit(CnfFormula.from_clauses(3, []))
+    assert list(r.pi) == [1, 2, 3] and len(r.po_var) == 0 and r.circuit.n_nodes == 3
+    r = extract_circuit(CnfFormula.from_clauses(2, [[1], [-1]]))
+    assert r.unsat and "forced" in r.unsat_note
