@@ -2,9 +2,10 @@
  * satgrad_b200 -- C-ABI of the B200-native (sm_100a) sampling loop.
  *
  * This is the drop-in boundary for the reference's data-parallel sampling
- * path (satgrad, arXiv 2502.08673).  Everything below this header runs on the
- * GPU; everything above it (CNF parsing, circuit extraction, path
- * classification) stays in the caller.  Plain C types only: no C++ or torch
+ * path (satgrad, arXiv 2502.08673).  The sampling loop below this header runs
+ * on the GPU; CNF parsing and path classification stay in the caller, and
+ * circuit extraction may (the reference's) or may not (sgx_extract, host
+ * C++ in this library, node-for-node equal).  Plain C types only: no C++ or torch
  * types cross the boundary, arrays are host pointers with explicit sizes, and
  * every function returns 0 on success or a negative SGX_E* code, with a
  * thread-local message in sgx_last_error().
@@ -32,6 +33,8 @@
  *                        (sampler.hpp:37-55), packed like dedupe_key.
  *   sgx_forward /        forward<float> / backward<float> (autodiff.hpp:52-78)
  *   sgx_backward         as parity taps, in the reference's layouts.
+ *   sgx_extract          extract + build (extract.hpp:53, circuit.hpp:42;
+ *                        src/extract.cpp:43-172, src/circuit.cpp:60-122).
  */
 #ifndef SATGRAD_B200_H
 #define SATGRAD_B200_H

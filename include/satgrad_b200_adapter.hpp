@@ -95,6 +95,61 @@ struct Desc {
   }
 };
 
+// satgrad::extract + satgrad::build + satgrad::classify_paths (extract.hpp:53,
+// 65; circuit.hpp:42) through sgx_extract: the same Circuit node for node,
+// the same ExtractionResult lists (pi, iv, po, aux, unsat, unsat_note).
+// res.be is left empty -- the definitions live in the circuit's nodes -- so
+// paths are classified on the node graph (an input is constrained iff it is
+// in the fan-in of an output node), which equals classify_paths(res).
+struct Extracted {
+  satgrad::ExtractionResult res;
+  satgrad::Circuit circuit;
+  satgrad::PathClassification paths;
+};
+
+inline Extracted extract(const satgrad::CnfFormula& cnf, const satgrad::ExtractorConfig& cfg = {}) {
+  std::vector<int32_t> ptr{0}, lits;
+  for (const satgrad::Clause& cl : cnf.clauses) {
+    for (const satgrad::Literal& l : cl) lits.push_back(satgrad::to_dimacs(l));
+    ptr.push_back(static_cast<int32_t>(lits.size()));
+  }
+  sgx_extraction* x = nullptr;
+  check(sgx_extract(cnf.num_vars, ptr.data(), lits.data(), static_cast<int64_t>(cnf.clauses.size()),
+                    cfg.complement_cap, cfg.minimize_cap, &x));
+  std::unique_ptr<sgx_extraction, void (*)(sgx_extraction*)> hold(x, sgx_extraction_free);
+  int64_t sz[7];
+  check(sgx_extraction_sizes(x, sz));
+  std::vector<int32_t> kind(sz[0]), a(sz[0]), b(sz[0]), var(sz[0]), pi(sz[1]), ov(sz[2]), iv(sz[3]), aux(sz[4]);
+  std::vector<uint8_t> ot(sz[2]);
+  check(sgx_extraction_export(x, kind.data(), a.data(), b.data(), var.data(), pi.data(), ov.data(), ot.data(),
+                              iv.data(), aux.data()));
+  Extracted e;
+  e.res.num_vars = cnf.num_vars;
+  e.res.pi.assign(pi.begin(), pi.end());
+  e.res.iv.assign(iv.begin(), iv.end());
+  e.res.aux.assign(aux.begin(), aux.end());
+  for (size_t i = 0; i < ov.size(); ++i) e.res.po.push_back({ov[i], ot[i] != 0});
+  e.res.unsat = sz[6] != 0;
+  e.res.unsat_note = sgx_extraction_note(x);
+  satgrad::Circuit& c = e.circuit;
+  c.num_vars = cnf.num_vars;
+  c.inputs = e.res.pi;
+  c.outputs = e.res.po;
+  for (int64_t i = 0; i < sz[0]; ++i) {
+    c.nodes.push_back({static_cast<satgrad::GateKind>(kind[i]), a[i], b[i], var[i]});
+    if (var[i] != 0) c.var_to_node.emplace(var[i], static_cast<int>(i));
+  }
+  std::vector<char> reach(c.nodes.size(), 0);
+  for (const satgrad::PoEntry& p : c.outputs) reach[c.node_of(p.var)] = 1;
+  for (int64_t i = static_cast<int64_t>(c.nodes.size()) - 1; i >= 0; --i) {
+    if (!reach[i]) continue;
+    if (c.nodes[i].a >= 0) reach[c.nodes[i].a] = 1;
+    if (c.nodes[i].b >= 0) reach[c.nodes[i].b] = 1;
+  }
+  for (int v : c.inputs) (reach[c.node_of(v)] ? e.paths.constrained_pi : e.paths.unconstrained_pi).push_back(v);
+  return e;
+}
+
 // satgrad::run (sampler.hpp:79-81) on device `device`.
 inline satgrad::RunResult run(const satgrad::CnfFormula& cnf, const satgrad::Circuit& c,
                               const satgrad::ExtractionResult& res,

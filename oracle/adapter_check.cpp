@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <fstream>
 #include <sstream>
+#include <string>
 
 #include "satgrad/sampler.hpp"
 #include "satgrad_b200_adapter.hpp"
@@ -26,6 +27,35 @@ int main(int argc, char** argv) {
   satgrad::ExtractionResult res = satgrad::extract(cnf);
   satgrad::Circuit c = satgrad::build(res);
   satgrad::PathClassification paths = satgrad::classify_paths(res);
+  if (argc > 2 && std::string(argv[2]) == "--extract-only") {
+    // satgrad_b200::extract against the reference's extract + build + classify_paths
+    satgrad_b200::Extracted x = satgrad_b200::extract(cnf);
+    int bad = 0;
+    auto same = [&](bool ok, const char* what) {
+      if (!ok) {
+        std::printf("MISMATCH %s\n", what);
+        ++bad;
+      }
+    };
+    same(x.circuit.nodes.size() == c.nodes.size(), "node count");
+    for (size_t i = 0; i < c.nodes.size() && i < x.circuit.nodes.size(); ++i) {
+      const auto &p = c.nodes[i], &q = x.circuit.nodes[i];
+      if (p.kind != q.kind || p.a != q.a || p.b != q.b || p.var != q.var) {
+        same(false, "node");
+        break;
+      }
+    }
+    same(x.circuit.inputs == c.inputs, "inputs");
+    same(x.circuit.var_to_node == c.var_to_node, "var_to_node");
+    same(x.res.po.size() == res.po.size(), "po count");
+    for (size_t i = 0; i < res.po.size() && i < x.res.po.size(); ++i)
+      same(x.res.po[i].var == res.po[i].var && x.res.po[i].target == res.po[i].target, "po");
+    same(x.res.iv == res.iv && x.res.aux == res.aux && x.res.pi == res.pi, "iv / aux / pi");
+    same(x.res.unsat == res.unsat && x.res.unsat_note == res.unsat_note, "unsat");
+    same(x.paths.constrained_pi == paths.constrained_pi && x.paths.unconstrained_pi == paths.unconstrained_pi, "paths");
+    std::printf("%s: %zu nodes\n", bad ? "extract MISMATCH" : "extract ok", x.circuit.nodes.size());
+    return bad ? 1 : 0;
+  }
   satgrad::SamplerConfig cfg;
   cfg.use_f32 = true;
   if (argc > 2) cfg.batch = std::atoi(argv[2]);

@@ -140,3 +140,22 @@ def test_extract_empty_and_trivial():
     assert list(r.pi) == [1, 2, 3] and len(r.po_var) == 0 and r.circuit.n_nodes == 3
     r = extract_circuit(CnfFormula.from_clauses(2, [[1], [-1]]))
     assert r.unsat and "forced" in r.unsat_note
+
+
+@pytest.mark.parametrize("name", ["c1b_random", "c2_iscas", "c4_blasted", "mux_chain14", "unsat_unit",
+                                  "free_inputs", "single_model"])
+def test_reference_adapter_extract_drop_in(tmp_path, name):
+    """include/satgrad_b200_adapter.hpp's satgrad_b200::extract inside the
+    UNMODIFIED reference pipeline (oracle/adapter_check.cpp --extract-only):
+    Circuit, ExtractionResult lists and PathClassification equal the
+    reference's extract + build + classify_paths."""
+    import gzip
+    import subprocess
+    from helpers import ROOT
+    exe = os.path.join(ROOT, "oracle", "_ref", "adapter_check")
+    if not os.path.exists(exe):
+        pytest.skip("adapter check not built (make -C oracle adapter)")
+    cnf = tmp_path / f"{name}.cnf"
+    cnf.write_bytes(gzip.open(os.path.join(DATA_DIR, f"{name}.cnf.gz")).read())
+    r = subprocess.run([exe, str(cnf), "--extract-only"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "extract ok" in r.stdout, r.stdout + r.stderr
