@@ -146,8 +146,8 @@ class Exprs {
 
   // boolexpr.cpp:74-132
   int nary(Kind k, const std::vector<int>& es) {
-    std::vector<int> kids;
-    kids.reserve(es.size());
+    std::vector<int>& kids = nk_;  // scratch: nary never re-enters itself
+    kids.clear();
     if (k == kAnd || k == kOr) {
       const bool is_and = k == kAnd;
       for (int e : es) {
@@ -417,6 +417,7 @@ class Exprs {
   std::vector<uint32_t> seen_;
   std::vector<int> stack_;
   std::vector<int> var_id_, nvar_id_;  // var -> Var node, var -> Not(Var) node
+  std::vector<int> nk_;                // nary scratch
   uint32_t epoch_ = 0;
 
   static uint64_t mix(uint64_t h, uint64_t x) {
@@ -465,21 +466,27 @@ class Exprs {
     bool operator==(const Imp& o) const { return value == o.value && mask == o.mask; }
     bool covers(uint32_t m) const { return (m & ~mask) == value; }
   };
+  std::vector<uint32_t> qm_min_;  // sop scratch (sop never re-enters)
+  std::vector<Imp> qm_cur_, qm_next_, qm_primes_;
+  std::vector<char> qm_cov_, qm_cho_;
   int sop(const TT& tt, const std::vector<int>& vars) {
     const int nv = static_cast<int>(vars.size());
-    std::vector<uint32_t> minterms;
+    std::vector<uint32_t>& minterms = qm_min_;  // scratch (sop never re-enters)
+    minterms.clear();
     for (uint32_t r = 0; r < tt.rows(); ++r)
       if (tt.bit(r)) minterms.push_back(r);
     if (minterms.empty()) return 0;
     if (minterms.size() == tt.rows()) return 1;
-    std::vector<Imp> cur, primes;
+    std::vector<Imp>&cur = qm_cur_, &primes = qm_primes_, &next = qm_next_;
+    cur.clear();
+    primes.clear();
     for (uint32_t m : minterms) cur.push_back({m, 0});
     while (!cur.empty()) {
-      // cur is sorted and unique; one mask per round
+      // cur is sorted and unique (every mask of one popcount)
       auto has = [&](uint32_t value, uint32_t mask) {
         return std::binary_search(cur.begin(), cur.end(), Imp{value, mask});
       };
-      std::vector<Imp> next;
+      next.clear();
       for (const Imp& x : cur) {
         bool combined = false;
         for (int b = 0; b < nv; ++b) {
@@ -494,12 +501,14 @@ class Exprs {
       }
       std::sort(next.begin(), next.end());
       next.erase(std::unique(next.begin(), next.end()), next.end());
-      cur = std::move(next);
+      cur.swap(next);
     }
     std::sort(primes.begin(), primes.end());
     primes.erase(std::unique(primes.begin(), primes.end()), primes.end());
 
-    std::vector<char> covered(minterms.size(), 0), chosen(primes.size(), 0);
+    std::vector<char>&covered = qm_cov_, &chosen = qm_cho_;
+    covered.assign(minterms.size(), 0);
+    chosen.assign(primes.size(), 0);
     size_t uncovered = minterms.size();
     auto take = [&](size_t p) {
       chosen[p] = 1;
@@ -602,7 +611,7 @@ class Extractor {
   std::vector<char> in_iv_;
   std::vector<int> iv_order_;
   int next_aux_ = 0;
-  std::vector<int64_t> scratch_;
+  std::vector<int> conj_, disj_;  // definition_expr scratch
 
   int var_at(int64_t k) const { return std::abs(lit_[k]); }
 
@@ -800,7 +809,8 @@ class Extractor {
 
   // find_boolean_expression(target = (v, negated = false)) (boolexpr.cpp:247-264)
   int definition_expr(int v, const std::vector<int64_t>& cls) {
-    std::vector<int> conj;
+    std::vector<int>& conj = conj_;
+    conj.clear();
     for (int64_t c : cls) {
       bool pos = false, neg = false;
       for (int64_t k = ptr_[c]; k < ptr_[c + 1]; ++k) {
@@ -808,7 +818,8 @@ class Extractor {
         if (lit_[k] == -v) neg = true;
       }
       if (!neg || pos) continue;
-      std::vector<int> disj;
+      std::vector<int>& disj = disj_;
+      disj.clear();
       for (int64_t k = ptr_[c]; k < ptr_[c + 1]; ++k)
         if (var_at(k) != v) disj.push_back(X.literal(lit_[k]));
       conj.push_back(X.nary(kOr, disj));
