@@ -57,8 +57,13 @@ enum sgx_gate_kind {
   SGX_AND2, SGX_OR2, SGX_XOR2, SGX_XNOR2
 };
 
-/* RestartPolicy, sampler.hpp:21. */
-enum sgx_restart_policy { SGX_RESTART_NONE = 0, SGX_RESTART_REINIT_ON_EXHAUST = 1 };
+/* RestartPolicy, sampler.hpp:21.  SGX_RESTART_REINIT_ROWS is an extension
+ * (no reference counterpart, so no count parity): as
+ * REINIT_ON_EXHAUST, plus after every harvest the rows that are valid but not
+ * new redraw their logits; steps wait for the harvest (no overlap). */
+enum sgx_restart_policy {
+  SGX_RESTART_NONE = 0, SGX_RESTART_REINIT_ON_EXHAUST = 1, SGX_RESTART_REINIT_ROWS = 2
+};
 
 typedef struct sgx_ctx sgx_ctx;
 typedef struct sgx_circuit sgx_circuit;

@@ -383,6 +383,23 @@ void sampler_init(sgx_sampler* s, int restart) {
   CK(cudaGetLastError());
 }
 
+// SGX_RESTART_REINIT_ROWS: redraw the logits of the rows the harvest just
+// found valid but not new (the harvest has finished: finish() waited on it).
+void reinit_rows(sgx_sampler* s, int restart, int it) {
+  const auto& L = s->c->L;
+  if (L.cpi.empty()) return;
+  const uint64_t prefix =
+      sgx::fold(sgx::fold(sgx::fold(sgx::fold(sgx::kPi, s->cfg.seed), sgx::kInitTag),
+                          static_cast<uint64_t>(static_cast<int64_t>(restart))),
+                0x726f7773ull + static_cast<uint64_t>(it));  // "rows" + iteration
+  CK(cudaEventRecord(s->ev_join, s->sh));  // valid / newmask of that harvest
+  CK(cudaStreamWaitEvent(s->st, s->ev_join, 0));
+  sgx::launch_reinit_rows(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, 32 * s->vec, prefix,
+                          s->cfg.row_offset, s->valid.p, s->newmask.p);
+  s->launches += 1;
+  CK(cudaGetLastError());
+}
+
 // One GD step; returns its parity slot (loss total in dloss[slot], timing in sev[slot]).
 int sampler_step(sgx_sampler* s) {
   sgx_circuit* c = s->c;
@@ -701,6 +718,7 @@ void sampler_run(sgx_sampler* s) {
     return !(e && e[0] == '0');
   }();
   const int max_restarts = cfg.max_restarts > 0 ? cfg.max_restarts : 1000;
+  const bool per_row = cfg.restart_policy == SGX_RESTART_REINIT_ROWS;
   bool timed_out = false;
   cudaEvent_t e0, e1, r0, r1;
   CK(cudaEventCreate(&e0));
@@ -734,7 +752,7 @@ void sampler_run(sgx_sampler* s) {
     for (;;) {
       const int it = h_iter + 1;
       int slot = -1;
-      if (overlap && !quota && it <= cfg.iterations && !out_of_time()) slot = sampler_step(s);
+      if (overlap && !per_row && !quota && it <= cfg.iterations && !out_of_time()) slot = sampler_step(s);
       hlap(4);
       finish(h_iter, h_quota, h_slot);
       if (h_iter == 0) s->phase_ms[0] += elapsed(e0, e1);
@@ -744,6 +762,7 @@ void sampler_run(sgx_sampler* s) {
         timed_out = true;
         break;
       }
+      if (per_row && slot < 0) reinit_rows(s, restart, it);
       if (slot < 0) slot = sampler_step(s);
       h_quota = quota_left();
       hlap(4);
@@ -754,7 +773,7 @@ void sampler_run(sgx_sampler* s) {
       h_slot = slot;
     }
     if (quota_met() || timed_out) break;
-    if (cfg.restart_policy != SGX_RESTART_REINIT_ON_EXHAUST) break;
+    if (cfg.restart_policy == SGX_RESTART_NONE) break;
     if (s->n_solutions == before) break;
     if (restart >= max_restarts) break;
     if (out_of_time()) {
@@ -926,6 +945,8 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
     need(out, "out");
     if (cfg->batch < 1) throw std::invalid_argument("batch must be positive");  // sampler.cpp:93
     if (cfg->iterations < 0) throw std::invalid_argument("iterations must be non-negative");
+    if (cfg->restart_policy < SGX_RESTART_NONE || cfg->restart_policy > SGX_RESTART_REINIT_ROWS)
+      throw std::invalid_argument("unknown restart policy");
     CK(cudaSetDevice(c->ctx->device));
     auto s = std::make_unique<sgx_sampler>();
     s->c = c;

@@ -612,6 +612,8 @@ class Extractor {
   std::vector<int> iv_order_;
   int next_aux_ = 0;
   std::vector<int> conj_, disj_;  // definition_expr scratch
+  std::vector<int> cs_;             // complement scratch
+  std::vector<int64_t> cf_, cg_;
 
   int var_at(int64_t k) const { return std::abs(lit_[k]); }
 
@@ -725,8 +727,11 @@ class Extractor {
   bool complement(int v, const std::vector<int64_t>& cls) {
     // f: clauses with ~v and not v; g: clauses with v and not ~v
     bool f_any = false, g_any = false, f_zero = false, g_zero = false;
-    std::vector<int> s;
-    std::vector<int64_t> fc, gc;
+    std::vector<int>& s = cs_;
+    std::vector<int64_t>&fc = cf_, &gc = cg_;
+    s.clear();
+    fc.clear();
+    gc.clear();
     for (int64_t c : cls) {
       bool pos = false, neg = false;
       int others = 0;

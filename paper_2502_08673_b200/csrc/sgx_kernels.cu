@@ -36,6 +36,30 @@ k_init_v(float* __restrict__ V, int ncols, int Bp, int tile_rows, uint64_t prefi
   }
 }
 
+// Per-row restart (an extension: the reference restarts
+// the whole batch, sampler.cpp:178-185).  Rows whose hardened assignment was
+// valid but not new at the last harvest have converged onto a known
+// solution; their logits are redrawn (u01 keyed by a per-iteration prefix,
+// row and column, like init_soft_inputs), the others keep theirs.  The next
+// step's backward epilogue re-hardens every row, so hb is not touched here.
+__global__ void __launch_bounds__(kThreads)
+k_reinit_rows(float* __restrict__ V, int ncols, int Bp, int tile_rows, uint64_t prefix, long long row_offset,
+              const uint32_t* __restrict__ valid, const uint32_t* __restrict__ newmask) {
+  const long long total = static_cast<long long>(ncols) * Bp;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long tile = i / (static_cast<long long>(ncols) * tile_rows);
+    const int within = static_cast<int>(i - tile * ncols * tile_rows);
+    const int c = within / tile_rows;
+    const int r = static_cast<int>(tile * tile_rows) + within % tile_rows;
+    const uint32_t stuck = __ldg(valid + (r >> 5)) & ~__ldg(newmask + (r >> 5));
+    if (!((stuck >> (r & 31)) & 1u)) continue;
+    const uint64_t h = fold(fold(prefix, static_cast<uint64_t>(row_offset + r)), static_cast<uint64_t>(c));
+    const double u = static_cast<double>(h >> 11) * 0x1.0p-53;
+    V[i] = __double2float_rn(__dsub_rn(__dmul_rn(2.0, u), 1.0));
+  }
+}
+
 // Vector access of V consecutive samples of one tape row.
 template <int V>
 __device__ __forceinline__ void vload(const float* p, float (&o)[V]) {
@@ -2152,6 +2176,13 @@ void launch_init_v(cudaStream_t st, float* V, int ncols, int Bp, int tile_rows, 
   if (ncols == 0) return;
   k_init_v<<<grid_for(static_cast<long long>(ncols) * Bp, kThreads, 148 * 64), kThreads, 0, st>>>(
       V, ncols, Bp, tile_rows, prefix, row_offset, hb);
+}
+
+void launch_reinit_rows(cudaStream_t st, float* V, int ncols, int Bp, int tile_rows, uint64_t prefix,
+                        long long row_offset, const uint32_t* valid, const uint32_t* newmask) {
+  if (ncols == 0) return;
+  k_reinit_rows<<<grid_for(static_cast<long long>(ncols) * Bp, kThreads, 148 * 64), kThreads, 0, st>>>(
+      V, ncols, Bp, tile_rows, prefix, row_offset, valid, newmask);
 }
 
 // Forward variant (measured on B200, c2_iscas @ 64k rows): the

@@ -25,6 +25,9 @@ from .cnf import CnfFormula, format_solution_line, key_to_assignment
 class RestartPolicy(enum.IntEnum):
     NONE = 0
     REINIT_ON_EXHAUST = 1
+    # extension (no reference counterpart): REINIT_ON_EXHAUST plus, after every
+    # harvest, valid-but-duplicate rows redraw their logits (SGX_RESTART_REINIT_ROWS)
+    REINIT_ROWS = 2
 
 
 @dataclass

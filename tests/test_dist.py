@@ -212,3 +212,10 @@ def test_c5_suite_two_ranks_equal_one_process():
         assert set(summ["families"]) == {"or", "q", "s15850", "prod", "blasted"}
         assert all(f["batch_per_gpu"] == FAMILY_BATCH[k] for k, f in summ["families"].items())
     assert summarize(want, 1)["unique"] == got[0][2]["unique"]
+
+
+def test_reinit_rows_policy_is_single_device_only():
+    from paper_2502_08673_b200 import RestartPolicy, SamplerConfig
+    from paper_2502_08673_b200.dist import run_sharded
+    with pytest.raises(ValueError):
+        run_sharded(None, None, SamplerConfig(restart=RestartPolicy.REINIT_ROWS), 0, 1, 1024)

@@ -341,3 +341,37 @@ def test_device_format_matches_reference(gpu, name, batch, iters):
     finally:
         s.close()
         dc.close()
+
+
+@pytest.mark.parametrize("name,batch", [("c2_iscas", 8192), ("c3a_or50", 1 << 16), ("mux_chain14", 4096)])
+def test_reinit_rows_policy(gpu, name, batch):
+    """RestartPolicy.REINIT_ROWS (no reference counterpart):
+    every stored solution satisfies the CNF and is distinct, runs are
+    deterministic, the first harvest equals the whole-batch policy's (re-init
+    starts after it), and redrawing converged duplicate rows does not lose
+    solutions against REINIT_ON_EXHAUST at the same step count."""
+    from paper_2502_08673_b200 import verify_keys
+    i = inst(name)
+    base = dict(batch=batch, iterations=5, seed=5, max_restarts=3)
+    dc = DeviceCircuit.from_instance(i)
+    try:
+        runs = {}
+        for pol in (RestartPolicy.REINIT_ROWS, RestartPolicy.REINIT_ROWS, RestartPolicy.REINIT_ON_EXHAUST):
+            s = Sampler(dc, SamplerConfig(restart=pol, **base))
+            try:
+                st = s.run()
+                runs.setdefault(pol, []).append((st, s.fetch(), list(st.new_unique)))
+            finally:
+                s.close()
+        (a, ka, ta), (b, kb, tb) = runs[RestartPolicy.REINIT_ROWS]
+        (w, kw, tw), = runs[RestartPolicy.REINIT_ON_EXHAUST]
+        assert a.unique_count == b.unique_count and np.array_equal(ka, kb) and ta == tb
+        assert len(ka) == a.unique_count > 0
+        assert len(np.unique(ka, axis=0)) == len(ka)
+        assert verify_keys(i.cnf, ka).all()
+        assert ta[0] == tw[0]
+        assert a.unique_count >= 0.95 * w.unique_count, (a.unique_count, w.unique_count)
+        print(f"{name}: rows {a.unique_count} vs whole-batch {w.unique_count} "
+              f"({a.unique_count / max(1, w.unique_count):.3f}x)")
+    finally:
+        dc.close()
