@@ -394,6 +394,20 @@ void reinit_rows(sgx_sampler* s, int restart, int it) {
                 0x726f7773ull + static_cast<uint64_t>(it));  // "rows" + iteration
   CK(cudaEventRecord(s->ev_join, s->sh));  // valid / newmask of that harvest
   CK(cudaStreamWaitEvent(s->st, s->ev_join, 0));
+  if (std::getenv("SGX_REINIT_DEBUG")) {
+    std::vector<uint32_t> v(s->W), m(s->W);
+    CK(cudaStreamSynchronize(s->st));
+    CK(cudaMemcpy(v.data(), s->valid.p, s->W * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(m.data(), s->newmask.p, s->W * 4, cudaMemcpyDeviceToHost));
+    long long nv = 0, nn = 0, nf = 0;
+    for (int w = 0; w < s->W; ++w) {
+      nv += __builtin_popcount(v[w]);
+      nn += __builtin_popcount(m[w]);
+      nf += __builtin_popcount(v[w] & ~m[w]);
+    }
+    std::fprintf(stderr, "[sgx] reinit restart %d it %d: valid %lld new %lld flagged %lld (W %d)\n", restart, it, nv,
+                 nn, nf, s->W);
+  }
   sgx::launch_reinit_rows(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, 32 * s->vec, prefix,
                           s->cfg.row_offset, s->valid.p, s->newmask.p);
   s->launches += 1;
