@@ -151,7 +151,7 @@ def dist_setup(args):
     return world, rank, local, pg
 
 
-def cpu_reference(inst_name, batch, iterations, seed, steps=1, timeout_s=0.0):
+def cpu_reference(inst_name, batch, iterations, seed, steps=1, timeout_s=0.0, f32=True):
     """The reference's satgrad::run on the host cores (oracle/_ref); falls back
     to the C port (oracle/libsgx_oracle.so) when the reference was not built."""
     from paper_2502_08673_b200 import load_instance, write_dimacs
@@ -164,7 +164,7 @@ def cpu_reference(inst_name, batch, iterations, seed, steps=1, timeout_s=0.0):
         kind = "reference"
         for _ in range(steps):
             r = ri.run(batch=batch, iterations=iterations, seed=seed, threads=cores,
-                       use_f32=True, timeout_s=timeout_s)
+                       use_f32=f32, timeout_s=timeout_s)
             uniq += r.unique
             wall += r.wall
     else:
@@ -176,7 +176,7 @@ def cpu_reference(inst_name, batch, iterations, seed, steps=1, timeout_s=0.0):
             wall += r.wall
     return {"value": uniq / wall if wall > 0 else 0.0, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"{steps} x satgrad::run(batch={batch}, iterations={iterations}, seed={seed}, "
-                      f"f32, threads={cores}) on {inst_name}: rows are independent, so unique/s "
+                      f"{'f32' if f32 else 'f64'}, threads={cores}) on {inst_name}: rows are independent, so unique/s "
                       f"per row is batch-invariant; {uniq} unique in {wall:.2f} s",
             "unique": uniq, "wall_s": wall}
 
@@ -375,6 +375,9 @@ def run_b200_arm(args, world, rank, local, dist):
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference(name, ref_batch, args.iterations, 1, steps=1)
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        if cpu["kind"] == "reference":  # the reference's default precision (sampler.hpp:32), beside f32
+            c64 = cpu_reference(name, ref_batch, args.iterations, 1, steps=1, f32=False)
+            cpu["f64"] = {"value": c64["value"], "sample": c64["sample"]}
     ttk = None
     if world == 1 and not args.no_ttk:
         ttk = time_to_1k(dev, with_cpu=not args.no_cpu_baseline)
