@@ -33,6 +33,7 @@
  *                        (sampler.hpp:37-55), packed like dedupe_key.
  *   sgx_forward /        forward<float> / backward<float> (autodiff.hpp:52-78)
  *   sgx_backward         as parity taps, in the reference's layouts.
+ *   sgx_verify_solutions cmd_verify (tools/satgrad_main.cpp:242-302).
  *   sgx_extract          extract + build (extract.hpp:53, circuit.hpp:42;
  *                        src/extract.cpp:43-172, src/circuit.cpp:60-122).
  */
@@ -223,6 +224,16 @@ int sgx_embed(sgx_ctx* ctx, const float* v, int64_t n, float* p);
 /* Bit-exact device sigmoid / expf over a host array (parity of the glibc
  * expf restatement used by embed/backward). */
 int sgx_expf(sgx_ctx* ctx, const float* x, int64_t n, float* out);
+
+/* cmd_verify (tools/satgrad_main.cpp:242-302): check a solution text of
+ * "v1 -v2 ... 0" lines against the circuit's CNF -- every line a complete,
+ * consistent assignment that satisfies the formula, all pairwise distinct --
+ * parsed on host threads, CNF-checked on the GPU.  out[5] = {checked,
+ * err_line (1-based, 0 = none), err_var, err_kind, kernel launches}; err_kind
+ * 0 ok, 1 variable exceeds the count, 2 assigned both ways, 3 missing 0
+ * terminator, 4 unassigned (err_var = first), 5 does not satisfy the formula,
+ * 6 duplicate assignment.  checked = solutions verified before the error. */
+int sgx_verify_solutions(sgx_circuit* c, const char* text, int64_t len, int64_t* out);
 
 /* ---- Circuit extraction (host) -------------------------
  * extract + build (src/extract.cpp:43-172, src/boolexpr.cpp, src/circuit.cpp:

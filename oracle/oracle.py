@@ -105,6 +105,7 @@ class RefLib:
             L.ref_format_keys.argtypes = [_u64p, C.c_longlong, C.c_int, C.c_void_p, C.c_longlong]
             L.ref_extract_seconds.argtypes = [C.c_char_p, C.c_int, _f64p]
             L.ref_extraction_lists.argtypes = [C.c_void_p, _i64p, _i32p, _i32p]
+            L.ref_verify_text.argtypes = [C.c_void_p, C.c_char_p, C.c_int64, _i64p]
             RefLib._lib = L
         self.L = RefLib._lib
 
@@ -244,6 +245,16 @@ class RefInstance:
         aux = np.zeros(n, np.int32)
         self.lib.L.ref_extraction_lists(self.h, sz, iv, aux)
         return [int(x) for x in sz], iv[: sz[2]], aux[: sz[3]]
+
+    def verify_text(self, text) -> dict:
+        """cmd_verify's checks over the reference's eval_cnf / SolutionSet
+        (ref_shim.cpp): {checked, line, var, kind, wall_s}."""
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        out = np.zeros(5, np.int64)
+        if self.lib.L.ref_verify_text(self.h, data, len(data), out) != 0:
+            raise ValueError(self.lib.error())
+        return {"checked": int(out[0]), "line": int(out[1]), "var": int(out[2]), "kind": int(out[3]),
+                "wall_s": out[4] / 1e9}
 
     def dimacs(self) -> str:
         n = C.c_int64()

@@ -19,6 +19,7 @@
 #include <cstring>
 #include <memory>
 #include <stdexcept>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -499,6 +500,77 @@ void ref_extraction_lists(void* hv, int64_t* sizes, int32_t* iv, int32_t* aux) {
   sizes[4] = static_cast<int64_t>(r.be.size());
   if (iv) std::copy(r.iv.begin(), r.iv.end(), iv);
   if (aux) std::copy(r.aux.begin(), r.aux.end(), aux);
+}
+
+// The verify subcommand's per-line checks (cmd_verify, tools/satgrad_main.cpp:
+// 242-302; the tool itself needs CLI11, absent here) restated over the
+// reference's own parse_dimacs / eval_cnf / SolutionSet, with istream token
+// semantics.  out = {checked, err_line, err_var, err_kind, wall_ns}; kinds as
+// sgx_verify_solutions.  TEST INFRASTRUCTURE: the checker and CPU baseline.
+int ref_verify_text(void* hv, const char* text, int64_t len, int64_t* out) {
+  GUARD_BEGIN
+  const CnfFormula& cnf = static_cast<RefInst*>(hv)->cnf;
+  const auto t0 = std::chrono::steady_clock::now();
+  std::istringstream in(std::string(text, static_cast<size_t>(len)));
+  SolutionSet seen(cnf.num_vars);
+  std::string row;
+  int64_t lineno = 0, checked = 0, err_line = 0, err_var = 0, kind = 0;
+  while (kind == 0 && std::getline(in, row)) {
+    ++lineno;
+    std::istringstream tok(row);
+    Assignment a(cnf.num_vars + 1, 0xFF);
+    bool done = false, nonblank = false;
+    long long x;
+    while (tok >> x) {
+      nonblank = true;
+      if (x == 0) {
+        done = true;
+        break;
+      }
+      const long long v = x < 0 ? -x : x;
+      if (v > cnf.num_vars) {
+        kind = 1;
+        err_var = v;
+        break;
+      }
+      const uint8_t b = x > 0 ? 1 : 0;
+      if (a[v] != 0xFF && a[v] != b) {
+        kind = 2;
+        err_var = v;
+        break;
+      }
+      a[v] = b;
+    }
+    if (kind) break;
+    if (!nonblank) continue;
+    if (!done) {
+      kind = 3;
+      break;
+    }
+    for (int v = 1; v <= cnf.num_vars && !kind; ++v)
+      if (a[v] == 0xFF) {
+        kind = 4;
+        err_var = v;
+      }
+    if (kind) break;
+    if (!eval_cnf(cnf, a)) {
+      kind = 5;
+      break;
+    }
+    if (!seen.insert(a)) {
+      kind = 6;
+      break;
+    }
+    ++checked;
+  }
+  if (kind) err_line = lineno;
+  out[0] = checked;
+  out[1] = err_line;
+  out[2] = err_var;
+  out[3] = kind;
+  out[4] = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+  return 0;
+  GUARD_END(-1)
 }
 
 }  // extern "C"

@@ -25,7 +25,7 @@ EXPORTS = [
     "sgx_harvest_local", "sgx_harvest_merge", "sgx_harvest_commit", "sgx_read_logits",
     "sgx_set_host_stream", "sgx_solutions_take", "sgx_host_free", "sgx_step_async", "sgx_step_loss",
     "sgx_format_solutions", "sgx_launch_count", "sgx_extract", "sgx_extraction_sizes",
-    "sgx_extraction_export", "sgx_extraction_note", "sgx_extraction_free",
+    "sgx_extraction_export", "sgx_extraction_note", "sgx_extraction_free", "sgx_verify_solutions",
 ]
 
 
@@ -128,6 +128,7 @@ def load() -> C.CDLL:
                                   + [C.POINTER(i32)] * 2),
         "sgx_extraction_note": (C.c_char_p, [vp]),
         "sgx_extraction_free": (None, [vp]),
+        "sgx_verify_solutions": (C.c_int, [vp, C.c_char_p, i64, i64p]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

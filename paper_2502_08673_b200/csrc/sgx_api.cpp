@@ -1314,6 +1314,22 @@ int sgx_host_free(uint64_t* keys, int64_t map_bytes) {
   return guard([&] { sgx::host_free(keys, static_cast<size_t>(map_bytes)); });
 }
 
+int sgx_verify_solutions(sgx_circuit* c, const char* text, int64_t len, int64_t* out) {
+  return guard([&] {
+    need(c, "circuit");
+    need(out, "out");
+    if (len < 0) throw std::invalid_argument("negative text length");
+    if (len > 0) need(text, "text");
+    sgx::VerifyResult r;
+    sgx::verify_solutions(c->ctx->device, c->L.clause_ptr, c->L.clause_lit, c->L.num_vars, text, len, &r);
+    out[0] = r.checked;
+    out[1] = r.err_line;
+    out[2] = r.err_var;
+    out[3] = r.err_kind;
+    out[4] = r.launches;
+  });
+}
+
 int sgx_format_solutions(sgx_sampler* s, int64_t first, int64_t count, char* out, int64_t cap, int64_t* len) {
   return guard([&] {
     need(s, "sampler");

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 namespace sgx {
 
@@ -147,4 +148,15 @@ void launch_rehash(cudaStream_t st, const unsigned long long* okeys, const unsig
                    uint64_t ocap, unsigned long long* nkeys, unsigned long long* nmeta, uint64_t nmask);
 void launch_expf(cudaStream_t st, const float* x, long long n, float* out, const uint64_t* tab, int sigmoid);
 
+
+// cmd_verify (tools/satgrad_main.cpp:242-302) on the device (sgx_verify.cu).
+// err_kind: 0 ok, 1 exceeds the variable count, 2 assigned both ways,
+// 3 missing 0 terminator, 4 unassigned, 5 does not satisfy, 6 duplicate.
+struct VerifyResult {
+  int64_t checked = 0, err_line = 0, err_var = 0;
+  int32_t err_kind = 0;
+  int64_t launches = 0;
+};
+void verify_solutions(int device, const std::vector<int64_t>& clause_ptr, const std::vector<int32_t>& clause_lit,
+                      int num_vars, const char* text, int64_t len, VerifyResult* out);
 }  // namespace sgx

@@ -130,6 +130,24 @@ class DeviceCircuit:
                 "outputs", "num_vars", "unsat"]
         return dict(zip(keys, (int(x) for x in out)))
 
+    # cmd_verify messages (tools/satgrad_main.cpp:265-295), by err_kind
+    VERIFY_MESSAGES = {1: "x{var} exceeds the variable count", 2: "x{var} assigned both ways",
+                       3: "missing 0 terminator", 4: "x{var} unassigned",
+                       5: "assignment does not satisfy the formula", 6: "duplicate assignment"}
+
+    def verify_solutions(self, text) -> dict:
+        """``satgrad verify`` (cmd_verify, tools/satgrad_main.cpp:242-302) of a
+        solution text against this circuit's CNF, CNF checks on the GPU.
+        Returns {checked, ok, line, kind, var, message, launches}."""
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        out = np.zeros(5, np.int64)
+        _lib.check(self.L.sgx_verify_solutions(self.h, data, len(data), _lib.ptr(out, C.c_int64)))
+        checked, line, var, kind, launches = (int(x) for x in out)
+        msg = (f"{line}: " + self.VERIFY_MESSAGES[kind].format(var=var)) if kind else \
+            f"verify: {checked} solutions, all satisfying and pairwise distinct"
+        return {"checked": checked, "ok": kind == 0, "line": line, "kind": kind, "var": var,
+                "message": msg, "launches": launches}
+
     def close(self):
         if getattr(self, "h", None):
             self.L.sgx_circuit_free(self.h)
