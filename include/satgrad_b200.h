@@ -234,6 +234,10 @@ int sgx_expf(sgx_ctx* ctx, const float* x, int64_t n, float* out);
  * terminator, 4 unassigned (err_var = first), 5 does not satisfy the formula,
  * 6 duplicate assignment.  checked = solutions verified before the error. */
 int sgx_verify_solutions(sgx_circuit* c, const char* text, int64_t len, int64_t* out);
+/* The same from the CNF alone (what cmd_verify has): CSR clause_ptr[n_clauses
+ * + 1] over DIMACS literals. */
+int sgx_verify_cnf(sgx_ctx* ctx, int32_t num_vars, const int64_t* clause_ptr, const int32_t* clause_lit,
+                   int64_t n_clauses, const char* text, int64_t len, int64_t* out);
 
 /* ---- Circuit extraction (host) -------------------------
  * extract + build (src/extract.cpp:43-172, src/boolexpr.cpp, src/circuit.cpp:

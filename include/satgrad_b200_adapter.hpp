@@ -150,6 +150,31 @@ inline Extracted extract(const satgrad::CnfFormula& cnf, const satgrad::Extracto
   return e;
 }
 
+// `satgrad verify` (cmd_verify, tools/satgrad_main.cpp:242-302) of a
+// solution text: the CNF checks run on the GPU.  Returns 0 when every line
+// is a distinct satisfying assignment; otherwise the reference's message
+// ("<line>: <what>") in *message and the error kind (sgx_verify_solutions).
+inline int verify(const satgrad::CnfFormula& cnf, const std::string& text, std::string* message = nullptr,
+                  long long* checked = nullptr, int device = 0) {
+  std::vector<int64_t> ptr{0};
+  std::vector<int32_t> lits;
+  for (const satgrad::Clause& cl : cnf.clauses) {
+    for (const satgrad::Literal& l : cl) lits.push_back(satgrad::to_dimacs(l));
+    ptr.push_back(static_cast<int64_t>(lits.size()));
+  }
+  int64_t out[5];
+  check(sgx_verify_cnf(context(device), cnf.num_vars, ptr.data(), lits.data(),
+                       static_cast<int64_t>(cnf.clauses.size()), text.data(), static_cast<int64_t>(text.size()), out));
+  static const char* what[7] = {"", "exceeds the variable count", "assigned both ways", "missing 0 terminator",
+                                "unassigned", "assignment does not satisfy the formula", "duplicate assignment"};
+  if (checked) *checked = out[0];
+  if (message) {
+    const int k = static_cast<int>(out[3]);
+    *message = k == 0 ? "" : std::to_string(out[1]) + ": " + ((k == 1 || k == 2 || k == 4) ? "x" + std::to_string(out[2]) + " " : "") + what[k];
+  }
+  return static_cast<int>(out[3]);
+}
+
 // satgrad::run (sampler.hpp:79-81) on device `device`.
 inline satgrad::RunResult run(const satgrad::CnfFormula& cnf, const satgrad::Circuit& c,
                               const satgrad::ExtractionResult& res,

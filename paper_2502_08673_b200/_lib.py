@@ -26,6 +26,7 @@ EXPORTS = [
     "sgx_set_host_stream", "sgx_solutions_take", "sgx_host_free", "sgx_step_async", "sgx_step_loss",
     "sgx_format_solutions", "sgx_launch_count", "sgx_extract", "sgx_extraction_sizes",
     "sgx_extraction_export", "sgx_extraction_note", "sgx_extraction_free", "sgx_verify_solutions",
+    "sgx_verify_cnf",
 ]
 
 
@@ -129,6 +130,7 @@ def load() -> C.CDLL:
         "sgx_extraction_note": (C.c_char_p, [vp]),
         "sgx_extraction_free": (None, [vp]),
         "sgx_verify_solutions": (C.c_int, [vp, C.c_char_p, i64, i64p]),
+        "sgx_verify_cnf": (C.c_int, [vp, i32, i64p, C.POINTER(i32), i64, C.c_char_p, i64, i64p]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -1330,6 +1330,36 @@ int sgx_verify_solutions(sgx_circuit* c, const char* text, int64_t len, int64_t*
   });
 }
 
+int sgx_verify_cnf(sgx_ctx* ctx, int32_t num_vars, const int64_t* clause_ptr, const int32_t* clause_lit,
+                   int64_t n_clauses, const char* text, int64_t len, int64_t* out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(out, "out");
+    if (num_vars < 0 || n_clauses < 0 || len < 0) throw std::invalid_argument("negative size");
+    if (len > 0) need(text, "text");
+    std::vector<int64_t> ptr{0};
+    std::vector<int32_t> lit;
+    if (n_clauses > 0) {
+      need(clause_ptr, "clause_ptr");
+      need(clause_lit, "clause_lit");
+      ptr.assign(clause_ptr, clause_ptr + n_clauses + 1);
+      if (ptr[0] != 0) throw std::invalid_argument("clause_ptr[0] must be 0");
+      for (int64_t c = 0; c < n_clauses; ++c)
+        if (ptr[c + 1] < ptr[c]) throw std::invalid_argument("clause_ptr not monotone");
+      lit.assign(clause_lit, clause_lit + ptr[n_clauses]);
+      for (int32_t l : lit)
+        if (l == 0 || l > num_vars || -l > num_vars) throw std::invalid_argument("literal out of range");
+    }
+    sgx::VerifyResult r;
+    sgx::verify_solutions(ctx->device, ptr, lit, num_vars, text, len, &r);
+    out[0] = r.checked;
+    out[1] = r.err_line;
+    out[2] = r.err_var;
+    out[3] = r.err_kind;
+    out[4] = r.launches;
+  });
+}
+
 int sgx_format_solutions(sgx_sampler* s, int64_t first, int64_t count, char* out, int64_t cap, int64_t* len) {
   return guard([&] {
     need(s, "sampler");

@@ -100,6 +100,25 @@ def device_context(device: int = 0) -> int:
     return _ctx[device]
 
 
+def verify_solutions(cnf: CnfFormula, text, device: int = 0) -> dict:
+    """``satgrad verify`` (cmd_verify, tools/satgrad_main.cpp:242-302) from the
+    CNF alone: CNF checks on the GPU (sgx_verify_cnf).  Same result dict as
+    DeviceCircuit.verify_solutions."""
+    L = _lib.load()
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    ptr = np.ascontiguousarray(cnf.clause_ptr, np.int64)
+    lit = np.ascontiguousarray(cnf.clause_lit, np.int32)
+    out = np.zeros(5, np.int64)
+    _lib.check(L.sgx_verify_cnf(C.c_void_p(device_context(device)), int(cnf.num_vars), _lib.ptr(ptr, C.c_int64),
+                                _lib.ptr(lit, C.c_int32), int(cnf.n_clauses), data, len(data),
+                                _lib.ptr(out, C.c_int64)))
+    checked, line, var, kind, launches = (int(x) for x in out)
+    msg = (f"{line}: " + DeviceCircuit.VERIFY_MESSAGES[kind].format(var=var)) if kind else \
+        f"verify: {checked} solutions, all satisfying and pairwise distinct"
+    return {"checked": checked, "ok": kind == 0, "line": line, "kind": kind, "var": var, "message": msg,
+            "launches": launches}
+
+
 class DeviceCircuit:
     """A circuit + CNF uploaded and levelized on one GPU (sgx_circuit_upload)."""
 

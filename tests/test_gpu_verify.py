@@ -99,3 +99,16 @@ def test_verify_large_text_chunks(gpu):
     # distinct lines only up to the first repeat: the duplicate error lands at len(lines) + 1
     _same(dc, ref, "\n".join(big) + "\n")
     _same(dc, ref, "\n".join(lines) + "\n")
+
+
+def test_verify_from_cnf_alone(gpu):
+    """sgx_verify_cnf (the entry point for cmd_verify, which has no circuit)
+    equals the circuit-bound call, error cases included."""
+    from paper_2502_08673_b200 import verify_solutions
+    inst, dc, ref, text = _setup("c1b_random", 2048)
+    lines = text.rstrip("\n").split("\n")
+    rng = np.random.default_rng(3)
+    for what, ls in _mutations(lines, inst.cnf.num_vars, rng).items():
+        t = "\n".join(ls) + "\n"
+        a, b = verify_solutions(inst.cnf, t), dc.verify_solutions(t)
+        assert (a["checked"], a["line"], a["kind"], a["var"]) == (b["checked"], b["line"], b["kind"], b["var"])
