@@ -7,9 +7,9 @@
 //     solutions per word: keys are transposed into [var][word] rows by warp
 //     ballots, then each thread ANDs the clause ORs of one word (eval_cnf,
 //     cnf.cpp:129-147), clause data read as broadcasts;
-//   * the GPU fingerprints every key; the host finds duplicates
-//     (SolutionSet::insert, sampler.cpp:28-44) by fingerprint with an exact
-//     key compare.
+//   * the GPU fingerprints every key and radix-sorts (fingerprint, row); the
+//     host walks runs of equal fingerprints with an exact key compare to find
+//     duplicates (SolutionSet::insert, sampler.cpp:28-44).
 // The first error in line order wins, as in the reference's single pass.
 #include <cuda_runtime.h>
 
@@ -19,8 +19,9 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
-#include <unordered_map>
 #include <vector>
+
+#include <cub/cub.cuh>
 
 #include "sgx_kernels.cuh"
 #include "sgx_launch.hpp"
@@ -66,6 +67,11 @@ __global__ void k_cnf_words(const uint32_t* __restrict__ BT, int W, int64_t n, c
     ok &= any;
   }
   ok_out[w] = ok;
+}
+
+__global__ void k_iota(int64_t* __restrict__ v, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) v[i] = i;
 }
 
 __global__ void k_key_fp(const uint64_t* __restrict__ keys, int64_t n, int kw, uint64_t* __restrict__ fp) {
@@ -207,8 +213,10 @@ void verify_solutions(int device, const std::vector<int64_t>& cptr, const std::v
   const int64_t n = static_cast<int64_t>(line_of.size());
   // ---- device: CNF check (bit-sliced) + fingerprints, in row chunks
   std::vector<uint32_t> ok((n + 31) / 32, 0u);
-  std::vector<uint64_t> fp(n);
+  std::vector<uint64_t> sfp(n);  // fingerprints, sorted
+  std::vector<int64_t> srow(n);  // their rows (stable: ascending within a run)
   if (n > 0) {
+    if (n > (int64_t{1} << 31) - 1) throw std::invalid_argument("too many solutions for one verify call");
     ck(cudaSetDevice(device), "cudaSetDevice");
     cudaStream_t st;
     ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "verify stream");
@@ -218,12 +226,16 @@ void verify_solutions(int device, const std::vector<int64_t>& cptr, const std::v
     const int64_t R = std::min<int64_t>(n, int64_t{1} << 16);  // rows per chunk
     const int Wc = static_cast<int>((R + 31) / 32);
     int *dptr = nullptr, *denc = nullptr;
-    uint64_t *dkeys = nullptr, *dfp = nullptr;
+    uint64_t *dkeys = nullptr, *dfp = nullptr, *dfp2 = nullptr;
+    int64_t *drow = nullptr, *drow2 = nullptr;
     uint32_t *dbt = nullptr, *dok = nullptr;
     ck(cudaMallocAsync(&dptr, p32.size() * sizeof(int), st), "verify alloc");
     ck(cudaMallocAsync(&denc, std::max<size_t>(1, enc.size()) * sizeof(int), st), "verify alloc");
     ck(cudaMallocAsync(&dkeys, static_cast<size_t>(R) * kw * sizeof(uint64_t), st), "verify alloc");
-    ck(cudaMallocAsync(&dfp, static_cast<size_t>(R) * sizeof(uint64_t), st), "verify alloc");
+    ck(cudaMallocAsync(&dfp, static_cast<size_t>(n) * sizeof(uint64_t), st), "verify alloc");
+    ck(cudaMallocAsync(&dfp2, static_cast<size_t>(n) * sizeof(uint64_t), st), "verify alloc");
+    ck(cudaMallocAsync(&drow, static_cast<size_t>(n) * sizeof(int64_t), st), "verify alloc");
+    ck(cudaMallocAsync(&drow2, static_cast<size_t>(n) * sizeof(int64_t), st), "verify alloc");
     ck(cudaMallocAsync(&dbt, static_cast<size_t>(std::max(1, num_vars)) * Wc * sizeof(uint32_t), st), "verify alloc");
     ck(cudaMallocAsync(&dok, static_cast<size_t>(Wc) * sizeof(uint32_t), st), "verify alloc");
     ck(cudaMemcpyAsync(dptr, p32.data(), p32.size() * sizeof(int), cudaMemcpyHostToDevice, st), "verify h2d");
@@ -237,15 +249,24 @@ void verify_solutions(int device, const std::vector<int64_t>& cptr, const std::v
       const long long warps = static_cast<long long>(W) * kw;
       k_keys_to_bt<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(dkeys, m, kw, num_vars, W, dbt);
       k_cnf_words<<<(W + 127) / 128, 128, 0, st>>>(dbt, W, m, dptr, denc, nc, dok);
-      k_key_fp<<<static_cast<unsigned>((m + 255) / 256), 256, 0, st>>>(dkeys, m, kw, dfp);
+      k_key_fp<<<static_cast<unsigned>((m + 255) / 256), 256, 0, st>>>(dkeys, m, kw, dfp + r0);
       ck(cudaMemcpyAsync(ok.data() + r0 / 32, dok, W * sizeof(uint32_t), cudaMemcpyDeviceToHost, st), "verify d2h");
-      ck(cudaMemcpyAsync(fp.data() + r0, dfp, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, st), "verify d2h");
       ck(cudaStreamSynchronize(st), "verify sync");  // the key chunk buffer is reused
       out->launches += 3;
     }
+    k_iota<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(drow, n);
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dfp, dfp2, drow, drow2, static_cast<int>(n), 0, 64, st);
+    void* tmp = nullptr;
+    ck(cudaMallocAsync(&tmp, std::max<size_t>(1, tmp_bytes), st), "verify alloc");
+    cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, dfp, dfp2, drow, drow2, static_cast<int>(n), 0, 64, st);
+    ck(cudaMemcpyAsync(sfp.data(), dfp2, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st), "verify d2h");
+    ck(cudaMemcpyAsync(srow.data(), drow2, n * sizeof(int64_t), cudaMemcpyDeviceToHost, st), "verify d2h");
+    out->launches += 3;
     ck(cudaGetLastError(), "verify kernels");
     for (void* p : {static_cast<void*>(dptr), static_cast<void*>(denc), static_cast<void*>(dkeys),
-                    static_cast<void*>(dfp), static_cast<void*>(dbt), static_cast<void*>(dok)})
+                    static_cast<void*>(dfp), static_cast<void*>(dbt), static_cast<void*>(dok),
+                    static_cast<void*>(dfp2), static_cast<void*>(drow), static_cast<void*>(drow2), tmp})
       cudaFreeAsync(p, st);
     ck(cudaStreamSynchronize(st), "verify free");
     cudaStreamDestroy(st);
@@ -253,33 +274,27 @@ void verify_solutions(int device, const std::vector<int64_t>& cptr, const std::v
   // ---- first unsatisfied row, first duplicate row (of an earlier, valid row)
   int64_t bad = n;
   int bad_kind = 0;
-  std::unordered_map<uint64_t, int64_t> first;  // fingerprint -> first row (chain on collision below)
-  std::unordered_multimap<uint64_t, int64_t> more;
-  first.reserve(static_cast<size_t>(n) * 2);
-  for (int64_t r = 0; r < n; ++r) {
+  for (int64_t r = 0; r < n; ++r)
     if (!((ok[r >> 5] >> (r & 31)) & 1u)) {
       bad = r;
       bad_kind = 5;
       break;
     }
-    const uint64_t* k = keys.data() + r * kw;
-    auto it = first.find(fp[r]);
-    if (it == first.end()) {
-      first.emplace(fp[r], r);
-      continue;
+  // a row duplicates an earlier one iff an earlier member of its fingerprint
+  // run has the same key; only rows before the first error matter
+  for (int64_t a = 0; a < n;) {
+    int64_t b = a + 1;
+    while (b < n && sfp[b] == sfp[a]) ++b;
+    for (int64_t j = a + 1; j < b && srow[j] < bad; ++j) {
+      const uint64_t* kj = keys.data() + srow[j] * kw;
+      for (int64_t i = a; i < j; ++i)
+        if (std::memcmp(keys.data() + srow[i] * kw, kj, kw * sizeof(uint64_t)) == 0) {
+          bad = srow[j];
+          bad_kind = 6;
+          break;
+        }
     }
-    bool dup = std::memcmp(keys.data() + it->second * kw, k, kw * sizeof(uint64_t)) == 0;
-    if (!dup) {
-      auto range = more.equal_range(fp[r]);
-      for (auto j = range.first; j != range.second && !dup; ++j)
-        dup = std::memcmp(keys.data() + j->second * kw, k, kw * sizeof(uint64_t)) == 0;
-      if (!dup) more.emplace(fp[r], r);
-    }
-    if (dup) {
-      bad = r;
-      bad_kind = 6;
-      break;
-    }
+    a = b;
   }
   if (bad < n) {  // a row error precedes any parse error (rows stop before it)
     out->checked = bad;
