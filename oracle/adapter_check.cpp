@@ -85,6 +85,22 @@ int main(int argc, char** argv) {
     double a = cpu.stats.loss_trace[i], b = gpu.stats.loss_trace[i];
     expect(std::fabs(a - b) <= 1e-4 * std::fmax(std::fabs(a), 1e-30), "loss_trace value");
   }
+  // satgrad_b200::verify (cmd_verify on the GPU) on the reference's own text:
+  // all lines pass; a repeated first line is a duplicate one line past the end
+  {
+    const std::string text = satgrad::format_solutions(cpu.solutions);
+    std::string msg;
+    long long checked = -1;
+    const int k = satgrad_b200::verify(cnf, text, &msg, &checked);
+    expect(k == 0 && checked == cpu.stats.unique_count, "verify of the reference's solutions");
+    if (cpu.stats.unique_count > 0) {
+      const std::string dup = text + text.substr(0, text.find('\n') + 1);
+      const int k2 = satgrad_b200::verify(cnf, dup, &msg, &checked);
+      expect(k2 == 6 && checked == cpu.stats.unique_count &&
+                 msg == std::to_string(cpu.stats.unique_count + 1) + ": duplicate assignment",
+             "verify duplicate");
+    }
+  }
   std::printf("%s: %lld unique (cpu %.3f s, b200 %.3f s)\n", bad ? "adapter MISMATCH" : "adapter ok",
               static_cast<long long>(gpu.stats.unique_count), cpu.stats.wall_time_s, gpu.stats.wall_time_s);
   return bad ? 1 : 0;
