@@ -43,48 +43,60 @@ constexpr int kMaxTT = 16;  // kMaxTruthTableVars, truth_table.hpp
 // Bit r of a table over n variables is the function at the assignment whose
 // variable i is (r >> i) & 1 (truth_table.hpp).
 struct TT {
+  // one inline word for <= 6 variables (nearly every table), heap words above
   int n = 0;
-  std::vector<uint64_t> w;
-  explicit TT(int nv = 0) : n(nv), w(nv <= 6 ? 1 : size_t{1} << (nv - 6), 0) {}
+  size_t nw = 1;
+  uint64_t one = 0;
+  std::vector<uint64_t> big;
+  explicit TT(int nv = 0) : n(nv), nw(nv <= 6 ? 1 : size_t{1} << (nv - 6)) {
+    if (nw > 1) big.assign(nw, 0);
+  }
+  uint64_t* w() { return nw == 1 ? &one : big.data(); }
+  const uint64_t* w() const { return nw == 1 ? &one : big.data(); }
   uint64_t top() const { return n >= 6 ? ~0ull : ((1ull << (1u << n)) - 1ull); }
-  void mask() { w.back() &= top(); }
+  void mask() { w()[nw - 1] &= top(); }
   static TT var(int nv, int i) {
     static const uint64_t pat[6] = {0xAAAAAAAAAAAAAAAAull, 0xCCCCCCCCCCCCCCCCull, 0xF0F0F0F0F0F0F0F0ull,
                                     0xFF00FF00FF00FF00ull, 0xFFFF0000FFFF0000ull, 0xFFFFFFFF00000000ull};
     TT t(nv);
-    for (size_t j = 0; j < t.w.size(); ++j) t.w[j] = i < 6 ? pat[i] : (((j >> (i - 6)) & 1) ? ~0ull : 0ull);
+    uint64_t* x = t.w();
+    for (size_t j = 0; j < t.nw; ++j) x[j] = i < 6 ? pat[i] : (((j >> (i - 6)) & 1) ? ~0ull : 0ull);
     t.mask();
     return t;
   }
   void flip() {
-    for (auto& x : w) x = ~x;
+    uint64_t* x = w();
+    for (size_t j = 0; j < nw; ++j) x[j] = ~x[j];
     mask();
   }
   bool zero() const {
-    for (auto x : w)
-      if (x) return false;
+    const uint64_t* x = w();
+    for (size_t j = 0; j < nw; ++j)
+      if (x[j]) return false;
     return true;
   }
   bool ones() const {
-    for (size_t j = 0; j + 1 < w.size(); ++j)
-      if (w[j] != ~0ull) return false;
-    return w.back() == top();
+    const uint64_t* x = w();
+    for (size_t j = 0; j + 1 < nw; ++j)
+      if (x[j] != ~0ull) return false;
+    return x[nw - 1] == top();
   }
   bool complement_of(const TT& o) const {
-    for (size_t j = 0; j + 1 < w.size(); ++j)
-      if ((w[j] ^ o.w[j]) != ~0ull) return false;
-    return (w.back() ^ o.w.back()) == top();
+    const uint64_t *x = w(), *y = o.w();
+    for (size_t j = 0; j + 1 < nw; ++j)
+      if ((x[j] ^ y[j]) != ~0ull) return false;
+    return (x[nw - 1] ^ y[nw - 1]) == top();
   }
-  bool operator==(const TT& o) const { return w == o.w; }
-  bool bit(uint32_t r) const { return (w[r >> 6] >> (r & 63)) & 1ull; }
+  bool operator==(const TT& o) const { return nw == o.nw && std::equal(w(), w() + nw, o.w()); }
+  bool bit(uint32_t r) const { return (w()[r >> 6] >> (r & 63)) & 1ull; }
   uint32_t rows() const { return 1u << n; }
 };
 
 TT parity_tt(int nv) {
   TT t(nv);
   for (int i = 0; i < nv; ++i) {
-    TT v = TT::var(nv, i);
-    for (size_t j = 0; j < t.w.size(); ++j) t.w[j] ^= v.w[j];
+    const TT v = TT::var(nv, i);
+    for (size_t j = 0; j < t.nw; ++j) t.w()[j] ^= v.w()[j];
   }
   return t;
 }
@@ -238,8 +250,10 @@ class Exprs {
         TT acc = table(kids(e)[0], vars);
         for (int i = 1; i < nkids(e); ++i) {
           const TT t = table(kids(e)[i], vars);
-          for (size_t j = 0; j < acc.w.size(); ++j)
-            acc.w[j] = kind(e) == kAnd ? (acc.w[j] & t.w[j]) : kind(e) == kOr ? (acc.w[j] | t.w[j]) : (acc.w[j] ^ t.w[j]);
+          uint64_t* x = acc.w();
+          const uint64_t* y = t.w();
+          for (size_t j = 0; j < acc.nw; ++j)
+            x[j] = kind(e) == kAnd ? (x[j] & y[j]) : kind(e) == kOr ? (x[j] | y[j]) : (x[j] ^ y[j]);
         }
         if (kind(e) == kXnor) acc.flip();
         return acc;
@@ -803,9 +817,9 @@ class Extractor {
           const int i = static_cast<int>(std::lower_bound(s.begin(), s.end(), std::abs(l)) - s.begin());
           TT x = TT::var(n, i);
           if (l < 0) x.flip();
-          for (size_t j = 0; j < d.w.size(); ++j) d.w[j] |= x.w[j];
+          for (size_t j = 0; j < d.nw; ++j) d.w()[j] |= x.w()[j];
         }
-        for (size_t j = 0; j < t.w.size(); ++j) t.w[j] &= d.w[j];
+        for (size_t j = 0; j < t.nw; ++j) t.w()[j] &= d.w()[j];
       }
       return t;
     };
