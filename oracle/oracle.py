@@ -62,6 +62,8 @@ class RefLib:
             L.ref_last_error.restype = C.c_char_p
             L.ref_from_dimacs.restype = C.c_void_p
             L.ref_from_dimacs.argtypes = [C.c_char_p]
+            L.ref_from_dimacs_cfg.restype = C.c_void_p
+            L.ref_from_dimacs_cfg.argtypes = [C.c_char_p, C.c_int, C.c_int]
             L.ref_generate.restype = C.c_void_p
             L.ref_generate.argtypes = [C.c_int, _i64p]
             L.ref_free.argtypes = [C.c_void_p]
@@ -214,6 +216,10 @@ class RefInstance:
     @classmethod
     def from_dimacs(cls, text: str) -> "RefInstance":
         return cls(RefLib().L.ref_from_dimacs(text.encode()))
+
+    @classmethod
+    def from_dimacs_cfg(cls, text: str, complement_cap: int, minimize_cap: int) -> "RefInstance":
+        return cls(RefLib().L.ref_from_dimacs_cfg(text.encode(), complement_cap, minimize_cap))
 
     @classmethod
     def random_circuit(cls, seed, inputs, levels, gpl, outs) -> "RefInstance":

@@ -48,10 +48,10 @@ struct RefInst {
   bool has_run = false;
 };
 
-RefInst* finish(CnfFormula cnf) {
+RefInst* finish(CnfFormula cnf, const ExtractorConfig& cfg = {}) {
   auto inst = std::make_unique<RefInst>();
   inst->cnf = std::move(cnf);
-  inst->res = extract(inst->cnf);
+  inst->res = extract(inst->cnf, cfg);
   inst->circuit = build(inst->res);
   inst->paths = classify_paths(inst->res);
   int max_var = inst->circuit.num_vars;
@@ -191,6 +191,16 @@ const char* ref_last_error() { return g_err.c_str(); }
 void* ref_from_dimacs(const char* text) {
   GUARD_BEGIN
   return finish(parse_dimacs(text));
+  GUARD_END(nullptr)
+}
+
+// The same with a non-default ExtractorConfig (extract.hpp:14-17).
+void* ref_from_dimacs_cfg(const char* text, int complement_cap, int minimize_cap) {
+  GUARD_BEGIN
+  ExtractorConfig cfg;
+  cfg.complement_cap = complement_cap;
+  cfg.minimize_cap = minimize_cap;
+  return finish(parse_dimacs(text), cfg);
   GUARD_END(nullptr)
 }
 

@@ -159,3 +159,23 @@ def test_reference_adapter_extract_drop_in(tmp_path, name):
     cnf.write_bytes(gzip.open(os.path.join(DATA_DIR, f"{name}.cnf.gz")).read())
     r = subprocess.run([exe, str(cnf), "--extract-only"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "extract ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("ccap,mcap", [(0, 12), (2, 0), (4, 2), (8, 6), (16, 16), (40, 12)])
+def test_extract_caps_match_reference(ccap, mcap):
+    """Non-default ExtractorConfig (extract.hpp:14-17): the complement-check cap
+    (clamped to the 16-variable truth-table limit, boolexpr.cpp:271-283) and
+    the two-level minimisation cap change which definitions are found and how
+    they are simplified; the circuit must still match the reference's."""
+    from oracle.oracle import RefInstance, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    cnfs = [load_instance(n).cnf for n in ("c1b_random", "mux_chain14", "c3a_or50")]
+    rng = np.random.default_rng(ccap * 31 + mcap)
+    cnfs += [_random_cnf(rng, int(rng.integers(5, 30)), int(rng.integers(5, 80))) for _ in range(8)]
+    for cnf in cnfs:
+        text = write_dimacs(cnf)
+        ref = RefInstance.from_dimacs_cfg(text, ccap, mcap)
+        r = extract_circuit(parse_dimacs(text), complement_cap=ccap, minimize_cap=mcap)
+        _same(r.circuit, ref)
+        assert r.unsat == ref.unsat and r.unsat_note == ref.unsat_note
