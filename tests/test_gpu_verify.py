@@ -112,3 +112,26 @@ def test_verify_from_cnf_alone(gpu):
         t = "\n".join(ls) + "\n"
         a, b = verify_solutions(inst.cnf, t), dc.verify_solutions(t)
         assert (a["checked"], a["line"], a["kind"], a["var"]) == (b["checked"], b["line"], b["kind"], b["var"])
+
+
+def test_full_size_format_verify_round_trip(gpu):
+    """BASELINE's headline configuration (C2, B = 65,536, 5 iterations): every
+    stored solution, rendered as the reference's text on the device, passes
+    the device verify -- satisfying, complete, pairwise distinct -- and the
+    count verified is the run's unique count (a size-independent property)."""
+    from paper_2502_08673_b200 import verify_solutions
+    inst = load_instance("c2_iscas")
+    dc = DeviceCircuit.from_instance(inst)
+    s = Sampler(dc, SamplerConfig(batch=65536, iterations=5, seed=1))
+    try:
+        st = s.run()
+        text = s.format_solutions()
+        v = verify_solutions(inst.cnf, text)
+        assert v["ok"] and v["checked"] == st.unique_count > 10000, v
+        # the last line repeated is reported one line past the end, like the reference
+        last = text[text.rstrip(b"\n").rfind(b"\n") + 1:]
+        v2 = dc.verify_solutions(text + last)
+        assert v2["kind"] == 6 and v2["line"] == st.unique_count + 1 and v2["checked"] == st.unique_count
+    finally:
+        s.close()
+        dc.close()
