@@ -276,6 +276,69 @@ struct sgx_circuit {
   DBuf<int2> lb_cpi, lb_ucpi;
 };
 
+// Streams and events of a sampler, pooled per (device, priority): creating
+// and destroying 2 streams and 23 events per sampler costs a few hundred
+// microseconds, a third of a quota-1000 run end to end.  A kit is returned
+// only after both streams were synchronised, so every event in it has
+// completed and a wait on one is a no-op for the next owner.
+struct StreamKit {
+  int device = -1;
+  bool prio = false;
+  cudaStream_t st = nullptr, sh = nullptr;
+  cudaEvent_t ev[8] = {}, sev[2][4] = {}, soft = nullptr, front = nullptr, join = nullptr, run[4] = {};
+};
+std::mutex g_kit_mu;
+std::vector<StreamKit> g_kits;
+
+StreamKit kit_take(int device, bool prio, int prio_lo, int prio_hi) {
+  {
+    std::lock_guard<std::mutex> lk(g_kit_mu);
+    for (size_t i = 0; i < g_kits.size(); ++i)
+      if (g_kits[i].device == device && g_kits[i].prio == prio) {
+        StreamKit k = g_kits[i];
+        g_kits.erase(g_kits.begin() + static_cast<long>(i));
+        return k;
+      }
+  }
+  StreamKit k;
+  k.device = device;
+  k.prio = prio;
+  CK(cudaStreamCreateWithPriority(&k.st, cudaStreamNonBlocking, prio ? prio_hi : prio_lo));
+  CK(cudaStreamCreateWithPriority(&k.sh, cudaStreamNonBlocking, prio_lo));
+  for (auto& e : k.ev) CK(cudaEventCreate(&e));
+  for (auto& row : k.sev)
+    for (auto& e : row) CK(cudaEventCreate(&e));
+  for (auto& e : k.run) CK(cudaEventCreate(&e));
+  for (auto* e : {&k.soft, &k.front, &k.join}) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  return k;
+}
+
+void kit_destroy(StreamKit& k) {
+  for (auto& e : k.ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& row : k.sev)
+    for (auto& e : row)
+      if (e) cudaEventDestroy(e);
+  for (auto& e : k.run)
+    if (e) cudaEventDestroy(e);
+  for (auto e : {k.soft, k.front, k.join})
+    if (e) cudaEventDestroy(e);
+  if (k.st) cudaStreamDestroy(k.st);
+  if (k.sh) cudaStreamDestroy(k.sh);
+}
+
+// Return a kit whose streams are idle; at most 4 are kept per process.
+void kit_give(StreamKit k) {
+  {
+    std::lock_guard<std::mutex> lk(g_kit_mu);
+    if (g_kits.size() < 4) {
+      g_kits.push_back(k);
+      return;
+    }
+  }
+  kit_destroy(k);
+}
+
 struct sgx_sampler {
   sgx_circuit* c = nullptr;
   sgx_sampler_cfg cfg{};
@@ -307,6 +370,8 @@ struct sgx_sampler {
   cudaStream_t sh = nullptr;
   cudaEvent_t ev_soft = nullptr, ev_front = nullptr, ev_join = nullptr;
   cudaEvent_t sev[2][4] = {};  // per step parity: fwd begin / end, bwd begin / end
+  cudaEvent_t rev[4] = {};     // sampler_run's init / run brackets
+  bool kit_prio = false;
   DBuf<double> dloss;          // per step parity: loss total (sum over rows)
   double* hloss = nullptr;     // pinned copies of dloss (sgx_step_async / sgx_step_loss)
   long long steps = 0;         // steps launched (parity of the next)
@@ -734,11 +799,7 @@ void sampler_run(sgx_sampler* s) {
   const int max_restarts = cfg.max_restarts > 0 ? cfg.max_restarts : 1000;
   const bool per_row = cfg.restart_policy == SGX_RESTART_REINIT_ROWS;
   bool timed_out = false;
-  cudaEvent_t e0, e1, r0, r1;
-  CK(cudaEventCreate(&e0));
-  CK(cudaEventCreate(&e1));
-  CK(cudaEventCreate(&r0));
-  CK(cudaEventCreate(&r1));
+  cudaEvent_t e0 = s->rev[0], e1 = s->rev[1], r0 = s->rev[2], r1 = s->rev[3];
   CK(cudaEventRecord(r0, s->st));
   for (int restart = 0;; ++restart) {
     CK(cudaEventRecord(e0, s->st));
@@ -808,10 +869,6 @@ void sampler_run(sgx_sampler* s) {
                  "run wall %.2f ms\n", s->stats.device_ms, s->host_ms[0], s->host_ms[1],
                  s->host_ms[2], s->phase_ms[0], s->phase_ms[1], s->phase_ms[2], s->host_ms[3], s->host_ms[4],
                  s->host_ms[5], 1000.0 * now_s());
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaEventDestroy(r0);
-  cudaEventDestroy(r1);
   s->stats.timed_out = timed_out ? 1 : 0;
   s->stats.unique_count = s->n_solutions;
   s->stats.wall_time_s = now_s();
@@ -972,12 +1029,18 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
     CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     const char* pe = std::getenv("SGX_PRIO");
     const bool prio = pe && pe[0] == '1';
-    CK(cudaStreamCreateWithPriority(&s->st, cudaStreamNonBlocking, prio ? prio_hi : prio_lo));
-    CK(cudaStreamCreateWithPriority(&s->sh, cudaStreamNonBlocking, prio_lo));
-    for (auto& e : s->ev) CK(cudaEventCreate(&e));
-    for (auto& row : s->sev)
-      for (auto& e : row) CK(cudaEventCreate(&e));
-    for (auto* e : {&s->ev_soft, &s->ev_front, &s->ev_join}) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    {
+      StreamKit k = kit_take(c->ctx->device, prio, prio_lo, prio_hi);
+      s->kit_prio = prio;
+      s->st = k.st;
+      s->sh = k.sh;
+      std::copy(k.ev, k.ev + 8, s->ev);
+      for (int p = 0; p < 2; ++p) std::copy(k.sev[p], k.sev[p] + 4, s->sev[p]);
+      std::copy(k.run, k.run + 4, s->rev);
+      s->ev_soft = k.soft;
+      s->ev_front = k.front;
+      s->ev_join = k.join;
+    }
     // Nothing recorded yet: a wait on a never-recorded event is a no-op.
     s->dloss.alloc_async(2, s->st);  // pool memory: freed without cudaFree's device sync
     static_assert(sizeof(sgx::HarvestOut) <= kPinSlot, "pinned slot too small");
@@ -1128,19 +1191,22 @@ int sgx_sampler_free(sgx_sampler* s) {
     const double t_reset = ms();
     if (st) cudaStreamSynchronize(st);
     const double t_sync2 = ms();
-    for (auto& e : s->ev)
-      if (e) cudaEventDestroy(e);
-    for (auto& row : s->sev)
-      for (auto& e : row)
-        if (e) cudaEventDestroy(e);
-    for (auto e : {s->ev_soft, s->ev_front, s->ev_join})
-      if (e) cudaEventDestroy(e);
+    StreamKit k;
+    k.device = s->c->ctx->device;
+    k.prio = s->kit_prio;
+    k.st = s->st;
+    k.sh = s->sh;
+    std::copy(s->ev, s->ev + 8, k.ev);
+    for (int p = 0; p < 2; ++p) std::copy(s->sev[p], s->sev[p] + 4, k.sev[p]);
+    std::copy(s->rev, s->rev + 4, k.run);
+    k.soft = s->ev_soft;
+    k.front = s->ev_front;
+    k.join = s->ev_join;
     pin_release(s->hpin);  // (the streams were synchronised above)
     pin_release(s->hloss);
-    cudaStream_t sh = s->sh;
     delete s;
-    if (st) cudaStreamDestroy(st);
-    if (sh) cudaStreamDestroy(sh);
+    if (k.st && k.sh) kit_give(k);  // both streams idle: every event has completed
+    else kit_destroy(k);
     if (std::getenv("SGX_TRACE"))
       std::fprintf(stderr, "[sgx] sampler free: harvest sync %.2f, drain %.2f, frees %.2f, stream sync %.2f, total %.2f ms\n",
                    t_sync, t_drain, t_reset, t_sync2, ms());
