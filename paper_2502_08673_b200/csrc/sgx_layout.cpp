@@ -820,15 +820,18 @@ Layout build_layout(const sgx_circuit_desc& d) {
   // programs below read the validated inputs only and write disjoint fields:
   // the first two are compiled on their own threads.
   L.key_words = (L.num_vars + 63) / 64;
+  // (inline below 4096 nodes: there, three thread spawns cost more than the work)
+  const bool par = n >= 4096;
+  auto spawn = [par](auto&& f) { return par ? std::thread(f) : (f(), std::thread()); };
   std::exception_ptr err_soft, err_live;
-  std::thread t_soft([&] {
+  std::thread t_soft = spawn([&] {
     try {
       L.cone = build_soft(L, cone);
     } catch (...) {
       err_soft = std::current_exception();
     }
   });
-  std::thread t_live([&] {
+  std::thread t_live = spawn([&] {
     try {
       build_live_bits(L);
     } catch (...) {
@@ -836,7 +839,7 @@ Layout build_layout(const sgx_circuit_desc& d) {
     }
   });
   std::exception_ptr err_fold;
-  std::thread t_fold([&] {
+  std::thread t_fold = spawn([&] {
     try {
       build_folded_bits(L);
     } catch (...) {
@@ -893,9 +896,9 @@ Layout build_layout(const sgx_circuit_desc& d) {
   L.key_bit_row.assign(static_cast<size_t>(L.key_words) * 64, -1);
   for (int v = 1; v <= L.num_vars; ++v) L.key_bit_row[v - 1] = L.bit_row_of_node[L.node_of_var[v]];
   lap("bits");
-  t_soft.join();
-  t_live.join();
-  t_fold.join();
+  if (t_soft.joinable()) t_soft.join();
+  if (t_live.joinable()) t_live.join();
+  if (t_fold.joinable()) t_fold.join();
   lap("threads join");
   if (err_soft) std::rethrow_exception(err_soft);
   if (err_live) std::rethrow_exception(err_live);
