@@ -108,8 +108,18 @@ typedef struct {
   int64_t row_offset;      /* global row of local row 0 (RNG coordinates)*/
   int64_t solution_capacity; /* initial device solution store, 0 = auto  */
   int32_t max_restarts;    /* safety valve, reference uses 1000          */
-  int32_t reserved;
+  int32_t soft_kernel;     /* sgx_soft_kernel: which soft-pass kernels    */
 } sgx_sampler_cfg;
+
+/* Soft pass (embed + forward + loss + backward + GD + harden) kernels.  All
+ * are bit-identical; they differ only in speed.
+ *   AUTO: small circuits (cone tape <= 1,536 rows) get a circuit-specialised
+ *         kernel compiled at run time (NVRTC, sm_100a) on a worker thread;
+ *         steps run the HBM-tape kernels until it is ready.  Env SGX_JIT=0
+ *         disables it, SGX_JIT=sync waits for the compile.
+ *   HBM:  the level-synchronous tape kernels only.
+ *   JIT:  compile at sampler creation and wait (HBM kernels if ineligible). */
+enum sgx_soft_kernel { SGX_SOFT_AUTO = 0, SGX_SOFT_HBM = 1, SGX_SOFT_JIT = 2 };
 
 typedef struct {
   int64_t unique_count;
@@ -143,8 +153,17 @@ int sgx_circuit_free(sgx_circuit* c);
  * device program construction sgx_circuit_upload performs.  For CPU tests. */
 int sgx_layout_stats(const sgx_circuit_desc* desc, int64_t* info16);
 
+/* Source of the circuit-specialised soft-pass kernel (host only, no device
+ * calls; SGX_E_INVALID if the circuit is not eligible).  *len = bytes incl.
+ * the NUL; out = NULL only sizes. */
+int sgx_jit_source(const sgx_circuit_desc* desc, char* out, int64_t cap, int64_t* len);
+
 int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler** out);
 int sgx_sampler_free(sgx_sampler* s);
+/* info[0] soft kernel of the last step (0 HBM tape, 1 JIT, 2 on-chip),
+ * info[1] steps run by the JIT kernel, info[2] JIT state (-1 none,
+ * 0 compiling, 1 ready, 2 failed), info[3] its compile time in us. */
+int sgx_sampler_soft_info(const sgx_sampler* s, int64_t* info4);
 
 /* One restart's building blocks (what sgx_run loops over). */
 int sgx_init(sgx_sampler* s, int32_t restart);

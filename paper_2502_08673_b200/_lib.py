@@ -26,7 +26,7 @@ EXPORTS = [
     "sgx_set_host_stream", "sgx_solutions_take", "sgx_host_free", "sgx_step_async", "sgx_step_loss",
     "sgx_format_solutions", "sgx_launch_count", "sgx_extract", "sgx_extraction_sizes",
     "sgx_extraction_export", "sgx_extraction_note", "sgx_extraction_free", "sgx_verify_solutions",
-    "sgx_verify_cnf",
+    "sgx_verify_cnf", "sgx_jit_source", "sgx_sampler_soft_info",
 ]
 
 
@@ -53,7 +53,7 @@ class SamplerCfg(C.Structure):
         ("batch", C.c_int32), ("iterations", C.c_int32), ("learning_rate", C.c_double),
         ("seed", C.c_uint64), ("max_solutions", C.c_int64), ("timeout_s", C.c_double),
         ("restart_policy", C.c_int32), ("row_offset", C.c_int64),
-        ("solution_capacity", C.c_int64), ("max_restarts", C.c_int32), ("reserved", C.c_int32),
+        ("solution_capacity", C.c_int64), ("max_restarts", C.c_int32), ("soft_kernel", C.c_int32),
     ]
 
 
@@ -131,6 +131,8 @@ def load() -> C.CDLL:
         "sgx_extraction_free": (None, [vp]),
         "sgx_verify_solutions": (C.c_int, [vp, C.c_char_p, i64, i64p]),
         "sgx_verify_cnf": (C.c_int, [vp, i32, i64p, C.POINTER(i32), i64, C.c_char_p, i64, i64p]),
+        "sgx_jit_source": (C.c_int, [C.POINTER(CircuitDesc), C.c_char_p, i64, i64p]),
+        "sgx_sampler_soft_info": (C.c_int, [vp, i64p]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -17,6 +17,7 @@
 #include "../../include/satgrad_b200.h"
 #include "sgx_drain.hpp"
 #include "sgx_extract.hpp"
+#include "sgx_jit.hpp"
 #include "sgx_kernels.cuh"
 #include "sgx_launch.hpp"
 #include "sgx_layout.hpp"
@@ -274,6 +275,8 @@ struct sgx_circuit {
   DBuf<int4> lb_ops, lb_chk;
   DBuf<int> lb_op_ptr, lb_chk_ptr, lb_big, lb_key_enc;
   DBuf<int2> lb_cpi, lb_ucpi;
+  // circuit-specialised soft pass (sgx_jit.hpp), shared by its samplers
+  std::shared_ptr<sgx::JitKernel> jit;
 };
 
 // Streams and events of a sampler, pooled per (device, priority): creating
@@ -347,6 +350,10 @@ struct sgx_sampler {
   int hwpc = 0;  // words per CTA of the shared-memory harvest (0: global-memory path)
   int hlive = 0;  // words per CTA of the liveness-allocated harvest (0: not used)
   bool onchip = false;  // small circuit: fused on-chip soft pass (k_soft_onchip)
+  sgx::JitKernel* jit = nullptr;  // circuit-specialised soft pass (c->jit), once compiled
+  bool have_tape = false;         // tape / adjoint buffers allocated (HBM soft kernels usable)
+  int last_soft = 0;              // kernels of the last step: 0 HBM tape, 1 JIT, 2 on-chip
+  long long jit_steps = 0;        // steps run by the JIT kernel
   int hb_cur = 0;       // HB holds two buffers; the last init / step wrote this one
   DBuf<uint32_t> SP;  // its spill tape of CNF-variable rows [n_spill][W]
   DBuf<float> V, tape, adj, row_loss;
@@ -488,7 +495,19 @@ int sampler_step(sgx_sampler* s) {
   CK(cudaEventRecord(ev[0], s->st));
   const int ncpi = static_cast<int>(c->L.cpi.size());
   uint32_t* hb = hb_write(s);
-  if (s->onchip) {
+  if (s->jit && sgx::jit_ready(s->jit)) {
+    // circuit-specialised kernel: the whole soft pass in registers
+    if (harvest_reads_v(s)) CK(cudaStreamWaitEvent(s->st, s->ev_front, 0));
+    CK(cudaEventRecord(ev[1], s->st));
+    CK(cudaEventRecord(ev[2], s->st));
+    sgx::jit_launch(s->jit, s->st, s->V.p, 32 * s->vec, hb, s->row_loss.p, tab,
+                    static_cast<float>(s->cfg.learning_rate), s->Bp);
+    s->last_soft = 1;
+    ++s->jit_steps;
+  } else if (!s->have_tape && !s->onchip) {
+    throw StateError("soft pass: no kernel available (JIT not ready, no tape allocated)");
+  } else if (s->onchip) {
+    s->last_soft = 2;
     // forward + loss rows + backward + GD + harden in one kernel
     if (harvest_reads_v(s)) CK(cudaStreamWaitEvent(s->st, s->ev_front, 0));
     CK(cudaEventRecord(ev[1], s->st));
@@ -515,6 +534,7 @@ int sampler_step(sgx_sampler* s) {
     a.n_tiles = s->Bp / 32;
     if (!sgx::launch_soft_onchip(s->st, a)) throw CudaError("on-chip soft pass does not fit");
   } else {
+    s->last_soft = 0;
     sgx::launch_forward(s->st, s->vec, c->cone.fwd.p, c->cone.fwd_lvl.p, c->cone.n_fwd_levels, s->V.p, ncpi,
                         s->tape.p, c->cone.n_rows, s->Bp, 0, tab, &c->cone.fb);
     CK(cudaEventRecord(ev[1], s->st));
@@ -525,7 +545,7 @@ int sampler_step(sgx_sampler* s) {
              s->row_loss.p, tab, hb);
   }
   sgx::launch_loss(s->st, s->row_loss.p, s->cfg.batch, s->partial.p, s->n_partial, s->dloss.p + slot);
-  s->launches += 4;
+  s->launches += s->last_soft == 0 ? 4 : 3;
   if (s->hloss)
     CK(cudaMemcpyAsync(s->hloss + slot, s->dloss.p + slot, sizeof(double), cudaMemcpyDeviceToHost, s->st));
   CK(cudaEventRecord(ev[3], s->st));
@@ -934,6 +954,33 @@ int sgx_layout_stats(const sgx_circuit_desc* desc, int64_t* info16) {
   });
 }
 
+int sgx_jit_source(const sgx_circuit_desc* desc, char* out, int64_t cap, int64_t* len) {
+  return guard([&] {
+    need(desc, "desc");
+    need(len, "len");
+    sgx::Layout L = sgx::build_layout(*desc);
+    if (!sgx::jit_eligible(L)) throw std::invalid_argument("circuit is not eligible for the specialised soft pass");
+    const std::string src = sgx::jit_source(L);
+    *len = static_cast<int64_t>(src.size()) + 1;
+    if (out) {
+      if (cap < *len) throw std::invalid_argument("buffer too small");
+      std::memcpy(out, src.c_str(), src.size() + 1);
+    }
+  });
+}
+
+int sgx_sampler_soft_info(const sgx_sampler* s, int64_t* info4) {
+  return guard([&] {
+    need(s, "sampler");
+    need(info4, "info4");
+    const sgx::JitKernel* k = s->c->jit.get();
+    info4[0] = s->last_soft;
+    info4[1] = s->jit_steps;
+    info4[2] = !k ? -1 : (sgx::jit_ready(k) ? 1 : (sgx::jit_failed(k) ? 2 : 0));
+    info4[3] = k ? static_cast<int64_t>(sgx::jit_compile_ms(k) * 1000.0) : 0;
+  });
+}
+
 int sgx_circuit_upload(sgx_ctx* ctx, const sgx_circuit_desc* d, sgx_circuit** out) {
   return guard([&] {
     need(ctx, "ctx");
@@ -1072,6 +1119,19 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
                     sgx::onchip_warps(c->cone.n_rows, c->cone.oc_slots, c->cone.oc_n4) >= 2;
         if (s->onchip) s->vec = 1;
       }
+      // Circuit-specialised soft pass (sgx_jit.hpp) for small cones.
+      {
+        int mode = cfg->soft_kernel;
+        if (const char* e = std::getenv("SGX_JIT")) {
+          if (e[0] == '0') mode = SGX_SOFT_HBM;
+          else if (e[0] == 's') mode = SGX_SOFT_JIT;
+        }
+        if (mode != SGX_SOFT_HBM && !s->onchip && sgx::jit_eligible(L)) {
+          if (!c->jit) c->jit = sgx::jit_get(L, mode != SGX_SOFT_JIT);
+          if (mode == SGX_SOFT_JIT) sgx::jit_wait(c->jit.get());
+          if (!sgx::jit_failed(c->jit.get())) s->jit = c->jit.get();
+        }
+      }
       // Shared-memory harvest: the widest word block whose folded bit tape
       // fits ~100 KB (two CTAs per SM) while leaving >= 2 CTAs per SM of work;
       // one word (up to 200 KB) for deep circuits; else the global path.
@@ -1134,9 +1194,11 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       cudaStream_t st = s->st;
       s->V.alloc_async(L.cpi.size() * Bp, st);
       s->HB.alloc_async(2 * L.cpi.size() * s->W, st);
-      if (!s->onchip) {  // the on-chip pass keeps tape and adjoints in shared memory
+      // The on-chip and the (compiled) JIT passes keep tape and adjoints on chip.
+      if (!s->onchip && !(s->jit && sgx::jit_ready(s->jit))) {
         s->tape.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
         s->adj.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
+        s->have_tape = true;
       }
       s->row_loss.alloc_async(Bp, st);
       s->partial.alloc_async(s->n_partial, st);

@@ -22,6 +22,13 @@ from .circuit import Circuit, Instance, PathClassification
 from .cnf import CnfFormula, format_solution_line, key_to_assignment
 
 
+class SoftKernel(enum.IntEnum):
+    """Soft-pass kernels (sgx_soft_kernel); all are bit-identical."""
+    AUTO = 0  # circuit-specialised (NVRTC) kernel for small cones once compiled, else HBM tape
+    HBM = 1   # level-synchronous HBM-tape kernels only
+    JIT = 2   # compile the specialised kernel at sampler creation and wait for it
+
+
 class RestartPolicy(enum.IntEnum):
     NONE = 0
     REINIT_ON_EXHAUST = 1
@@ -44,6 +51,7 @@ class SamplerConfig:
     row_offset: int = 0       # global row of local row 0 (sample sharding)
     max_restarts: int = 1000  # sampler.cpp:180 safety valve
     solution_capacity: int = 0
+    soft_kernel: SoftKernel = SoftKernel.AUTO
 
 
 @dataclass
@@ -212,6 +220,20 @@ def layout_stats(cnf, circuit, paths, unsat=False) -> dict:
     return dict(zip(keys, (int(x) for x in out)))
 
 
+def jit_source(cnf, circuit, paths, unsat=False) -> str:
+    """CUDA source of the circuit-specialised soft pass (host only, no GPU)."""
+    L = _lib.load()
+    keep = [np.ascontiguousarray(x) for x in (
+        circuit.kind, circuit.a, circuit.b, circuit.var, circuit.out_var, circuit.out_tgt,
+        paths.constrained_pi, paths.unconstrained_pi, cnf.clause_ptr, cnf.clause_lit)]
+    d = make_desc(cnf, circuit, paths, unsat, keep)
+    n = C.c_int64()
+    _lib.check(L.sgx_jit_source(C.byref(d), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value)
+    _lib.check(L.sgx_jit_source(C.byref(d), buf, n.value, C.byref(n)))
+    return buf.value.decode()
+
+
 class Sampler:
     """sgx_sampler: device buffers for one batch shape + the run loop."""
 
@@ -233,6 +255,7 @@ class Sampler:
         c.row_offset = cfg.row_offset
         c.solution_capacity = cfg.solution_capacity
         c.max_restarts = cfg.max_restarts
+        c.soft_kernel = int(cfg.soft_kernel)
         self._cfg = c
         h = C.c_void_p()
         _lib.check(self.L.sgx_sampler_create(dc.h, C.byref(c), C.byref(h)))
@@ -258,6 +281,15 @@ class Sampler:
                         timed_out=bool(st.timed_out), note=note,
                         phase_ms=dict(zip(names, (float(x) for x in ph))),
                         device_ms=st.device_ms, launches=st.launches)
+
+    def soft_info(self) -> dict:
+        """Which soft-pass kernel ran the last step ("hbm" / "jit" / "onchip"),
+        steps run by the specialised kernel, its compile state and time."""
+        out = np.zeros(4, np.int64)
+        _lib.check(self.L.sgx_sampler_soft_info(self.h, _lib.ptr(out, C.c_int64)))
+        return {"last": ["hbm", "jit", "onchip"][int(out[0])], "jit_steps": int(out[1]),
+                "jit_state": {-1: "none", 0: "compiling", 1: "ready", 2: "failed"}[int(out[2])],
+                "jit_compile_ms": out[3] / 1000.0}
 
     def launch_count(self) -> int:
         """Kernels launched since the last run() (or creation)."""
