@@ -1,23 +1,30 @@
 #!/usr/bin/env python
 """Benchmark: unique valid SAT solutions per second (BASELINE.json metric).
 
-Workload (configs[1], SURVEY.md section 8 "C2"): the ISCAS89-shaped synthetic
-CNF encode(random_circuit(15850, 600, 40, 240, 7)) -- 10,200 vars, 31,685
-clauses, 21,895-node circuit -- sampled at batch 65,536 rows per GPU with the
-reference hyper-parameters (GD, lr 10, 5 iterations, seed 1, f32).
+Workload (default, the largest single-GPU config, BASELINE configs[3] /
+SURVEY.md section 8 "C4"): the blasted_case-shaped synthetic CNF
+encode(random_circuit(31337, 400, 400, 100, 2)) -- 40,400 vars, 132,151
+clauses, an 88,866-node circuit 877 levels deep -- sampled at batch 65,536
+rows per GPU with the reference hyper-parameters (GD, lr 10, 5 iterations,
+seed 1, f32).  --workload c2_iscas is configs[1] (ISCAS89-shaped), c3a_or50
+the or-50 shape of the time-to-1k metric.
 
 One "step" = one restart of satgrad::run: init_soft_inputs, the iteration-0
 harvest, then 5 x (embed+forward+loss+backward+GD, harvest) over the whole
 batch.  K steps run back to back inside one sgx_run (ReinitOnExhaust with a
-restart budget of K), W warm-up restarts before.  Inputs (tape 3.5 GB, V 135
-MB) exceed the 126 MB L2, so no explicit flush is needed between steps.
+restart budget of K), W warm-up restarts before.  Inputs (C4 tape 17.4 GB,
+C2 3.5 GB) exceed the 126 MB L2, so no explicit flush is needed between steps.
 
   value   unique solutions found in the timed restarts / device time
           (CUDA events on the sampler stream, max over ranks)
   e2e     the same metric through the public API run() from host buffers:
           circuit upload (H2D), the run, and fetching every solution key (D2H)
+  invalid solutions among the e2e result that fail the CNF, are malformed or
+          repeat (device re-verification after the timed region)
   --impl reference   the reference's own CPU sampler (oracle/_ref, built from
-          /root/reference sources) on the host cores.
+          /root/reference sources) on every host core, at the SAME workload,
+          batch and hyper-parameters, bounded by the reference's own
+          timeout_s.
 
 Multi-GPU (torchrun): rank g samples global rows [g*B, (g+1)*B) (RNG keyed by
 global row, so shards are disjoint slices of one big batch); solutions are
@@ -42,9 +49,9 @@ import numpy as np  # noqa: E402
 METRIC = "unique valid solutions/sec"
 UNIT = "solutions/s"
 WORKLOADS = {
-    # name: (instance file, default batch, reference-arm batch)
-    "c2_iscas": ("c2_iscas", 65536, 2048),
+    # name: (instance file, default batch, cpu_baseline sample batch)
     "c4_blasted": ("c4_blasted", 65536, 512),
+    "c2_iscas": ("c2_iscas", 65536, 2048),
     "c3a_or50": ("c3a_or50", 1 << 20, 20000),
     "c3b_or100": ("c3b_or100", 1 << 20, 20000),
     "c1b_random": ("c1b_random", 1024, 1024),
@@ -158,7 +165,7 @@ def cpu_reference(inst_name, batch, iterations, seed, steps=1, timeout_s=0.0, f3
     from oracle.oracle import PortLib, RefInstance, ref_available
     cores = os.cpu_count() or 1
     inst = load_instance(inst_name)
-    uniq, wall = 0, 0.0
+    uniq, wall, timed_out, attempts, new_unique = 0, 0.0, False, 0, []
     if ref_available():
         ri = RefInstance.from_dimacs(write_dimacs(inst.cnf))
         kind = "reference"
@@ -167,6 +174,9 @@ def cpu_reference(inst_name, batch, iterations, seed, steps=1, timeout_s=0.0, f3
                        use_f32=f32, timeout_s=timeout_s)
             uniq += r.unique
             wall += r.wall
+            timed_out |= r.timed_out
+            attempts += r.attempts
+            new_unique += r.new_unique
     else:
         kind, cores = "port", 1
         for _ in range(steps):
@@ -174,11 +184,16 @@ def cpu_reference(inst_name, batch, iterations, seed, steps=1, timeout_s=0.0, f3
                               timeout_s=timeout_s)
             uniq += r.unique
             wall += r.wall
+            timed_out |= r.timed_out
+            attempts += r.attempts
+            new_unique += r.new_unique
+    tmo = f", timeout_s={timeout_s:g}" if timeout_s > 0 else ""
     return {"value": uniq / wall if wall > 0 else 0.0, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"{steps} x satgrad::run(batch={batch}, iterations={iterations}, seed={seed}, "
-                      f"{'f32' if f32 else 'f64'}, threads={cores}) on {inst_name}: rows are independent, so unique/s "
-                      f"per row is batch-invariant; {uniq} unique in {wall:.2f} s",
-            "unique": uniq, "wall_s": wall}
+                      f"{'f32' if f32 else 'f64'}, threads={cores}{tmo}) on {inst_name}: {uniq} unique "
+                      f"in {wall:.2f} s" + (" (stopped by the timeout)" if timed_out else ""),
+            "unique": uniq, "wall_s": wall, "timed_out": timed_out, "attempts": attempts,
+            "new_unique": new_unique}
 
 
 def time_to_1k(dev, with_cpu=True, name="c3a_or50", batch=1 << 20):
@@ -220,20 +235,33 @@ def time_to_1k(dev, with_cpu=True, name="c3a_or50", batch=1 << 20):
 
 
 def run_reference_arm(args, world, rank):
-    name, batch, ref_batch = WORKLOADS[args.workload]
+    """The reference's satgrad::run on this box's host cores at the SAME
+    config as the B200 arm (workload, batch, iterations, lr, seed, f32).  One
+    run of the whole batch is minutes of CPU work (its harvest is single
+    threaded), so the K timed steps share ONE run bounded by
+    the reference's own timeout_s (checked before each iteration,
+    sampler.cpp:164-168), as SURVEY.md 8(d) prescribes; W warm-up steps are a
+    small run that pages the library and instance in."""
+    name, batch, sample_batch = WORKLOADS[args.workload]
     batch = args.batch or batch
     if rank != 0:
         return
-    for _ in range(args.warmup):
-        cpu_reference(name, ref_batch, args.iterations, 1, steps=1)
-    res = cpu_reference(name, ref_batch, args.iterations, 1, steps=args.steps)
+    if args.warmup > 0:
+        cpu_reference(name, 256, 1, 1, steps=1)
+    budget = float(os.environ.get("BENCH_REF_TIMEOUT", "120"))
+    res = cpu_reference(name, batch, args.iterations, 1, steps=1, timeout_s=budget)
     line = {
         "impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * res["wall_s"] / max(1, args.steps), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": name, "batch": batch, "iterations": args.iterations,
-                   "reference_sample_batch": ref_batch, "lr": 10.0, "seed": 1},
+        "config": {"workload": name, "batch": batch, "global_batch": batch * world,
+                   "iterations": args.iterations, "lr": 10.0, "seed": 1},
+        "reference_run": {"runs": 1, "timeout_s": budget, "timed_out": res["timed_out"],
+                          "attempts": res["attempts"], "new_unique": res["new_unique"],
+                          "wall_s": res["wall_s"],
+                          "note": "the K steps share one timeout-bounded satgrad::run of the full batch; "
+                                  "ms_per_step = its wall / K"},
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -320,16 +348,19 @@ def run_b200_arm(args, world, rank, local, dist):
         dist.barrier()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
+    e2e_keys = None
     if world == 1:
         res = run_instance(inst, e2e_cfg, device=dev)
         e2e_unique, d2h = res.stats.unique_count, res.solutions.keys.nbytes
+        e2e_keys = res.solutions.keys
     else:
         from paper_2502_08673_b200.dist import DeviceShard, TorchExchange, run_sharded
         dc2 = DeviceCircuit.from_instance(inst, device=dev)
         s2 = Sampler(dc2, e2e_cfg)
         sh2 = DeviceShard(s2)
         est = run_sharded(sh2, TorchExchange(device=f"cuda:{dev}"), e2e_cfg, rank, world, sh2.stride)
-        d2h = s2.fetch().nbytes
+        e2e_keys = s2.fetch()
+        d2h = e2e_keys.nbytes
         e2e_unique = est.unique_count
         s2.close()
         dc2.close()
@@ -340,6 +371,14 @@ def run_b200_arm(args, world, rank, local, dist):
         e2e_wall = float(t_e.item())
     h2d = sum(x.nbytes for x in (inst.kind, inst.a, inst.b, inst.var, inst.out_var, inst.out_tgt,
                                  inst.cpi, inst.ucpi, inst.clause_ptr, inst.clause_lit))
+    # 0 invalid: every solution the public API returned re-verified on the
+    # device against the CNF (and for duplicates), outside the timed region.
+    chk = dc.verify_keys(e2e_keys)
+    if dist:  # each rank stores the solutions it won: sum over ranks
+        t_i = torch.tensor([chk["invalid"], chk["checked"]], dtype=torch.float64, device=coll_dev)
+        dist.all_reduce(t_i, op=dist.ReduceOp.SUM)
+        chk["invalid"], chk["checked"] = int(t_i[0].item()), int(t_i[1].item())
+    del e2e_keys
     e2e = {"value": e2e_unique / e2e_wall, "unit": UNIT,
            "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
            "wall_s": e2e_wall}
@@ -392,6 +431,7 @@ def run_b200_arm(args, world, rank, local, dist):
                    "parallelism": f"sample-shard x{world}",
                    "l2": "inputs > L2 (tape %.1f GB)" % (4 * ncone * batch / 1e9)},
         "unique": global_unique, "restarts": restarts_done, "attempts": attempts,
+        "invalid": chk["invalid"], "verified": chk["checked"],
         "wall_s": wall, "device_s": device_s,
         "phase_ms": {k: round(v, 3) for k, v in ph.items()} if ph else None,
         "gpu_launches": launches,
@@ -410,7 +450,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="c2_iscas", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c4_blasted", choices=sorted(WORKLOADS))
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--iterations", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -253,6 +253,11 @@ int sgx_expf(sgx_ctx* ctx, const float* x, int64_t n, float* out);
  * terminator, 4 unassigned (err_var = first), 5 does not satisfy the formula,
  * 6 duplicate assignment.  checked = solutions verified before the error. */
 int sgx_verify_solutions(sgx_circuit* c, const char* text, int64_t len, int64_t* out);
+/* The same checks on packed keys ([n][key_words], dedupe_key layout, host
+ * memory), counting instead of stopping at the first error: out[0] checked,
+ * out[1] keys that do not satisfy the CNF, out[2] keys with bits above
+ * num_vars, out[3] keys equal to an earlier key, out[4] kernels launched. */
+int sgx_verify_keys(sgx_circuit* c, const uint64_t* keys, int64_t n, int64_t* out);
 /* The same from the CNF alone (what cmd_verify has): CSR clause_ptr[n_clauses
  * + 1] over DIMACS literals. */
 int sgx_verify_cnf(sgx_ctx* ctx, int32_t num_vars, const int64_t* clause_ptr, const int32_t* clause_lit,

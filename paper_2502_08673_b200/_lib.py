@@ -26,7 +26,7 @@ EXPORTS = [
     "sgx_set_host_stream", "sgx_solutions_take", "sgx_host_free", "sgx_step_async", "sgx_step_loss",
     "sgx_format_solutions", "sgx_launch_count", "sgx_extract", "sgx_extraction_sizes",
     "sgx_extraction_export", "sgx_extraction_note", "sgx_extraction_free", "sgx_verify_solutions",
-    "sgx_verify_cnf", "sgx_jit_source", "sgx_sampler_soft_info",
+    "sgx_verify_cnf", "sgx_jit_source", "sgx_sampler_soft_info", "sgx_verify_keys",
 ]
 
 
@@ -133,6 +133,7 @@ def load() -> C.CDLL:
         "sgx_verify_cnf": (C.c_int, [vp, i32, i64p, C.POINTER(i32), i64, C.c_char_p, i64, i64p]),
         "sgx_jit_source": (C.c_int, [C.POINTER(CircuitDesc), C.c_char_p, i64, i64p]),
         "sgx_sampler_soft_info": (C.c_int, [vp, i64p]),
+        "sgx_verify_keys": (C.c_int, [vp, u64p, i64, i64p]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -382,6 +382,7 @@ struct sgx_sampler {
   DBuf<double> dloss;          // per step parity: loss total (sum over rows)
   double* hloss = nullptr;     // pinned copies of dloss (sgx_step_async / sgx_step_loss)
   long long steps = 0;         // steps launched (parity of the next)
+  bool slot_pending[2] = {false, false};  // step slot launched, loss not read yet (sgx_step_loss)
   uint64_t epoch = 0;
   long long launches = 0;
   DBuf<sgx::HarvestOut> hout;
@@ -491,6 +492,7 @@ int sampler_step(sgx_sampler* s) {
   sgx_circuit* c = s->c;
   const uint64_t* tab = c->ctx->exp_tab.p;
   const int slot = static_cast<int>(s->steps++ & 1);
+  s->slot_pending[slot] = true;
   cudaEvent_t* ev = s->sev[slot];
   CK(cudaEventRecord(ev[0], s->st));
   const int ncpi = static_cast<int>(c->L.cpi.size());
@@ -960,7 +962,7 @@ int sgx_jit_source(const sgx_circuit_desc* desc, char* out, int64_t cap, int64_t
     need(len, "len");
     sgx::Layout L = sgx::build_layout(*desc);
     if (!sgx::jit_eligible(L)) throw std::invalid_argument("circuit is not eligible for the specialised soft pass");
-    const std::string src = sgx::jit_source(L);
+    const std::string src = sgx::jit_source(L, sgx::jit_min_blocks(L));
     *len = static_cast<int64_t>(src.size()) + 1;
     if (out) {
       if (cap < *len) throw std::invalid_argument("buffer too small");
@@ -1088,141 +1090,151 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       s->ev_front = k.front;
       s->ev_join = k.join;
     }
-    // Nothing recorded yet: a wait on a never-recorded event is a no-op.
-    s->dloss.alloc_async(2, s->st);  // pool memory: freed without cudaFree's device sync
-    static_assert(sizeof(sgx::HarvestOut) <= kPinSlot, "pinned slot too small");
-    s->hloss = static_cast<double*>(pin_slot());
-    s->hpin = static_cast<sgx::HarvestOut*>(pin_slot());
-    std::memset(s->hpin, 0, sizeof(sgx::HarvestOut));
-    s->hout.alloc_async(1, s->st);
-    CK(cudaStreamSynchronize(s->st));
-    if (c->layout_ok && !c->L.unsat) {
-      const auto& L = c->L;
-      s->Bp = round_up(cfg->batch, 1024);
-      s->W = s->Bp / 32;
-      s->wpc = s->W / 32 >= 2 * 148 ? 32 : (s->W / 16 >= 2 * 148 ? 16 : 8);
-      // Widest samples-per-thread that still leaves >= 3 tiles per SM
-      // (SGX_VEC overrides, for tuning).
-      s->vec = s->Bp / 128 >= 3 * 148 ? 4 : (s->Bp / 64 >= 3 * 148 ? 2 : 1);
-      if (const char* e = std::getenv("SGX_VEC")) {
-        int v = std::atoi(e);
-        if (v == 1 || v == 2 || v == 4) s->vec = v;
-      }
-      // SGX_ONCHIP=1: small circuits (>= 2 tiles of tape + adjoint slots per
-      // SM) run the fused on-chip soft pass on 32-sample tiles.  Opt-in:
-      // measured on C3a it is 2.3x SLOWER than the HBM-tape kernels (one
-      // sample per lane spends ~23k warp instructions per 32-sample tile on
-      // record control, at 8 warps per SM).
-      {
-        const char* e = std::getenv("SGX_ONCHIP");
-        s->onchip = e && e[0] == '1' && c->cone.oc_n4 > 0 &&
-                    sgx::onchip_warps(c->cone.n_rows, c->cone.oc_slots, c->cone.oc_n4) >= 2;
-        if (s->onchip) s->vec = 1;
-      }
-      // Circuit-specialised soft pass (sgx_jit.hpp) for small cones.
-      {
-        int mode = cfg->soft_kernel;
-        if (const char* e = std::getenv("SGX_JIT")) {
-          if (e[0] == '0') mode = SGX_SOFT_HBM;
-          else if (e[0] == 's') mode = SGX_SOFT_JIT;
-        }
-        if (mode != SGX_SOFT_HBM && !s->onchip && sgx::jit_eligible(L)) {
-          if (!c->jit) c->jit = sgx::jit_get(L, mode != SGX_SOFT_JIT);
-          if (mode == SGX_SOFT_JIT) sgx::jit_wait(c->jit.get());
-          if (!sgx::jit_failed(c->jit.get())) s->jit = c->jit.get();
-        }
-      }
-      // Shared-memory harvest: the widest word block whose folded bit tape
-      // fits ~100 KB (two CTAs per SM) while leaving >= 2 CTAs per SM of work;
-      // one word (up to 200 KB) for deep circuits; else the global path.
-      const size_t row_bytes = static_cast<size_t>(L.fb_rows + 1) * sizeof(uint32_t);
-      s->hwpc = 0;
-      // (<= 8 words: the CNF check keeps one accumulator pair per word in
-      // registers)
-      for (int w = 8; w >= 1; w /= 2)
-        if (row_bytes * w <= 100 * 1024 && s->W / w >= 2 * 148) {
-          s->hwpc = w;
-          break;
-        }
-      if (!s->hwpc && row_bytes <= 200 * 1024) s->hwpc = 1;
-      if (const char* e = std::getenv("SGX_HARVEST")) {
-        if (e[0] == 'g') s->hwpc = 0;  // force the global-memory harvest
-      }
-      if (const char* e = std::getenv("SGX_HWPC")) {  // A/B: words per harvest CTA
-        const int w = std::atoi(e);
-        if ((w == 1 || w == 2 || w == 4 || w == 8) && row_bytes * w <= 220 * 1024) s->hwpc = w;
-      }
-      // Liveness-allocated harvest (default): the words per CTA that keep the
-      // most words resident per SM (8 CTAs of 256 threads at most, ~227 KB of
-      // shared memory) with at least one CTA per SM; ties go to more words per
-      // CTA (per-level overhead amortised).  SGX_HARVEST=smem / g force the
-      // full-tape shared-memory / global-memory harvests.
-      s->hlive = 0;
-      {
-        const char* e = std::getenv("SGX_HARVEST");
-        const bool live_ok = !(e && (e[0] == 'g' || e[0] == 's'));
-        // words resident per SM for a tape of `rows` rows per word
-        auto best = [&](long long rows, int* wpc) {
-          int words = 0;
-          for (int w = 1; w <= 8; w *= 2) {
-            const size_t smem = static_cast<size_t>(rows) * w * sizeof(uint32_t) + 3 * 1024;
-            if (smem > 200 * 1024 || s->W / w < 148) continue;
-            const int ctas = std::min<int>(8, static_cast<int>((227 * 1024) / (smem + 1024)));
-            if (ctas * w >= words) {
-              words = ctas * w;
-              *wpc = w;
-            }
-          }
-          return words;
-        };
-        int wl = 0, wf = 0;
-        const int live_words = live_ok ? best(L.lb_slots, &wl) : 0;
-        const int full_words = best(L.fb_rows + 1, &wf);
-        // The full tape needs no spill round trip for the keys: it wins ties.
-        if (live_words > full_words) s->hlive = wl;
-        if (const char* v = std::getenv("SGX_LWPC")) {  // A/B: words per live-harvest CTA
-          const int w = std::atoi(v);
-          if ((w == 1 || w == 2 || w == 4 || w == 8) && live_ok &&
-              static_cast<size_t>(L.lb_slots) * w * 4 <= 200 * 1024)
-            s->hlive = w;
-        }
-        if (s->hlive) s->hwpc = 0;
-      }
-      // Stream-ordered pool allocations: a sampler created after another one
-      // reuses its memory without cudaMalloc / cudaFree round trips.
-      const size_t Bp = static_cast<size_t>(s->Bp);
-      cudaStream_t st = s->st;
-      s->V.alloc_async(L.cpi.size() * Bp, st);
-      s->HB.alloc_async(2 * L.cpi.size() * s->W, st);
-      // The on-chip and the (compiled) JIT passes keep tape and adjoints on chip.
-      if (!s->onchip && !(s->jit && sgx::jit_ready(s->jit))) {
-        s->tape.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
-        s->adj.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
-        s->have_tape = true;
-      }
-      s->row_loss.alloc_async(Bp, st);
-      s->partial.alloc_async(s->n_partial, st);
-      if (!s->hwpc && !s->hlive) s->BT.alloc_async(static_cast<size_t>(L.n_bit_rows) * s->W, st);
-      if (s->hlive) s->SP.alloc_async(static_cast<size_t>(std::max(L.lb_n_spill, 1)) * s->W, st);
-      s->valid.alloc_async(s->W, st);
-      s->newmask.alloc_async(s->W, st);
-      s->slot_of_row.alloc_async(Bp, st);
-      s->block_count.alloc_async(Bp / sgx::kThreads, st);
-      s->K.alloc_async(static_cast<size_t>(L.key_words) * Bp, st);
-      // Room for a few restarts' worth of solutions (16 harvests of unique
-      // rows, at most 4 GB of keys) before the first growth -- a growth waits
-      // for the host drain and copies the store; a quota caps it.
-      long long want_rows = 16 * static_cast<long long>(Bp);
-      const long long cap_4g = (4ll << 30) / (static_cast<long long>(L.key_words) * 8);
-      want_rows = std::max<long long>(std::min(want_rows, cap_4g), 2 * static_cast<long long>(Bp));
-      if (cfg->max_solutions > 0) want_rows = std::min<long long>(want_rows, cfg->max_solutions + Bp);
-      s->store_cap = cfg->solution_capacity > 0 ? cfg->solution_capacity : want_rows;
-      s->store.alloc_async(static_cast<size_t>(s->store_cap) * L.key_words, st);
-      CK(cudaMemsetAsync(s->V.p, 0, s->V.n * sizeof(float), s->st));
-      CK(cudaMemsetAsync(s->HB.p, 0xff, s->HB.n * sizeof(uint32_t), s->st));  // harden(0) = 1
-      ensure_table(s.get());
+    // From here on a failure (e.g. out of memory for the tape) must hand the
+    // stream kit, the pinned slots and every buffer back: sgx_sampler_free
+    // does exactly that on the half-built sampler.
+    try {
+      // The kit's events may carry its previous owner's completed records: a
+      // wait on them is a no-op, and sgx_step_loss only reads the slots this
+      // sampler launched (slot_pending).
+      s->dloss.alloc_async(2, s->st);  // pool memory: freed without cudaFree's device sync
+      static_assert(sizeof(sgx::HarvestOut) <= kPinSlot, "pinned slot too small");
+      s->hloss = static_cast<double*>(pin_slot());
+      s->hpin = static_cast<sgx::HarvestOut*>(pin_slot());
+      std::memset(s->hpin, 0, sizeof(sgx::HarvestOut));
+      s->hout.alloc_async(1, s->st);
       CK(cudaStreamSynchronize(s->st));
-      CK(cudaStreamSynchronize(s->sh));
+      if (c->layout_ok && !c->L.unsat) {
+        const auto& L = c->L;
+        s->Bp = round_up(cfg->batch, 1024);
+        s->W = s->Bp / 32;
+        s->wpc = s->W / 32 >= 2 * 148 ? 32 : (s->W / 16 >= 2 * 148 ? 16 : 8);
+        // Widest samples-per-thread that still leaves >= 3 tiles per SM
+        // (SGX_VEC overrides, for tuning).
+        s->vec = s->Bp / 128 >= 3 * 148 ? 4 : (s->Bp / 64 >= 3 * 148 ? 2 : 1);
+        if (const char* e = std::getenv("SGX_VEC")) {
+          int v = std::atoi(e);
+          if (v == 1 || v == 2 || v == 4) s->vec = v;
+        }
+        // SGX_ONCHIP=1: small circuits (>= 2 tiles of tape + adjoint slots per
+        // SM) run the fused on-chip soft pass on 32-sample tiles.  Opt-in:
+        // measured on C3a it is 2.3x SLOWER than the HBM-tape kernels (one
+        // sample per lane spends ~23k warp instructions per 32-sample tile on
+        // record control, at 8 warps per SM).
+        {
+          const char* e = std::getenv("SGX_ONCHIP");
+          s->onchip = e && e[0] == '1' && c->cone.oc_n4 > 0 &&
+                      sgx::onchip_warps(c->cone.n_rows, c->cone.oc_slots, c->cone.oc_n4) >= 2;
+          if (s->onchip) s->vec = 1;
+        }
+        // Circuit-specialised soft pass (sgx_jit.hpp) for small cones.
+        {
+          int mode = cfg->soft_kernel;
+          if (const char* e = std::getenv("SGX_JIT")) {
+            if (e[0] == '0') mode = SGX_SOFT_HBM;
+            else if (e[0] == 's') mode = SGX_SOFT_JIT;
+          }
+          if (mode != SGX_SOFT_HBM && !s->onchip && sgx::jit_eligible(L)) {
+            if (!c->jit) c->jit = sgx::jit_get(L, mode != SGX_SOFT_JIT);
+            if (mode == SGX_SOFT_JIT) sgx::jit_wait(c->jit.get());
+            if (!sgx::jit_failed(c->jit.get())) s->jit = c->jit.get();
+          }
+        }
+        // Shared-memory harvest: the widest word block whose folded bit tape
+        // fits ~100 KB (two CTAs per SM) while leaving >= 2 CTAs per SM of work;
+        // one word (up to 200 KB) for deep circuits; else the global path.
+        const size_t row_bytes = static_cast<size_t>(L.fb_rows + 1) * sizeof(uint32_t);
+        s->hwpc = 0;
+        // (<= 8 words: the CNF check keeps one accumulator pair per word in
+        // registers)
+        for (int w = 8; w >= 1; w /= 2)
+          if (row_bytes * w <= 100 * 1024 && s->W / w >= 2 * 148) {
+            s->hwpc = w;
+            break;
+          }
+        if (!s->hwpc && row_bytes <= 200 * 1024) s->hwpc = 1;
+        if (const char* e = std::getenv("SGX_HARVEST")) {
+          if (e[0] == 'g') s->hwpc = 0;  // force the global-memory harvest
+        }
+        if (const char* e = std::getenv("SGX_HWPC")) {  // A/B: words per harvest CTA
+          const int w = std::atoi(e);
+          if ((w == 1 || w == 2 || w == 4 || w == 8) && row_bytes * w <= 220 * 1024) s->hwpc = w;
+        }
+        // Liveness-allocated harvest (default): the words per CTA that keep the
+        // most words resident per SM (8 CTAs of 256 threads at most, ~227 KB of
+        // shared memory) with at least one CTA per SM; ties go to more words per
+        // CTA (per-level overhead amortised).  SGX_HARVEST=smem / g force the
+        // full-tape shared-memory / global-memory harvests.
+        s->hlive = 0;
+        {
+          const char* e = std::getenv("SGX_HARVEST");
+          const bool live_ok = !(e && (e[0] == 'g' || e[0] == 's'));
+          // words resident per SM for a tape of `rows` rows per word
+          auto best = [&](long long rows, int* wpc) {
+            int words = 0;
+            for (int w = 1; w <= 8; w *= 2) {
+              const size_t smem = static_cast<size_t>(rows) * w * sizeof(uint32_t) + 3 * 1024;
+              if (smem > 200 * 1024 || s->W / w < 148) continue;
+              const int ctas = std::min<int>(8, static_cast<int>((227 * 1024) / (smem + 1024)));
+              if (ctas * w >= words) {
+                words = ctas * w;
+                *wpc = w;
+              }
+            }
+            return words;
+          };
+          int wl = 0, wf = 0;
+          const int live_words = live_ok ? best(L.lb_slots, &wl) : 0;
+          const int full_words = best(L.fb_rows + 1, &wf);
+          // The full tape needs no spill round trip for the keys: it wins ties.
+          if (live_words > full_words) s->hlive = wl;
+          if (const char* v = std::getenv("SGX_LWPC")) {  // A/B: words per live-harvest CTA
+            const int w = std::atoi(v);
+            if ((w == 1 || w == 2 || w == 4 || w == 8) && live_ok &&
+                static_cast<size_t>(L.lb_slots) * w * 4 <= 200 * 1024)
+              s->hlive = w;
+          }
+          if (s->hlive) s->hwpc = 0;
+        }
+        // Stream-ordered pool allocations: a sampler created after another one
+        // reuses its memory without cudaMalloc / cudaFree round trips.
+        const size_t Bp = static_cast<size_t>(s->Bp);
+        cudaStream_t st = s->st;
+        s->V.alloc_async(L.cpi.size() * Bp, st);
+        s->HB.alloc_async(2 * L.cpi.size() * s->W, st);
+        // The on-chip and the (compiled) JIT passes keep tape and adjoints on chip.
+        if (!s->onchip && !(s->jit && sgx::jit_ready(s->jit))) {
+          s->tape.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
+          s->adj.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
+          s->have_tape = true;
+        }
+        s->row_loss.alloc_async(Bp, st);
+        s->partial.alloc_async(s->n_partial, st);
+        if (!s->hwpc && !s->hlive) s->BT.alloc_async(static_cast<size_t>(L.n_bit_rows) * s->W, st);
+        if (s->hlive) s->SP.alloc_async(static_cast<size_t>(std::max(L.lb_n_spill, 1)) * s->W, st);
+        s->valid.alloc_async(s->W, st);
+        s->newmask.alloc_async(s->W, st);
+        s->slot_of_row.alloc_async(Bp, st);
+        s->block_count.alloc_async(Bp / sgx::kThreads, st);
+        s->K.alloc_async(static_cast<size_t>(L.key_words) * Bp, st);
+        // Room for a few restarts' worth of solutions (16 harvests of unique
+        // rows, at most 4 GB of keys) before the first growth -- a growth waits
+        // for the host drain and copies the store; a quota caps it.
+        long long want_rows = 16 * static_cast<long long>(Bp);
+        const long long cap_4g = (4ll << 30) / (static_cast<long long>(L.key_words) * 8);
+        want_rows = std::max<long long>(std::min(want_rows, cap_4g), 2 * static_cast<long long>(Bp));
+        if (cfg->max_solutions > 0) want_rows = std::min<long long>(want_rows, cfg->max_solutions + Bp);
+        s->store_cap = cfg->solution_capacity > 0 ? cfg->solution_capacity : want_rows;
+        s->store.alloc_async(static_cast<size_t>(s->store_cap) * L.key_words, st);
+        CK(cudaMemsetAsync(s->V.p, 0, s->V.n * sizeof(float), s->st));
+        CK(cudaMemsetAsync(s->HB.p, 0xff, s->HB.n * sizeof(uint32_t), s->st));  // harden(0) = 1
+        ensure_table(s.get());
+        CK(cudaStreamSynchronize(s->st));
+        CK(cudaStreamSynchronize(s->sh));
+      }
+    } catch (...) {
+      sgx_sampler_free(s.release());
+      throw;
     }
     *out = s.release();
   });
@@ -1314,6 +1326,10 @@ int sgx_step_loss(sgx_sampler* s, int32_t slot, double* loss_total) {
   return guard([&] {
     need_ready(s);
     if (slot != 0 && slot != 1) throw std::invalid_argument("step slot must be 0 or 1");
+    // Pooled stream kits hand over events the previous owner recorded: only a
+    // slot this sampler launched (and has not read yet) carries its step.
+    if (!s->slot_pending[slot]) throw StateError("sgx_step_loss: no step pending in this slot");
+    s->slot_pending[slot] = false;
     CK(cudaSetDevice(s->c->ctx->device));
     CK(cudaEventSynchronize(s->sev[slot][3]));
     if (loss_total) *loss_total = s->hloss[slot];
@@ -1454,6 +1470,22 @@ int sgx_verify_solutions(sgx_circuit* c, const char* text, int64_t len, int64_t*
     out[1] = r.err_line;
     out[2] = r.err_var;
     out[3] = r.err_kind;
+    out[4] = r.launches;
+  });
+}
+
+int sgx_verify_keys(sgx_circuit* c, const uint64_t* keys, int64_t n, int64_t* out) {
+  return guard([&] {
+    need(c, "circuit");
+    need(out, "out");
+    if (n < 0) throw std::invalid_argument("negative key count");
+    if (n > 0) need(keys, "keys");
+    sgx::KeyCheck r;
+    sgx::verify_keys(c->ctx->device, c->L.clause_ptr, c->L.clause_lit, c->L.num_vars, keys, n, &r);
+    out[0] = r.checked;
+    out[1] = r.unsat;
+    out[2] = r.malformed;
+    out[3] = r.duplicate;
     out[4] = r.launches;
   });
 }

@@ -30,8 +30,11 @@ constexpr int64_t kJitMaxRecs = 6144;
 struct JitKernel;  // compiled kernel, shared by every sampler of the circuit
 
 bool jit_eligible(const Layout& L);
-// CUDA C++ source of the kernel `sgx_jit_step` for L.cone (deterministic).
-std::string jit_source(const Layout& L);
+// CUDA C++ source of the kernel `sgx_jit_step` for L.cone (deterministic);
+// min_blocks = __launch_bounds__ minimum CTAs per SM (register budget).
+std::string jit_source(const Layout& L, int min_blocks);
+// The min_blocks the sampler uses for L (SGX_JIT_MINB overrides).
+int jit_min_blocks(const Layout& L);
 
 // Compile (or find in the process cache) the kernel for L.  async: compile on
 // a worker thread and return at once; the handle becomes ready() later.

@@ -2,10 +2,31 @@
 
 #include <algorithm>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "sgx_kernels.cuh"
 #include "sgx_launch.hpp"
 
 namespace sgx {
+
+// Dynamic shared-memory opt-in, recorded per (kernel, device): the attribute
+// belongs to one device, and samplers on several devices (or host threads)
+// share these launchers.
+static void opt_in_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{kernel, dev}];
+  if (bytes > have) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    have = bytes;
+  }
+}
+
 
 // ---------------------------------------------------------------------------
 // K1: V0 = (float)(2 * u01(hash{seed, 'init', restart, row, col}) - 1)
@@ -1313,11 +1334,7 @@ bool launch_soft_onchip(cudaStream_t st, const OnchipArgs& a) {
   if (nw == 0) return false;
   const size_t smem = static_cast<size_t>(a.prog_n4) * 16 +
                       static_cast<size_t>(nw) * (a.n_rows + a.n_slots) * 32 * sizeof(float);
-  static size_t opted = 0;
-  if (smem > opted) {
-    cudaFuncSetAttribute(k_soft_onchip, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    opted = smem;
-  }
+  opt_in_smem(reinterpret_cast<const void*>(k_soft_onchip), smem);
   int ctas = (a.n_tiles + nw - 1) / nw;
   if (ctas > 148) ctas = 148;  // persistent: one CTA per SM (the program is copied once)
   k_soft_onchip<<<ctas, 32 * nw, smem, st>>>(a);
@@ -1950,11 +1967,7 @@ template <int WPC>
 static bool harvest_live_t(cudaStream_t st, const HarvestLiveArgs& a) {
   const size_t smem = static_cast<size_t>(a.slots) * WPC * sizeof(uint32_t);
   if (smem > 200 * 1024) return false;
-  static size_t opted = 0;
-  if (smem > opted) {
-    cudaFuncSetAttribute(k_harvest_live<WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    opted = smem;
-  }
+  opt_in_smem(reinterpret_cast<const void*>(k_harvest_live<WPC>), smem);
   k_harvest_live<WPC><<<a.W / WPC, kThreads, smem, st>>>(a);
   return true;
 }
@@ -2215,11 +2228,7 @@ void launch_forward(cudaStream_t st, int vec, const int4* grp, const int2* lvl, 
   if (vec == 4 && async_enabled_fwd() && tma && fb && fb->fblk) {
     const size_t smem = static_cast<size_t>(kAsyncSmem) + 2 * static_cast<size_t>(fb->blk_max) * 16;
     if (smem <= 200 * 1024) {
-      static size_t opted = 0;
-      if (smem > opted) {
-        cudaFuncSetAttribute(k_forward_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        opted = smem;
-      }
+      opt_in_smem(reinterpret_cast<const void*>(k_forward_tma), smem);
       static const int gcap = tile_grid("SGX_GRID_FWD", 1 << 30);
       const int grid = gcap < tiles ? gcap : tiles;
       k_forward_tma<<<grid, 32 * kWarps, smem, st>>>(fb->fblk, fb->blk0_n4, fb->blk_max, n_levels, src, ncols, tape,
@@ -2285,11 +2294,7 @@ void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* 
     const size_t s2 = static_cast<size_t>(kWarps) * 2 * kBU * 2 * 32 * 16 + blk;
     const int disc = discard_enabled() ? 1 : 0;
     if (s3 <= 54 * 1024) {
-      static size_t opted = 0;
-      if (s3 > opted) {
-        cudaFuncSetAttribute(k_backward_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s3));
-        opted = s3;
-      }
+      opt_in_smem(reinterpret_cast<const void*>(k_backward_tma<3>), s3);
       k_backward_tma<3><<<grid, 32 * kWarps, s3, st>>>(bb->sblk, bb->blk0_n4, bb->blk_max, n_levels, tape, adj, V,
                                                      ncols, n_rows, col_row, dv_out, dp_out, lr, out_enc, out_tgt,
                                                      n_out, row_loss, exp_tab, hb, tiles, bb->tail_dead,
@@ -2297,11 +2302,7 @@ void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* 
       return;
     }
     if (s2 <= 200 * 1024) {
-      static size_t opted = 0;
-      if (s2 > opted) {
-        cudaFuncSetAttribute(k_backward_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s2));
-        opted = s2;
-      }
+      opt_in_smem(reinterpret_cast<const void*>(k_backward_tma<2>), s2);
       k_backward_tma<2><<<grid, 32 * kWarps, s2, st>>>(bb->sblk, bb->blk0_n4, bb->blk_max, n_levels, tape, adj, V,
                                                      ncols, n_rows, col_row, dv_out, dp_out, lr, out_enc, out_tgt,
                                                      n_out, row_loss, exp_tab, hb, tiles, bb->tail_dead,
@@ -2399,11 +2400,7 @@ void launch_append(cudaStream_t st, const uint32_t* newmask, const int* block_of
 template <int WPC>
 static void harvest_smem_t(cudaStream_t st, int grid, int n_rows, size_t smem, const HarvestSmemArgs& a) {
   // Opt in whenever static (~10 KB) + dynamic could pass the 48 KB default.
-  static size_t opted = 0;  // dynamic bytes this instantiation may use
-  if (smem > opted) {
-    cudaFuncSetAttribute(k_harvest_smem<WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    opted = smem;
-  }
+  opt_in_smem(reinterpret_cast<const void*>(k_harvest_smem<WPC>), smem);
   k_harvest_smem<WPC><<<grid, kThreads, smem, st>>>(
       n_rows, a.hb, a.ncpi, a.nucpi, a.cpi_row, a.ucpi_row, a.free_prefix, a.row_offset, a.ops, a.lvl_ptr,
       a.n_levels, a.out_enc, a.out_tgt, a.n_out, a.cnf4, a.cnf_steps, a.key_enc, a.key_words,

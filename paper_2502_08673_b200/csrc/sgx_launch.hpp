@@ -157,6 +157,13 @@ struct VerifyResult {
   int32_t err_kind = 0;
   int64_t launches = 0;
 };
+// The same checks on packed keys (no text): rows that do not satisfy the CNF,
+// rows with bits set above num_vars, rows that repeat an earlier row.
+struct KeyCheck {
+  int64_t checked = 0, unsat = 0, malformed = 0, duplicate = 0, launches = 0;
+};
+void verify_keys(int device, const std::vector<int64_t>& clause_ptr, const std::vector<int32_t>& clause_lit,
+                 int num_vars, const uint64_t* keys, int64_t n, KeyCheck* out);
 void verify_solutions(int device, const std::vector<int64_t>& clause_ptr, const std::vector<int32_t>& clause_lit,
                       int num_vars, const char* text, int64_t len, VerifyResult* out);
 }  // namespace sgx

@@ -149,6 +149,76 @@ struct Chunk {
 
 }  // namespace
 
+// The device half of a check: ok[w] bit i = row 32w+i satisfies every clause;
+// sfp / srow = fingerprints of all rows radix-sorted, with their rows.
+void check_keys_device(int device, const std::vector<int64_t>& cptr, const std::vector<int32_t>& clit, int num_vars,
+                       int kw, const uint64_t* keys, int64_t n, std::vector<uint32_t>& ok,
+                       std::vector<uint64_t>& sfp, std::vector<int64_t>& srow, int64_t* launches) {
+  VerifyResult launch_count;
+  VerifyResult* out = &launch_count;
+  // ---- device: CNF check (bit-sliced) + fingerprints, in row chunks
+  ok.assign((n + 31) / 32, 0u);
+  sfp.resize(n);  // fingerprints, sorted
+  srow.resize(n);  // their rows (stable: ascending within a run)
+  if (n > 0) {
+    if (n > (int64_t{1} << 31) - 1) throw std::invalid_argument("too many solutions for one verify call");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    cudaStream_t st;
+    ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "verify stream");
+    const int nc = static_cast<int>(cptr.size()) - 1;
+    std::vector<int> p32(cptr.begin(), cptr.end()), enc(clit.size());
+    for (size_t k = 0; k < clit.size(); ++k) enc[k] = ((std::abs(clit[k]) - 1) << 1) | (clit[k] < 0 ? 1 : 0);
+    const int64_t R = std::min<int64_t>(n, int64_t{1} << 16);  // rows per chunk
+    const int Wc = static_cast<int>((R + 31) / 32);
+    int *dptr = nullptr, *denc = nullptr;
+    uint64_t *dkeys = nullptr, *dfp = nullptr, *dfp2 = nullptr;
+    int64_t *drow = nullptr, *drow2 = nullptr;
+    uint32_t *dbt = nullptr, *dok = nullptr;
+    ck(cudaMallocAsync(&dptr, p32.size() * sizeof(int), st), "verify alloc");
+    ck(cudaMallocAsync(&denc, std::max<size_t>(1, enc.size()) * sizeof(int), st), "verify alloc");
+    ck(cudaMallocAsync(&dkeys, static_cast<size_t>(R) * kw * sizeof(uint64_t), st), "verify alloc");
+    ck(cudaMallocAsync(&dfp, static_cast<size_t>(n) * sizeof(uint64_t), st), "verify alloc");
+    ck(cudaMallocAsync(&dfp2, static_cast<size_t>(n) * sizeof(uint64_t), st), "verify alloc");
+    ck(cudaMallocAsync(&drow, static_cast<size_t>(n) * sizeof(int64_t), st), "verify alloc");
+    ck(cudaMallocAsync(&drow2, static_cast<size_t>(n) * sizeof(int64_t), st), "verify alloc");
+    ck(cudaMallocAsync(&dbt, static_cast<size_t>(std::max(1, num_vars)) * Wc * sizeof(uint32_t), st), "verify alloc");
+    ck(cudaMallocAsync(&dok, static_cast<size_t>(Wc) * sizeof(uint32_t), st), "verify alloc");
+    ck(cudaMemcpyAsync(dptr, p32.data(), p32.size() * sizeof(int), cudaMemcpyHostToDevice, st), "verify h2d");
+    if (!enc.empty())
+      ck(cudaMemcpyAsync(denc, enc.data(), enc.size() * sizeof(int), cudaMemcpyHostToDevice, st), "verify h2d");
+    for (int64_t r0 = 0; r0 < n; r0 += R) {
+      const int64_t m = std::min(R, n - r0);
+      const int W = static_cast<int>((m + 31) / 32);
+      ck(cudaMemcpyAsync(dkeys, keys + r0 * kw, static_cast<size_t>(m) * kw * sizeof(uint64_t),
+                         cudaMemcpyHostToDevice, st), "verify h2d");
+      const long long warps = static_cast<long long>(W) * kw;
+      k_keys_to_bt<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(dkeys, m, kw, num_vars, W, dbt);
+      k_cnf_words<<<(W + 127) / 128, 128, 0, st>>>(dbt, W, m, dptr, denc, nc, dok);
+      k_key_fp<<<static_cast<unsigned>((m + 255) / 256), 256, 0, st>>>(dkeys, m, kw, dfp + r0);
+      ck(cudaMemcpyAsync(ok.data() + r0 / 32, dok, W * sizeof(uint32_t), cudaMemcpyDeviceToHost, st), "verify d2h");
+      ck(cudaStreamSynchronize(st), "verify sync");  // the key chunk buffer is reused
+      out->launches += 3;
+    }
+    k_iota<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(drow, n);
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dfp, dfp2, drow, drow2, static_cast<int>(n), 0, 64, st);
+    void* tmp = nullptr;
+    ck(cudaMallocAsync(&tmp, std::max<size_t>(1, tmp_bytes), st), "verify alloc");
+    cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, dfp, dfp2, drow, drow2, static_cast<int>(n), 0, 64, st);
+    ck(cudaMemcpyAsync(sfp.data(), dfp2, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st), "verify d2h");
+    ck(cudaMemcpyAsync(srow.data(), drow2, n * sizeof(int64_t), cudaMemcpyDeviceToHost, st), "verify d2h");
+    out->launches += 3;
+    ck(cudaGetLastError(), "verify kernels");
+    for (void* p : {static_cast<void*>(dptr), static_cast<void*>(denc), static_cast<void*>(dkeys),
+                    static_cast<void*>(dfp), static_cast<void*>(dbt), static_cast<void*>(dok),
+                    static_cast<void*>(dfp2), static_cast<void*>(drow), static_cast<void*>(drow2), tmp})
+      cudaFreeAsync(p, st);
+    ck(cudaStreamSynchronize(st), "verify free");
+    cudaStreamDestroy(st);
+  }
+  *launches += out->launches;
+}
+
 void verify_solutions(int device, const std::vector<int64_t>& cptr, const std::vector<int32_t>& clit, int num_vars,
                       const char* text, int64_t len, VerifyResult* out) {
   *out = VerifyResult{};
@@ -211,66 +281,10 @@ void verify_solutions(int device, const std::vector<int64_t>& cptr, const std::v
     base += C.lines;
   }
   const int64_t n = static_cast<int64_t>(line_of.size());
-  // ---- device: CNF check (bit-sliced) + fingerprints, in row chunks
-  std::vector<uint32_t> ok((n + 31) / 32, 0u);
-  std::vector<uint64_t> sfp(n);  // fingerprints, sorted
-  std::vector<int64_t> srow(n);  // their rows (stable: ascending within a run)
-  if (n > 0) {
-    if (n > (int64_t{1} << 31) - 1) throw std::invalid_argument("too many solutions for one verify call");
-    ck(cudaSetDevice(device), "cudaSetDevice");
-    cudaStream_t st;
-    ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "verify stream");
-    const int nc = static_cast<int>(cptr.size()) - 1;
-    std::vector<int> p32(cptr.begin(), cptr.end()), enc(clit.size());
-    for (size_t k = 0; k < clit.size(); ++k) enc[k] = ((std::abs(clit[k]) - 1) << 1) | (clit[k] < 0 ? 1 : 0);
-    const int64_t R = std::min<int64_t>(n, int64_t{1} << 16);  // rows per chunk
-    const int Wc = static_cast<int>((R + 31) / 32);
-    int *dptr = nullptr, *denc = nullptr;
-    uint64_t *dkeys = nullptr, *dfp = nullptr, *dfp2 = nullptr;
-    int64_t *drow = nullptr, *drow2 = nullptr;
-    uint32_t *dbt = nullptr, *dok = nullptr;
-    ck(cudaMallocAsync(&dptr, p32.size() * sizeof(int), st), "verify alloc");
-    ck(cudaMallocAsync(&denc, std::max<size_t>(1, enc.size()) * sizeof(int), st), "verify alloc");
-    ck(cudaMallocAsync(&dkeys, static_cast<size_t>(R) * kw * sizeof(uint64_t), st), "verify alloc");
-    ck(cudaMallocAsync(&dfp, static_cast<size_t>(n) * sizeof(uint64_t), st), "verify alloc");
-    ck(cudaMallocAsync(&dfp2, static_cast<size_t>(n) * sizeof(uint64_t), st), "verify alloc");
-    ck(cudaMallocAsync(&drow, static_cast<size_t>(n) * sizeof(int64_t), st), "verify alloc");
-    ck(cudaMallocAsync(&drow2, static_cast<size_t>(n) * sizeof(int64_t), st), "verify alloc");
-    ck(cudaMallocAsync(&dbt, static_cast<size_t>(std::max(1, num_vars)) * Wc * sizeof(uint32_t), st), "verify alloc");
-    ck(cudaMallocAsync(&dok, static_cast<size_t>(Wc) * sizeof(uint32_t), st), "verify alloc");
-    ck(cudaMemcpyAsync(dptr, p32.data(), p32.size() * sizeof(int), cudaMemcpyHostToDevice, st), "verify h2d");
-    if (!enc.empty())
-      ck(cudaMemcpyAsync(denc, enc.data(), enc.size() * sizeof(int), cudaMemcpyHostToDevice, st), "verify h2d");
-    for (int64_t r0 = 0; r0 < n; r0 += R) {
-      const int64_t m = std::min(R, n - r0);
-      const int W = static_cast<int>((m + 31) / 32);
-      ck(cudaMemcpyAsync(dkeys, keys.data() + r0 * kw, static_cast<size_t>(m) * kw * sizeof(uint64_t),
-                         cudaMemcpyHostToDevice, st), "verify h2d");
-      const long long warps = static_cast<long long>(W) * kw;
-      k_keys_to_bt<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(dkeys, m, kw, num_vars, W, dbt);
-      k_cnf_words<<<(W + 127) / 128, 128, 0, st>>>(dbt, W, m, dptr, denc, nc, dok);
-      k_key_fp<<<static_cast<unsigned>((m + 255) / 256), 256, 0, st>>>(dkeys, m, kw, dfp + r0);
-      ck(cudaMemcpyAsync(ok.data() + r0 / 32, dok, W * sizeof(uint32_t), cudaMemcpyDeviceToHost, st), "verify d2h");
-      ck(cudaStreamSynchronize(st), "verify sync");  // the key chunk buffer is reused
-      out->launches += 3;
-    }
-    k_iota<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(drow, n);
-    size_t tmp_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dfp, dfp2, drow, drow2, static_cast<int>(n), 0, 64, st);
-    void* tmp = nullptr;
-    ck(cudaMallocAsync(&tmp, std::max<size_t>(1, tmp_bytes), st), "verify alloc");
-    cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, dfp, dfp2, drow, drow2, static_cast<int>(n), 0, 64, st);
-    ck(cudaMemcpyAsync(sfp.data(), dfp2, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st), "verify d2h");
-    ck(cudaMemcpyAsync(srow.data(), drow2, n * sizeof(int64_t), cudaMemcpyDeviceToHost, st), "verify d2h");
-    out->launches += 3;
-    ck(cudaGetLastError(), "verify kernels");
-    for (void* p : {static_cast<void*>(dptr), static_cast<void*>(denc), static_cast<void*>(dkeys),
-                    static_cast<void*>(dfp), static_cast<void*>(dbt), static_cast<void*>(dok),
-                    static_cast<void*>(dfp2), static_cast<void*>(drow), static_cast<void*>(drow2), tmp})
-      cudaFreeAsync(p, st);
-    ck(cudaStreamSynchronize(st), "verify free");
-    cudaStreamDestroy(st);
-  }
+  std::vector<uint32_t> ok;
+  std::vector<uint64_t> sfp;
+  std::vector<int64_t> srow;
+  check_keys_device(device, cptr, clit, num_vars, kw, keys.data(), n, ok, sfp, srow, &out->launches);
   // ---- first unsatisfied row, first duplicate row (of an earlier, valid row)
   int64_t bad = n;
   int bad_kind = 0;
@@ -308,6 +322,38 @@ void verify_solutions(int device, const std::vector<int64_t>& cptr, const std::v
       out->err_kind = 0;
       out->err_var = 0;
     }
+  }
+}
+
+void verify_keys(int device, const std::vector<int64_t>& cptr, const std::vector<int32_t>& clit, int num_vars,
+                 const uint64_t* keys, int64_t n, KeyCheck* out) {
+  *out = KeyCheck{};
+  const int kw = std::max(1, (num_vars + 63) / 64);
+  std::vector<uint32_t> ok;
+  std::vector<uint64_t> sfp;
+  std::vector<int64_t> srow;
+  check_keys_device(device, cptr, clit, num_vars, kw, keys, n, ok, sfp, srow, &out->launches);
+  out->checked = n;
+  for (int64_t r = 0; r < n; ++r)
+    if (!((ok[r >> 5] >> (r & 31)) & 1u)) ++out->unsat;
+  // bits above num_vars must be zero in a packed key (dedupe_key, sampler.cpp:18-26)
+  if (num_vars % 64) {
+    const uint64_t hi = ~uint64_t{0} << (num_vars % 64);
+    for (int64_t r = 0; r < n; ++r)
+      if (keys[r * kw + kw - 1] & hi) ++out->malformed;
+  }
+  for (int64_t a = 0; a < n;) {
+    int64_t b = a + 1;
+    while (b < n && sfp[b] == sfp[a]) ++b;
+    for (int64_t j = a + 1; j < b; ++j) {
+      const uint64_t* kj = keys + srow[j] * kw;
+      for (int64_t i = a; i < j; ++i)
+        if (std::memcmp(keys + srow[i] * kw, kj, kw * sizeof(uint64_t)) == 0) {
+          ++out->duplicate;
+          break;
+        }
+    }
+    a = b;
   }
 }
 

@@ -175,6 +175,16 @@ class DeviceCircuit:
         return {"checked": checked, "ok": kind == 0, "line": line, "kind": kind, "var": var,
                 "message": msg, "launches": launches}
 
+    def verify_keys(self, keys: np.ndarray) -> dict:
+        """Device check of packed solution keys against the CNF: counts of keys
+        that do not satisfy it, that are malformed, and that repeat an earlier key."""
+        keys = np.ascontiguousarray(keys, dtype=np.uint64)
+        out = np.zeros(5, np.int64)
+        _lib.check(self.L.sgx_verify_keys(self.h, _lib.ptr(keys, C.c_uint64) if keys.size else None,
+                                          keys.shape[0] if keys.ndim == 2 else 0, _lib.ptr(out, C.c_int64)))
+        return {"checked": int(out[0]), "unsat": int(out[1]), "malformed": int(out[2]),
+                "duplicate": int(out[3]), "invalid": int(out[1] + out[2] + out[3])}
+
     def close(self):
         if getattr(self, "h", None):
             self.L.sgx_circuit_free(self.h)
