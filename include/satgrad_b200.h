@@ -162,8 +162,11 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
 int sgx_sampler_free(sgx_sampler* s);
 /* info[0] soft kernel of the last step (0 HBM tape, 1 JIT, 2 on-chip),
  * info[1] steps run by the JIT kernel, info[2] JIT state (-1 none,
- * 0 compiling, 1 ready, 2 failed), info[3] its compile time in us. */
-int sgx_sampler_soft_info(const sgx_sampler* s, int64_t* info4);
+ * 0 compiling, 1 ready, 2 failed), info[3] its compile time in us,
+ * info[4] harvest kernel (0 global-memory, 1 full-tape shared-memory,
+ * 2 live-slot), info[5] its words per CTA, info[6] samples per lane of the
+ * HBM soft kernels, info[7] padded batch. */
+int sgx_sampler_soft_info(const sgx_sampler* s, int64_t* info8);
 
 /* One restart's building blocks (what sgx_run loops over). */
 int sgx_init(sgx_sampler* s, int32_t restart);
@@ -201,6 +204,49 @@ int sgx_harvest_local(sgx_sampler* s, int32_t restart, int32_t iter, int64_t* n_
 int sgx_harvest_merge(sgx_sampler* s, const uint64_t* all_fps, const int64_t* counts, int32_t nranks,
                       int32_t rank, int64_t stride, int64_t* n_won);
 int sgx_harvest_commit(sgx_sampler* s, int64_t quota_left, int64_t* attempts, int64_t* added);
+
+/* ---- Multi-GPU run through the C-ABI ----------------
+ * Sample sharding: rank g of nranks runs its own sampler with
+ * cfg.row_offset = g * cfg.batch (global rows [g*B, (g+1)*B); every random
+ * draw is keyed by global row, so the union of the shards IS a one-device run
+ * at batch nranks * B).  sgx_run_sharded is satgrad::run over that union:
+ * per harvest ONE all-gather of the new 64-bit fingerprints (+ their count);
+ * a fingerprint found by several ranks counts once, for the lowest rank (the
+ * reference's row order); quota / restart / timeout decisions are taken on
+ * gathered values, so every rank takes the same branch.  stats.unique_count
+ * is the global count; each rank stores the solutions it won
+ * (sgx_fetch_solutions), their union is the global solution set.
+ *
+ * The collective comes from the caller as an sgx_exchange, or from the
+ * library: sgx_exchange_nccl_create (one process per GPU; NCCL over
+ * NVLink / NVSwitch, libnccl.so.2 resolved at run time -- the copy already
+ * loaded in the process if any) or sgx_exchange_local_create (one process,
+ * one host thread per rank, device-to-device copies; ranks may share a GPU). */
+typedef struct sgx_exchange {
+  void* user;
+  int32_t rank;
+  int32_t nranks;
+  /* All-gather `bytes` of DEVICE memory `send` from every rank into DEVICE
+   * memory `recv` (nranks * bytes, rank-major), ordered on `stream` (a
+   * cudaStream_t): producers of `send` precede it there, and consumers of
+   * `recv` follow it there.  0 on success. */
+  int (*allgather_device)(void* user, const void* send, void* recv, int64_t bytes, void* stream);
+  /* All-gather n int64 host values per rank into recv[nranks * n]; blocking. */
+  int (*allgather_host)(void* user, const int64_t* send, int64_t* recv, int32_t n);
+} sgx_exchange;
+
+int sgx_run_sharded(sgx_sampler* s, const sgx_exchange* ex, sgx_run_stats* stats);
+
+/* NCCL: rank 0 makes the id, the caller distributes it (MPI, torch.distributed,
+ * a file), every rank creates its exchange on its device. */
+int sgx_nccl_unique_id(uint8_t id[128]);
+int sgx_exchange_nccl_create(int32_t nranks, const uint8_t id[128], int32_t rank, int32_t device,
+                             sgx_exchange* out);
+int sgx_exchange_nccl_destroy(sgx_exchange* ex);
+/* In-process group of nranks: fills out[0..nranks-1], one per rank / thread.
+ * Destroy once, with any of them, after every rank has finished. */
+int sgx_exchange_local_create(int32_t nranks, sgx_exchange* out);
+int sgx_exchange_local_destroy(sgx_exchange* ex);
 
 /* satgrad::run: the whole restart x iteration loop with quota, timeout and
  * restart policy; solutions stay on the device until fetched. */

@@ -27,6 +27,8 @@ EXPORTS = [
     "sgx_format_solutions", "sgx_launch_count", "sgx_extract", "sgx_extraction_sizes",
     "sgx_extraction_export", "sgx_extraction_note", "sgx_extraction_free", "sgx_verify_solutions",
     "sgx_verify_cnf", "sgx_jit_source", "sgx_sampler_soft_info", "sgx_verify_keys",
+    "sgx_run_sharded", "sgx_nccl_unique_id", "sgx_exchange_nccl_create", "sgx_exchange_nccl_destroy",
+    "sgx_exchange_local_create", "sgx_exchange_local_destroy",
 ]
 
 
@@ -64,6 +66,16 @@ class RunStatsC(C.Structure):
         ("n_loss", C.c_int32), ("n_harvest", C.c_int32), ("unsat", C.c_int32),
         ("reserved", C.c_int32), ("device_ms", C.c_double), ("launches", C.c_int64),
     ]
+
+
+ALLGATHER_DEVICE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+ALLGATHER_HOST = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_int32)
+
+
+class Exchange(C.Structure):
+    """sgx_exchange: the collectives of sgx_run_sharded."""
+    _fields_ = [("user", C.c_void_p), ("rank", C.c_int32), ("nranks", C.c_int32),
+                ("allgather_device", ALLGATHER_DEVICE), ("allgather_host", ALLGATHER_HOST)]
 
 
 _lib = None
@@ -134,6 +146,12 @@ def load() -> C.CDLL:
         "sgx_jit_source": (C.c_int, [C.POINTER(CircuitDesc), C.c_char_p, i64, i64p]),
         "sgx_sampler_soft_info": (C.c_int, [vp, i64p]),
         "sgx_verify_keys": (C.c_int, [vp, u64p, i64, i64p]),
+        "sgx_run_sharded": (C.c_int, [vp, C.POINTER(Exchange), C.POINTER(RunStatsC)]),
+        "sgx_nccl_unique_id": (C.c_int, [C.c_char_p]),
+        "sgx_exchange_nccl_create": (C.c_int, [i32, C.c_char_p, i32, i32, C.POINTER(Exchange)]),
+        "sgx_exchange_nccl_destroy": (C.c_int, [C.POINTER(Exchange)]),
+        "sgx_exchange_local_create": (C.c_int, [i32, C.POINTER(Exchange)]),
+        "sgx_exchange_local_destroy": (C.c_int, [C.POINTER(Exchange)]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

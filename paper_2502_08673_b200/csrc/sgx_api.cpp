@@ -364,6 +364,7 @@ struct sgx_sampler {
   DBuf<uint64_t> K, store;
   DBuf<unsigned long long> fps_local;  // multi-GPU: this harvest's new fingerprints
   DBuf<long long> n_of;                // multi-GPU: per-rank counts of the gathered lists
+  DBuf<unsigned long long> fps_all;    // multi-GPU: the gathered lists [nranks][Bp + 1] (sgx_run_sharded)
   int dist_stage = 0;                  // 0 idle, 1 after local, 2 after merge
   DBuf<unsigned long long> tkeys, tmeta;
   uint64_t tcap = 0;
@@ -899,6 +900,211 @@ void sampler_run(sgx_sampler* s) {
   s->stats.n_harvest = static_cast<int32_t>(s->new_unique.size());
 }
 
+// ------------------------------------------------------------ multi-GPU
+// The split harvest (sample sharding): the local front half
+// publishes this harvest's new fingerprints in row order (count at [Bp]),
+// the caller's all-gather exchanges them, the merge revokes rows a lower rank
+// also found (lowest rank wins = the reference's row order over the union)
+// and inserts every remote fingerprint, the commit appends the winners.
+long long dist_local(sgx_sampler* s, int restart, int iter) {
+  if (s->dist_stage != 0) throw StateError("sgx_harvest_local: previous harvest not committed");
+  if (!s->fps_local.p) s->fps_local.alloc_async(static_cast<size_t>(s->Bp) + 1, s->sh);
+  harvest_front(s, restart, iter, -1);
+  sgx::launch_compact_new(s->sh, s->newmask.p, s->block_count.p, s->slot_of_row.p, s->tkeys.p, s->Bp,
+                          s->fps_local.p);
+  s->launches += 1;
+  CK(cudaGetLastError());
+  // the count rides at [stride] so one all-gather carries fingerprints and counts
+  CK(cudaMemcpyAsync(s->fps_local.p + s->Bp, &s->hout.p->new_rows, sizeof(long long), cudaMemcpyDeviceToDevice,
+                     s->sh));
+  CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->sh));
+  CK(cudaStreamSynchronize(s->sh));
+  s->dist_stage = 1;
+  return s->hpin->new_rows;
+}
+
+// Returns the rows still new here; *fresh = remote fingerprints new to the
+// table, so |union of this harvest| = local new + *fresh on every rank.
+long long dist_merge(sgx_sampler* s, const uint64_t* all_fps, const std::vector<long long>& cnt, int rank,
+                     long long stride, long long* fresh) {
+  if (s->dist_stage != 1) throw StateError("sgx_harvest_merge: call sgx_harvest_local first");
+  const int nranks = static_cast<int>(cnt.size());
+  const long long n_local = s->hpin->new_rows;
+  long long remote = 0;
+  for (int r = 0; r < nranks; ++r) {
+    if (cnt[r] < 0 || cnt[r] > stride) throw std::invalid_argument("fingerprint count out of range");
+    if (r != rank) remote += cnt[r];
+  }
+  // Room for every remote fingerprint at load factor <= 1/2.
+  s->table_count += remote;
+  ensure_table(s);
+  if (!s->n_of.p || static_cast<int>(s->n_of.n) < nranks) s->n_of.alloc_async(std::max(nranks, 64), s->sh);
+  CK(cudaMemcpyAsync(s->n_of.p, cnt.data(), nranks * sizeof(long long), cudaMemcpyHostToDevice, s->sh));
+  sgx::launch_merge_remote(s->sh, reinterpret_cast<const unsigned long long*>(all_fps), s->n_of.p,
+                           nranks > 1 ? nranks : 0, rank, stride, s->tkeys.p, s->tmeta.p, s->tcap - 1, s->epoch,
+                           s->newmask.p, s->Bp, s->block_count.p, s->hout.p);
+  s->launches += nranks > 1 ? 3 : 2;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->sh));
+  CK(cudaStreamSynchronize(s->sh));
+  // Locally-new rows another rank claimed still occupy table slots; so do
+  // the remote fingerprints (counted above), minus those already present.
+  s->table_count += n_local - s->hpin->new_rows;
+  s->table_count -= remote - static_cast<long long>(s->hpin->fresh);
+  *fresh = static_cast<long long>(s->hpin->fresh);
+  s->dist_stage = 2;
+  return s->hpin->new_rows;
+}
+
+void dist_commit(sgx_sampler* s, long long quota_left, long long* attempts, long long* added) {
+  if (s->dist_stage != 2) throw StateError("sgx_harvest_commit: call sgx_harvest_merge first");
+  sgx::HarvestOut h = *s->hpin;
+  h.accepted = quota_left < 0 ? h.new_rows : std::min<long long>(h.new_rows, quota_left);
+  h.last_row = -1;
+  h.overflow = 0;
+  *s->hpin = h;
+  CK(cudaMemcpyAsync(s->hout.p, s->hpin, sizeof(sgx::HarvestOut), cudaMemcpyHostToDevice, s->sh));
+  harvest_back_launch(s, -1);
+  harvest_back_finish(s, quota_left, attempts, added, -1);  // counts the winners into table_count
+  s->dist_stage = 0;
+}
+
+void check_ex(int rc, const char* what) {
+  if (rc != 0) throw CudaError(std::string("exchange ") + what + " failed (" + std::to_string(rc) + ")");
+}
+
+// run_impl<float> (sampler.cpp:89-194) over the union of nranks sample
+// shards, one sampler per rank (rank g owns global rows [g*B, (g+1)*B) via
+// cfg.row_offset).  One device all-gather per harvest carries every rank's
+// new fingerprints and their counts; the union's size is derived locally
+// (local new + fresh remote inserts).  Under a quota the winners' counts are
+// all-gathered too (the cut goes in rank order), and with a timeout a late
+// flag, so every rank takes the same branch.  The next step is launched as
+// soon as the local harvest kernels are done, so the exchange overlaps it.
+void sampler_run_sharded(sgx_sampler* s, const sgx_exchange* ex) {
+  using clock = std::chrono::steady_clock;
+  const auto t0 = clock::now();
+  auto now_s = [&] { return std::chrono::duration<double>(clock::now() - t0).count(); };
+  const sgx_sampler_cfg& cfg = s->cfg;
+  const int R = ex->nranks, me = ex->rank;
+  s->loss_trace.clear();
+  s->new_unique.clear();
+  s->stats = sgx_run_stats{};
+  std::fill(s->phase_ms, s->phase_ms + 8, 0.0);
+  std::fill(s->host_ms, s->host_ms + 8, 0.0);
+  s->launches = 0;
+  if (s->c->L.unsat) {
+    s->stats.unsat = 1;
+    s->stats.wall_time_s = now_s();
+    return;
+  }
+  const long long stride = static_cast<long long>(s->Bp) + 1;
+  if (!s->fps_local.p) s->fps_local.alloc_async(static_cast<size_t>(stride), s->sh);
+  if (s->fps_all.n < static_cast<size_t>(R * stride)) s->fps_all.alloc_async(static_cast<size_t>(R * stride), s->sh);
+  std::vector<long long> counts(R);
+  std::vector<int64_t> hv(R);
+  const bool quota = cfg.max_solutions > 0;
+  long long unique = 0;  // global
+  auto quota_met = [&] { return quota && unique >= cfg.max_solutions; };
+  auto gather1 = [&](int64_t x) {
+    check_ex(ex->allgather_host(ex->user, &x, hv.data(), 1), "allgather_host");
+    return hv;
+  };
+  auto out_of_time = [&] {  // any rank over time stops every rank
+    if (cfg.timeout_s <= 0.0) return false;
+    const auto all = gather1(now_s() >= cfg.timeout_s ? 1 : 0);
+    return std::any_of(all.begin(), all.end(), [](int64_t v) { return v != 0; });
+  };
+  const bool overlap = [] {
+    const char* e = std::getenv("SGX_OVERLAP");
+    return !(e && e[0] == '0');
+  }();
+  auto harvest = [&](int restart, int it, bool launch_next) {
+    const auto h0 = clock::now();
+    dist_local(s, restart, it);
+    const int slot = launch_next ? sampler_step(s) : -1;
+    check_ex(ex->allgather_device(ex->user, s->fps_local.p, s->fps_all.p, stride * 8, s->sh), "allgather_device");
+    CK(cudaMemcpy2DAsync(counts.data(), sizeof(long long), s->fps_all.p + s->Bp, stride * sizeof(long long),
+                         sizeof(long long), R, cudaMemcpyDeviceToHost, s->sh));
+    CK(cudaStreamSynchronize(s->sh));
+    long long fresh = 0;
+    const long long n_local = s->hpin->new_rows;
+    const long long won = dist_merge(s, reinterpret_cast<const uint64_t*>(s->fps_all.p), counts, me, stride, &fresh);
+    long long att = 0, add = 0, acc = 0;
+    if (!quota) {
+      dist_commit(s, -1, &att, &add);
+      acc = n_local + fresh;
+      s->stats.attempts += static_cast<long long>(cfg.batch) * R;
+    } else {
+      const long long left = cfg.max_solutions - unique;
+      const auto wons = gather1(won);
+      long long before = 0;
+      for (int q = 0; q < me; ++q) before += wons[q];
+      const long long my_left = std::max(0LL, left - before);
+      dist_commit(s, my_left, &att, &add);
+      if (my_left == 0) att = 0;  // a lower rank filled the quota: these rows come after the cut
+      for (int q = 0; q < R; ++q) acc += std::max(0LL, std::min<long long>(wons[q], left - acc));
+      const auto atts = gather1(att);
+      for (int q = 0; q < R; ++q) s->stats.attempts += atts[q];
+    }
+    unique += acc;
+    s->new_unique.push_back(acc);
+    s->host_ms[0] += std::chrono::duration<double, std::milli>(clock::now() - h0).count();
+    return slot;
+  };
+  auto speculate = [&](int it) { return overlap && !quota && cfg.timeout_s <= 0.0 && it <= cfg.iterations; };
+  auto step_loss = [&](int slot) {
+    CK(cudaEventSynchronize(s->sev[slot][3]));
+    s->slot_pending[slot] = false;
+    cudaEvent_t* ev = s->sev[slot];
+    s->phase_ms[1] += elapsed(ev[0], ev[3]);
+    s->phase_ms[3] += elapsed(ev[0], ev[1]);
+    s->phase_ms[4] += elapsed(ev[2], ev[3]);
+    return s->hloss[slot];
+  };
+  const int max_restarts = cfg.max_restarts > 0 ? cfg.max_restarts : 1000;
+  bool timed_out = false;
+  cudaEvent_t r0 = s->rev[2], r1 = s->rev[3];
+  CK(cudaEventRecord(r0, s->st));
+  for (int restart = 0;; ++restart) {
+    sampler_init(s, restart);
+    const long long before = unique;
+    int slot = harvest(restart, 0, speculate(1));
+    for (int it = 1; it <= cfg.iterations; ++it) {
+      if (quota_met()) break;
+      if (out_of_time()) {
+        timed_out = true;
+        break;
+      }
+      if (slot < 0) slot = sampler_step(s);
+      s->loss_trace.push_back(step_loss(slot) / cfg.batch);
+      slot = harvest(restart, it, speculate(it + 1));
+    }
+    if (slot >= 0) step_loss(slot);  // a speculative step nobody harvests: let it finish
+    if (quota_met() || timed_out) break;
+    if (cfg.restart_policy == SGX_RESTART_NONE) break;
+    if (unique == before) break;
+    if (restart >= max_restarts) break;
+    if (out_of_time()) {
+      timed_out = true;
+      break;
+    }
+    s->stats.restarts = restart + 1;
+  }
+  CK(cudaEventRecord(s->ev_join, s->sh));
+  CK(cudaStreamWaitEvent(s->st, s->ev_join, 0));
+  CK(cudaEventRecord(r1, s->st));
+  CK(cudaEventSynchronize(r1));
+  s->stats.device_ms = elapsed(r0, r1);
+  s->stats.launches = s->launches;
+  s->stats.timed_out = timed_out ? 1 : 0;
+  s->stats.unique_count = unique;
+  s->stats.wall_time_s = now_s();
+  s->stats.throughput = s->stats.wall_time_s > 0.0 ? unique / s->stats.wall_time_s : 0.0;
+  s->stats.n_loss = static_cast<int32_t>(s->loss_trace.size());
+  s->stats.n_harvest = static_cast<int32_t>(s->new_unique.size());
+}
+
 void reset_solutions(sgx_sampler* s) {
   s->n_solutions = 0;
   if (s->drain) s->drain->reset();
@@ -911,6 +1117,10 @@ void reset_solutions(sgx_sampler* s) {
 }
 
 }  // namespace
+
+namespace sgx {
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace sgx
 
 extern "C" {
 
@@ -971,15 +1181,20 @@ int sgx_jit_source(const sgx_circuit_desc* desc, char* out, int64_t cap, int64_t
   });
 }
 
-int sgx_sampler_soft_info(const sgx_sampler* s, int64_t* info4) {
+int sgx_sampler_soft_info(const sgx_sampler* s, int64_t* info8) {
   return guard([&] {
     need(s, "sampler");
-    need(info4, "info4");
+    need(info8, "info8");
+    int64_t* info4 = info8;
     const sgx::JitKernel* k = s->c->jit.get();
     info4[0] = s->last_soft;
     info4[1] = s->jit_steps;
     info4[2] = !k ? -1 : (sgx::jit_ready(k) ? 1 : (sgx::jit_failed(k) ? 2 : 0));
     info4[3] = k ? static_cast<int64_t>(sgx::jit_compile_ms(k) * 1000.0) : 0;
+    info8[4] = s->hlive ? 2 : (s->hwpc ? 1 : 0);  // harvest: live-slot / full-tape smem / global
+    info8[5] = s->hlive ? s->hlive : s->hwpc;     // its words per CTA
+    info8[6] = s->vec;                            // samples per lane of the HBM soft kernels
+    info8[7] = s->Bp;
   });
 }
 
@@ -1255,6 +1470,9 @@ int sgx_sampler_free(sgx_sampler* s) {
       for (auto* b : {&s->V, &s->tape, &s->adj, &s->row_loss}) b->reset_async(st);
       s->partial.reset_async(st);
       for (auto* b : {&s->BT, &s->valid, &s->newmask, &s->HB, &s->SP}) b->reset_async(st);
+      s->fps_local.reset_async(st);
+      s->fps_all.reset_async(st);
+      s->n_of.reset_async(st);
       s->slot_of_row.reset_async(st);
       s->block_count.reset_async(st);
       s->K.reset_async(st);
@@ -1600,22 +1818,10 @@ int sgx_fingerprint_stride(const sgx_sampler* s) { return s ? s->Bp : -1; }
 int sgx_harvest_local(sgx_sampler* s, int32_t restart, int32_t iter, int64_t* n_new, uint64_t** fps) {
   return guard([&] {
     need_ready(s);
-    if (s->dist_stage != 0) throw StateError("sgx_harvest_local: previous harvest not committed");
     CK(cudaSetDevice(s->c->ctx->device));
-    if (!s->fps_local.p) s->fps_local.alloc_async(static_cast<size_t>(s->Bp) + 1, s->sh);
-    harvest_front(s, restart, iter, -1);
-    sgx::launch_compact_new(s->sh, s->newmask.p, s->block_count.p, s->slot_of_row.p, s->tkeys.p, s->Bp,
-                            s->fps_local.p);
-    s->launches += 1;
-    CK(cudaGetLastError());
-    // the count rides at [stride] so one all-gather carries fingerprints and counts
-    CK(cudaMemcpyAsync(s->fps_local.p + s->Bp, &s->hout.p->new_rows, sizeof(long long), cudaMemcpyDeviceToDevice,
-                       s->sh));
-    CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->sh));
-    CK(cudaStreamSynchronize(s->sh));
-    if (n_new) *n_new = s->hpin->new_rows;
+    const long long n = dist_local(s, restart, iter);
+    if (n_new) *n_new = n;
     if (fps) *fps = reinterpret_cast<uint64_t*>(s->fps_local.p);
-    s->dist_stage = 1;
   });
 }
 
@@ -1623,57 +1829,48 @@ int sgx_harvest_merge(sgx_sampler* s, const uint64_t* all_fps, const int64_t* co
                       int32_t rank, int64_t stride, int64_t* n_won) {
   return guard([&] {
     need_ready(s);
-    if (s->dist_stage != 1) throw StateError("sgx_harvest_merge: call sgx_harvest_local first");
     if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank / nranks");
     if (nranks > 1) {
       need(all_fps, "all_fps");
       need(counts, "counts");
     }
     CK(cudaSetDevice(s->c->ctx->device));
-    const long long n_local = s->hpin->new_rows;
-    long long remote = 0;
     std::vector<long long> cnt(nranks, 0);
-    for (int r = 0; r < nranks; ++r) {
-      cnt[r] = counts ? counts[r] : (r == rank ? n_local : 0);
-      if (cnt[r] < 0 || cnt[r] > stride) throw std::invalid_argument("fingerprint count out of range");
-      if (r != rank) remote += cnt[r];
-    }
-    // Room for every remote fingerprint at load factor <= 1/2.
-    s->table_count += remote;
-    ensure_table(s);
-    if (!s->n_of.p || static_cast<int>(s->n_of.n) < nranks) s->n_of.alloc_async(std::max(nranks, 64), s->sh);
-    CK(cudaMemcpyAsync(s->n_of.p, cnt.data(), nranks * sizeof(long long), cudaMemcpyHostToDevice, s->sh));
-    sgx::launch_merge_remote(s->sh, reinterpret_cast<const unsigned long long*>(all_fps), s->n_of.p,
-                             nranks > 1 ? nranks : 0, rank, stride, s->tkeys.p, s->tmeta.p, s->tcap - 1,
-                             s->epoch, s->newmask.p, s->Bp, s->block_count.p, s->hout.p);
-    s->launches += nranks > 1 ? 3 : 2;
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->sh));
-    CK(cudaStreamSynchronize(s->sh));
-    // Locally-new rows another rank claimed still occupy table slots.
-    s->table_count += n_local - s->hpin->new_rows;
-    if (n_won) *n_won = s->hpin->new_rows;
-    s->dist_stage = 2;
+    for (int r = 0; r < nranks; ++r) cnt[r] = counts ? counts[r] : (r == rank ? s->hpin->new_rows : 0);
+    long long fresh = 0;
+    const long long won = dist_merge(s, all_fps, cnt, rank, stride, &fresh);
+    if (n_won) *n_won = won;
   });
 }
 
 int sgx_harvest_commit(sgx_sampler* s, int64_t quota_left, int64_t* attempts, int64_t* added) {
   return guard([&] {
     need_ready(s);
-    if (s->dist_stage != 2) throw StateError("sgx_harvest_commit: call sgx_harvest_merge first");
     CK(cudaSetDevice(s->c->ctx->device));
-    sgx::HarvestOut h = *s->hpin;
-    h.accepted = quota_left < 0 ? h.new_rows : std::min<long long>(h.new_rows, quota_left);
-    h.last_row = -1;
-    h.overflow = 0;
-    *s->hpin = h;
-    CK(cudaMemcpyAsync(s->hout.p, s->hpin, sizeof(sgx::HarvestOut), cudaMemcpyHostToDevice, s->sh));
     long long att = 0, add = 0;
-    harvest_back_launch(s, -1);
-    harvest_back_finish(s, quota_left, &att, &add, -1);  // counts the winners into table_count
+    dist_commit(s, quota_left, &att, &add);
     if (attempts) *attempts = att;
     if (added) *added = add;
-    s->dist_stage = 0;
+  });
+}
+
+int sgx_run_sharded(sgx_sampler* s, const sgx_exchange* ex, sgx_run_stats* stats) {
+  return guard([&] {
+    need(s, "sampler");
+    need(ex, "exchange");
+    if (ex->nranks < 1 || ex->rank < 0 || ex->rank >= ex->nranks) throw std::invalid_argument("bad rank / nranks");
+    if (!ex->allgather_device || !ex->allgather_host) throw std::invalid_argument("exchange without collectives");
+    if (s->cfg.restart_policy == SGX_RESTART_REINIT_ROWS)
+      throw std::invalid_argument("SGX_RESTART_REINIT_ROWS is single-device only (sgx_run)");
+    CK(cudaSetDevice(s->c->ctx->device));
+    if (s->c->layout_ok && !s->c->L.unsat) {
+      reset_solutions(s);
+    } else {
+      s->n_solutions = 0;
+      if (s->drain) s->drain->reset();
+    }
+    sampler_run_sharded(s, ex);
+    if (stats) *stats = s->stats;
   });
 }
 

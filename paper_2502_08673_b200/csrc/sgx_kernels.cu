@@ -2101,7 +2101,7 @@ k_compact_new(const uint32_t* __restrict__ newmask, const int* __restrict__ bloc
 __global__ void __launch_bounds__(kThreads)
 k_merge_remote(const unsigned long long* __restrict__ all_fps, const long long* __restrict__ n_of,
                int nranks, int me, long long stride, unsigned long long* tkeys, unsigned long long* tmeta,
-               uint64_t tmask, uint64_t epoch, uint32_t* newmask) {
+               uint64_t tmask, uint64_t epoch, uint32_t* newmask, unsigned long long* fresh) {
   const long long total = static_cast<long long>(nranks) * stride;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -2117,6 +2117,7 @@ k_merge_remote(const unsigned long long* __restrict__ all_fps, const long long* 
         cur = atomicCAS(tkeys + idx, 0ull, fp);
         if (cur == 0ull) {
           atomicMin(tmeta + idx, static_cast<unsigned long long>((epoch << 32) | 0xffffffffull));
+          atomicAdd(fresh, 1ull);  // |union| = local new + fresh, the same on every rank
           cur = fp;
           idx = ~0ull;  // freshly inserted: nothing local to revoke
           break;
@@ -2430,9 +2431,11 @@ void launch_merge_remote(cudaStream_t st, const unsigned long long* all_fps, con
                          uint64_t tmask, uint64_t epoch, uint32_t* newmask, int Bp, int* block_count,
                          HarvestOut* out) {
   const long long total = static_cast<long long>(nranks) * stride;
+  cudaMemsetAsync(&out->fresh, 0, sizeof(unsigned long long), st);
   if (total > 0)
     k_merge_remote<<<grid_for(total, kThreads, 148 * 32), kThreads, 0, st>>>(all_fps, n_of, nranks, me, stride,
-                                                                          tkeys, tmeta, tmask, epoch, newmask);
+                                                                          tkeys, tmeta, tmask, epoch, newmask,
+                                                                          &out->fresh);
   const int nb = Bp / kThreads;
   k_count_new<<<nb, kThreads, 0, st>>>(newmask, Bp, block_count);
   k_scan_blocks<<<1, 1024, 0, st>>>(block_count, nb, -1, out);

@@ -88,6 +88,7 @@ struct HarvestOut {
   long long accepted;    // rows appended to the solution store
   long long last_row;    // row of the last accepted solution (quota cut)
   long long overflow;    // solution store too small: grow and re-append
+  unsigned long long fresh;  // multi-GPU merge: remote fingerprints new to the table
 };
 
 }  // namespace sgx

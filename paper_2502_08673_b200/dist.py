@@ -227,3 +227,121 @@ def run_sharded(shard, ex, cfg, rank: int, world: int, stride: int) -> ShardStat
         restart += 1
     st.wall_time_s = time.perf_counter() - t0
     return st
+
+
+# --------------------------------------------------------------- native loop
+# sgx_run_sharded: the same protocol in C++ below the C-ABI (one all-gather
+# of fingerprints per harvest; the union's size is derived locally).  Python
+# only supplies the collective: the library's NCCL exchange (one process per
+# GPU), its in-process exchange (one thread per rank), or torch.distributed
+# through callbacks (gloo, host-staged: several ranks on one GPU in tests).
+
+def nccl_unique_id() -> bytes:
+    L = _lib.load()
+    buf = C.create_string_buffer(128)
+    _lib.check(L.sgx_nccl_unique_id(buf))
+    return buf.raw
+
+
+class NcclExchange:
+    """The library's NCCL communicator (ncclAllGather on the sampler stream)."""
+
+    def __init__(self, world: int, uid: bytes, rank: int, device: int):
+        self.L = _lib.load()
+        self.ex = _lib.Exchange()
+        _lib.check(self.L.sgx_exchange_nccl_create(world, uid, rank, device, C.byref(self.ex)))
+
+    def close(self):
+        if self.ex.user:
+            _lib.check(self.L.sgx_exchange_nccl_destroy(C.byref(self.ex)))
+
+
+class LocalExchanges:
+    """In-process group: exchanges[r] for the host thread running rank r."""
+
+    def __init__(self, world: int):
+        self.L = _lib.load()
+        self.arr = (_lib.Exchange * world)()
+        _lib.check(self.L.sgx_exchange_local_create(world, self.arr))
+
+    def __getitem__(self, r):
+        return self.arr[r]
+
+    def close(self):
+        if self.arr[0].user:
+            _lib.check(self.L.sgx_exchange_local_destroy(C.byref(self.arr[0])))
+
+
+class TorchCallbackExchange:
+    """torch.distributed collectives behind the C callbacks.  With gloo the
+    device payload is staged through host memory (the sampler stream is
+    synchronised first, and recv is written before returning)."""
+
+    def __init__(self, device: int, group=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.group = torch, dist, group
+        self.device = device
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.host_staged = dist.get_backend(group) == "gloo"
+        self._dev = _lib.ALLGATHER_DEVICE(self._allgather_device)
+        self._host = _lib.ALLGATHER_HOST(self._allgather_host)
+        self.ex = _lib.Exchange(None, self.rank, self.world, self._dev, self._host)
+
+    def _view(self, ptr, nbytes):
+        t = self.torch
+        arr = _DevArray(ptr, nbytes // 8, self.device)
+        return t.as_tensor(arr, device=f"cuda:{self.device}")
+
+    def _allgather_device(self, user, send, recv, nbytes, stream):
+        try:
+            t = self.torch
+            t.cuda.ExternalStream(stream, device=f"cuda:{self.device}").synchronize()
+            src = self._view(send, nbytes)
+            dst = self._view(recv, nbytes * self.world)
+            if self.host_staged:
+                out = t.empty(self.world * (nbytes // 8), dtype=t.int64)
+                self.dist.all_gather_into_tensor(out, src.cpu(), group=self.group)
+                dst.copy_(out)
+            else:
+                self.dist.all_gather_into_tensor(dst, src.clone(), group=self.group)
+            t.cuda.synchronize(self.device)
+            return 0
+        except Exception as e:  # noqa: BLE001 -- reported through the status code
+            print(f"allgather_device failed: {e!r}", flush=True)
+            return -1
+
+    def _allgather_host(self, user, send, recv, n):
+        try:
+            t = self.torch
+            x = t.tensor([send[i] for i in range(n)], dtype=t.int64)
+            dev = "cpu" if self.host_staged else f"cuda:{self.device}"
+            out = t.empty(self.world * n, dtype=t.int64, device=dev)
+            self.dist.all_gather_into_tensor(out, x.to(dev), group=self.group)
+            for i, v in enumerate(out.cpu().tolist()):
+                recv[i] = v
+            return 0
+        except Exception as e:  # noqa: BLE001
+            print(f"allgather_host failed: {e!r}", flush=True)
+            return -1
+
+    def close(self):
+        pass
+
+
+def run_native(sampler, ex) -> ShardStats:
+    """sgx_run_sharded on this rank's sampler; ex is an _lib.Exchange or one
+    of the wrappers above.  Returns the global statistics."""
+    import numpy as np
+    L = _lib.load()
+    exs = ex.ex if hasattr(ex, "ex") else ex
+    st = _lib.RunStatsC()
+    _lib.check(L.sgx_run_sharded(sampler.h, C.byref(exs), C.byref(st)))
+    loss = np.zeros(max(1, st.n_loss), np.float64)
+    nu = np.zeros(max(1, st.n_harvest), np.int64)
+    _lib.check(L.sgx_run_traces(sampler.h, _lib.ptr(loss, C.c_double), _lib.ptr(nu, C.c_int64)))
+    return ShardStats(unique_count=st.unique_count, local_count=int(L.sgx_solution_count(sampler.h)),
+                      attempts=st.attempts, restarts=st.restarts, timed_out=bool(st.timed_out),
+                      loss_trace=[float(x) for x in loss[:st.n_loss]],
+                      new_unique=[int(x) for x in nu[:st.n_harvest]], wall_time_s=st.wall_time_s)

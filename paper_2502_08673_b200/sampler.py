@@ -294,12 +294,15 @@ class Sampler:
 
     def soft_info(self) -> dict:
         """Which soft-pass kernel ran the last step ("hbm" / "jit" / "onchip"),
-        steps run by the specialised kernel, its compile state and time."""
-        out = np.zeros(4, np.int64)
+        steps run by the specialised kernel, its compile state and time, and
+        the harvest kernel / words per CTA / samples per lane selected."""
+        out = np.zeros(8, np.int64)
         _lib.check(self.L.sgx_sampler_soft_info(self.h, _lib.ptr(out, C.c_int64)))
         return {"last": ["hbm", "jit", "onchip"][int(out[0])], "jit_steps": int(out[1]),
                 "jit_state": {-1: "none", 0: "compiling", 1: "ready", 2: "failed"}[int(out[2])],
-                "jit_compile_ms": out[3] / 1000.0}
+                "jit_compile_ms": out[3] / 1000.0,
+                "harvest": ["global", "smem", "live"][int(out[4])], "harvest_wpc": int(out[5]),
+                "vec": int(out[6]), "padded_batch": int(out[7])}
 
     def launch_count(self) -> int:
         """Kernels launched since the last run() (or creation)."""
