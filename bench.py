@@ -296,9 +296,21 @@ def run_b200_arm(args, world, rank, local, dist):
                              RestartPolicy.NONE, max_restarts=max(1, restarts - 1),
                              row_offset=rank * batch, solution_capacity=cap)
 
+    ex = None
+    if world > 1:
+        from paper_2502_08673_b200 import dist as D
+        if dist.get_backend() == "gloo":  # test set-up: ranks share GPUs, payloads via the host
+            ex = D.TorchCallbackExchange(device=dev)
+        else:  # the library's own NCCL communicator (id from rank 0)
+            uid = [D.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            ex = D.NcclExchange(world, uid[0], rank, dev)
     sampler = Sampler(dc, cfg_for(max(1, args.warmup)))
     if args.warmup > 0:
-        sampler.run()
+        if world > 1:
+            D.run_native(sampler, ex)
+        else:
+            sampler.run()
     sampler.close()
     sampler = Sampler(dc, cfg_for(args.steps))
     if dist:
@@ -316,15 +328,13 @@ def run_b200_arm(args, world, rank, local, dist):
         global_unique = st.unique_count
         restarts_done, attempts, launches, ph = st.restarts + 1, st.attempts, st.launches, st.phase_ms
     else:
-        # Sample sharding with the per-harvest NCCL all-gather of fingerprints
-        # (dist.py); every harvest synchronises the device, so the timed
-        # wall clock is device-bound.  Max over ranks.
-        from paper_2502_08673_b200.dist import DeviceShard, TorchExchange, run_sharded
-        shard = DeviceShard(sampler)
-        ex = TorchExchange(device=f"cuda:{dev}")
+        # Sample sharding, the loop in C++ (sgx_run_sharded): one NCCL
+        # all-gather of the harvest's new fingerprints per harvest, on the
+        # sampler's stream.  Every harvest synchronises the host with its
+        # device, so the timed wall clock is device-bound.  Max over ranks.
         with ClockSampler(dev) as clk:
             t0 = time.perf_counter()
-            sst = run_sharded(shard, ex, cfg_for(args.steps), rank, world, shard.stride)
+            sst = D.run_native(sampler, ex)
             torch.cuda.synchronize(dev)
             wall = time.perf_counter() - t0
         t_dev = torch.tensor([wall], dtype=torch.float64, device=coll_dev)
@@ -354,11 +364,9 @@ def run_b200_arm(args, world, rank, local, dist):
         e2e_unique, d2h = res.stats.unique_count, res.solutions.keys.nbytes
         e2e_keys = res.solutions.keys
     else:
-        from paper_2502_08673_b200.dist import DeviceShard, TorchExchange, run_sharded
         dc2 = DeviceCircuit.from_instance(inst, device=dev)
         s2 = Sampler(dc2, e2e_cfg)
-        sh2 = DeviceShard(s2)
-        est = run_sharded(sh2, TorchExchange(device=f"cuda:{dev}"), e2e_cfg, rank, world, sh2.stride)
+        est = D.run_native(s2, ex)
         e2e_keys = s2.fetch()
         d2h = e2e_keys.nbytes
         e2e_unique = est.unique_count
@@ -379,6 +387,8 @@ def run_b200_arm(args, world, rank, local, dist):
         dist.all_reduce(t_i, op=dist.ReduceOp.SUM)
         chk["invalid"], chk["checked"] = int(t_i[0].item()), int(t_i[1].item())
     del e2e_keys
+    if ex is not None:
+        ex.close()
     e2e = {"value": e2e_unique / e2e_wall, "unit": UNIT,
            "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
            "wall_s": e2e_wall}

@@ -109,7 +109,19 @@ typedef struct {
   int64_t solution_capacity; /* initial device solution store, 0 = auto  */
   int32_t max_restarts;    /* safety valve, reference uses 1000          */
   int32_t soft_kernel;     /* sgx_soft_kernel: which soft-pass kernels    */
+  int32_t optimizer;       /* sgx_optimizer; 0 = the reference's GD       */
+  double adam_beta1;       /* SGX_OPT_ADAM only; 0 = 0.9                  */
+  double adam_beta2;       /* 0 = 0.999                                   */
+  double adam_eps;         /* 0 = 1e-8                                    */
 } sgx_sampler_cfg;
+
+/* Logit update.  GD is the reference's gd_step (V -= lr dV, autodiff.cpp:
+ * 285-290) and the default.  ADAM is an extension the reference lacks
+ * (SPEC.md:418 lists adaptive optimizers as a non-goal, so it has no parity
+ * anchor): per logit m = b1 m + (1 - b1) dV, v = b2 v + (1 - b2) dV^2,
+ * V -= lr (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps), with m, v, t reset
+ * by every init (restart).  It runs the HBM soft kernels. */
+enum sgx_optimizer { SGX_OPT_GD = 0, SGX_OPT_ADAM = 1 };
 
 /* Soft pass (embed + forward + loss + backward + GD + harden) kernels.  All
  * are bit-identical; they differ only in speed.
@@ -236,6 +248,10 @@ typedef struct sgx_exchange {
 } sgx_exchange;
 
 int sgx_run_sharded(sgx_sampler* s, const sgx_exchange* ex, sgx_run_stats* stats);
+/* After sgx_run_sharded: how many of each harvest's new solutions this rank
+ * stored (stats.n_harvest entries).  Rank order within a harvest is the
+ * reference's insertion order over the union. */
+int sgx_run_local_added(const sgx_sampler* s, int64_t* added);
 
 /* NCCL: rank 0 makes the id, the caller distributes it (MPI, torch.distributed,
  * a file), every rank creates its exchange on its device. */

@@ -22,6 +22,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "satgrad/circuit.hpp"
@@ -175,17 +176,10 @@ inline int verify(const satgrad::CnfFormula& cnf, const std::string& text, std::
   return static_cast<int>(out[3]);
 }
 
-// satgrad::run (sampler.hpp:79-81) on device `device`.
-inline satgrad::RunResult run(const satgrad::CnfFormula& cnf, const satgrad::Circuit& c,
-                              const satgrad::ExtractionResult& res,
-                              const satgrad::PathClassification& paths,
-                              const satgrad::SamplerConfig& cfg, int device = 0) {
+namespace detail {
+inline sgx_sampler_cfg sampler_cfg(const satgrad::SamplerConfig& cfg) {
   if (!cfg.use_f32)
     throw std::invalid_argument("satgrad_b200 implements the f32 instantiation (use_f32 = true)");
-  Desc desc(cnf, c, res, paths);
-  sgx_circuit* circ = nullptr;
-  check(sgx_circuit_upload(context(device), &desc.d, &circ));
-  std::unique_ptr<sgx_circuit, int (*)(sgx_circuit*)> circ_guard(circ, sgx_circuit_free);
   sgx_sampler_cfg sc{};
   sc.batch = cfg.batch;
   sc.iterations = cfg.iterations;
@@ -195,6 +189,52 @@ inline satgrad::RunResult run(const satgrad::CnfFormula& cnf, const satgrad::Cir
   sc.timeout_s = cfg.timeout_s;
   sc.restart_policy = cfg.restart == satgrad::RestartPolicy::ReinitOnExhaust ? SGX_RESTART_REINIT_ON_EXHAUST
                                                                               : SGX_RESTART_NONE;
+  return sc;
+}
+
+inline void fill_stats(satgrad::RunResult& out, const sgx_run_stats& st, const satgrad::ExtractionResult& res) {
+  out.stats.unique_count = st.unique_count;
+  out.stats.attempts = st.attempts;
+  out.stats.wall_time_s = st.wall_time_s;
+  out.stats.throughput = st.throughput;
+  out.stats.restarts = st.restarts;
+  out.stats.timed_out = st.timed_out != 0;
+  if (st.unsat) out.stats.note = res.unsat_note.empty() ? "unsatisfiable by construction" : res.unsat_note;
+}
+
+// Keys [first, first + n) of the packed [rows][words] block -> SolutionSet.
+inline void insert_keys(satgrad::RunResult& out, const uint64_t* keys, int64_t first, int64_t n, int words,
+                        int num_vars) {
+  satgrad::Assignment a(num_vars + 1, 0);
+  for (int64_t i = first; i < first + n; ++i) {
+    for (int v = 1; v <= num_vars; ++v)
+      a[v] = (keys[static_cast<size_t>(i) * words + (v - 1) / 64] >> ((v - 1) % 64)) & 1;
+    out.solutions.insert(a);
+  }
+}
+
+struct HostKeys {
+  uint64_t* p = nullptr;
+  int64_t n = 0, bytes = 0;
+  HostKeys() = default;
+  HostKeys(const HostKeys&) = delete;
+  HostKeys& operator=(const HostKeys&) = delete;
+  ~HostKeys() {
+    if (p) sgx_host_free(p, bytes);
+  }
+};
+}  // namespace detail
+
+// satgrad::run (sampler.hpp:79-81) on device `device`.
+inline satgrad::RunResult run(const satgrad::CnfFormula& cnf, const satgrad::Circuit& c,
+                              const satgrad::ExtractionResult& res,
+                              const satgrad::PathClassification& paths,
+                              const satgrad::SamplerConfig& cfg, int device = 0) {
+  sgx_sampler_cfg sc = detail::sampler_cfg(cfg);
+  Desc desc(cnf, c, res, paths);
+  sgx_circuit* circ = nullptr;
+  check(sgx_circuit_upload(context(device), &desc.d, &circ));
+  std::unique_ptr<sgx_circuit, int (*)(sgx_circuit*)> circ_guard(circ, sgx_circuit_free);
   sgx_sampler* s = nullptr;
   check(sgx_sampler_create(circ, &sc, &s));
   std::unique_ptr<sgx_sampler, int (*)(sgx_sampler*)> s_guard(s, sgx_sampler_free);
@@ -205,13 +245,7 @@ inline satgrad::RunResult run(const satgrad::CnfFormula& cnf, const satgrad::Cir
 
   satgrad::RunResult out;
   out.solutions = satgrad::SolutionSet(cnf.num_vars);
-  out.stats.unique_count = st.unique_count;
-  out.stats.attempts = st.attempts;
-  out.stats.wall_time_s = st.wall_time_s;
-  out.stats.throughput = st.throughput;
-  out.stats.restarts = st.restarts;
-  out.stats.timed_out = st.timed_out != 0;
-  if (st.unsat) out.stats.note = res.unsat_note.empty() ? "unsatisfiable by construction" : res.unsat_note;
+  detail::fill_stats(out, st, res);
   out.stats.loss_trace.resize(st.n_loss);
   std::vector<int64_t> nu(st.n_harvest);
   check(sgx_run_traces(s, out.stats.loss_trace.data(), nu.data()));
@@ -220,22 +254,97 @@ inline satgrad::RunResult run(const satgrad::CnfFormula& cnf, const satgrad::Cir
   // Solutions in insertion order -> SolutionSet (dedupe_key layout).  The
   // keys are already on the host: take them without a copy.
   const int32_t words = sgx_key_words(s);
-  uint64_t* kp = nullptr;
-  int64_t n = 0, map_bytes = 0;
-  check(sgx_solutions_take(s, &kp, &n, &map_bytes));
-  struct HostKeys {
-    uint64_t* p;
-    int64_t bytes;
-    ~HostKeys() { sgx_host_free(p, bytes); }
-  } hold{kp, map_bytes};
-  const uint64_t* keys = kp;
-  satgrad::Assignment a(cnf.num_vars + 1, 0);
-  for (int64_t i = 0; i < n; ++i) {
-    for (int v = 1; v <= cnf.num_vars; ++v)
-      a[v] = (keys[static_cast<size_t>(i) * words + (v - 1) / 64] >> ((v - 1) % 64)) & 1;
-    out.solutions.insert(a);
-  }
+  detail::HostKeys hk;
+  check(sgx_solutions_take(s, &hk.p, &hk.n, &hk.bytes));
+  detail::insert_keys(out, hk.p, 0, hk.n, words, cnf.num_vars);
   return out;
+}
+
+// satgrad::run sample-sharded over several GPUs: one host
+// thread per entry of `devices` (entries may repeat: {0, 0} runs two ranks on
+// one GPU).  Rank g samples global rows [g*b, (g+1)*b) with
+// b = cfg.batch / devices.size(), and the ranks exchange 64-bit fingerprints
+// once per harvest (sgx_run_sharded over the library's in-process exchange),
+// so the result -- the same solutions in the same order, the same counters --
+// is satgrad::run at cfg.batch.  The loss trace is the mean over ranks of
+// each rank's mean row loss, i.e. the union's mean.
+inline satgrad::RunResult run(const satgrad::CnfFormula& cnf, const satgrad::Circuit& c,
+                              const satgrad::ExtractionResult& res,
+                              const satgrad::PathClassification& paths,
+                              const satgrad::SamplerConfig& cfg, const std::vector<int>& devices) {
+  const int R = static_cast<int>(devices.size());
+  if (R < 1) throw std::invalid_argument("run: empty device list");
+  if (R == 1) return run(cnf, c, res, paths, cfg, devices[0]);
+  if (cfg.batch % R != 0) throw std::invalid_argument("run: batch must divide evenly over the devices");
+  sgx_sampler_cfg sc = detail::sampler_cfg(cfg);
+  sc.batch = cfg.batch / R;
+  Desc desc(cnf, c, res, paths);
+  std::vector<sgx_exchange> ex(R);
+  check(sgx_exchange_local_create(R, ex.data()));
+  struct Rank {
+    sgx_circuit* circ = nullptr;
+    sgx_sampler* s = nullptr;
+    sgx_run_stats st{};
+    int rc = 0;
+    std::string err;
+  };
+  std::vector<Rank> rk(R);
+  auto cleanup = [&] {
+    for (Rank& r : rk) {
+      if (r.s) sgx_sampler_free(r.s);
+      if (r.circ) sgx_circuit_free(r.circ);
+    }
+    sgx_exchange_local_destroy(&ex[0]);
+  };
+  try {
+    for (int g = 0; g < R; ++g) {
+      check(sgx_circuit_upload(context(devices[g]), &desc.d, &rk[g].circ));
+      sgx_sampler_cfg cg = sc;
+      cg.row_offset = static_cast<int64_t>(g) * sc.batch;
+      check(sgx_sampler_create(rk[g].circ, &cg, &rk[g].s));
+    }
+    std::vector<std::thread> th;
+    for (int g = 0; g < R; ++g)
+      th.emplace_back([&, g] {
+        rk[g].rc = sgx_run_sharded(rk[g].s, &ex[g], &rk[g].st);
+        if (rk[g].rc) rk[g].err = sgx_last_error();
+      });
+    for (auto& t : th) t.join();
+    for (Rank& r : rk)
+      if (r.rc) throw std::runtime_error("satgrad_b200 sharded run: " + r.err);
+
+    satgrad::RunResult out;
+    out.solutions = satgrad::SolutionSet(cnf.num_vars);
+    detail::fill_stats(out, rk[0].st, res);
+    const int nh = rk[0].st.n_harvest, nl = rk[0].st.n_loss;
+    out.stats.loss_trace.assign(nl, 0.0);
+    std::vector<std::vector<int64_t>> added(R, std::vector<int64_t>(nh));
+    std::vector<std::unique_ptr<detail::HostKeys>> keys(R);
+    for (int g = 0; g < R; ++g) {
+      std::vector<double> lt(nl);
+      std::vector<int64_t> nu(nh);
+      check(sgx_run_traces(rk[g].s, lt.data(), nu.data()));
+      for (int i = 0; i < nl; ++i) out.stats.loss_trace[i] += lt[i] / R;
+      if (g == 0) out.stats.new_unique.assign(nu.begin(), nu.end());
+      check(sgx_run_local_added(rk[g].s, added[g].data()));
+      keys[g] = std::make_unique<detail::HostKeys>();
+      check(sgx_solutions_take(rk[g].s, &keys[g]->p, &keys[g]->n, &keys[g]->bytes));
+    }
+    // insertion order over the union: harvest by harvest, ranks in order
+    const int32_t words = sgx_key_words(rk[0].s);
+    std::vector<int64_t> at(R, 0);
+    for (int h = 0; h < nh; ++h)
+      for (int g = 0; g < R; ++g) {
+        detail::insert_keys(out, keys[g]->p, at[g], added[g][h], words, cnf.num_vars);
+        at[g] += added[g][h];
+      }
+    keys.clear();
+    cleanup();
+    return out;
+  } catch (...) {
+    cleanup();
+    throw;
+  }
 }
 
 }  // namespace satgrad_b200

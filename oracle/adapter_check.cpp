@@ -85,6 +85,21 @@ int main(int argc, char** argv) {
     double a = cpu.stats.loss_trace[i], b = gpu.stats.loss_trace[i];
     expect(std::fabs(a - b) <= 1e-4 * std::fmax(std::fabs(a), 1e-30), "loss_trace value");
   }
+  // satgrad_b200::run over two ranks (sgx_run_sharded, in-process exchange,
+  // both on device 0): the union of the shards is the reference's run
+  if (cfg.batch % 2 == 0) {
+    satgrad::RunResult sh = satgrad_b200::run(cnf, c, res, paths, cfg, std::vector<int>{0, 0});
+    expect(satgrad::format_solutions(cpu.solutions) == satgrad::format_solutions(sh.solutions), "sharded solutions");
+    expect(cpu.stats.unique_count == sh.stats.unique_count, "sharded unique_count");
+    expect(cpu.stats.attempts == sh.stats.attempts, "sharded attempts");
+    expect(cpu.stats.new_unique == sh.stats.new_unique, "sharded new_unique");
+    expect(cpu.stats.restarts == sh.stats.restarts, "sharded restarts");
+    expect(cpu.stats.loss_trace.size() == sh.stats.loss_trace.size(), "sharded loss_trace length");
+    for (size_t i = 0; i < cpu.stats.loss_trace.size() && i < sh.stats.loss_trace.size(); ++i) {
+      double a = cpu.stats.loss_trace[i], b = sh.stats.loss_trace[i];
+      expect(std::fabs(a - b) <= 1e-4 * std::fmax(std::fabs(a), 1e-30), "sharded loss_trace value");
+    }
+  }
   // satgrad_b200::verify (cmd_verify on the GPU) on the reference's own text:
   // all lines pass; a repeated first line is a duplicate one line past the end
   {

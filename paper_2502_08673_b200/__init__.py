@@ -9,7 +9,7 @@ from .cnf import CnfFormula, ParseError, eval_cnf, parse_dimacs, verify_keys, wr
 from .circuit import (Circuit, Instance, PathClassification, SchemaError, classify_paths,
                       export_json, import_json, load_instance)
 from .extract import ExtractionResult, extract_circuit, instance_from_cnf
-from .sampler import (DeviceCircuit, RestartPolicy, SoftKernel, jit_source, RunResult, RunStats, Sampler, SamplerConfig,
+from .sampler import (DeviceCircuit, Optimizer, RestartPolicy, SoftKernel, jit_source, RunResult, RunStats, Sampler, SamplerConfig,
                       SolutionSet, layout_stats, run, run_instance, verify_solutions)
 
 __all__ = [

@@ -28,7 +28,7 @@ EXPORTS = [
     "sgx_extraction_export", "sgx_extraction_note", "sgx_extraction_free", "sgx_verify_solutions",
     "sgx_verify_cnf", "sgx_jit_source", "sgx_sampler_soft_info", "sgx_verify_keys",
     "sgx_run_sharded", "sgx_nccl_unique_id", "sgx_exchange_nccl_create", "sgx_exchange_nccl_destroy",
-    "sgx_exchange_local_create", "sgx_exchange_local_destroy",
+    "sgx_exchange_local_create", "sgx_exchange_local_destroy", "sgx_run_local_added",
 ]
 
 
@@ -56,6 +56,8 @@ class SamplerCfg(C.Structure):
         ("seed", C.c_uint64), ("max_solutions", C.c_int64), ("timeout_s", C.c_double),
         ("restart_policy", C.c_int32), ("row_offset", C.c_int64),
         ("solution_capacity", C.c_int64), ("max_restarts", C.c_int32), ("soft_kernel", C.c_int32),
+        ("optimizer", C.c_int32), ("adam_beta1", C.c_double), ("adam_beta2", C.c_double),
+        ("adam_eps", C.c_double),
     ]
 
 
@@ -152,6 +154,7 @@ def load() -> C.CDLL:
         "sgx_exchange_nccl_destroy": (C.c_int, [C.POINTER(Exchange)]),
         "sgx_exchange_local_create": (C.c_int, [i32, C.POINTER(Exchange)]),
         "sgx_exchange_local_destroy": (C.c_int, [C.POINTER(Exchange)]),
+        "sgx_run_local_added": (C.c_int, [vp, i64p]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

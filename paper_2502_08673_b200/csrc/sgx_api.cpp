@@ -357,6 +357,8 @@ struct sgx_sampler {
   int hb_cur = 0;       // HB holds two buffers; the last init / step wrote this one
   DBuf<uint32_t> SP;  // its spill tape of CNF-variable rows [n_spill][W]
   DBuf<float> V, tape, adj, row_loss;
+  DBuf<float> adam_dv, adam_dp, adam_m, adam_v;  // SGX_OPT_ADAM: dV (and dP) of the step, moments
+  int adam_t = 0;                                // steps since the last init
   DBuf<double> partial;
   DBuf<uint32_t> BT, valid, newmask;
   DBuf<uint32_t> HB;  // hardened V columns [word][ncpi] (shared-memory harvest input)
@@ -391,6 +393,7 @@ struct sgx_sampler {
   // last run
   std::vector<double> loss_trace;
   std::vector<int64_t> new_unique;
+  std::vector<int64_t> local_added;  // sgx_run_sharded: this rank's share of each harvest
   sgx_run_stats stats{};
   double phase_ms[8] = {0};
   double host_ms[8] = {0};  // harvest wall, table growth, store growth, (spare)
@@ -453,6 +456,11 @@ void sampler_init(sgx_sampler* s, int restart) {
   sgx::launch_init_v(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, 32 * s->vec, prefix,
                      s->cfg.row_offset, hb_write(s));
   s->launches += L.cpi.empty() ? 0 : 1;
+  if (s->cfg.optimizer == SGX_OPT_ADAM) {
+    CK(cudaMemsetAsync(s->adam_m.p, 0, s->adam_m.n * sizeof(float), s->st));
+    CK(cudaMemsetAsync(s->adam_v.p, 0, s->adam_v.n * sizeof(float), s->st));
+    s->adam_t = 0;
+  }
   CK(cudaEventRecord(s->ev_soft, s->st));
   CK(cudaGetLastError());
 }
@@ -543,9 +551,22 @@ int sampler_step(sgx_sampler* s) {
     CK(cudaEventRecord(ev[1], s->st));
     if (harvest_reads_v(s)) CK(cudaStreamWaitEvent(s->st, s->ev_front, 0));  // the running harvest reads V
     CK(cudaEventRecord(ev[2], s->st));
-    backward(s->st, s->vec, c->cone, s->tape.p, s->adj.p, s->V.p, ncpi, nullptr, nullptr, s->Bp,
-             static_cast<float>(s->cfg.learning_rate), c->out_tgt.p, static_cast<int>(c->L.out_node.size()),
-             s->row_loss.p, tab, hb);
+    if (s->cfg.optimizer == SGX_OPT_ADAM) {
+      // dV out of the backward (its V update and hardening skipped), then Adam
+      backward(s->st, s->vec, c->cone, s->tape.p, s->adj.p, s->V.p, ncpi, s->adam_dv.p, s->adam_dp.p, s->Bp,
+               static_cast<float>(s->cfg.learning_rate), c->out_tgt.p, static_cast<int>(c->L.out_node.size()),
+               s->row_loss.p, tab, nullptr);
+      const auto& cf = s->cfg;
+      sgx::launch_adam(s->st, s->V.p, s->adam_dv.p, s->adam_m.p, s->adam_v.p, ncpi, s->Bp, 32 * s->vec,
+                       static_cast<float>(cf.learning_rate), static_cast<float>(cf.adam_beta1 > 0 ? cf.adam_beta1 : 0.9),
+                       static_cast<float>(cf.adam_beta2 > 0 ? cf.adam_beta2 : 0.999), ++s->adam_t,
+                       static_cast<float>(cf.adam_eps > 0 ? cf.adam_eps : 1e-8), hb);
+      s->launches += 1;
+    } else {
+      backward(s->st, s->vec, c->cone, s->tape.p, s->adj.p, s->V.p, ncpi, nullptr, nullptr, s->Bp,
+               static_cast<float>(s->cfg.learning_rate), c->out_tgt.p, static_cast<int>(c->L.out_node.size()),
+               s->row_loss.p, tab, hb);
+    }
   }
   sgx::launch_loss(s->st, s->row_loss.p, s->cfg.batch, s->partial.p, s->n_partial, s->dloss.p + slot);
   s->launches += s->last_soft == 0 ? 4 : 3;
@@ -989,6 +1010,7 @@ void sampler_run_sharded(sgx_sampler* s, const sgx_exchange* ex) {
   const int R = ex->nranks, me = ex->rank;
   s->loss_trace.clear();
   s->new_unique.clear();
+  s->local_added.clear();
   s->stats = sgx_run_stats{};
   std::fill(s->phase_ms, s->phase_ms + 8, 0.0);
   std::fill(s->host_ms, s->host_ms + 8, 0.0);
@@ -1049,6 +1071,7 @@ void sampler_run_sharded(sgx_sampler* s, const sgx_exchange* ex) {
     }
     unique += acc;
     s->new_unique.push_back(acc);
+    s->local_added.push_back(add);
     s->host_ms[0] += std::chrono::duration<double, std::milli>(clock::now() - h0).count();
     return slot;
   };
@@ -1282,6 +1305,10 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
     if (cfg->iterations < 0) throw std::invalid_argument("iterations must be non-negative");
     if (cfg->restart_policy < SGX_RESTART_NONE || cfg->restart_policy > SGX_RESTART_REINIT_ROWS)
       throw std::invalid_argument("unknown restart policy");
+    if (cfg->optimizer != SGX_OPT_GD && cfg->optimizer != SGX_OPT_ADAM) throw std::invalid_argument("unknown optimizer");
+    if (cfg->optimizer == SGX_OPT_ADAM &&
+        (cfg->adam_beta1 < 0 || cfg->adam_beta1 >= 1 || cfg->adam_beta2 < 0 || cfg->adam_beta2 >= 1 || cfg->adam_eps < 0))
+      throw std::invalid_argument("Adam needs 0 <= beta1, beta2 < 1 and eps >= 0");
     CK(cudaSetDevice(c->ctx->device));
     auto s = std::make_unique<sgx_sampler>();
     s->c = c;
@@ -1349,7 +1376,8 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
             if (e[0] == '0') mode = SGX_SOFT_HBM;
             else if (e[0] == 's') mode = SGX_SOFT_JIT;
           }
-          if (mode != SGX_SOFT_HBM && !s->onchip && sgx::jit_eligible(L)) {
+          if (cfg->optimizer == SGX_OPT_ADAM) mode = SGX_SOFT_HBM;  // Adam runs the HBM kernels' dV tap
+        if (mode != SGX_SOFT_HBM && !s->onchip && sgx::jit_eligible(L)) {
             if (!c->jit) c->jit = sgx::jit_get(L, mode != SGX_SOFT_JIT);
             if (mode == SGX_SOFT_JIT) sgx::jit_wait(c->jit.get());
             if (!sgx::jit_failed(c->jit.get())) s->jit = c->jit.get();
@@ -1467,7 +1495,8 @@ int sgx_sampler_free(sgx_sampler* s) {
     s->drain.reset();                          // no host copy left reading the store
     const double t_drain = ms();
     if (st) {  // hand the big buffers back to the pool in stream order
-      for (auto* b : {&s->V, &s->tape, &s->adj, &s->row_loss}) b->reset_async(st);
+      for (auto* b : {&s->V, &s->tape, &s->adj, &s->row_loss, &s->adam_dv, &s->adam_dp, &s->adam_m, &s->adam_v})
+        b->reset_async(st);
       s->partial.reset_async(st);
       for (auto* b : {&s->BT, &s->valid, &s->newmask, &s->HB, &s->SP}) b->reset_async(st);
       s->fps_local.reset_async(st);
@@ -1851,6 +1880,14 @@ int sgx_harvest_commit(sgx_sampler* s, int64_t quota_left, int64_t* attempts, in
     dist_commit(s, quota_left, &att, &add);
     if (attempts) *attempts = att;
     if (added) *added = add;
+  });
+}
+
+int sgx_run_local_added(const sgx_sampler* s, int64_t* added) {
+  return guard([&] {
+    need(s, "sampler");
+    need(added, "added");
+    std::copy(s->local_added.begin(), s->local_added.end(), added);
   });
 }
 

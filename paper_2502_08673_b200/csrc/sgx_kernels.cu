@@ -1341,6 +1341,46 @@ bool launch_soft_onchip(cudaStream_t st, const OnchipArgs& a) {
   return true;
 }
 
+// Opt-in Adam update (sgx_optimizer SGX_OPT_ADAM; no reference counterpart,
+// SPEC.md:418): the backward stored dV (same tile-major layout as V); per
+// logit m, v moments, bias-corrected step, then the harvest's hardened words
+// of the new V (harden, autodiff.cpp:292-297).  One thread per logit, in
+// layout order, so a warp's 32 logits are 32 consecutive samples of one
+// column of one tile (tile_rows >= 32).
+__global__ void __launch_bounds__(kThreads)
+k_adam(float* __restrict__ Vp, const float* __restrict__ dV, float* __restrict__ m, float* __restrict__ v, int ncols,
+       int Bp, int tile_rows, float lr, float b1, float b2, float c1, float c2, float eps, uint32_t* __restrict__ hb) {
+  const long long n = static_cast<long long>(ncols) * Bp;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const float g = dV[i];
+    const float mi = b1 * m[i] + (1.0f - b1) * g;
+    const float vi = b2 * v[i] + (1.0f - b2) * g * g;
+    m[i] = mi;
+    v[i] = vi;
+    const float nv = Vp[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+    Vp[i] = nv;
+    const uint32_t word = __ballot_sync(kFull, nv >= 0.0f);
+    if ((threadIdx.x & 31) == 0) {
+      const long long per_tile = static_cast<long long>(ncols) * tile_rows;
+      const long long tile = i / per_tile, rem = i - tile * per_tile;
+      const int col = static_cast<int>(rem / tile_rows), pos = static_cast<int>(rem - static_cast<long long>(col) * tile_rows);
+      hb[static_cast<size_t>((tile * tile_rows + pos) >> 5) * ncols + col] = word;
+    }
+  }
+}
+
+static int grid_for(long long n, int per_block, int cap);
+
+void launch_adam(cudaStream_t st, float* V, const float* dV, float* m, float* v, int ncols, int Bp, int tile_rows,
+                 float lr, float b1, float b2, int t, float eps, uint32_t* hb) {
+  const long long n = static_cast<long long>(ncols) * Bp;
+  if (n == 0) return;
+  const float c1 = 1.0f - powf(b1, static_cast<float>(t)), c2 = 1.0f - powf(b2, static_cast<float>(t));
+  k_adam<<<grid_for(n, kThreads, 148 * 16), kThreads, 0, st>>>(V, dV, m, v, ncols, Bp, tile_rows, lr, b1, b2, c1, c2,
+                                                              eps, hb);
+}
+
 // Deterministic loss total: fixed per-block partial sums in double, then one
 // block folds the partials in block order.
 __global__ void __launch_bounds__(kThreads)

@@ -37,6 +37,9 @@ void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* 
                          float* dv_out, float* dp_out, int Bp, float lr, const int* out_enc,
                          const uint8_t* out_tgt, int n_out, float* row_loss, const uint64_t* exp_tab,
                          uint32_t* hb, const int* dead, const int2* dead_lvl, const BwdBlocks* bb);
+// Opt-in Adam logit update from a stored dV (step t >= 1 since the last init).
+void launch_adam(cudaStream_t st, float* V, const float* dV, float* m, float* v, int ncols, int Bp, int tile_rows,
+                 float lr, float b1, float b2, int t, float eps, uint32_t* hb);
 void launch_loss(cudaStream_t st, const float* row_loss, int batch, double* partial, int n_partial,
                  double* out);
 void launch_harden(cudaStream_t st, const float* V, int ncpi, int nucpi, const int* cpi_row,

@@ -29,6 +29,13 @@ class SoftKernel(enum.IntEnum):
     JIT = 2   # compile the specialised kernel at sampler creation and wait for it
 
 
+class Optimizer(enum.IntEnum):
+    """Logit update (sgx_optimizer).  GD is the reference's gd_step; ADAM is an
+    opt-in extension with no reference counterpart."""
+    GD = 0
+    ADAM = 1
+
+
 class RestartPolicy(enum.IntEnum):
     NONE = 0
     REINIT_ON_EXHAUST = 1
@@ -52,6 +59,10 @@ class SamplerConfig:
     max_restarts: int = 1000  # sampler.cpp:180 safety valve
     solution_capacity: int = 0
     soft_kernel: SoftKernel = SoftKernel.AUTO
+    optimizer: Optimizer = Optimizer.GD
+    adam_beta1: float = 0.9
+    adam_beta2: float = 0.999
+    adam_eps: float = 1e-8
 
 
 @dataclass
@@ -266,6 +277,8 @@ class Sampler:
         c.solution_capacity = cfg.solution_capacity
         c.max_restarts = cfg.max_restarts
         c.soft_kernel = int(cfg.soft_kernel)
+        c.optimizer = int(cfg.optimizer)
+        c.adam_beta1, c.adam_beta2, c.adam_eps = cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps
         self._cfg = c
         h = C.c_void_p()
         _lib.check(self.L.sgx_sampler_create(dc.h, C.byref(c), C.byref(h)))

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Build an A/B variant of the library: tools/build_variant.sh TAG -DFOO=1 ...
-# -> paper_2502_08673_b200/libsatgrad_b200_TAG.so (run with tools/gpu_ab.sh TAGS=TAG)
+# -> paper_2502_08673_b200/libsatgrad_b200_TAG.so (A/B it with tools/ab.sh "<workloads>" base so:TAG)
 set -e
 tag=$1; shift
 cd "$(dirname "$0")/../paper_2502_08673_b200/csrc"
