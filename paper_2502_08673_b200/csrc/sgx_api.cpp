@@ -655,6 +655,7 @@ void harvest_front(sgx_sampler* s, int restart, int iter, long long quota_left) 
     a.slots = L.lb_slots;
     a.spill = s->SP.p;
     a.W = s->W;
+    a.n_spill = std::max(L.lb_n_spill, 1);
     a.key_enc = c->lb_key_enc.p;
     a.key_words = L.key_words;
     a.batch = s->cfg.batch;
@@ -1365,7 +1366,7 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
         // record control, at 8 warps per SM).
         {
           const char* e = std::getenv("SGX_ONCHIP");
-          s->onchip = e && e[0] == '1' && c->cone.oc_n4 > 0 &&
+          s->onchip = e && e[0] == '1' && cfg->optimizer == SGX_OPT_GD && c->cone.oc_n4 > 0 &&
                       sgx::onchip_warps(c->cone.n_rows, c->cone.oc_slots, c->cone.oc_n4) >= 2;
           if (s->onchip) s->vec = 1;
         }
@@ -1450,6 +1451,11 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
           s->tape.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
           s->adj.alloc_async(static_cast<size_t>(L.cone.n_rows) * Bp, st);
           s->have_tape = true;
+        }
+        if (cfg->optimizer == SGX_OPT_ADAM) {
+          for (auto* b : {&s->adam_dv, &s->adam_dp, &s->adam_m, &s->adam_v}) b->alloc_async(L.cpi.size() * Bp, st);
+          CK(cudaMemsetAsync(s->adam_m.p, 0, s->adam_m.n * sizeof(float), st));
+          CK(cudaMemsetAsync(s->adam_v.p, 0, s->adam_v.n * sizeof(float), st));
         }
         s->row_loss.alloc_async(Bp, st);
         s->partial.alloc_async(s->n_partial, st);

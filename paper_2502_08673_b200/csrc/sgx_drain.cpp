@@ -13,6 +13,7 @@ namespace sgx {
 
 namespace {
 
+struct Done {};  // a job finished early (direct copy)
 constexpr size_t kHuge = size_t{2} << 20;
 
 size_t round_huge(size_t b) { return (b + kHuge - 1) / kHuge * kHuge; }
@@ -83,12 +84,58 @@ Staging& staging(int device) {
 
 // Released result mappings are parked (up to two, 16 GB in all) and handed
 // to the next run: their pages are already faulted in, so a run does not pay
-// the first touch -- or the kernel's huge-page compaction -- again.
+// the first touch -- or the kernel's huge-page compaction -- again.  A parked
+// mapping is also page-locked (cudaHostRegister, once, when it is parked), so
+// the next run's drain DMAs straight into it at PCIe speed instead of through
+// the staging buffers and a host memcpy (C4: 1.3 GB of keys per restart;
+// staged, the copy-out bounded the end-to-end rate).  SGX_PIN_PARKED=0 turns
+// the locking off.
 namespace {
 std::mutex g_cache_mu;
 std::vector<std::pair<void*, size_t>> g_cache;
+std::vector<std::pair<void*, size_t>> g_pinned;  // page-locked mappings (base, bytes)
 constexpr size_t kCacheEntries = 2, kCacheBytes = size_t{16} << 30;
+
+bool pin_parked() {
+  static const bool on = [] {
+    const char* e = std::getenv("SGX_PIN_PARKED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// (g_cache_mu held)
+size_t pinned_bytes(const void* p) {
+  for (auto& e : g_pinned)
+    if (e.first == p) return e.second;
+  return 0;
+}
+void unpin(void* p) {
+  for (size_t i = 0; i < g_pinned.size(); ++i)
+    if (g_pinned[i].first == p) {
+      cudaHostUnregister(p);
+      g_pinned.erase(g_pinned.begin() + static_cast<long>(i));
+      return;
+    }
+}
 }  // namespace
+
+// [dst, dst + n) lies inside one page-locked mapping.
+bool host_range_pinned(const void* dst, size_t n) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  const char* d = static_cast<const char*>(dst);
+  for (auto& e : g_pinned) {
+    const char* b = static_cast<const char*>(e.first);
+    if (d >= b && d + n <= b + e.second) return true;
+  }
+  return false;
+}
+
+// Before a mapping moves or shrinks (mremap / munmap): drop its page lock.
+void host_unpin(void* p) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  unpin(p);
+}
 
 void* host_map(size_t bytes, size_t* actual) {
   const size_t b = round_huge(std::max<size_t>(bytes, 1));
@@ -101,6 +148,7 @@ void* host_map(size_t bytes, size_t* actual) {
       auto [p, n] = g_cache[best];
       g_cache.erase(g_cache.begin() + static_cast<long>(best));
       if (n < b) {
+        unpin(p);
         void* q = mremap(p, n, b, MREMAP_MAYMOVE);
         if (q == MAP_FAILED) {
           munmap(p, n);
@@ -131,8 +179,16 @@ void host_free(void* p, size_t bytes) {
     for (auto& e : g_cache) held += e.second;
     if (g_cache.size() < kCacheEntries && held + b <= kCacheBytes) {
       g_cache.emplace_back(p, b);
+      if (pin_parked() && pinned_bytes(p) != b) {
+        unpin(p);
+        if (cudaHostRegister(p, b, cudaHostRegisterPortable) == cudaSuccess)
+          g_pinned.emplace_back(p, b);
+        else
+          cudaGetLastError();  // (e.g. a locked-memory limit): the staged path stays correct
+      }
       return;
     }
+    unpin(p);
   }
   munmap(p, b);
 }
@@ -205,6 +261,7 @@ void HostDrain::ensure(int64_t rows) {
       cap_bytes_ = got;
       return;
     } else {
+      host_unpin(buf_);
       void* p = mremap(buf_, cap_bytes_, ncap, MREMAP_MAYMOVE);
       if (p == MAP_FAILED) throw std::runtime_error("host result mapping could not grow");
       buf_ = static_cast<char*>(p);
@@ -231,13 +288,19 @@ void HostDrain::loop() {
       if (err_.empty()) {
         ensure(j.first + j.count);
         check(cudaStreamWaitEvent(cst_, j.ev, 0), "drain wait");
+        const char* src = reinterpret_cast<const char*>(j.src + static_cast<size_t>(j.first) * (row_bytes_ / sizeof(uint64_t)));
+        char* dst = buf_ + static_cast<size_t>(j.first) * row_bytes_;
+        const size_t total = static_cast<size_t>(j.count) * row_bytes_;
+        if (host_range_pinned(dst, total)) {  // a page-locked (parked) mapping: DMA straight in
+          check(cudaMemcpyAsync(dst, src, total, cudaMemcpyDeviceToHost, cst_), "drain copy");
+          check(cudaStreamSynchronize(cst_), "drain copy wait");
+          landed_ = j.first + j.count;
+          throw Done{};
+        }
         // D2H through the pinned double buffer: chunk c lands in buf[c % 2]
         // while chunk c - 1 is copied out of the other one.
         Staging& sg = staging(device_);
         std::lock_guard<std::mutex> lk(sg.mu);
-        const char* src = reinterpret_cast<const char*>(j.src + static_cast<size_t>(j.first) * (row_bytes_ / sizeof(uint64_t)));
-        char* dst = buf_ + static_cast<size_t>(j.first) * row_bytes_;
-        const size_t total = static_cast<size_t>(j.count) * row_bytes_;
         const size_t nchunk = (total + kStage - 1) / kStage;
         for (size_t c = 0; c <= nchunk; ++c) {
           if (c < nchunk) {
@@ -253,6 +316,7 @@ void HostDrain::loop() {
         }
         landed_ = j.first + j.count;
       }
+    } catch (const Done&) {
     } catch (const std::exception& x) {
       e = x.what();
     }

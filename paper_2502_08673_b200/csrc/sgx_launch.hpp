@@ -130,7 +130,7 @@ struct HarvestLiveArgs {
   const int* big_lits;
   int n_phases, slots;
   uint32_t* spill;  // [n_spill][W]
-  int W;
+  int W, n_spill;
   const int* key_enc;
   int key_words, batch, Bp;
   uint32_t* valid;

@@ -328,6 +328,32 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
     }
   }
   lap("bwd records");
+  if (getenv("SGX_TRACE_DIST")) {  // reuse distances of the backward's row reads, in passes
+    const int nl = P.n_levels;
+    std::vector<int32_t> def_pass(P.n_rows, -1), last_t(P.n_rows, -1);
+    std::vector<int64_t> hA(8, 0), hT(8, 0);
+    auto bucket = [](int d) { return d <= 0 ? 0 : d == 1 ? 1 : d <= 2 ? 2 : d <= 4 ? 3 : d <= 8 ? 4 : d <= 32 ? 5 : d <= 128 ? 6 : 7; };
+    int64_t nA = 0, nT = 0;
+    for (int li = 0; li < nl; ++li)
+      for (int w = 0; w < kWarps; ++w) {
+        const int32_t first = P.rec_lvl[2 * (li * kWarps + w)], cnt = P.rec_lvl[2 * (li * kWarps + w) + 1];
+        for (int32_t k = first; k < first + cnt; ++k) {
+          const I4 r = P.rec[k];
+          if (r.y >= 0) { ++hA[bucket(li - def_pass[r.y])]; ++nA; }
+          if (r.z >= 0) {  // tape row re-read distance (passes since its previous backward read)
+            if (last_t[r.z] >= 0) ++hT[bucket(li - last_t[r.z])]; else ++hT[0];
+            last_t[r.z] = li;
+            ++nT;
+          }
+          if (r.x & kRLast) def_pass[r.w] = li;
+        }
+      }
+    fprintf(stderr, "[sgx] bwd reads: %lld adjoint, %lld tape (rows %d, passes %d)\n", (long long)nA, (long long)nT, P.n_rows, nl);
+    const char* names[8] = {"<=0", "1", "2", "3-4", "5-8", "9-32", "33-128", ">128"};
+    for (int b = 0; b < 8; ++b)
+      fprintf(stderr, "[sgx]   distance %-7s adjoint %6.2f%%  tape re-read (<=0: first read) %6.2f%%\n", names[b], 100.0 * hA[b] / std::max<int64_t>(1, nA),
+              100.0 * hT[b] / std::max<int64_t>(1, nT));
+  }
   // Dead-adjoint lists: the last pass reading each adjoint row (a record's
   // .y), passes numbered in backward order.
   {
@@ -703,9 +729,18 @@ void build_live_bits(Layout& L) {
     const int x = L.node_of_var[v];
     L.lb_key_enc[v - 1] = (spill[base(x)] << 1) | (negv(x) ? 1 : 0);
   }
-  if (getenv("SGX_TRACE"))
+  if (getenv("SGX_TRACE")) {
     fprintf(stderr, "[sgx] live harvest: %d phases, %d slots, %d spill rows, %zu ops, %zu checks\n", P, nslots, nsp,
             L.lb_ops.size(), L.lb_chk.size());
+    std::vector<int> no, nc;
+    for (int ph = 0; ph < P; ++ph) {
+      no.push_back(L.lb_op_ptr[ph + 1] - L.lb_op_ptr[ph]);
+      nc.push_back(L.lb_chk_ptr[ph + 1] - L.lb_chk_ptr[ph]);
+    }
+    auto pct = [](std::vector<int> v, double q) { std::sort(v.begin(), v.end()); return v[static_cast<size_t>(q * (v.size() - 1))]; };
+    fprintf(stderr, "[sgx] live harvest per phase: ops p50 %d p90 %d p99 %d max %d; checks p50 %d p90 %d p99 %d max %d\n",
+            pct(no, .5), pct(no, .9), pct(no, .99), pct(no, 1), pct(nc, .5), pct(nc, .9), pct(nc, .99), pct(nc, 1));
+  }
 }
 
 Layout build_layout(const sgx_circuit_desc& d) {

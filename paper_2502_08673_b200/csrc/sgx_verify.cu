@@ -51,13 +51,18 @@ __global__ void k_keys_to_bt(const uint64_t* __restrict__ keys, int64_t n, int k
 }
 
 // ok[w] bit i: solution 32w+i satisfies every clause (enc = var << 1 | neg).
+// Clauses are split over blockIdx.y chunks (a thread per (word, chunk)),
+// folded by atomicAnd into ok_out, which starts all-ones.
+constexpr int kVerifyClauseChunk = 256;
 __global__ void k_cnf_words(const uint32_t* __restrict__ BT, int W, int64_t n, const int* __restrict__ cptr,
                             const int* __restrict__ enc, int n_clauses, uint32_t* __restrict__ ok_out) {
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= W) return;
   const int64_t r0 = static_cast<int64_t>(w) * 32;
-  uint32_t ok = r0 + 32 <= n ? 0xffffffffu : (r0 >= n ? 0u : ((1u << (n - r0)) - 1u));
-  for (int c = 0; c < n_clauses && ok; ++c) {
+  uint32_t ok = blockIdx.y > 0 ? 0xffffffffu : (r0 + 32 <= n ? 0xffffffffu : (r0 >= n ? 0u : ((1u << (n - r0)) - 1u)));
+  const int c0 = blockIdx.y * kVerifyClauseChunk;
+  const int c1 = min(n_clauses, c0 + kVerifyClauseChunk);
+  for (int c = c0; c < c1 && ok; ++c) {
     uint32_t any = 0u;
     const int e = __ldg(cptr + c + 1);
     for (int k = __ldg(cptr + c); k < e; ++k) {
@@ -66,7 +71,7 @@ __global__ void k_cnf_words(const uint32_t* __restrict__ BT, int W, int64_t n, c
     }
     ok &= any;
   }
-  ok_out[w] = ok;
+  if (ok != 0xffffffffu) atomicAnd(ok_out + w, ok);
 }
 
 __global__ void k_iota(int64_t* __restrict__ v, int64_t n) {
@@ -193,7 +198,9 @@ void check_keys_device(int device, const std::vector<int64_t>& cptr, const std::
                          cudaMemcpyHostToDevice, st), "verify h2d");
       const long long warps = static_cast<long long>(W) * kw;
       k_keys_to_bt<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(dkeys, m, kw, num_vars, W, dbt);
-      k_cnf_words<<<(W + 127) / 128, 128, 0, st>>>(dbt, W, m, dptr, denc, nc, dok);
+      ck(cudaMemsetAsync(dok, 0xff, W * sizeof(uint32_t), st), "verify memset");
+      k_cnf_words<<<dim3((W + 127) / 128, std::max(1, (nc + kVerifyClauseChunk - 1) / kVerifyClauseChunk)), 128, 0, st>>>(
+          dbt, W, m, dptr, denc, nc, dok);
       k_key_fp<<<static_cast<unsigned>((m + 255) / 256), 256, 0, st>>>(dkeys, m, kw, dfp + r0);
       ck(cudaMemcpyAsync(ok.data() + r0 / 32, dok, W * sizeof(uint32_t), cudaMemcpyDeviceToHost, st), "verify d2h");
       ck(cudaStreamSynchronize(st), "verify sync");  // the key chunk buffer is reused

@@ -83,12 +83,18 @@ CASES = [(name, mode) for name, rec in sorted(BENCH.items()) for mode in soft_mo
 
 @pytest.mark.parametrize("name,mode", CASES, ids=lambda x: x if isinstance(x, str) else x.name)
 def test_bench_size_run_matches_reference(gpu, name, mode):
+    _bench_size(name, mode)
+
+
+def _bench_size(name, mode, harvest=None):
     rec = BENCH[name]
     i = inst(rec["instance"])
     st, keys, info = run(i, mode, **cfg_kwargs(rec["config"]))
     check(st, keys, rec)
     assert info["last"] == ("jit" if mode == SoftKernel.JIT else "hbm"), info
-    if rec["instance"] in ("c2_iscas", "c4_blasted"):
+    if harvest:
+        assert info["harvest"] == harvest, info
+    elif rec["instance"] in ("c2_iscas", "c4_blasted"):
         # what bench.py runs: the live-slot harvest, 4 samples per lane
         assert info["harvest"] == "live" and info["vec"] == 4, info
     step = max(1, len(keys) // 3000)
