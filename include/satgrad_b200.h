@@ -165,6 +165,14 @@ int sgx_circuit_free(sgx_circuit* c);
  * device program construction sgx_circuit_upload performs.  For CPU tests. */
 int sgx_layout_stats(const sgx_circuit_desc* desc, int64_t* info16);
 
+/* Host only: implied[c] = 1 for every CNF clause the harvest does not check
+ * because the gate definitions or the output targets imply it (every row
+ * that passes eval_discrete + the output check satisfies it; replaces part
+ * of eval_cnf, src/cnf.cpp:129-147, without changing any row's verdict).
+ * implied holds n_clauses bytes.  SGX_ALL_CLAUSES=1 in the environment
+ * disables the pruning (all zeros). */
+int sgx_harvest_clause_mask(const sgx_circuit_desc* desc, uint8_t* implied);
+
 /* Source of the circuit-specialised soft-pass kernel (host only, no device
  * calls; SGX_E_INVALID if the circuit is not eligible).  *len = bytes incl.
  * the NUL; out = NULL only sizes. */

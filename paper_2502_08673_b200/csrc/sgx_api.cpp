@@ -709,7 +709,7 @@ void harvest_front(sgx_sampler* s, int restart, int iter, long long quota_left) 
                        s->cfg.row_offset);
     sgx::launch_bit_eval(s->sh, s->wpc, c->bit_ops.p, c->bit_lvl_ptr.p, c->n_bit_levels, s->BT.p, s->W,
                          c->out_bit_row.p, c->out_tgt.p, static_cast<int>(L.out_node.size()), c->clause_ptr.p,
-                         c->clause_enc.p, static_cast<int>(L.clause_ptr.size()) - 1, s->valid.p, s->cfg.batch);
+                         c->clause_enc.p, static_cast<int>(L.hclause_ptr.size()) - 1, s->valid.p, s->cfg.batch);
     CK(cudaEventRecord(s->ev[4], s->sh));
     sgx::launch_keys(s->sh, s->BT.p, s->W, c->key_bit_row.p, L.key_words, s->valid.p, s->Bp, s->K.p,
                      s->slot_of_row.p, s->tkeys.p, s->tmeta.p, s->tcap - 1, s->epoch);
@@ -1187,6 +1187,17 @@ int sgx_layout_stats(const sgx_circuit_desc* desc, int64_t* info16) {
     need(info16, "info16");
     sgx::Layout L = sgx::build_layout(*desc);
     sgx::layout_info(L, info16);
+  });
+}
+
+int sgx_harvest_clause_mask(const sgx_circuit_desc* desc, uint8_t* implied) {
+  return guard([&] {
+    need(desc, "desc");
+    sgx::Layout L = sgx::build_layout(*desc);
+    if (!L.clause_implied.empty()) {
+      need(implied, "implied");
+      std::copy(L.clause_implied.begin(), L.clause_implied.end(), implied);
+    }
   });
 }
 

@@ -1,6 +1,7 @@
 #include "sgx_drain.hpp"
 
 #include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -82,7 +83,7 @@ Staging& staging(int device) {
 
 }  // namespace
 
-// Released result mappings are parked (up to two, 16 GB in all) and handed
+// Released result mappings are parked (up to two; cache_bytes() in all) and handed
 // to the next run: their pages are already faulted in, so a run does not pay
 // the first touch -- or the kernel's huge-page compaction -- again.  A parked
 // mapping is also page-locked (cudaHostRegister, once, when it is parked), so
@@ -94,7 +95,17 @@ namespace {
 std::mutex g_cache_mu;
 std::vector<std::pair<void*, size_t>> g_cache;
 std::vector<std::pair<void*, size_t>> g_pinned;  // page-locked mappings (base, bytes)
-constexpr size_t kCacheEntries = 2, kCacheBytes = size_t{16} << 30;
+constexpr size_t kCacheEntries = 2;
+// Parked bytes in all: a quarter of physical memory, 16-96 GB (a 10-restart
+// C4 run returns 13 GB of keys in a mapping grown to ~20 GB).
+size_t cache_bytes() {
+  static const size_t lim = [] {
+    const long pages = sysconf(_SC_PHYS_PAGES), psz = sysconf(_SC_PAGESIZE);
+    const size_t phys = pages > 0 && psz > 0 ? static_cast<size_t>(pages) * static_cast<size_t>(psz) : 0;
+    return std::clamp<size_t>(phys / 4, size_t{16} << 30, size_t{96} << 30);
+  }();
+  return lim;
+}
 
 bool pin_parked() {
   static const bool on = [] {
@@ -177,7 +188,20 @@ void host_free(void* p, size_t bytes) {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     size_t held = 0;
     for (auto& e : g_cache) held += e.second;
-    if (g_cache.size() < kCacheEntries && held + b <= kCacheBytes) {
+    // A larger mapping displaces smaller parked ones (the next run of the
+    // same size can then take it without growing).
+    while (!g_cache.empty() && (g_cache.size() >= kCacheEntries || held + b > cache_bytes())) {
+      size_t s = 0;
+      for (size_t i = 1; i < g_cache.size(); ++i)
+        if (g_cache[i].second < g_cache[s].second) s = i;
+      if (g_cache[s].second >= b || b > cache_bytes()) break;
+      auto [q, n] = g_cache[s];
+      g_cache.erase(g_cache.begin() + static_cast<long>(s));
+      held -= n;
+      unpin(q);
+      munmap(q, n);
+    }
+    if (g_cache.size() < kCacheEntries && held + b <= cache_bytes()) {
       g_cache.emplace_back(p, b);
       if (pin_parked() && pinned_bytes(p) != b) {
         unpin(p);

@@ -2003,6 +2003,180 @@ k_harvest_live(const HarvestLiveArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-synchronous live harvest (default for deep circuits): ONE WARP owns one
+// 32-row word and walks the whole folded bit program alone, so a phase ends
+// with __syncwarp instead of a CTA barrier and no warp idles through another
+// warp's phase.  The program is the live program above (same slots, spill
+// rows and checks) re-cut into 32-record iterations (sgx_layout.cpp lw_ops):
+// lane l runs record l of each iteration; the last iteration of a phase
+// carries kLwEnd (and kLwChk when the phase has checks).  Records are read
+// kLwAhead iterations ahead into registers, so no iteration waits on L2.
+// Keys, fingerprints and the table insert follow in k_keys_spill, which
+// reads the spill tape in whole sectors.  eval_discrete (circuit.cpp:124-152),
+// output check (sampler.cpp:140-145), eval_cnf (cnf.cpp:129-147).
+// ---------------------------------------------------------------------------
+constexpr int kLwAhead = 4;
+
+__global__ void __launch_bounds__(256)
+k_harvest_lw(const HarvestLiveArgs a, const int4* __restrict__ lw, int n_iters) {
+  extern __shared__ uint32_t lwbits[];  // [warp][slots + 1]; slot 0 = 0, slot `slots` = padding sink
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (w >= a.W) return;  // warp-uniform; no CTA barrier below
+  uint32_t* bits = lwbits + static_cast<size_t>(warp) * (a.slots + 1);
+  const size_t Wz = static_cast<size_t>(a.W);
+  if (lane == 0) bits[0] = 0u;
+  // phase 0 inputs: hardened V (autodiff.cpp:292-297) and free bits (sampler.cpp:132-137)
+  for (int j = lane; j < a.ncpi; j += 32) {
+    const int2 cs = __ldg(a.cpi + j);
+    const uint32_t word = __ldg(a.hb + static_cast<size_t>(w) * a.ncpi + j);
+    bits[cs.x] = word;
+    if (cs.y >= 0) a.spill[cs.y * Wz + w] = word;
+  }
+  const int r = w * 32 + lane;
+  for (int k = 0; k < a.nucpi; ++k) {
+    const bool bit = fold(fold(a.free_prefix, static_cast<uint64_t>(a.row_offset + r)), static_cast<uint64_t>(k)) & 1;
+    const uint32_t word = __ballot_sync(kFull, bit);
+    if (lane == 0) {
+      const int2 cs = __ldg(a.ucpi + k);
+      bits[cs.x] = word;
+      if (cs.y >= 0) a.spill[cs.y * Wz + w] = word;
+    }
+  }
+  __syncwarp();
+  uint32_t ok = kFull;
+  int4 pre[kLwAhead];
+#pragma unroll
+  for (int k = 0; k < kLwAhead; ++k) pre[k] = k < n_iters ? __ldg(lw + k * 32 + lane) : make_int4(0, 0, 0, -1);
+  int ph = 0;
+  for (int it0 = 0; it0 < n_iters; it0 += kLwAhead) {
+#pragma unroll
+    for (int k = 0; k < kLwAhead; ++k) {
+      const int it = it0 + k;
+      if (it >= n_iters) break;
+      const int4 op = pre[k];
+      pre[k] = it + kLwAhead < n_iters ? __ldg(lw + (it + kLwAhead) * 32 + lane) : make_int4(0, 0, 0, -1);
+      const uint32_t x = bits[op.y >> 1] ^ neg_mask(op.y);
+      const uint32_t y = bits[op.z >> 1] ^ neg_mask(op.z);
+      const uint32_t v = bit_gate(op.x & 0xf, x, y);
+      bits[(op.x >> 4) & 0xffffff] = v;
+      if (op.w >= 0) a.spill[op.w * Wz + w] = v;
+      if (op.x & kLwEnd) {  // warp-uniform: the phase's last iteration
+        if (op.x & kLwChk) {  // output checks and clauses of this phase (read-only)
+          const int cb = __ldg(a.chk_ptr + ph), ce = __ldg(a.chk_ptr + ph + 1);
+          for (int i = cb + lane; i < ce; i += 32) {
+            const int4 rec = __ldg(a.chk + i);
+            uint32_t any = 0u;
+            if (rec.w == kLbBig) {  // a long clause, literal by literal
+              for (int l = rec.x; l < rec.x + rec.y; ++l) {
+                const int lit = __ldg(a.big_lits + l), sgn = lit >> 31;
+                any |= bits[lit ^ sgn] ^ static_cast<uint32_t>(sgn);
+              }
+            } else {
+              const int lit[4] = {rec.x, rec.y, rec.z, rec.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int sgn = lit[u] >> 31;
+                any |= bits[lit[u] ^ sgn] ^ static_cast<uint32_t>(sgn);
+              }
+            }
+            ok &= any;
+          }
+        }
+        ++ph;
+        __syncwarp();
+      }
+    }
+  }
+  const uint32_t v = __reduce_and_sync(kFull, ok);
+  const int r0 = w * 32;
+  const uint32_t mask = r0 + 32 <= a.batch ? kFull : (r0 >= a.batch ? 0u : ((1u << (a.batch - r0)) - 1u));
+  if (lane == 0) a.valid[w] = v & mask;
+}
+
+// Keys from the spill tape (dedupe_key, sampler.cpp:18-26): a CTA owns 8
+// consecutive words (256 rows) and its 8 warps split the key words; lane k of
+// a warp loads the 8 words of variable 32g+k as one 32-byte sector, 8 warp
+// transposes give per-row key bits.  Fingerprint = mix64 of the sum of
+// key_term over the key words (the same as every other harvest path), then
+// the first-row-wins table insert.
+__global__ void __launch_bounds__(256)
+k_keys_spill(const HarvestLiveArgs a) {
+  __shared__ unsigned long long hsum[256];
+  __shared__ uint32_t vw[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w0 = blockIdx.x * 8;
+  hsum[threadIdx.x] = 0ull;
+  if (threadIdx.x < 8) vw[threadIdx.x] = w0 + threadIdx.x < a.W ? a.valid[w0 + threadIdx.x] : 0u;
+  __syncthreads();
+  uint32_t vm[8], anyv = 0u;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    vm[j] = vw[j];
+    anyv |= vm[j];
+  }
+  if (anyv == 0u) return;  // block-uniform
+  const size_t Wz = static_cast<size_t>(a.W);
+  uint64_t h[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) h[j] = 0ull;
+  for (int q = warp; q < a.key_words; q += 8) {
+    uint32_t half[2][8];
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const int e = __ldg(a.key_enc + (2 * q + hf) * 32 + lane);
+      uint4 A = make_uint4(0, 0, 0, 0), Bv = make_uint4(0, 0, 0, 0);
+      if (e >= 0) {
+        const uint4* p = reinterpret_cast<const uint4*>(a.spill + (e >> 1) * Wz + w0);
+        A = __ldg(p);
+        Bv = __ldg(p + 1);
+      }
+      const uint32_t m = e >= 0 ? neg_mask(e) : 0u;
+      const uint32_t x[8] = {A.x ^ m, A.y ^ m, A.z ^ m, A.w ^ m, Bv.x ^ m, Bv.y ^ m, Bv.z ^ m, Bv.w ^ m};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) half[hf][j] = transpose32(x[j], lane);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (!vm[j]) continue;  // block-uniform
+      const uint64_t kw = static_cast<uint64_t>(half[0][j]) | (static_cast<uint64_t>(half[1][j]) << 32);
+      h[j] += key_term(kw, q);
+      if ((vm[j] >> lane) & 1u) a.K[static_cast<size_t>(q) * a.Bp + (w0 + j) * 32 + lane] = kw;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (vm[j]) atomicAdd(hsum + j * 32 + lane, static_cast<unsigned long long>(h[j]));
+  __syncthreads();
+  const int j = threadIdx.x >> 5;
+  if (!((vm[j] >> lane) & 1u)) return;
+  const int rr = (w0 + j) * 32 + lane;
+  const uint64_t hf = mix64(hsum[threadIdx.x]);
+  const unsigned long long fp = hf ? hf : 1ull;  // 0 marks an empty slot
+  uint64_t idx = (fp ^ (fp >> 29)) & a.tmask;
+  for (;;) {
+    unsigned long long cur = a.tkeys[idx];
+    if (cur == fp) break;
+    if (cur == 0ull) {
+      cur = atomicCAS(a.tkeys + idx, 0ull, fp);
+      if (cur == 0ull || cur == fp) break;
+    }
+    idx = (idx + 1) & a.tmask;
+  }
+  atomicMin(a.tmeta + idx, static_cast<unsigned long long>((a.epoch << 32) | static_cast<uint32_t>(rr)));
+  a.slot_of_row[rr] = static_cast<int>(idx);
+}
+
+bool launch_harvest_lw(cudaStream_t st, int warps_per_cta, const HarvestLiveArgs& a, const int4* lw, int n_iters) {
+  const size_t smem = static_cast<size_t>(a.slots + 1) * sizeof(uint32_t) * warps_per_cta;
+  if (smem > 220 * 1024) return false;
+  opt_in_smem(reinterpret_cast<const void*>(k_harvest_lw), smem);
+  k_harvest_lw<<<(a.W + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, smem, st>>>(a, lw, n_iters);
+  k_keys_spill<<<(a.W + 7) / 8, 256, 0, st>>>(a);
+  return true;
+}
+
 template <int WPC>
 static bool harvest_live_t(cudaStream_t st, const HarvestLiveArgs& a) {
   const size_t smem = static_cast<size_t>(a.slots) * WPC * sizeof(uint32_t);

@@ -1,6 +1,7 @@
 #include "sgx_layout.hpp"
 
 #include <algorithm>
+#include <array>
 #include <exception>
 #include <thread>
 #include <chrono>
@@ -31,6 +32,174 @@ int operand_count(int32_t k) {
 }
 
 std::string xv(int v) { return "x" + std::to_string(v); }
+
+// Harvest clause set: the CNF minus the clauses every harvested row satisfies
+// by construction.  The harvest evaluates every gate (eval_discrete,
+// circuit.cpp:124-152) before it checks the CNF (sampler.cpp:140-147,
+// cnf.cpp:129-147), and a row is valid only if its outputs also match their
+// targets.  So a clause C is implied -- true on every row that passes the
+// other checks -- when, for some CNF variable o of C defined by a gate, C
+// holds for every assignment of o's support (the CNF variables and inputs
+// the gate's definition reads, through unnamed internal nodes) with o set to
+// its definition's value; or when C has a literal an output target forces
+// true.  Both are exhaustive checks of a small truth table (support <= 10),
+// so dropping C changes no row's verdict: the valid mask, and hence the
+// harvest's counts and keys, are bit-identical to checking the whole CNF.
+// SGX_ALL_CLAUSES=1 keeps every clause (A/B and parity tests).
+void harvest_clauses(Layout& L) {
+  const int64_t nc = static_cast<int64_t>(L.clause_ptr.size()) - 1;
+  L.hclause_ptr.assign(1, 0);
+  L.hclause_lit.clear();
+  L.n_implied = 0;
+  L.clause_implied.assign(static_cast<size_t>(std::max<int64_t>(nc, 0)), 0);
+  const char* all = getenv("SGX_ALL_CLAUSES");
+  const bool keep_all = all && all[0] == '1';
+  constexpr int kMaxSup = 10, kWords = (1 << kMaxSup) / 64, kMaxNodes = 256;
+  using TT = std::array<uint64_t, kWords>;
+  const int n = L.n_nodes;
+  auto named = [&](int i) { return L.var[i] >= 1 && L.var[i] <= L.num_vars; };
+  // Per defining node (a gate carrying a CNF variable): its support vars and
+  // truth table over them, built on first use.  sup empty + ok=false: no table.
+  struct Def {
+    bool done = false, ok = false;
+    std::vector<int32_t> sup;  // CNF variables, truth-table bit order
+    TT tt{};
+  };
+  std::vector<Def> defs(static_cast<size_t>(L.max_var) + 1);
+  std::vector<int32_t> mark(n, -1), stack;
+  std::vector<TT> val(n);
+  int32_t epoch = 0;
+  auto pattern = [&](int j, int k) {  // truth table of support variable j of k
+    TT t{};
+    const int rows = 1 << k;
+    for (int r = 0; r < rows; ++r)
+      if ((r >> j) & 1) t[r >> 6] |= uint64_t{1} << (r & 63);
+    return t;
+  };
+  auto define = [&](int v) -> Def& {
+    Def& D = defs[v];
+    if (D.done) return D;
+    D.done = true;
+    const int g = L.node_of_var[v];
+    if (g < 0 || L.kind[g] == SGX_INPUT) return D;
+    // internal nodes (reachable from g through unnamed nodes), index order
+    ++epoch;
+    std::vector<int32_t> inner, leaves;
+    stack.assign(1, g);
+    mark[g] = epoch;
+    while (!stack.empty()) {
+      const int x = stack.back();
+      stack.pop_back();
+      if (x != g && (named(x) || L.kind[x] == SGX_INPUT)) {
+        leaves.push_back(x);
+        continue;
+      }
+      inner.push_back(x);
+      if (static_cast<int>(inner.size()) > kMaxNodes) return D;
+      const int oc = operand_count(L.kind[x]);
+      for (int s = 0; s < oc; ++s) {
+        const int y = s == 0 ? L.a[x] : L.b[x];
+        if (mark[y] != epoch) {
+          mark[y] = epoch;
+          stack.push_back(y);
+        }
+      }
+    }
+    if (static_cast<int>(leaves.size()) > kMaxSup) return D;
+    std::sort(leaves.begin(), leaves.end());
+    std::sort(inner.begin(), inner.end());
+    const int k = static_cast<int>(leaves.size());
+    for (int j = 0; j < k; ++j) {
+      const int x = leaves[j];
+      if (!named(x)) return D;  // an input without a CNF variable: keep the clause
+      D.sup.push_back(L.var[x]);
+      val[x] = pattern(j, k);
+    }
+    const TT ones = [&] {
+      TT t{};
+      const int rows = 1 << k;
+      for (int r = 0; r < rows; ++r) t[r >> 6] |= uint64_t{1} << (r & 63);
+      return t;
+    }();
+    for (int x : inner) {
+      const TT& A = L.a[x] >= 0 ? val[L.a[x]] : ones;
+      const TT& B = L.b[x] >= 0 ? val[L.b[x]] : ones;
+      TT& o = val[x];
+      for (int w = 0; w < kWords; ++w) {
+        switch (L.kind[x]) {
+          case SGX_CONST0: o[w] = 0; break;
+          case SGX_CONST1: o[w] = ones[w]; break;
+          case SGX_BUF: o[w] = A[w]; break;
+          case SGX_NOT: o[w] = ~A[w] & ones[w]; break;
+          case SGX_AND2: o[w] = A[w] & B[w]; break;
+          case SGX_OR2: o[w] = A[w] | B[w]; break;
+          case SGX_XOR2: o[w] = A[w] ^ B[w]; break;
+          default: o[w] = ~(A[w] ^ B[w]) & ones[w]; break;  // XNOR2
+        }
+      }
+    }
+    D.tt = val[g];
+    D.ok = true;
+    return D;
+  };
+  // literal forced true by an output target
+  std::vector<int8_t> po_val(static_cast<size_t>(L.max_var) + 1, -1);
+  for (size_t m = 0; m < L.out_node.size(); ++m) {
+    const int v = L.var[L.out_node[m]];
+    if (v >= 1 && v <= L.num_vars) po_val[v] = L.out_tgt[m] ? 1 : 0;
+  }
+  auto implied = [&](int64_t c) {
+    const int64_t l0 = L.clause_ptr[c], l1 = L.clause_ptr[c + 1];
+    for (int64_t l = l0; l < l1; ++l) {
+      const int32_t lit = L.clause_lit[l];
+      const int v = lit < 0 ? -lit : lit;
+      if (po_val[v] >= 0 && po_val[v] == (lit > 0 ? 1 : 0)) return true;
+    }
+    for (int64_t l = l0; l < l1; ++l) {
+      const int32_t lo = L.clause_lit[l];
+      Def& D = define(lo < 0 ? -lo : lo);
+      if (!D.ok) continue;
+      const int k = static_cast<int>(D.sup.size());
+      TT sat = lo > 0 ? D.tt : TT{};
+      if (lo < 0)
+        for (int w = 0; w < kWords; ++w) sat[w] = ~D.tt[w];
+      for (int64_t m = l0; m < l1; ++m) {
+        const int32_t lit = L.clause_lit[m];
+        const int v = lit < 0 ? -lit : lit;
+        if (v == (lo < 0 ? -lo : lo)) {
+          if ((lit > 0) != (lo > 0)) return true;  // o and -o: a tautology
+          continue;
+        }
+        const auto it = std::find(D.sup.begin(), D.sup.end(), v);
+        if (it == D.sup.end()) continue;  // free variable: may be false
+        const TT p = pattern(static_cast<int>(it - D.sup.begin()), k);
+        for (int w = 0; w < kWords; ++w) sat[w] |= lit > 0 ? p[w] : ~p[w];
+      }
+      const int rows = 1 << k;
+      bool full = true;
+      for (int r = 0; r < rows && full; r += 64) {
+        const uint64_t want = rows - r >= 64 ? ~uint64_t{0} : ((uint64_t{1} << (rows - r)) - 1);
+        full = (sat[r >> 6] & want) == want;
+      }
+      if (full) return true;
+    }
+    return false;
+  };
+  for (int64_t c = 0; c < nc; ++c) {
+    if (!keep_all && implied(c)) {
+      ++L.n_implied;
+      L.clause_implied[c] = 1;
+      continue;
+    }
+    L.hclause_lit.insert(L.hclause_lit.end(), L.clause_lit.begin() + L.clause_ptr[c],
+                         L.clause_lit.begin() + L.clause_ptr[c + 1]);
+    L.hclause_ptr.push_back(static_cast<int64_t>(L.hclause_lit.size()));
+  }
+  if (getenv("SGX_TRACE"))
+    fprintf(stderr, "[sgx] harvest clauses: %lld of %lld implied by gate definitions / targets, %lld checked\n",
+            static_cast<long long>(L.n_implied), static_cast<long long>(nc),
+            static_cast<long long>(L.hclause_ptr.size()) - 1);
+}
 
 // SGX_TRACE stage timer for the layout compiler.
 struct Lap {
@@ -348,6 +517,37 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
           if (r.x & kRLast) def_pass[r.w] = li;
         }
       }
+    {  // live sets per pass: adjoint rows (defined .. last read), tape rows (first .. last backward read)
+      std::vector<int32_t> a_def(P.n_rows, -1), a_last(P.n_rows, -1), t_first(P.n_rows, -1), t_last(P.n_rows, -1);
+      for (int li = 0; li < nl; ++li)
+        for (int w = 0; w < kWarps; ++w) {
+          const int32_t first = P.rec_lvl[2 * (li * kWarps + w)], cnt = P.rec_lvl[2 * (li * kWarps + w) + 1];
+          for (int32_t k = first; k < first + cnt; ++k) {
+            const I4 r = P.rec[k];
+            if (r.y >= 0) a_last[r.y] = li;
+            if (r.z >= 0) {
+              if (t_first[r.z] < 0) t_first[r.z] = li;
+              t_last[r.z] = li;
+            }
+            if (r.x & kRLast) a_def[r.w] = li;
+          }
+        }
+      std::vector<int32_t> dA(nl + 1, 0), dT(nl + 1, 0), dU(nl + 1, 0);
+      for (int r = 0; r < P.n_rows; ++r) {
+        if (a_def[r] >= 0 && a_last[r] > a_def[r]) { ++dA[a_def[r] + 1]; --dA[a_last[r] + 1]; }
+        if (t_first[r] >= 0 && t_last[r] > t_first[r]) { ++dT[t_first[r] + 1]; --dT[t_last[r] + 1]; }
+        if (t_first[r] >= 0) { ++dU[t_first[r]]; --dU[t_last[r] + 1]; }
+      }
+      int32_t ca = 0, ct = 0, cu = 0, ma = 0, mt = 0, mu = 0;
+      int64_t sa = 0, st = 0;
+      for (int li = 0; li <= nl; ++li) {
+        ca += dA[li]; ct += dT[li]; cu += dU[li];
+        ma = std::max(ma, ca); mt = std::max(mt, ct); mu = std::max(mu, cu);
+        sa += ca; st += ct;
+      }
+      fprintf(stderr, "[sgx] bwd live rows across passes: adjoint max %d mean %.0f; tape (between reads) max %d mean %.0f; tape incl. single-read max %d\n",
+              ma, double(sa) / nl, mt, double(st) / nl, mu);
+    }
     fprintf(stderr, "[sgx] bwd reads: %lld adjoint, %lld tape (rows %d, passes %d)\n", (long long)nA, (long long)nT, P.n_rows, nl);
     const char* names[8] = {"<=0", "1", "2", "3-4", "5-8", "9-32", "33-128", ">128"};
     for (int b = 0; b < 8; ++b)
@@ -542,15 +742,15 @@ void build_folded_bits(Layout& L) {
   // literals + kCnfOpen, then a closing record.  Whole clauses dealt to
   // kCnfThreads threads, longest-first to the least loaded, then padded with
   // open all-zero records and transposed.
-  const int64_t n_clauses = static_cast<int64_t>(L.clause_ptr.size()) - 1;
+  const int64_t n_clauses = static_cast<int64_t>(L.hclause_ptr.size()) - 1;
   const int32_t zero_row = L.fb_rows;
   std::vector<I4> recs;                 // all clauses' records, flat
   std::vector<int64_t> rec_ptr(n_clauses + 1, 0);
   std::vector<int32_t> lits;
   for (int64_t c = 0; c < n_clauses; ++c) {
     lits.clear();
-    for (int64_t l = L.clause_ptr[c]; l < L.clause_ptr[c + 1]; ++l) {
-      const int32_t lit = L.clause_lit[l];
+    for (int64_t l = L.hclause_ptr[c]; l < L.hclause_ptr[c + 1]; ++l) {
+      const int32_t lit = L.hclause_lit[l];
       const int e = enc(L.node_of_var[lit < 0 ? -lit : lit]);
       const bool neg = ((e & 1) ^ (lit < 0 ? 1 : 0)) != 0;
       lits.push_back(neg ? ~(e >> 1) : (e >> 1));
@@ -620,17 +820,17 @@ void build_live_bits(Layout& L) {
     if (oc >= 1) last[base(L.a[i])] = std::max(last[base(L.a[i])], lev[i]);
     if (oc == 2) last[base(L.b[i])] = std::max(last[base(L.b[i])], lev[i]);
   }
-  const int64_t n_clauses = static_cast<int64_t>(L.clause_ptr.size()) - 1;
+  const int64_t n_clauses = static_cast<int64_t>(L.hclause_ptr.size()) - 1;
   std::vector<int32_t> cl_phase(n_clauses);
   for (int64_t c = 0; c < n_clauses; ++c) {
     int m = 0;
-    for (int64_t l = L.clause_ptr[c]; l < L.clause_ptr[c + 1]; ++l) {
-      const int32_t lit = L.clause_lit[l];
+    for (int64_t l = L.hclause_ptr[c]; l < L.hclause_ptr[c + 1]; ++l) {
+      const int32_t lit = L.hclause_lit[l];
       m = std::max(m, lev[base(L.node_of_var[lit < 0 ? -lit : lit])]);
     }
     cl_phase[c] = m + 1;
-    for (int64_t l = L.clause_ptr[c]; l < L.clause_ptr[c + 1]; ++l) {
-      const int32_t lit = L.clause_lit[l];
+    for (int64_t l = L.hclause_ptr[c]; l < L.hclause_ptr[c + 1]; ++l) {
+      const int32_t lit = L.hclause_lit[l];
       const int r = base(L.node_of_var[lit < 0 ? -lit : lit]);
       last[r] = std::max(last[r], m + 1);
     }
@@ -692,10 +892,10 @@ void build_live_bits(Layout& L) {
   }
   L.lb_big_lits.clear();
   for (int64_t c = 0; c < n_clauses; ++c) {
-    const int64_t k = L.clause_ptr[c + 1] - L.clause_ptr[c];
+    const int64_t k = L.hclause_ptr[c + 1] - L.hclause_ptr[c];
     std::vector<int32_t> lits;
-    for (int64_t l = L.clause_ptr[c]; l < L.clause_ptr[c + 1]; ++l) {
-      const int32_t lit = L.clause_lit[l];
+    for (int64_t l = L.hclause_ptr[c]; l < L.hclause_ptr[c + 1]; ++l) {
+      const int32_t lit = L.hclause_lit[l];
       lits.push_back(lit_of(L.node_of_var[lit < 0 ? -lit : lit], lit < 0));
     }
     if (k <= 4) {
@@ -834,6 +1034,8 @@ Layout build_layout(const sgx_circuit_desc& d) {
   }
 
   lap("validate");
+  harvest_clauses(L);
+  lap("implied");
   // ASAP levels.
   L.level.assign(n, 0);
   for (int i = 0; i < n; ++i) {
@@ -917,13 +1119,13 @@ Layout build_layout(const sgx_circuit_desc& d) {
   for (int v : L.cpi) L.cpi_bit_row.push_back(L.bit_row_of_node[L.node_of_var[v]]);
   for (int v : L.ucpi) L.ucpi_bit_row.push_back(L.bit_row_of_node[L.node_of_var[v]]);
   for (int o : L.out_node) L.out_bit_row.push_back(L.bit_row_of_node[o]);
-  L.clause_ptr32.resize(L.clause_ptr.size());
-  for (size_t c = 0; c < L.clause_ptr.size(); ++c) L.clause_ptr32[c] = static_cast<int32_t>(L.clause_ptr[c]);
-  for (int64_t c = 0; c + 1 < static_cast<int64_t>(L.clause_ptr.size()); ++c) {
-    for (int64_t l = L.clause_ptr[c]; l < L.clause_ptr[c + 1]; ++l) {
-      int32_t lit = L.clause_lit[l];
+  L.clause_ptr32.resize(L.hclause_ptr.size());
+  for (size_t c = 0; c < L.hclause_ptr.size(); ++c) L.clause_ptr32[c] = static_cast<int32_t>(L.hclause_ptr[c]);
+  for (int64_t c = 0; c + 1 < static_cast<int64_t>(L.hclause_ptr.size()); ++c) {
+    for (int64_t l = L.hclause_ptr[c]; l < L.hclause_ptr[c + 1]; ++l) {
+      int32_t lit = L.hclause_lit[l];
       int v = lit < 0 ? -lit : lit;
-      bool last = l + 1 == L.clause_ptr[c + 1];
+      bool last = l + 1 == L.hclause_ptr[c + 1];
       L.clause_enc.push_back((L.bit_row_of_node[L.node_of_var[v]] << 2) | (last ? 2 : 0) |
                              (lit < 0 ? 1 : 0));
     }

@@ -148,6 +148,12 @@ struct Layout {
   std::vector<int32_t> cpi, ucpi;
   std::vector<int64_t> clause_ptr;
   std::vector<int32_t> clause_lit;
+  // The clauses the harvest checks (sgx_layout.cpp harvest_clauses): the CNF
+  // minus those implied by gate definitions or output targets.
+  std::vector<int64_t> hclause_ptr;
+  std::vector<int32_t> hclause_lit;
+  int64_t n_implied = 0;
+  std::vector<uint8_t> clause_implied;  // per CNF clause: 1 = not checked by the harvest
   bool unsat = false;
   std::vector<int32_t> level;        // ASAP level per node
 

@@ -241,6 +241,20 @@ def layout_stats(cnf, circuit, paths, unsat=False) -> dict:
     return dict(zip(keys, (int(x) for x in out)))
 
 
+def harvest_clause_mask(cnf, circuit, paths, unsat=False) -> np.ndarray:
+    """Host only: uint8 per CNF clause, 1 = implied by the gate definitions or
+    the output targets, so the harvest does not check it
+    (sgx_harvest_clause_mask; SGX_ALL_CLAUSES=1 disables the pruning)."""
+    L = _lib.load()
+    keep = [np.ascontiguousarray(x) for x in (
+        circuit.kind, circuit.a, circuit.b, circuit.var, circuit.out_var, circuit.out_tgt,
+        paths.constrained_pi, paths.unconstrained_pi, cnf.clause_ptr, cnf.clause_lit)]
+    d = make_desc(cnf, circuit, paths, unsat, keep)
+    out = np.zeros(max(1, len(cnf.clause_ptr) - 1), np.uint8)
+    _lib.check(L.sgx_harvest_clause_mask(C.byref(d), _lib.ptr(out, C.c_uint8)))
+    return out[:len(cnf.clause_ptr) - 1]
+
+
 def jit_source(cnf, circuit, paths, unsat=False) -> str:
     """CUDA source of the circuit-specialised soft pass (host only, no GPU)."""
     L = _lib.load()

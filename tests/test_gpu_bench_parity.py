@@ -111,6 +111,9 @@ VARIANTS = [
     {"SGX_HARVEST": "g"}, {"SGX_HARVEST": "smem"},
     {"SGX_LWPC": "1"}, {"SGX_LWPC": "2"}, {"SGX_LWPC": "4"}, {"SGX_LWPC": "8"},
     {"SGX_VEC": "4", "SGX_HARVEST": "g"}, {"SGX_VEC": "1", "SGX_LWPC": "8"},
+    # the harvest checking every clause (no implied-clause pruning), per path
+    {"SGX_ALL_CLAUSES": "1"}, {"SGX_ALL_CLAUSES": "1", "SGX_HARVEST": "g"},
+    {"SGX_ALL_CLAUSES": "1", "SGX_HARVEST": "smem"},
 ]
 
 

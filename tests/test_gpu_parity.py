@@ -141,6 +141,21 @@ def test_corpus_matches_reference(gpu):
     assert emitted > 0
 
 
+def test_corpus_matches_reference_checking_every_clause(gpu, monkeypatch):
+    """The same corpus with the harvest's clause pruning off
+    (SGX_ALL_CLAUSES=1: every clause checked, as eval_cnf does): identical
+    ordered keys, so the pruned and unpruned verdicts agree."""
+    monkeypatch.setenv("SGX_ALL_CLAUSES", "1")
+    for entry in golden_corpus():
+        i = instance_from_corpus(entry)
+        res = run_instance(i, SamplerConfig(batch=128, iterations=3, seed=1))
+        g = entry["run"]
+        assert res.stats.unique_count == g["unique"], entry["name"]
+        assert res.stats.new_unique == g["new_unique"], entry["name"]
+        if g["keys"]:
+            assert np.array_equal(res.solutions.keys, keys_from_hex(g["keys"])), entry["name"]
+
+
 @pytest.mark.parametrize("name,batch,iters", [("c3a_or50", 3000, 3), ("c3b_or100", 2048, 5),
                                                ("c1b_random", 777, 4), ("c2_iscas", 256, 1)])
 def test_run_matches_port_oracle(gpu, name, batch, iters):
