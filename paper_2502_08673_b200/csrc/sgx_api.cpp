@@ -272,7 +272,7 @@ struct sgx_circuit {
   DBuf<int4> fb_cnf4;
   int fb_levels = 0;
   // liveness-allocated harvest (Layout::lb_*)
-  DBuf<int4> lb_ops, lb_chk;
+  DBuf<int4> lb_ops, lb_chk, lw_ops;
   DBuf<int> lb_op_ptr, lb_chk_ptr, lb_big, lb_key_enc;
   DBuf<int2> lb_cpi, lb_ucpi;
   // circuit-specialised soft pass (sgx_jit.hpp), shared by its samplers
@@ -349,6 +349,7 @@ struct sgx_sampler {
   int Bp = 0, W = 0, wpc = 8, vec = 2, n_partial = 148;
   int hwpc = 0;  // words per CTA of the shared-memory harvest (0: global-memory path)
   int hlive = 0;  // words per CTA of the liveness-allocated harvest (0: not used)
+  int hlw = 0;    // > 0: the live program runs warp-synchronously (k_harvest_lw), warps per CTA
   bool onchip = false;  // small circuit: fused on-chip soft pass (k_soft_onchip)
   sgx::JitKernel* jit = nullptr;  // circuit-specialised soft pass (c->jit), once compiled
   bool have_tape = false;         // tape / adjoint buffers allocated (HBM soft kernels usable)
@@ -667,7 +668,13 @@ void harvest_front(sgx_sampler* s, int restart, int iter, long long quota_left) 
     a.tmeta = s->tmeta.p;
     a.tmask = s->tcap - 1;
     a.epoch = s->epoch;
-    if (!sgx::launch_harvest_live(s->sh, s->hlive, a)) throw CudaError("live harvest does not fit shared memory");
+    if (s->hlw > 0) {
+      if (!sgx::launch_harvest_lw(s->sh, s->hlw, a, c->lw_ops.p, L.lw_iters))
+        throw CudaError("live harvest does not fit shared memory");
+      s->launches += 1;
+    } else if (!sgx::launch_harvest_live(s->sh, s->hlive, a)) {
+      throw CudaError("live harvest does not fit shared memory");
+    }
     CK(cudaEventRecord(s->ev[4], s->sh));
     CK(cudaEventRecord(s->ev[5], s->sh));
     s->launches += 1;
@@ -1226,8 +1233,8 @@ int sgx_sampler_soft_info(const sgx_sampler* s, int64_t* info8) {
     info4[1] = s->jit_steps;
     info4[2] = !k ? -1 : (sgx::jit_ready(k) ? 1 : (sgx::jit_failed(k) ? 2 : 0));
     info4[3] = k ? static_cast<int64_t>(sgx::jit_compile_ms(k) * 1000.0) : 0;
-    info8[4] = s->hlive ? 2 : (s->hwpc ? 1 : 0);  // harvest: live-slot / full-tape smem / global
-    info8[5] = s->hlive ? s->hlive : s->hwpc;     // its words per CTA
+    info8[4] = s->hlw ? 3 : (s->hlive ? 2 : (s->hwpc ? 1 : 0));  // harvest: warp-sync live / live / full-tape smem / global
+    info8[5] = s->hlw ? s->hlw : (s->hlive ? s->hlive : s->hwpc);  // its words per CTA
     info8[6] = s->vec;                            // samples per lane of the HBM soft kernels
     info8[7] = s->Bp;
   });
@@ -1279,6 +1286,7 @@ int sgx_circuit_upload(sgx_ctx* ctx, const sgx_circuit_desc* d, sgx_circuit** ou
       c->fb_key_enc.upload(L.fb_key_enc, st);
       c->fb_cnf4.upload(to_int4(L.fb_cnf4), st);
       c->lb_ops.upload(to_int4(L.lb_ops), st);
+      c->lw_ops.upload(to_int4(L.lw_ops), st);
       c->lb_chk.upload(to_int4(L.lb_chk), st);
       c->lb_op_ptr.upload(L.lb_op_ptr, st);
       c->lb_chk_ptr.upload(L.lb_chk_ptr, st);
@@ -1450,6 +1458,24 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
               s->hlive = w;
           }
           if (s->hlive) s->hwpc = 0;
+          // Warp-synchronous cut of the live program: one warp per word, as
+          // many words per CTA as fit ~227 KB (<= 8).  SGX_HARVEST=live keeps
+          // the CTA-synchronous kernel; SGX_HARVEST=lw selects this one even
+          // where the full tape would win.
+          s->hlw = 0;
+          const size_t per_warp = static_cast<size_t>(L.lb_slots + 1) * sizeof(uint32_t);
+          const int lw_fit = static_cast<int>(std::min<size_t>(8, (226 * 1024 - sgx::kLwRingBytes) / per_warp));
+          const bool want_lw = e && std::string(e) == "lw";
+          const bool cta_live = (e && std::string(e) == "live") || std::getenv("SGX_LWPC");
+          if (lw_fit >= 1 && (s->hlive || want_lw) && !cta_live) {
+            s->hlw = lw_fit;
+            if (!s->hlive) s->hlive = 1;
+            s->hwpc = 0;
+          }
+          if (const char* v = std::getenv("SGX_LWW")) {  // A/B: warps (words) per warp-synchronous CTA
+            const int k = std::atoi(v);
+            if (s->hlw && k >= 1 && k <= lw_fit) s->hlw = k;
+          }
         }
         // Stream-ordered pool allocations: a sampler created after another one
         // reuses its memory without cudaMalloc / cudaFree round trips.

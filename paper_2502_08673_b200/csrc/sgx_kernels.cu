@@ -2010,21 +2010,48 @@ k_harvest_live(const HarvestLiveArgs a) {
 // warp's phase.  The program is the live program above (same slots, spill
 // rows and checks) re-cut into 32-record iterations (sgx_layout.cpp lw_ops):
 // lane l runs record l of each iteration; the last iteration of a phase
-// carries kLwEnd (and kLwChk when the phase has checks).  Records are read
-// kLwAhead iterations ahead into registers, so no iteration waits on L2.
-// Keys, fingerprints and the table insert follow in k_keys_spill, which
-// reads the spill tape in whole sectors.  eval_discrete (circuit.cpp:124-152),
-// output check (sampler.cpp:140-145), eval_cnf (cnf.cpp:129-147).
+// carries kLwEnd (and kLwChk when the phase has checks).  Every warp of a CTA
+// reads the same record stream, so it is staged once per CTA: a ring of
+// kLwBuf chunks of kLwChunk iterations, each brought in by one cp.async.bulk
+// (TMA) completing on its `full` mbarrier; warps release a chunk on its
+// `empty` mbarrier and warp 0 refills it once all have.  Gates are evaluated
+// branch-free from their ANF (mixed kinds in a warp do not diverge).  Keys,
+// fingerprints and the table insert follow in k_keys_spill, which reads the
+// spill tape in whole sectors.  eval_discrete (circuit.cpp:124-152), output
+// check (sampler.cpp:140-145), eval_cnf (cnf.cpp:129-147).
 // ---------------------------------------------------------------------------
-constexpr int kLwAhead = 4;
+// f = c0 ^ c1 X ^ c2 Y ^ c3 XY, coefficient k = bit k of f (sgx_layout.cpp anf_of)
+__device__ __forceinline__ uint32_t anf_gate(uint32_t f, uint32_t X, uint32_t Y) {
+  const uint32_t c0 = 0u - (f & 1u), c1 = 0u - ((f >> 1) & 1u), c2 = 0u - ((f >> 2) & 1u), c3 = 0u - ((f >> 3) & 1u);
+  return c0 ^ (X & c1) ^ (Y & c2) ^ (X & Y & c3);
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* m) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(m)) : "memory");
+}
 
 __global__ void __launch_bounds__(256)
 k_harvest_lw(const HarvestLiveArgs a, const int4* __restrict__ lw, int n_iters) {
-  extern __shared__ uint32_t lwbits[];  // [warp][slots + 1]; slot 0 = 0, slot `slots` = padding sink
+  extern __shared__ __align__(128) int4 lwsm[];  // ring [kLwBuf][kLwChunk][32], then [warp][slots + 1] words
+  __shared__ __align__(8) uint64_t full[kLwBuf], empty[kLwBuf];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int w = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (w >= a.W) return;  // warp-uniform; no CTA barrier below
-  uint32_t* bits = lwbits + static_cast<size_t>(warp) * (a.slots + 1);
+  const int nw = blockDim.x >> 5;
+  const int w0 = blockIdx.x * nw;
+  const int active = min(nw, a.W - w0);  // warps with a word (the rest return at once)
+  const int n_chunks = n_iters / kLwChunk;  // lw_ops is padded to whole chunks
+  constexpr unsigned kChunkBytes = kLwChunk * 32 * sizeof(int4);
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kLwBuf; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], static_cast<unsigned>(active));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp >= active) return;
+  if (threadIdx.x == 0)
+    for (int b = 0; b < kLwBuf && b < n_chunks; ++b) bulk_load(lwsm + b * kLwChunk * 32, lw + static_cast<size_t>(b) * kLwChunk * 32, kChunkBytes / 16, &full[b]);
+  const int w = w0 + warp;
+  uint32_t* bits = reinterpret_cast<uint32_t*>(lwsm + kLwBuf * kLwChunk * 32) + static_cast<size_t>(warp) * (a.slots + 1);
   const size_t Wz = static_cast<size_t>(a.W);
   if (lane == 0) bits[0] = 0u;
   // phase 0 inputs: hardened V (autodiff.cpp:292-297) and free bits (sampler.cpp:132-137)
@@ -2046,20 +2073,17 @@ k_harvest_lw(const HarvestLiveArgs a, const int4* __restrict__ lw, int n_iters) 
   }
   __syncwarp();
   uint32_t ok = kFull;
-  int4 pre[kLwAhead];
-#pragma unroll
-  for (int k = 0; k < kLwAhead; ++k) pre[k] = k < n_iters ? __ldg(lw + k * 32 + lane) : make_int4(0, 0, 0, -1);
   int ph = 0;
-  for (int it0 = 0; it0 < n_iters; it0 += kLwAhead) {
-#pragma unroll
-    for (int k = 0; k < kLwAhead; ++k) {
-      const int it = it0 + k;
-      if (it >= n_iters) break;
-      const int4 op = pre[k];
-      pre[k] = it + kLwAhead < n_iters ? __ldg(lw + (it + kLwAhead) * 32 + lane) : make_int4(0, 0, 0, -1);
-      const uint32_t x = bits[op.y >> 1] ^ neg_mask(op.y);
-      const uint32_t y = bits[op.z >> 1] ^ neg_mask(op.z);
-      const uint32_t v = bit_gate(op.x & 0xf, x, y);
+  for (int c = 0; c < n_chunks; ++c) {
+    const int b = c % kLwBuf;
+    const unsigned par = static_cast<unsigned>(c / kLwBuf) & 1u;
+    mbar_wait(&full[b], par);
+    const int4* R = lwsm + b * kLwChunk * 32 + lane;
+#pragma unroll 4
+    for (int it = 0; it < kLwChunk; ++it) {
+      const int4 op = R[it * 32];
+      const uint32_t X = bits[op.y], Y = bits[op.z];
+      const uint32_t v = anf_gate(op.x, X, Y);
       bits[(op.x >> 4) & 0xffffff] = v;
       if (op.w >= 0) a.spill[op.w * Wz + w] = v;
       if (op.x & kLwEnd) {  // warp-uniform: the phase's last iteration
@@ -2087,6 +2111,12 @@ k_harvest_lw(const HarvestLiveArgs a, const int4* __restrict__ lw, int n_iters) 
         ++ph;
         __syncwarp();
       }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);
+    if (threadIdx.x == 0 && c + kLwBuf < n_chunks) {  // refill once every warp has released the chunk
+      mbar_wait(&empty[b], par);
+      bulk_load(lwsm + b * kLwChunk * 32, lw + static_cast<size_t>(c + kLwBuf) * kLwChunk * 32, kChunkBytes / 16, &full[b]);
     }
   }
   const uint32_t v = __reduce_and_sync(kFull, ok);
@@ -2169,8 +2199,8 @@ k_keys_spill(const HarvestLiveArgs a) {
 }
 
 bool launch_harvest_lw(cudaStream_t st, int warps_per_cta, const HarvestLiveArgs& a, const int4* lw, int n_iters) {
-  const size_t smem = static_cast<size_t>(a.slots + 1) * sizeof(uint32_t) * warps_per_cta;
-  if (smem > 220 * 1024) return false;
+  const size_t smem = static_cast<size_t>(a.slots + 1) * sizeof(uint32_t) * warps_per_cta + kLwRingBytes;
+  if (smem > 226 * 1024 || n_iters % kLwChunk) return false;
   opt_in_smem(reinterpret_cast<const void*>(k_harvest_lw), smem);
   k_harvest_lw<<<(a.W + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, smem, st>>>(a, lw, n_iters);
   k_keys_spill<<<(a.W + 7) / 8, 256, 0, st>>>(a);

@@ -141,6 +141,9 @@ struct HarvestLiveArgs {
 };
 // wpc words per CTA; returns false if the slots do not fit shared memory.
 bool launch_harvest_live(cudaStream_t st, int wpc, const HarvestLiveArgs& a);
+// Warp-synchronous live harvest (one warp per word, k_harvest_lw) + spill
+// keys (k_keys_spill); false if a CTA's slots do not fit shared memory.
+bool launch_harvest_lw(cudaStream_t st, int warps_per_cta, const HarvestLiveArgs& a, const int4* lw, int n_iters);
 void launch_compact_new(cudaStream_t st, const uint32_t* newmask, const int* block_off, const int* slot_of_row,
                         const unsigned long long* tkeys, int Bp, unsigned long long* out);
 void launch_merge_remote(cudaStream_t st, const unsigned long long* all_fps, const long long* n_of, int nranks,

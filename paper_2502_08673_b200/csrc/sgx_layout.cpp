@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <array>
 #include <exception>
+#include <future>
 #include <thread>
 #include <chrono>
 #include <cstdio>
@@ -32,6 +33,29 @@ int operand_count(int32_t k) {
 }
 
 std::string xv(int v) { return "x" + std::to_string(v); }
+
+// 32-row bit gate (circuit.cpp:137-144) with its operands read through
+// negations nx, ny, as the algebraic normal form over the raw operand words
+// X, Y: f = c0 ^ c1 X ^ c2 Y ^ c3 XY, coefficient k in bit k.  One branch-free
+// formula then evaluates every gate kind (lanes of a warp run mixed kinds).
+int32_t anf_of(int32_t kind, int nx, int ny) {
+  auto g = [&](int x, int y) {
+    x ^= nx;
+    y ^= ny;
+    switch (kind) {
+      case SGX_CONST0: return 0;
+      case SGX_CONST1: return 1;
+      case SGX_BUF: return x;
+      case SGX_NOT: return x ^ 1;
+      case SGX_AND2: return x & y;
+      case SGX_OR2: return x | y;
+      case SGX_XOR2: return x ^ y;
+      default: return (x ^ y) ^ 1;  // XNOR2
+    }
+  };
+  const int t00 = g(0, 0), t01 = g(0, 1), t10 = g(1, 0), t11 = g(1, 1);
+  return t00 | ((t00 ^ t10) << 1) | ((t00 ^ t01) << 2) | ((t00 ^ t01 ^ t10 ^ t11) << 3);
+}
 
 // Harvest clause set: the CNF minus the clauses every harvested row satisfies
 // by construction.  The harvest evaluates every gate (eval_discrete,
@@ -69,13 +93,13 @@ void harvest_clauses(Layout& L) {
   std::vector<int32_t> mark(n, -1), stack;
   std::vector<TT> val(n);
   int32_t epoch = 0;
-  auto pattern = [&](int j, int k) {  // truth table of support variable j of k
-    TT t{};
-    const int rows = 1 << k;
-    for (int r = 0; r < rows; ++r)
-      if ((r >> j) & 1) t[r >> 6] |= uint64_t{1} << (r & 63);
-    return t;
-  };
+  // truth table of support variable j: bit r = bit j of r (the same for
+  // every support size k; a k-variable table uses its first 2^k bits)
+  std::array<TT, kMaxSup> pat{};
+  for (int j = 0; j < kMaxSup; ++j)
+    for (int r = 0; r < (1 << kMaxSup); ++r)
+      if ((r >> j) & 1) pat[j][r >> 6] |= uint64_t{1} << (r & 63);
+  auto words_of = [](int k) { return k <= 6 ? 1 : 1 << (k - 6); };
   auto define = [&](int v) -> Def& {
     Def& D = defs[v];
     if (D.done) return D;
@@ -92,6 +116,7 @@ void harvest_clauses(Layout& L) {
       stack.pop_back();
       if (x != g && (named(x) || L.kind[x] == SGX_INPUT)) {
         leaves.push_back(x);
+        if (static_cast<int>(leaves.size()) > kMaxSup) return D;
         continue;
       }
       inner.push_back(x);
@@ -105,36 +130,29 @@ void harvest_clauses(Layout& L) {
         }
       }
     }
-    if (static_cast<int>(leaves.size()) > kMaxSup) return D;
     std::sort(leaves.begin(), leaves.end());
     std::sort(inner.begin(), inner.end());
-    const int k = static_cast<int>(leaves.size());
+    const int k = static_cast<int>(leaves.size()), nw = words_of(k);
     for (int j = 0; j < k; ++j) {
       const int x = leaves[j];
       if (!named(x)) return D;  // an input without a CNF variable: keep the clause
       D.sup.push_back(L.var[x]);
-      val[x] = pattern(j, k);
+      val[x] = pat[j];
     }
-    const TT ones = [&] {
-      TT t{};
-      const int rows = 1 << k;
-      for (int r = 0; r < rows; ++r) t[r >> 6] |= uint64_t{1} << (r & 63);
-      return t;
-    }();
     for (int x : inner) {
-      const TT& A = L.a[x] >= 0 ? val[L.a[x]] : ones;
-      const TT& B = L.b[x] >= 0 ? val[L.b[x]] : ones;
+      const TT& A = val[L.a[x] >= 0 ? L.a[x] : x];
+      const TT& B = val[L.b[x] >= 0 ? L.b[x] : x];
       TT& o = val[x];
-      for (int w = 0; w < kWords; ++w) {
+      for (int w = 0; w < nw; ++w) {
         switch (L.kind[x]) {
           case SGX_CONST0: o[w] = 0; break;
-          case SGX_CONST1: o[w] = ones[w]; break;
+          case SGX_CONST1: o[w] = ~uint64_t{0}; break;
           case SGX_BUF: o[w] = A[w]; break;
-          case SGX_NOT: o[w] = ~A[w] & ones[w]; break;
+          case SGX_NOT: o[w] = ~A[w]; break;
           case SGX_AND2: o[w] = A[w] & B[w]; break;
           case SGX_OR2: o[w] = A[w] | B[w]; break;
           case SGX_XOR2: o[w] = A[w] ^ B[w]; break;
-          default: o[w] = ~(A[w] ^ B[w]) & ones[w]; break;  // XNOR2
+          default: o[w] = ~(A[w] ^ B[w]); break;  // XNOR2
         }
       }
     }
@@ -159,10 +177,9 @@ void harvest_clauses(Layout& L) {
       const int32_t lo = L.clause_lit[l];
       Def& D = define(lo < 0 ? -lo : lo);
       if (!D.ok) continue;
-      const int k = static_cast<int>(D.sup.size());
-      TT sat = lo > 0 ? D.tt : TT{};
-      if (lo < 0)
-        for (int w = 0; w < kWords; ++w) sat[w] = ~D.tt[w];
+      const int k = static_cast<int>(D.sup.size()), nw = words_of(k);
+      TT sat;
+      for (int w = 0; w < nw; ++w) sat[w] = lo > 0 ? D.tt[w] : ~D.tt[w];
       for (int64_t m = l0; m < l1; ++m) {
         const int32_t lit = L.clause_lit[m];
         const int v = lit < 0 ? -lit : lit;
@@ -172,8 +189,8 @@ void harvest_clauses(Layout& L) {
         }
         const auto it = std::find(D.sup.begin(), D.sup.end(), v);
         if (it == D.sup.end()) continue;  // free variable: may be false
-        const TT p = pattern(static_cast<int>(it - D.sup.begin()), k);
-        for (int w = 0; w < kWords; ++w) sat[w] |= lit > 0 ? p[w] : ~p[w];
+        const TT& p = pat[it - D.sup.begin()];
+        for (int w = 0; w < nw; ++w) sat[w] |= lit > 0 ? p[w] : ~p[w];
       }
       const int rows = 1 << k;
       bool full = true;
@@ -545,8 +562,10 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
         ma = std::max(ma, ca); mt = std::max(mt, ct); mu = std::max(mu, cu);
         sa += ca; st += ct;
       }
-      fprintf(stderr, "[sgx] bwd live rows across passes: adjoint max %d mean %.0f; tape (between reads) max %d mean %.0f; tape incl. single-read max %d\n",
-              ma, double(sa) / nl, mt, double(st) / nl, mu);
+      int32_t never = 0;
+      for (int r = 0; r < P.n_rows; ++r) never += t_first[r] < 0 ? 1 : 0;
+      fprintf(stderr, "[sgx] bwd live rows across passes: adjoint max %d mean %.0f; tape (between reads) max %d mean %.0f; tape incl. single-read max %d; rows never read by the backward %d\n",
+              ma, double(sa) / nl, mt, double(st) / nl, mu, never);
     }
     fprintf(stderr, "[sgx] bwd reads: %lld adjoint, %lld tape (rows %d, passes %d)\n", (long long)nA, (long long)nT, P.n_rows, nl);
     const char* names[8] = {"<=0", "1", "2", "3-4", "5-8", "9-32", "33-128", ">128"};
@@ -914,6 +933,27 @@ void build_live_bits(Layout& L) {
     L.lb_chk.insert(L.lb_chk.end(), chk[ph].begin(), chk[ph].end());
   }
   L.lb_chk_ptr.push_back(static_cast<int32_t>(L.lb_chk.size()));
+  // warp-synchronous cut: 32 records per iteration, >= 1 iteration per phase
+  if (nslots >= (1 << 24)) throw std::invalid_argument("circuit too large for the live harvest");
+  L.lw_ops.clear();
+  for (int ph = 0; ph < P; ++ph) {
+    const int32_t ob = L.lb_op_ptr[ph], no = L.lb_op_ptr[ph + 1] - ob;
+    const int32_t iters = std::max<int32_t>(1, (no + 31) / 32);
+    const bool has_chk = L.lb_chk_ptr[ph + 1] > L.lb_chk_ptr[ph];
+    for (int32_t it = 0; it < iters; ++it)
+      for (int32_t ln = 0; ln < 32; ++ln) {
+        const int32_t k = it * 32 + ln;
+        I4 r{nslots << 4, 0, 0, -1};  // padding: sink <- 0 (ANF all zero)
+        if (k < no) {  // the gate with its operand negations as the ANF of f(X, Y) over raw slots
+          const I4 o = L.lb_ops[ob + k];
+          r = {(o.x & ~0xf) | anf_of(o.x & 0xf, o.y & 1, o.z & 1), o.y >> 1, o.z >> 1, o.w};
+        }
+        if (it + 1 == iters) r.x |= kLwEnd | (has_chk ? kLwChk : 0);
+        L.lw_ops.push_back(r);
+      }
+  }
+  while ((L.lw_ops.size() / 32) % kLwChunk) L.lw_ops.push_back({nslots << 4, 0, 0, -1});  // whole ring chunks
+  L.lw_iters = static_cast<int32_t>(L.lw_ops.size() / 32);
   L.lb_cpi.clear();
   L.lb_ucpi.clear();
   for (int v : L.cpi) {
@@ -930,8 +970,8 @@ void build_live_bits(Layout& L) {
     L.lb_key_enc[v - 1] = (spill[base(x)] << 1) | (negv(x) ? 1 : 0);
   }
   if (getenv("SGX_TRACE")) {
-    fprintf(stderr, "[sgx] live harvest: %d phases, %d slots, %d spill rows, %zu ops, %zu checks\n", P, nslots, nsp,
-            L.lb_ops.size(), L.lb_chk.size());
+    fprintf(stderr, "[sgx] live harvest: %d phases, %d slots, %d spill rows, %zu ops, %zu checks, %d warp iterations\n", P,
+            nslots, nsp, L.lb_ops.size(), L.lb_chk.size(), L.lw_iters);
     std::vector<int> no, nc;
     for (int ph = 0; ph < P; ++ph) {
       no.push_back(L.lb_op_ptr[ph + 1] - L.lb_op_ptr[ph]);
@@ -1034,8 +1074,6 @@ Layout build_layout(const sgx_circuit_desc& d) {
   }
 
   lap("validate");
-  harvest_clauses(L);
-  lap("implied");
   // ASAP levels.
   L.level.assign(n, 0);
   for (int i = 0; i < n; ++i) {
@@ -1068,8 +1106,20 @@ Layout build_layout(const sgx_circuit_desc& d) {
       err_soft = std::current_exception();
     }
   });
+  // The harvest clause set (harvest_clauses) feeds the three harvest
+  // programs; it runs first on the live-program thread, overlapping the
+  // soft program, and the other two wait for it.
+  std::promise<void> clauses_done;
+  std::shared_future<void> clauses = clauses_done.get_future().share();
   std::thread t_live = spawn([&] {
     try {
+      try {
+        harvest_clauses(L);
+        clauses_done.set_value();
+      } catch (...) {
+        clauses_done.set_exception(std::current_exception());
+        throw;
+      }
       build_live_bits(L);
     } catch (...) {
       err_live = std::current_exception();
@@ -1078,6 +1128,7 @@ Layout build_layout(const sgx_circuit_desc& d) {
   std::exception_ptr err_fold;
   std::thread t_fold = spawn([&] {
     try {
+      clauses.get();
       build_folded_bits(L);
     } catch (...) {
       err_fold = std::current_exception();
@@ -1119,6 +1170,7 @@ Layout build_layout(const sgx_circuit_desc& d) {
   for (int v : L.cpi) L.cpi_bit_row.push_back(L.bit_row_of_node[L.node_of_var[v]]);
   for (int v : L.ucpi) L.ucpi_bit_row.push_back(L.bit_row_of_node[L.node_of_var[v]]);
   for (int o : L.out_node) L.out_bit_row.push_back(L.bit_row_of_node[o]);
+  clauses.get();
   L.clause_ptr32.resize(L.hclause_ptr.size());
   for (size_t c = 0; c < L.hclause_ptr.size(); ++c) L.clause_ptr32[c] = static_cast<int32_t>(L.hclause_ptr[c]);
   for (int64_t c = 0; c + 1 < static_cast<int64_t>(L.hclause_ptr.size()); ++c) {

@@ -76,6 +76,9 @@ constexpr int32_t kRSlow = 1 << 16;
 constexpr int kOcSlotShift = 17;  // oc_rec: adjoint store slot in the flag word
 constexpr int kCnfThreads = 256;               // threads of the shared-memory harvest CTA
 constexpr int32_t kCnfOpen = INT32_MIN;        // CNF record continues (see fb_cnf4)
+constexpr int32_t kLwEnd = 1 << 30, kLwChk = 1 << 29;
+// k_harvest_lw record ring: kLwBuf chunks of kLwChunk iterations (32 int4 each); lw_ops is padded to whole chunks
+constexpr int kLwChunk = 8, kLwBuf = 4, kLwRingBytes = kLwChunk * kLwBuf * 32 * 16;  // lw_ops .x flags (op kind | out_slot << 4 below)
 constexpr int32_t kLbBig = INT32_MIN;          // lb_chk: long clause, literals in lb_big_lits
 constexpr int kGroup = 4;                      // ops per forward group
 constexpr int kGroupRecs = 1 + kGroup / 2;     // int4 records per group
@@ -211,6 +214,14 @@ struct Layout {
   std::vector<int32_t> lb_big_lits;
   std::vector<int32_t> lb_cpi, lb_ucpi;  // {slot, spill} pairs
   std::vector<int32_t> lb_key_enc;   // key_words * 64: spill << 1 | negate (-1 padding)
+  // The same program for the warp-synchronous harvest (k_harvest_lw): each
+  // phase's ops cut into iterations of 32 records (one per lane), padded with
+  // records writing the sink slot lb_slots; the last iteration of a phase has
+  // kLwEnd (+ kLwChk when the phase has checks) in .x.  Record:
+  // {anf | out_slot << 4 | flags, a_slot, b_slot, spill}: the gate and its
+  // operand negations as f = c0 ^ c1 X ^ c2 Y ^ c3 XY (coefficient k = bit k).
+  std::vector<I4> lw_ops;            // n_iters * 32
+  int32_t lw_iters = 0;
 
   int64_t n_lits() const { return static_cast<int64_t>(clause_lit.size()); }
 };

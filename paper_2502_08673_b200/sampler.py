@@ -328,7 +328,7 @@ class Sampler:
         return {"last": ["hbm", "jit", "onchip"][int(out[0])], "jit_steps": int(out[1]),
                 "jit_state": {-1: "none", 0: "compiling", 1: "ready", 2: "failed"}[int(out[2])],
                 "jit_compile_ms": out[3] / 1000.0,
-                "harvest": ["global", "smem", "live"][int(out[4])], "harvest_wpc": int(out[5]),
+                "harvest": ["global", "smem", "live", "lw"][int(out[4])], "harvest_wpc": int(out[5]),
                 "vec": int(out[6]), "padded_batch": int(out[7])}
 
     def launch_count(self) -> int:

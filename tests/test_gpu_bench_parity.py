@@ -86,6 +86,14 @@ def test_bench_size_run_matches_reference(gpu, name, mode):
     _bench_size(name, mode)
 
 
+@pytest.mark.parametrize("name", sorted(n for n, r in BENCH.items() if r["instance"] in ("c2_iscas", "c4_blasted")))
+def test_bench_size_cta_live_harvest(gpu, name, monkeypatch):
+    """The CTA-synchronous live harvest (k_harvest_live), no longer the
+    default, at bench size against the same reference goldens."""
+    monkeypatch.setenv("SGX_HARVEST", "live")
+    _bench_size(name, SoftKernel.HBM, harvest="live")
+
+
 def _bench_size(name, mode, harvest=None):
     rec = BENCH[name]
     i = inst(rec["instance"])
@@ -95,8 +103,8 @@ def _bench_size(name, mode, harvest=None):
     if harvest:
         assert info["harvest"] == harvest, info
     elif rec["instance"] in ("c2_iscas", "c4_blasted"):
-        # what bench.py runs: the live-slot harvest, 4 samples per lane
-        assert info["harvest"] == "live" and info["vec"] == 4, info
+        # what bench.py runs: the warp-synchronous live-slot harvest, 4 samples per lane
+        assert info["harvest"] == "lw" and info["vec"] == 4, info
     step = max(1, len(keys) // 3000)
     assert verify_keys(i.cnf, keys[::step]).all()
 
@@ -114,6 +122,10 @@ VARIANTS = [
     # the harvest checking every clause (no implied-clause pruning), per path
     {"SGX_ALL_CLAUSES": "1"}, {"SGX_ALL_CLAUSES": "1", "SGX_HARVEST": "g"},
     {"SGX_ALL_CLAUSES": "1", "SGX_HARVEST": "smem"},
+    # the CTA-synchronous live kernel, and the warp-synchronous one forced
+    # (also where the full tape would win) at one and at two words per CTA
+    {"SGX_HARVEST": "live"}, {"SGX_HARVEST": "lw"}, {"SGX_HARVEST": "lw", "SGX_LWW": "1"},
+    {"SGX_HARVEST": "lw", "SGX_LWW": "2", "SGX_ALL_CLAUSES": "1"},
 ]
 
 
@@ -130,6 +142,12 @@ def test_forced_variant_matches_reference(gpu, rec, variant, monkeypatch):
         assert info["harvest"] == "global", info
     if "SGX_LWPC" in variant and info["harvest"] == "live":
         assert info["harvest_wpc"] == int(variant["SGX_LWPC"]), info
+    if variant.get("SGX_HARVEST") == "lw":
+        assert info["harvest"] == "lw", info
+        if "SGX_LWW" in variant:
+            assert info["harvest_wpc"] == int(variant["SGX_LWW"]), info
+    if variant.get("SGX_HARVEST") == "live":
+        assert info["harvest"] != "lw", info
     assert st.unique_count == rec["unique"]
     assert st.attempts == rec["attempts"]
     assert st.new_unique == rec["new_unique"]
