@@ -4,6 +4,8 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -107,6 +109,14 @@ size_t cache_bytes() {
   return lim;
 }
 
+bool trace_on() {
+  static const bool on = std::getenv("SGX_TRACE") != nullptr;
+  return on;
+}
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 bool pin_parked() {
   static const bool on = [] {
     const char* e = std::getenv("SGX_PIN_PARKED");
@@ -205,15 +215,21 @@ void host_free(void* p, size_t bytes) {
       g_cache.emplace_back(p, b);
       if (pin_parked() && pinned_bytes(p) != b) {
         unpin(p);
-        if (cudaHostRegister(p, b, cudaHostRegisterPortable) == cudaSuccess)
+        const double t0 = now_ms();
+        const cudaError_t rc = cudaHostRegister(p, b, cudaHostRegisterPortable);
+        if (rc == cudaSuccess)
           g_pinned.emplace_back(p, b);
         else
           cudaGetLastError();  // (e.g. a locked-memory limit): the staged path stays correct
+        if (trace_on())
+          fprintf(stderr, "[sgx] drain: parked %.2f GB, page-lock %s in %.1f ms\n", b / 1e9,
+                  rc == cudaSuccess ? "ok" : cudaGetErrorString(rc), now_ms() - t0);
       }
       return;
     }
     unpin(p);
   }
+  if (trace_on()) fprintf(stderr, "[sgx] drain: released %.2f GB (not parked)\n", b / 1e9);
   munmap(p, b);
 }
 
@@ -315,6 +331,9 @@ void HostDrain::loop() {
         const char* src = reinterpret_cast<const char*>(j.src + static_cast<size_t>(j.first) * (row_bytes_ / sizeof(uint64_t)));
         char* dst = buf_ + static_cast<size_t>(j.first) * row_bytes_;
         const size_t total = static_cast<size_t>(j.count) * row_bytes_;
+        if (trace_on() && (j.first == 0 || !host_range_pinned(dst, total)))
+          fprintf(stderr, "[sgx] drain: rows %lld+%lld into a %.2f GB mapping, %s\n", (long long)j.first,
+                  (long long)j.count, cap_bytes_ / 1e9, host_range_pinned(dst, total) ? "page-locked: direct DMA" : "staged");
         if (host_range_pinned(dst, total)) {  // a page-locked (parked) mapping: DMA straight in
           check(cudaMemcpyAsync(dst, src, total, cudaMemcpyDeviceToHost, cst_), "drain copy");
           check(cudaStreamSynchronize(cst_), "drain copy wait");
