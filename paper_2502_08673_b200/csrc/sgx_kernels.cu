@@ -2482,11 +2482,7 @@ void launch_forward(cudaStream_t st, int vec, const int4* grp, const int2* lvl, 
     }
   }
   if (vec == 4 && async_enabled_fwd()) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_forward_async, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsyncSmem);
-      attr = true;
-    }
+    opt_in_smem(reinterpret_cast<const void*>(k_forward_async), kAsyncSmem);
     static const int gcap = tile_grid("SGX_GRID_FWD", 1 << 30);
     const int grid = gcap < tiles ? gcap : tiles;
     k_forward_async<<<grid, 32 * kWarps, kAsyncSmem, st>>>(grp, lvl, n_levels, src, ncols, tape, n_rows,
@@ -2556,11 +2552,7 @@ void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* 
     }
   }
   if (vec == 4 && staged) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_backward_async, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
-      attr = true;
-    }
+    opt_in_smem(reinterpret_cast<const void*>(k_backward_async), kBwdSmem);
     k_backward_async<<<grid, 32 * kWarps, kBwdSmem, st>>>(rec, lvl, n_levels, tape, adj, V, ncols, n_rows, col_row,
                                                           dv_out, dp_out, lr, out_enc, out_tgt, n_out, row_loss,
                                                           exp_tab, hb, tiles, discard_enabled() ? dead : nullptr,
