@@ -1333,13 +1333,14 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
     auto s = std::make_unique<sgx_sampler>();
     s->c = c;
     s->cfg = *cfg;
-    // SGX_PRIO=1: the soft passes (st) outrank the harvest (sh) at the block
-    // scheduler.  Measured: C2 even, C4 +4.7 %, C3a -1.8 %, and the in-run
-    // backward launch 1.43 -> 1.47 ms; equal priorities by default.
+    // The soft passes (st) outrank the harvest (sh) at the block scheduler:
+    // the harvest has a whole iteration of slack (double-buffered input).
+    // Measured with the warp-synchronous harvest: C4 +2-3 %, C2 even.
+    // SGX_PRIO=0: equal priorities.
     int prio_lo = 0, prio_hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     const char* pe = std::getenv("SGX_PRIO");
-    const bool prio = pe && pe[0] == '1';
+    const bool prio = !(pe && pe[0] == '0');
     {
       StreamKit k = kit_take(c->ctx->device, prio, prio_lo, prio_hi);
       s->kit_prio = prio;

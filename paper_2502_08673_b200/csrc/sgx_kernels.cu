@@ -2079,38 +2079,58 @@ k_harvest_lw(const HarvestLiveArgs a, const int4* __restrict__ lw, int n_iters) 
     const unsigned par = static_cast<unsigned>(c / kLwBuf) & 1u;
     mbar_wait(&full[b], par);
     const int4* R = lwsm + b * kLwChunk * 32 + lane;
-#pragma unroll 4
-    for (int it = 0; it < kLwChunk; ++it) {
-      const int4 op = R[it * 32];
-      const uint32_t X = bits[op.y], Y = bits[op.z];
-      const uint32_t v = anf_gate(op.x, X, Y);
-      bits[(op.x >> 4) & 0xffffff] = v;
-      if (op.w >= 0) a.spill[op.w * Wz + w] = v;
-      if (op.x & kLwEnd) {  // warp-uniform: the phase's last iteration
-        if (op.x & kLwChk) {  // output checks and clauses of this phase (read-only)
-          const int cb = __ldg(a.chk_ptr + ph), ce = __ldg(a.chk_ptr + ph + 1);
-          for (int i = cb + lane; i < ce; i += 32) {
-            const int4 rec = __ldg(a.chk + i);
-            uint32_t any = 0u;
-            if (rec.w == kLbBig) {  // a long clause, literal by literal
-              for (int l = rec.x; l < rec.x + rec.y; ++l) {
-                const int lit = __ldg(a.big_lits + l), sgn = lit >> 31;
-                any |= bits[lit ^ sgn] ^ static_cast<uint32_t>(sgn);
-              }
-            } else {
-              const int lit[4] = {rec.x, rec.y, rec.z, rec.w};
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int sgn = lit[u] >> 31;
-                any |= bits[lit[u] ^ sgn] ^ static_cast<uint32_t>(sgn);
-              }
+    // output checks and clauses of phase ph (read-only), at its last iteration
+    auto phase_end = [&](const int4 op) {
+      if (op.x & kLwChk) {
+        const int cb = __ldg(a.chk_ptr + ph), ce = __ldg(a.chk_ptr + ph + 1);
+        for (int i = cb + lane; i < ce; i += 32) {
+          const int4 rec = __ldg(a.chk + i);
+          uint32_t any = 0u;
+          if (rec.w == kLbBig) {  // a long clause, literal by literal
+            for (int l = rec.x; l < rec.x + rec.y; ++l) {
+              const int lit = __ldg(a.big_lits + l), sgn = lit >> 31;
+              any |= bits[lit ^ sgn] ^ static_cast<uint32_t>(sgn);
             }
-            ok &= any;
+          } else {
+            const int lit[4] = {rec.x, rec.y, rec.z, rec.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int sgn = lit[u] >> 31;
+              any |= bits[lit[u] ^ sgn] ^ static_cast<uint32_t>(sgn);
+            }
           }
+          ok &= any;
         }
-        ++ph;
-        __syncwarp();
       }
+      ++ph;
+      __syncwarp();
+    };
+    // Iterations in pairs: when the first of a pair does not end its phase,
+    // both read only slots of earlier phases (and write slots no op of this
+    // phase reads), so the second's operand loads go out before the first's
+    // store -- two independent chains per lane.
+#pragma unroll 2
+    for (int it = 0; it < kLwChunk; it += 2) {
+      const int4 o0 = R[it * 32], o1 = R[(it + 1) * 32];
+      const uint32_t X0 = bits[o0.y], Y0 = bits[o0.z];
+      const bool same = !(o0.x & kLwEnd);  // warp-uniform
+      uint32_t X1 = 0u, Y1 = 0u;
+      if (same) {
+        X1 = bits[o1.y];
+        Y1 = bits[o1.z];
+      }
+      const uint32_t v0 = anf_gate(o0.x, X0, Y0);
+      bits[(o0.x >> 4) & 0xffffff] = v0;
+      if (o0.w >= 0) a.spill[o0.w * Wz + w] = v0;
+      if (!same) {
+        phase_end(o0);
+        X1 = bits[o1.y];
+        Y1 = bits[o1.z];
+      }
+      const uint32_t v1 = anf_gate(o1.x, X1, Y1);
+      bits[(o1.x >> 4) & 0xffffff] = v1;
+      if (o1.w >= 0) a.spill[o1.w * Wz + w] = v1;
+      if (o1.x & kLwEnd) phase_end(o1);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[b]);

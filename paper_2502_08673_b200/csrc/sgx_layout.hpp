@@ -78,7 +78,8 @@ constexpr int kCnfThreads = 256;               // threads of the shared-memory h
 constexpr int32_t kCnfOpen = INT32_MIN;        // CNF record continues (see fb_cnf4)
 constexpr int32_t kLwEnd = 1 << 30, kLwChk = 1 << 29;
 // k_harvest_lw record ring: kLwBuf chunks of kLwChunk iterations (32 int4 each); lw_ops is padded to whole chunks
-constexpr int kLwChunk = 8, kLwBuf = 4, kLwRingBytes = kLwChunk * kLwBuf * 32 * 16;  // lw_ops .x flags (op kind | out_slot << 4 below)
+constexpr int kLwChunk = 8, kLwBuf = 4, kLwRingBytes = kLwChunk * kLwBuf * 32 * 16;
+static_assert(kLwChunk % 2 == 0, "k_harvest_lw runs iterations in pairs inside a chunk");  // lw_ops .x flags (op kind | out_slot << 4 below)
 constexpr int32_t kLbBig = INT32_MIN;          // lb_chk: long clause, literals in lb_big_lits
 constexpr int kGroup = 4;                      // ops per forward group
 constexpr int kGroupRecs = 1 + kGroup / 2;     // int4 records per group
