@@ -2171,18 +2171,33 @@ k_keys_spill(const HarvestLiveArgs a) {
   uint64_t h[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) h[j] = 0ull;
+  // Software-pipelined over this warp's key words: the spill rows of key word
+  // q + 8 are in flight while q is transposed and hashed.
+  uint4 nx[2][2];
+  uint32_t nm[2];
+  auto fetch = [&](int q) {
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const int e = q < a.key_words ? __ldg(a.key_enc + (2 * q + hf) * 32 + lane) : -1;
+      nx[hf][0] = nx[hf][1] = make_uint4(0, 0, 0, 0);
+      nm[hf] = e >= 0 ? neg_mask(e) : 0u;
+      if (e >= 0) {
+        const uint4* p = reinterpret_cast<const uint4*>(a.spill + (e >> 1) * Wz + w0);
+        nx[hf][0] = __ldg(p);
+        nx[hf][1] = __ldg(p + 1);
+      }
+    }
+  };
+  fetch(warp);
   for (int q = warp; q < a.key_words; q += 8) {
+    uint4 cx[2][2] = {{nx[0][0], nx[0][1]}, {nx[1][0], nx[1][1]}};
+    const uint32_t cm[2] = {nm[0], nm[1]};
+    fetch(q + 8);
     uint32_t half[2][8];
 #pragma unroll
     for (int hf = 0; hf < 2; ++hf) {
-      const int e = __ldg(a.key_enc + (2 * q + hf) * 32 + lane);
-      uint4 A = make_uint4(0, 0, 0, 0), Bv = make_uint4(0, 0, 0, 0);
-      if (e >= 0) {
-        const uint4* p = reinterpret_cast<const uint4*>(a.spill + (e >> 1) * Wz + w0);
-        A = __ldg(p);
-        Bv = __ldg(p + 1);
-      }
-      const uint32_t m = e >= 0 ? neg_mask(e) : 0u;
+      const uint4 A = cx[hf][0], Bv = cx[hf][1];
+      const uint32_t m = cm[hf];
       const uint32_t x[8] = {A.x ^ m, A.y ^ m, A.z ^ m, A.w ^ m, Bv.x ^ m, Bv.y ^ m, Bv.z ^ m, Bv.w ^ m};
 #pragma unroll
       for (int j = 0; j < 8; ++j) half[hf][j] = transpose32(x[j], lane);
