@@ -2569,7 +2569,11 @@ void launch_backward_rec(cudaStream_t st, int vec, const int4* rec, const int2* 
     const size_t s3 = static_cast<size_t>(kWarps) * 3 * kBU * 2 * 32 * 16 + blk;
     const size_t s2 = static_cast<size_t>(kWarps) * 2 * kBU * 2 * 32 * 16 + blk;
     const int disc = discard_enabled() ? 1 : 0;
-    if (s3 <= 54 * 1024) {
+    static const int force_bs = [] {  // SGX_BWD_BS=2|3 (A/B): stages regardless of occupancy
+      const char* e = std::getenv("SGX_BWD_BS");
+      return e ? std::atoi(e) : 0;
+    }();
+    if ((force_bs == 3 || (force_bs != 2 && s3 <= 54 * 1024)) && s3 <= 200 * 1024) {
       opt_in_smem(reinterpret_cast<const void*>(k_backward_tma<3>), s3);
       k_backward_tma<3><<<grid, 32 * kWarps, s3, st>>>(bb->sblk, bb->blk0_n4, bb->blk_max, n_levels, tape, adj, V,
                                                      ncols, n_rows, col_row, dv_out, dp_out, lr, out_enc, out_tgt,

@@ -7,7 +7,8 @@ processes with torch.distributed (gloo) behind the exchange callbacks -- on
 cuda:0 and compares with a single sampler at N*B: global unique count,
 per-harvest new-unique trace, attempts, restarts and the solution set.
 The NCCL exchange has the same contract (ncclAllGather on the sampler
-stream); it needs one GPU per rank.
+stream); NCCL needs one GPU per rank, so on a one-GPU box it runs as a world
+of one (communicator, collectives and host all-gather all exercised).
 """
 import os
 import tempfile
@@ -127,3 +128,26 @@ def test_processes_torch_exchange_equal_one_device(gpu, name, batch, kw):
         assert st == (want.unique_count, want.new_unique, want.attempts, want.restarts)
     union = set().union(*(as_set(k) for k in keys))
     assert union == as_set(want_keys)
+
+
+@pytest.mark.parametrize("name,batch,kw", [CASES[1], CASES[3]], ids=["c2", "c3a-quota"])
+def test_nccl_exchange_single_rank_equals_sgx_run(gpu, name, batch, kw):
+    """The NCCL exchange end to end on the one GPU a box gives: a world of one
+    (sgx_nccl_unique_id -> sgx_exchange_nccl_create -> sgx_run_sharded), so the
+    communicator set-up, ncclAllGather on the sampler stream and the host
+    all-gather all run.  A world of one is exactly sgx_run."""
+    inst = load_instance(name)
+    want, want_keys = single(inst, batch, kw)
+    ex = D.NcclExchange(1, D.nccl_unique_id(), 0, 0)
+    s = Sampler(DeviceCircuit.from_instance(inst), SamplerConfig(batch=batch, **kw))
+    try:
+        st = D.run_native(s, ex)
+        keys = s.fetch()
+    finally:
+        s.close()
+        ex.close()
+    assert st.unique_count == want.unique_count
+    assert st.new_unique == want.new_unique
+    assert st.attempts == want.attempts
+    assert st.restarts == want.restarts
+    assert np.array_equal(keys, want_keys)
