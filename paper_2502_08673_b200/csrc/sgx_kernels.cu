@@ -747,7 +747,15 @@ __device__ __forceinline__ void backward_record(const int4 r, const float4 gs, c
               const float fa = __fmaf_rn(C.y, __fmaf_rn(ns, y[v], no), C.x);
               acc[v] = __fadd_rn(acc[v], __fmul_rn(g[v], fa));
             }
-          } else {  // seeds, SUB runs (folded NOT/BUF consumers), empty nodes
+          } else if (f & kRSubOne) {  // a one-edge, unseeded SUB run: adj[j] = +0 + g*fa (the reference's
+                                      // fresh zero adjoint, autodiff.cpp:191), then acc -/+= adj[j] (:225-233)
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              const float fa = __fmaf_rn(C.y, __fmaf_rn(ns, y[v], no), C.x);
+              const float sj = __fadd_rn(0.0f, __fmul_rn(g[v], fa));
+              acc[v] = (f & kRSubNot) ? __fsub_rn(acc[v], sj) : __fadd_rn(acc[v], sj);
+            }
+          } else {  // seeds, longer SUB runs (folded NOT/BUF consumers), empty nodes
             if (f & (kRFirst | kRSubFirst)) {
               float sd[V] = {0.0f, 0.0f, 0.0f, 0.0f}, sd2[V] = {0.0f, 0.0f, 0.0f, 0.0f};
               if (f & (kRSeed | kRSubSeed)) {  // adj[out] += 2 (y - t) on a zero adjoint (autodiff.cpp:206)

@@ -273,6 +273,11 @@ void run_records(const std::vector<I4>& run, std::vector<I4>& out) {
   }
   for (size_t k = start; k < out.size(); ++k)
     if ((out[k].x & (kRInSub | kRSubFirst | kRSubLast | kRSeed | kRSubSeed)) || out[k].y < 0) out[k].x |= kRSlow;
+  for (size_t k = start; k < out.size(); ++k) {
+    const int32_t f = out[k].x;
+    if ((f & kRInSub) && (f & kRSubFirst) && (f & kRSubLast) && !(f & (kRSeed | kRSubSeed)) && out[k].y >= 0)
+      out[k].x |= kRSubOne;
+  }
 }
 
 // Soft program over the nodes with in_set[i] != 0 (closed under operands).
@@ -567,6 +572,25 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
       fprintf(stderr, "[sgx] bwd live rows across passes: adjoint max %d mean %.0f; tape (between reads) max %d mean %.0f; tape incl. single-read max %d; rows never read by the backward %d\n",
               ma, double(sa) / nl, mt, double(st) / nl, mu, never);
     }
+    {
+      int64_t slow = 0, sub = 0, lastc = 0, nrec = 0, sfirst = 0, slast = 0, sboth = 0;
+      for (int li = 0; li < nl; ++li)
+        for (int w = 0; w < kWarps; ++w) {
+          const int32_t first = P.rec_lvl[2 * (li * kWarps + w)], cnt = P.rec_lvl[2 * (li * kWarps + w) + 1];
+          for (int32_t k = first; k < first + cnt; ++k) {
+            ++nrec;
+            slow += (P.rec[k].x & kRSlow) ? 1 : 0;
+            sub += (P.rec[k].x & kRInSub) ? 1 : 0;
+            lastc += (P.rec[k].x & kRLast) ? 1 : 0;
+            sfirst += (P.rec[k].x & kRSubFirst) ? 1 : 0;
+            slast += (P.rec[k].x & kRSubLast) ? 1 : 0;
+            sboth += ((P.rec[k].x & kRSubFirst) && (P.rec[k].x & kRSubLast)) ? 1 : 0;
+          }
+        }
+      fprintf(stderr, "[sgx] bwd records: %lld, slow %lld (in SUB runs %lld: first %lld, last %lld, both %lld), node ends %lld\n",
+              (long long)nrec, (long long)slow, (long long)sub, (long long)sfirst, (long long)slast, (long long)sboth,
+              (long long)lastc);
+    }
     fprintf(stderr, "[sgx] bwd reads: %lld adjoint, %lld tape (rows %d, passes %d)\n", (long long)nA, (long long)nT, P.n_rows, nl);
     const char* names[8] = {"<=0", "1", "2", "3-4", "5-8", "9-32", "33-128", ">128"};
     for (int b = 0; b < 8; ++b)
@@ -652,6 +676,7 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
       for (int w = 0; w < kWarps; ++w) {
         const int32_t first = P.rec_lvl[2 * (li * kWarps + w)], cnt = P.rec_lvl[2 * (li * kWarps + w) + 1];
         P.oc_rec.insert(P.oc_rec.end(), P.rec.begin() + first, P.rec.begin() + first + cnt);
+        for (auto it = P.oc_rec.end() - cnt; it != P.oc_rec.end(); ++it) it->x &= ~kRSubOne;
       }
       P.oc_rec_lvl.push_back(static_cast<int32_t>(P.oc_rec.size()) - P.oc_rec_lvl.back());
     }

@@ -73,6 +73,11 @@ constexpr int32_t kRInSub = 1 << 4, kRNegOther = 1 << 5, kRFirst = 1 << 6, kRSub
 // SUB-run records, records without an edge) -- the staged kernel's fast path
 // is taken only without it.
 constexpr int32_t kRSlow = 1 << 16;
+// kRSubOne (with kRSlow, staged records only): a SUB run of ONE edge and no
+// seed -- adj[j] = +0 + g*fa, then acc -= / += adj[j] -- which the staged
+// kernel runs on a short branch of its own (79 % of the SUB-run records on
+// C4 and C2).  Cleared in oc_rec, whose bits 17+ hold slots.
+constexpr int32_t kRSubOne = 1 << 29;
 constexpr int kOcSlotShift = 17;  // oc_rec: adjoint store slot in the flag word
 constexpr int kCnfThreads = 256;               // threads of the shared-memory harvest CTA
 constexpr int32_t kCnfOpen = INT32_MIN;        // CNF record continues (see fb_cnf4)
