@@ -24,7 +24,7 @@ def val(r, key):
 
 
 fam = {"k_backward": "k_backward", "k_forward": "k_forward", "k_harvest_smem": "k_harvest",
-       "k_harvest_live": "k_harvest"}
+       "k_harvest_live": "k_harvest", "k_harvest_lw": "k_harvest", "k_keys_spill": "k_keys"}
 res = {}
 for r in rows[2:]:
     kname = r[hdr.index("Kernel Name")]
