@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -54,6 +55,72 @@ const uint64_t kExpTab[32] = {
     0x3feee89f995ad3adull, 0x3feeff76f2fb5e47ull, 0x3fef199bdd85529cull, 0x3fef3720dcef9069ull,
     0x3fef5818dcfba487ull, 0x3fef7c97337b9b5full, 0x3fefa4afa2a490daull, 0x3fefd0765b6e4540ull};
 
+// Quiescent big device blocks kept for the next sampler of the same shape
+// (exact byte size, per device): a run after a run of the same circuit and
+// batch allocates its tape / adjoint / store / key buffers without asking the
+// stream-ordered pool, which after a run with store growth can need new
+// physical mappings for them (10-175 ms of sampler creation measured on C4).
+// Capped at 40 % of device memory; flushed when an allocation fails.
+namespace blockcache {
+constexpr size_t kMin = size_t{64} << 20;
+std::mutex mu;
+std::map<std::pair<int, size_t>, std::vector<void*>> held;
+std::map<int, size_t> held_bytes;
+size_t cap(int dev) {
+  static std::map<int, size_t> caps;
+  auto it = caps.find(dev);
+  if (it == caps.end()) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+      cudaGetLastError();
+      tot = 0;
+    }
+    it = caps.emplace(dev, tot / 10 * 4).first;
+  }
+  return it->second;
+}
+void* take(size_t bytes) {
+  if (bytes < kMin) return nullptr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = held.find({dev, bytes});
+  if (std::getenv("SGX_TRACE"))
+    std::fprintf(stderr, "[sgx] block cache %s %.3f GB (held %.2f GB)\n",
+                 (it == held.end() || it->second.empty()) ? "miss" : "hit", bytes / 1e9, held_bytes[dev] / 1e9);
+  if (it == held.end() || it->second.empty()) return nullptr;
+  void* p = it->second.back();
+  it->second.pop_back();
+  held_bytes[dev] -= bytes;
+  return p;
+}
+bool give(void* p, size_t bytes) {
+  if (bytes < kMin || std::getenv("SGX_NO_BLOCK_CACHE")) return false;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  if (held_bytes[at.device] + bytes > cap(at.device)) return false;
+  held[{at.device, bytes}].push_back(p);
+  held_bytes[at.device] += bytes;
+  return true;
+}
+void flush() {  // back to the pool (current device's blocks)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& [k, v] : held)
+    if (k.first == dev) {
+      for (void* p : v) cudaFreeAsync(p, 0);
+      v.clear();
+    }
+  held_bytes[dev] = 0;
+  cudaStreamSynchronize(0);
+}
+}  // namespace blockcache
+
 // Owning device buffer.
 template <typename T>
 struct DBuf {
@@ -69,10 +136,11 @@ struct DBuf {
   // in the legacy stream's order instead of through cudaFree's device sync.
   void reset() {
     if (p) {
-      if (pooled)
-        cudaFreeAsync(p, 0);
-      else
+      if (pooled) {
+        if (!blockcache::give(p, std::max<size_t>(n, 1) * sizeof(T))) cudaFreeAsync(p, 0);
+      } else {
         cudaFree(p);
+      }
     }
     p = nullptr;
     n = 0;
@@ -94,7 +162,18 @@ struct DBuf {
   void alloc_async(size_t count, cudaStream_t st) {
     reset_async(st);
     size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    if (void* q = blockcache::take(bytes)) {  // quiescent: usable on any stream
+      p = static_cast<T*>(q);
+      n = count;
+      pooled = true;
+      return;
+    }
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, st);
+    if (e != cudaSuccess) {  // the cached blocks may be what is missing
+      cudaGetLastError();
+      blockcache::flush();
+      e = cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, st);
+    }
     if (e != cudaSuccess) {
       cudaGetLastError();
       p = nullptr;
@@ -1240,6 +1319,77 @@ int sgx_sampler_soft_info(const sgx_sampler* s, int64_t* info8) {
   });
 }
 
+// In-process layout cache: the levelized programs of the last few circuits,
+// keyed by a hash of the whole descriptor (and the environment knobs the
+// layout compiler reads), so a run() on a circuit this process has already
+// compiled copies its layout instead of rebuilding it (C4: ~30 ms of the
+// end-to-end call on the GPU host).  SGX_NO_LAYOUT_CACHE=1 turns it off.
+extern "C++" {
+namespace layoutcache {
+uint64_t mix(uint64_t h, uint64_t x) {
+  h ^= x + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  return h * 0xff51afd7ed558ccdull;
+}
+template <typename T>
+uint64_t add(uint64_t h, const T* p, int64_t n) {
+  h = mix(h, static_cast<uint64_t>(n));
+  if (!p || n <= 0) return h;
+  const size_t bytes = static_cast<size_t>(n) * sizeof(T);
+  const unsigned char* c = reinterpret_cast<const unsigned char*>(p);
+  size_t i = 0;
+  for (; i + 8 <= bytes; i += 8) {
+    uint64_t w;
+    std::memcpy(&w, c + i, 8);
+    h = mix(h, w);
+  }
+  uint64_t t = 0;
+  std::memcpy(&t, c + i, bytes - i);
+  return mix(h, t);
+}
+uint64_t key(const sgx_circuit_desc& d) {
+  uint64_t h = 0x5367785f6c61796full;
+  h = add(h, d.kind, d.n_nodes);
+  h = add(h, d.a, d.n_nodes);
+  h = add(h, d.b, d.n_nodes);
+  h = add(h, d.var, d.n_nodes);
+  h = mix(h, static_cast<uint64_t>(d.num_vars));
+  h = add(h, d.out_var, d.n_outputs);
+  h = add(h, d.out_target, d.n_outputs);
+  h = add(h, d.cpi, d.n_cpi);
+  h = add(h, d.ucpi, d.n_ucpi);
+  h = add(h, d.clause_ptr, d.n_clauses + 1);
+  h = add(h, d.clause_lit, d.clause_ptr && d.n_clauses >= 0 ? d.clause_ptr[d.n_clauses] : 0);
+  for (const char* k : {"SGX_ALL_CLAUSES", "SGX_SCHED"}) {
+    const char* v = std::getenv(k);
+    h = add(h, v, v ? static_cast<int64_t>(std::strlen(v)) : 0);
+  }
+  return h;
+}
+std::mutex mu;
+std::vector<std::pair<uint64_t, std::shared_ptr<const sgx::Layout>>> lru;  // most recent last
+bool on() { return !std::getenv("SGX_NO_LAYOUT_CACHE"); }
+sgx::Layout get(const sgx_circuit_desc& d) {
+  if (!on()) return sgx::build_layout(d);
+  const uint64_t k = key(d);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (size_t i = 0; i < lru.size(); ++i)
+      if (lru[i].first == k) {
+        auto e = lru[i];
+        lru.erase(lru.begin() + static_cast<long>(i));
+        lru.push_back(e);
+        return *e.second;
+      }
+  }
+  auto L = std::make_shared<const sgx::Layout>(sgx::build_layout(d));
+  std::lock_guard<std::mutex> lk(mu);
+  lru.emplace_back(k, L);
+  if (lru.size() > 4) lru.erase(lru.begin());
+  return *L;
+}
+}  // namespace layoutcache
+}  // extern "C++"
+
 int sgx_circuit_upload(sgx_ctx* ctx, const sgx_circuit_desc* d, sgx_circuit** out) {
   return guard([&] {
     need(ctx, "ctx");
@@ -1260,7 +1410,7 @@ int sgx_circuit_upload(sgx_ctx* ctx, const sgx_circuit_desc* d, sgx_circuit** ou
         c->L.key_words = (d->num_vars + 63) / 64;
       }
     } else {
-      c->L = sgx::build_layout(*d);
+      c->L = layoutcache::get(*d);
       c->layout_ok = true;
     }
     if (c->layout_ok) {
@@ -1317,6 +1467,7 @@ int sgx_circuit_free(sgx_circuit* c) {
 }
 
 int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler** out) {
+  const auto t_create = std::chrono::steady_clock::now();
   return guard([&] {
     need(c, "circuit");
     need(cfg, "cfg");
@@ -1367,6 +1518,7 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
       std::memset(s->hpin, 0, sizeof(sgx::HarvestOut));
       s->hout.alloc_async(1, s->st);
       CK(cudaStreamSynchronize(s->st));
+      const auto t_head = std::chrono::steady_clock::now();
       if (c->layout_ok && !c->L.unsat) {
         const auto& L = c->L;
         s->Bp = round_up(cfg->batch, 1024);
@@ -1504,20 +1656,48 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
         s->slot_of_row.alloc_async(Bp, st);
         s->block_count.alloc_async(Bp / sgx::kThreads, st);
         s->K.alloc_async(static_cast<size_t>(L.key_words) * Bp, st);
-        // Room for a few restarts' worth of solutions (16 harvests of unique
-        // rows, at most 4 GB of keys) before the first growth -- a growth waits
-        // for the host drain and copies the store; a quota caps it.
+        // Room for every row the run can harvest (restarts x (iterations + 1)
+        // batches, + 2 for the growth trigger) when that fits 24 GB and a
+        // quarter of the free device memory, else the old floor (16 harvests,
+        // at most 4 GB): a growth waits for the host drain, copies the store
+        // and allocates from the pool mid-run (C4: up to 1.7 s of fresh
+        // mappings on a first run).  A quota caps it.
+        const long long key_bytes = static_cast<long long>(L.key_words) * 8;
         long long want_rows = 16 * static_cast<long long>(Bp);
-        const long long cap_4g = (4ll << 30) / (static_cast<long long>(L.key_words) * 8);
+        const long long cap_4g = (4ll << 30) / key_bytes;
         want_rows = std::max<long long>(std::min(want_rows, cap_4g), 2 * static_cast<long long>(Bp));
+        {
+          const bool restarts = cfg->restart_policy != SGX_RESTART_NONE;
+          const long long n_restarts = restarts ? (cfg->max_restarts > 0 ? cfg->max_restarts : 1000) + 1 : 1;
+          const long long bound = (n_restarts * (static_cast<long long>(cfg->iterations) + 1) + 2) * Bp;
+          size_t fr = 0, tot = 0;
+          if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+            cudaGetLastError();
+            fr = 0;
+          }
+          const long long roomy = std::min<long long>((24ll << 30), static_cast<long long>(fr / 4)) / key_bytes;
+          if (bound <= roomy) want_rows = std::max(want_rows, bound);
+        }
         if (cfg->max_solutions > 0) want_rows = std::min<long long>(want_rows, cfg->max_solutions + Bp);
         s->store_cap = cfg->solution_capacity > 0 ? cfg->solution_capacity : want_rows;
         s->store.alloc_async(static_cast<size_t>(s->store_cap) * L.key_words, st);
         CK(cudaMemsetAsync(s->V.p, 0, s->V.n * sizeof(float), s->st));
         CK(cudaMemsetAsync(s->HB.p, 0xff, s->HB.n * sizeof(uint32_t), s->st));  // harden(0) = 1
+        const auto ta = std::chrono::steady_clock::now();
+        const double t_alloc = std::chrono::duration<double, std::milli>(ta - t_head).count();
+        const double t_front = std::chrono::duration<double, std::milli>(t_head - t_create).count();
         ensure_table(s.get());
+        const auto tb = std::chrono::steady_clock::now();
         CK(cudaStreamSynchronize(s->st));
         CK(cudaStreamSynchronize(s->sh));
+        if (std::getenv("SGX_TRACE")) {
+          const auto tc = std::chrono::steady_clock::now();
+          std::fprintf(stderr, "[sgx] sampler create: %.2f ms (streams + first sync %.2f, buffers %.2f, table %.2f ms, allocation / memset sync %.2f ms, store %.2f GB)\n",
+                       std::chrono::duration<double, std::milli>(tc - t_create).count(), t_front, t_alloc,
+                       std::chrono::duration<double, std::milli>(tb - ta).count(),
+                       std::chrono::duration<double, std::milli>(tc - tb).count(),
+                       s->store_cap * L.key_words * 8.0 / 1e9);
+        }
       }
     } catch (...) {
       sgx_sampler_free(s.release());
@@ -1538,24 +1718,24 @@ int sgx_sampler_free(sgx_sampler* s) {
     const double t_sync = ms();
     s->drain.reset();                          // no host copy left reading the store
     const double t_drain = ms();
-    if (st) {  // hand the big buffers back to the pool in stream order
-      for (auto* b : {&s->V, &s->tape, &s->adj, &s->row_loss, &s->adam_dv, &s->adam_dp, &s->adam_m, &s->adam_v})
-        b->reset_async(st);
-      s->partial.reset_async(st);
-      for (auto* b : {&s->BT, &s->valid, &s->newmask, &s->HB, &s->SP}) b->reset_async(st);
-      s->fps_local.reset_async(st);
-      s->fps_all.reset_async(st);
-      s->n_of.reset_async(st);
-      s->slot_of_row.reset_async(st);
-      s->block_count.reset_async(st);
-      s->K.reset_async(st);
-      s->store.reset_async(st);
-      s->tkeys.reset_async(st);
-      s->tmeta.reset_async(st);
-    }
-    const double t_reset = ms();
     if (st) cudaStreamSynchronize(st);
     const double t_sync2 = ms();
+    if (st) {  // quiescent: big buffers go to the block cache, the rest back to the pool
+      for (auto* b : {&s->V, &s->tape, &s->adj, &s->row_loss, &s->adam_dv, &s->adam_dp, &s->adam_m, &s->adam_v})
+        b->reset();
+      s->partial.reset();
+      for (auto* b : {&s->BT, &s->valid, &s->newmask, &s->HB, &s->SP}) b->reset();
+      s->fps_local.reset();
+      s->fps_all.reset();
+      s->n_of.reset();
+      s->slot_of_row.reset();
+      s->block_count.reset();
+      s->K.reset();
+      s->store.reset();
+      s->tkeys.reset();
+      s->tmeta.reset();
+    }
+    const double t_reset = ms();
     StreamKit k;
     k.device = s->c->ctx->device;
     k.prio = s->kit_prio;

@@ -435,6 +435,7 @@ def run(cnf: CnfFormula, circuit: Circuit, paths: PathClassification, cfg: Sampl
     dc.unsat_note = unsat_note
     t.append(time.perf_counter())
     s = Sampler(dc, cfg)
+    t_s = time.perf_counter()
     try:
         s.set_host_stream(True)  # the result streams to the host while sampling runs
         t.append(time.perf_counter())
@@ -449,8 +450,8 @@ def run(cnf: CnfFormula, circuit: Circuit, paths: PathClassification, cfg: Sampl
     t.append(time.perf_counter())
     if trace:
         d = [1000 * (b - a) for a, b in zip(t, t[1:])]
-        print("[run] circuit %.1f sampler %.1f run %.1f (device %.1f) take %.1f close sampler %.1f circuit %.1f ms" %
-              (d[0], d[1], d[2], stats.device_ms, d[3], d[4], d[5]), flush=True)
+        print("[run] circuit %.1f sampler %.1f (create %.1f) run %.1f (device %.1f) take %.1f close sampler %.1f "
+              "circuit %.1f ms" % (d[0], d[1], 1000 * (t_s - t[1]), d[2], stats.device_ms, d[3], d[4], d[5]), flush=True)
     return RunResult(SolutionSet(cnf.num_vars, keys), stats)
 
 
