@@ -10,6 +10,7 @@ epilogue.  Reports modelled DRAM GB per backward launch at B samples.
 usage: python tools/l2sim.py INSTANCE [--tiles T ...] [--l2 MB]
 """
 import argparse
+import os
 import sys
 from collections import OrderedDict
 
@@ -70,7 +71,7 @@ def simulate(P, tiles, l2_mb=110.0, y_first=False, discard=False, inline_end=Fal
     blk = tiles * 512
     cap = int(l2_mb * 1e6 // blk)
     lru = OrderedDict()  # key -> dirty
-    stats = dict(rd=0, wr=0)
+    stats = dict(rd=0, wr=0, rd_t=0, rd_a=0, rd_v=0)
 
     def evict():
         while len(lru) > cap:
@@ -83,6 +84,7 @@ def simulate(P, tiles, l2_mb=110.0, y_first=False, discard=False, inline_end=Fal
             lru.move_to_end(k)
         else:
             stats["rd"] += 1
+            stats["rd_" + k[0]] += 1
             lru[k] = False
             if cold:
                 lru.move_to_end(k, last=False)
@@ -133,6 +135,8 @@ def simulate(P, tiles, l2_mb=110.0, y_first=False, discard=False, inline_end=Fal
             stats["wr"] += 1
     waves = total_tiles / tiles
     gb = lambda x: x * blk * waves / 1e9
+    if os.environ.get("L2SIM_SPLIT"):
+        print(f"   reads: tape {gb(stats['rd_t']):.2f} adjoint {gb(stats['rd_a']):.2f} V {gb(stats['rd_v']):.2f} GB")
     return gb(stats["rd"]), gb(stats["wr"])
 
 
@@ -145,7 +149,7 @@ if __name__ == "__main__":
     args = ap.parse_args()
     P = program(args.inst, args.sched)
     for t in args.tiles:
-        for yf, dc, ie in [(0, 0, 0), (1, 0, 0), (0, 1, 0), (1, 1, 0), (1, 1, 1)]:
+        for yf, dc, ie in ([(1, 1, 0)] if os.environ.get("L2SIM_SPLIT") else [(0, 0, 0), (1, 0, 0), (0, 1, 0), (1, 1, 0), (1, 1, 1)]):
             rd, wr = simulate(P, t, args.l2, bool(yf), bool(dc), bool(ie))
             print(f"tiles {t:4d} y_first {yf} discard {dc} inline_end {ie}: rd {rd:.2f} wr {wr:.2f} "
                   f"total {rd + wr:.2f} GB")
