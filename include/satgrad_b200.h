@@ -155,6 +155,19 @@ int sgx_open(int device, sgx_ctx** out);
 int sgx_close(sgx_ctx* ctx);
 
 int sgx_circuit_upload(sgx_ctx* ctx, const sgx_circuit_desc* desc, sgx_circuit** out);
+
+/* Layout caches of sgx_circuit_upload.  In process: the compiled programs of
+ * the last 4 circuits, keyed by a hash of the whole descriptor
+ * (SGX_NO_LAYOUT_CACHE=1 turns it off).  On disk: with a directory set here
+ * (or SGX_LAYOUT_CACHE_DIR), an upload reads <dir>/<key>.sgxlayout if present
+ * and valid, else compiles and writes it -- the counterpart of the reference
+ * CLI's circuit-JSON cache (tools/satgrad_main.cpp:137-184) one stage later.
+ * NULL or "" disables the disk cache. */
+int sgx_set_layout_cache_dir(const char* dir);
+/* Host only: the layout sgx_circuit_upload would use (through both caches),
+ * as a digest of every persisted field; *source = 0 compiled, 1 from the
+ * in-process cache, 2 from the disk cache. */
+int sgx_layout_digest(const sgx_circuit_desc* desc, uint64_t* digest, int32_t* source);
 /* info[0..15]: nodes, cone nodes, cone edges, soft levels, bit levels,
  * fwd ops, bwd ops, bit ops, clauses, literals, key words, cpi, ucpi,
  * outputs, num_vars, unsat */

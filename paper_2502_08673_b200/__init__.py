@@ -10,12 +10,14 @@ from .circuit import (Circuit, Instance, PathClassification, SchemaError, classi
                       export_json, import_json, load_instance)
 from .extract import ExtractionResult, extract_circuit, instance_from_cnf
 from .sampler import (DeviceCircuit, Optimizer, RestartPolicy, SoftKernel, jit_source, RunResult, RunStats, Sampler, SamplerConfig,
-                      SolutionSet, layout_stats, run, run_instance, verify_solutions)
+                      SolutionSet, layout_digest, layout_stats, run, run_instance, set_layout_cache_dir,
+                      verify_solutions)
 
 __all__ = [
     "CnfFormula", "ParseError", "eval_cnf", "parse_dimacs", "verify_keys", "write_dimacs",
     "Circuit", "Instance", "PathClassification", "SchemaError", "classify_paths", "export_json",
     "import_json", "load_instance", "DeviceCircuit", "RestartPolicy", "RunResult", "RunStats",
-    "Sampler", "SamplerConfig", "SolutionSet", "layout_stats", "run", "run_instance",
+    "Sampler", "SamplerConfig", "SolutionSet", "layout_digest", "layout_stats", "run", "run_instance",
+    "set_layout_cache_dir",
     "ExtractionResult", "extract_circuit", "instance_from_cnf", "verify_solutions",
 ]

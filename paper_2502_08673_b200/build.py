@@ -17,7 +17,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsatgrad_b200.so")
-SOURCES = ["sgx_kernels.cu", "sgx_format.cu", "sgx_api.cpp", "sgx_layout.cpp", "sgx_drain.cpp", "sgx_extract.cpp", "sgx_verify.cu", "sgx_jit.cpp", "sgx_exchange.cpp"]
+SOURCES = ["sgx_kernels.cu", "sgx_format.cu", "sgx_api.cpp", "sgx_layout.cpp", "sgx_layout_io.cpp", "sgx_drain.cpp", "sgx_extract.cpp", "sgx_verify.cu", "sgx_jit.cpp", "sgx_exchange.cpp"]
 HEADERS = ["sgx_kernels.cuh", "sgx_launch.hpp", "sgx_layout.hpp", "sgx_drain.hpp", "sgx_extract.hpp", "sgx_jit.hpp"]
 
 NVCC_FLAGS = [

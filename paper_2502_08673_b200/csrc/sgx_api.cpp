@@ -1367,28 +1367,75 @@ uint64_t key(const sgx_circuit_desc& d) {
 }
 std::mutex mu;
 std::vector<std::pair<uint64_t, std::shared_ptr<const sgx::Layout>>> lru;  // most recent last
+std::string dir;  // on-disk cache directory (sgx_set_layout_cache_dir / SGX_LAYOUT_CACHE_DIR), "" = none
 bool on() { return !std::getenv("SGX_NO_LAYOUT_CACHE"); }
-sgx::Layout get(const sgx_circuit_desc& d) {
-  if (!on()) return sgx::build_layout(d);
+std::string disk_dir() {
+  std::lock_guard<std::mutex> lk(mu);
+  if (!dir.empty()) return dir;
+  const char* e = std::getenv("SGX_LAYOUT_CACHE_DIR");
+  return e ? std::string(e) : std::string();
+}
+// memory (last 4 circuits) -> disk (<dir>/<key>.sgxlayout) -> build (and save);
+// *source = 0 built, 1 memory, 2 disk
+sgx::Layout get(const sgx_circuit_desc& d, int* source = nullptr) {
+  if (source) *source = 0;
+  const std::string dd = disk_dir();
+  if (!on() && dd.empty()) return sgx::build_layout(d);
   const uint64_t k = key(d);
-  {
+  if (on()) {
     std::lock_guard<std::mutex> lk(mu);
     for (size_t i = 0; i < lru.size(); ++i)
       if (lru[i].first == k) {
         auto e = lru[i];
         lru.erase(lru.begin() + static_cast<long>(i));
         lru.push_back(e);
+        if (source) *source = 1;
         return *e.second;
       }
   }
-  auto L = std::make_shared<const sgx::Layout>(sgx::build_layout(d));
-  std::lock_guard<std::mutex> lk(mu);
-  lru.emplace_back(k, L);
-  if (lru.size() > 4) lru.erase(lru.begin());
+  std::shared_ptr<const sgx::Layout> L;
+  char name[32];
+  std::snprintf(name, sizeof(name), "/%016llx.sgxlayout", static_cast<unsigned long long>(k));
+  if (!dd.empty()) {
+    sgx::Layout x;
+    if (sgx::load_layout(&x, dd + name, k)) {
+      L = std::make_shared<const sgx::Layout>(std::move(x));
+      if (source) *source = 2;
+      if (std::getenv("SGX_TRACE")) std::fprintf(stderr, "[sgx] layout loaded from %s%s\n", dd.c_str(), name);
+    }
+  }
+  if (!L) {
+    L = std::make_shared<const sgx::Layout>(sgx::build_layout(d));
+    if (!dd.empty() && !sgx::save_layout(*L, dd + name, k) && std::getenv("SGX_TRACE"))
+      std::fprintf(stderr, "[sgx] layout not saved to %s%s\n", dd.c_str(), name);
+  }
+  if (on()) {
+    std::lock_guard<std::mutex> lk(mu);
+    lru.emplace_back(k, L);
+    if (lru.size() > 4) lru.erase(lru.begin());
+  }
   return *L;
 }
 }  // namespace layoutcache
 }  // extern "C++"
+
+int sgx_layout_digest(const sgx_circuit_desc* desc, uint64_t* digest, int32_t* source) {
+  return guard([&] {
+    need(desc, "desc");
+    need(digest, "digest");
+    int src = 0;
+    const sgx::Layout L = layoutcache::get(*desc, &src);
+    *digest = sgx::layout_digest(L);
+    if (source) *source = src;
+  });
+}
+
+int sgx_set_layout_cache_dir(const char* dir) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(layoutcache::mu);
+    layoutcache::dir = dir ? std::string(dir) : std::string();
+  });
+}
 
 int sgx_circuit_upload(sgx_ctx* ctx, const sgx_circuit_desc* d, sgx_circuit** out) {
   return guard([&] {

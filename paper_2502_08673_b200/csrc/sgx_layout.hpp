@@ -237,6 +237,13 @@ Layout build_layout(const sgx_circuit_desc& d);
 
 void layout_info(const Layout& L, int64_t* info16);
 
+// On-disk layout (sgx_layout_io.cpp): false on any I/O failure or mismatch
+// (magic, version, key, truncation); the caller then rebuilds.
+bool save_layout(const Layout& L, const std::string& path, uint64_t key);
+bool load_layout(Layout* L, const std::string& path, uint64_t key);
+// FNV-1a over every persisted field (tests: a loaded layout equals a built one).
+uint64_t layout_digest(const Layout& L);
+
 // The all-node soft program of the parity taps (sgx_forward / sgx_backward),
 // built on first use.
 void build_full_program(Layout& L);

@@ -241,6 +241,25 @@ def layout_stats(cnf, circuit, paths, unsat=False) -> dict:
     return dict(zip(keys, (int(x) for x in out)))
 
 
+def set_layout_cache_dir(path: str | None) -> None:
+    """On-disk layout cache for every later circuit upload (sgx_set_layout_cache_dir):
+    <path>/<descriptor hash>.sgxlayout is read if valid, else compiled and written."""
+    _lib.check(_lib.load().sgx_set_layout_cache_dir(path.encode() if path else None))
+
+
+def layout_digest(cnf, circuit, paths, unsat=False) -> tuple[int, int]:
+    """Host only: (digest of the layout an upload would use, source 0 compiled /
+    1 in-process cache / 2 disk cache)."""
+    L = _lib.load()
+    keep = [np.ascontiguousarray(x) for x in (
+        circuit.kind, circuit.a, circuit.b, circuit.var, circuit.out_var, circuit.out_tgt,
+        paths.constrained_pi, paths.unconstrained_pi, cnf.clause_ptr, cnf.clause_lit)]
+    d = make_desc(cnf, circuit, paths, unsat, keep)
+    dig, src = C.c_uint64(), C.c_int32()
+    _lib.check(L.sgx_layout_digest(C.byref(d), C.byref(dig), C.byref(src)))
+    return int(dig.value), int(src.value)
+
+
 def harvest_clause_mask(cnf, circuit, paths, unsat=False) -> np.ndarray:
     """Host only: uint8 per CNF clause, 1 = implied by the gate definitions or
     the output targets, so the harvest does not check it

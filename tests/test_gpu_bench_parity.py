@@ -157,3 +157,26 @@ def test_forced_variant_matches_reference(gpu, rec, variant, monkeypatch):
     assert sha(keys) == rec["keys_sha256"]
     if rec.get("keys"):
         assert np.array_equal(keys, keys_from_hex(rec["keys"]))
+
+
+@pytest.mark.parametrize("rec", [r for r in golden_runs() if r["instance"] in ("c2_iscas", "c4_blasted", "c1b_random")
+                                 and not r["config"].get("max_solutions")][:4],
+                         ids=lambda r: f"{r['instance']}-{r['config']['batch']}")
+def test_layout_from_disk_matches_reference(gpu, rec, tmp_path, monkeypatch):
+    """A layout read back from the on-disk cache (set_layout_cache_dir) runs
+    exactly like a compiled one: the first upload compiles and writes it, the
+    second reads it (the in-process cache off, so the file is what is used)."""
+    from paper_2502_08673_b200 import layout_digest, set_layout_cache_dir
+    monkeypatch.setenv("SGX_NO_LAYOUT_CACHE", "1")
+    set_layout_cache_dir(str(tmp_path))
+    try:
+        i = inst(rec["instance"])
+        for want_src in (0, 2):
+            assert layout_digest(i.cnf, i.circuit, i.paths)[1] == want_src
+            st, keys, info = run(i, SoftKernel.HBM, **cfg_kwargs(rec["config"]))
+            assert st.unique_count == rec["unique"]
+            assert st.new_unique == rec["new_unique"]
+            assert sha(keys) == rec["keys_sha256"]
+            monkeypatch.setenv("SGX_NO_LAYOUT_CACHE", "1")
+    finally:
+        set_layout_cache_dir(None)
