@@ -587,6 +587,22 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
             sboth += ((P.rec[k].x & kRSubFirst) && (P.rec[k].x & kRSubLast)) ? 1 : 0;
           }
         }
+      {
+        std::vector<uint8_t> is_in(P.n_rows, 0);
+        for (int32_t r : P.col_row)
+          if (r >= 0) is_in[r] = 1;
+        int64_t tin = 0, tall = 0;
+        for (int li = 0; li < nl; ++li)
+          for (int w = 0; w < kWarps; ++w) {
+            const int32_t first = P.rec_lvl[2 * (li * kWarps + w)], cnt = P.rec_lvl[2 * (li * kWarps + w) + 1];
+            for (int32_t k = first; k < first + cnt; ++k)
+              if (P.rec[k].z >= 0) {
+                ++tall;
+                tin += is_in[P.rec[k].z];
+              }
+          }
+        fprintf(stderr, "[sgx] bwd tape reads of column-input rows: %lld of %lld\n", (long long)tin, (long long)tall);
+      }
       fprintf(stderr, "[sgx] bwd records: %lld, slow %lld (in SUB runs %lld: first %lld, last %lld, both %lld), node ends %lld\n",
               (long long)nrec, (long long)slow, (long long)sub, (long long)sfirst, (long long)slast, (long long)sboth,
               (long long)lastc);
