@@ -215,12 +215,16 @@ def time_to_1k(dev, with_cpu=True, name="c3a_or50", batch=1 << 20):
         dev_ms.append(st.device_ms)
     s.close()
     run_instance(inst, cfg, device=dev)  # warm-up of the public path (pool, host mapping)
-    t0 = time.perf_counter()
-    res = run_instance(inst, cfg, device=dev)  # public API: upload, run, fetch
-    e2e_ms = 1000.0 * (time.perf_counter() - t0)
+    e2e = []
+    for _ in range(5):  # a ~1.5 ms latency: the median of 5 calls
+        t0 = time.perf_counter()
+        res = run_instance(inst, cfg, device=dev)  # public API: upload, run, fetch
+        e2e.append(1000.0 * (time.perf_counter() - t0))
+        assert res.stats.unique_count == 1000
+    e2e_ms = statistics.median(e2e)
     out = {"workload": name, "batch": batch, "quota": 1000,
            "device_ms": statistics.median(dev_ms), "e2e_ms": e2e_ms,
-           "unique": res.stats.unique_count}
+           "e2e_ms_min_max": [min(e2e), max(e2e)], "unique": res.stats.unique_count}
     if with_cpu:
         from paper_2502_08673_b200 import write_dimacs
         from oracle.oracle import RefInstance, ref_available
