@@ -164,6 +164,12 @@ int sgx_circuit_upload(sgx_ctx* ctx, const sgx_circuit_desc* desc, sgx_circuit**
  * CLI's circuit-JSON cache (tools/satgrad_main.cpp:137-184) one stage later.
  * NULL or "" disables the disk cache. */
 int sgx_set_layout_cache_dir(const char* dir);
+
+/* Waits for every background compile of the circuit-specialised soft pass
+ * (SGX_SOFT_AUTO compiles it with NVRTC on a worker thread).  Also run
+ * automatically at exit; a host that tears the process down some other way
+ * (e.g. _exit, or unloading this library) calls it first. */
+int sgx_jit_quiesce(void);
 /* Host only: the layout sgx_circuit_upload would use (through both caches),
  * as a digest of every persisted field; *source = 0 compiled, 1 from the
  * in-process cache, 2 from the disk cache. */

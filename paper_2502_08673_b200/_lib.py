@@ -6,6 +6,7 @@ raises.  The sm_100a library is the only implementation of the sampling loop.
 from __future__ import annotations
 
 import ctypes as C
+import atexit
 import os
 
 import numpy as np
@@ -18,7 +19,7 @@ SGX_OK, SGX_E_INVALID, SGX_E_CUDA, SGX_E_NOMEM, SGX_E_STATE = 0, -1, -2, -3, -4
 # Every symbol include/satgrad_b200.h declares (tests check the export table).
 EXPORTS = [
     "sgx_last_error", "sgx_version", "sgx_open", "sgx_close", "sgx_circuit_upload",
-    "sgx_circuit_info", "sgx_circuit_free", "sgx_set_layout_cache_dir", "sgx_layout_digest", "sgx_layout_stats", "sgx_harvest_clause_mask", "sgx_sampler_create",
+    "sgx_circuit_info", "sgx_circuit_free", "sgx_set_layout_cache_dir", "sgx_layout_digest", "sgx_jit_quiesce", "sgx_layout_stats", "sgx_harvest_clause_mask", "sgx_sampler_create",
     "sgx_sampler_free", "sgx_init", "sgx_step", "sgx_harvest", "sgx_run", "sgx_run_traces",
     "sgx_solution_count", "sgx_key_words", "sgx_fetch_solutions", "sgx_phase_times",
     "sgx_forward", "sgx_backward", "sgx_embed", "sgx_expf", "sgx_fingerprint_stride",
@@ -110,6 +111,7 @@ def load() -> C.CDLL:
         "sgx_circuit_info": (C.c_int, [vp, i64p]),
         "sgx_circuit_free": (C.c_int, [vp]),
         "sgx_set_layout_cache_dir": (C.c_int, [C.c_char_p]),
+        "sgx_jit_quiesce": (C.c_int, []),
         "sgx_layout_digest": (C.c_int, [C.POINTER(CircuitDesc), C.POINTER(C.c_uint64), C.POINTER(C.c_int32)]),
         "sgx_layout_stats": (C.c_int, [C.POINTER(CircuitDesc), i64p]),
         "sgx_harvest_clause_mask": (C.c_int, [C.POINTER(CircuitDesc), C.POINTER(C.c_uint8)]),
@@ -164,6 +166,9 @@ def load() -> C.CDLL:
         fn.restype = res
         fn.argtypes = args
     _lib = L
+    # Background NVRTC compiles (the circuit-specialised soft pass) must end
+    # before the interpreter and the C++ runtime tear down (sgx_jit_quiesce).
+    atexit.register(L.sgx_jit_quiesce)
     return L
 
 

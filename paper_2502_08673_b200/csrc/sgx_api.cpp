@@ -1430,6 +1430,10 @@ int sgx_layout_digest(const sgx_circuit_desc* desc, uint64_t* digest, int32_t* s
   });
 }
 
+int sgx_jit_quiesce(void) {
+  return guard([&] { sgx::jit_quiesce(); });
+}
+
 int sgx_set_layout_cache_dir(const char* dir) {
   return guard([&] {
     std::lock_guard<std::mutex> lk(layoutcache::mu);

@@ -30,6 +30,8 @@ constexpr int64_t kJitMaxRecs = 6144;
 struct JitKernel;  // compiled kernel, shared by every sampler of the circuit
 
 bool jit_eligible(const Layout& L);
+// Waits for every background compile (sgx_jit_quiesce; also run at exit).
+void jit_quiesce();
 // CUDA C++ source of the kernel `sgx_jit_step` for L.cone (deterministic);
 // min_blocks = __launch_bounds__ minimum CTAs per SM (register budget).
 std::string jit_source(const Layout& L, int min_blocks);

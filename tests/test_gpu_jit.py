@@ -7,6 +7,8 @@ same V trajectory as the port oracle's init / embed / forward / backward /
 gd_step.  Every test forces the kernel (SoftKernel.JIT: compile at sampler
 creation and wait) and asserts that it is the kernel that ran.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -104,3 +106,17 @@ def test_jit_and_hbm_kernels_agree_at_bench_batch(gpu):
     assert st_j.new_unique == st_h.new_unique
     assert st_j.loss_trace == st_h.loss_trace
     assert np.array_equal(k_j, k_h)
+
+
+def test_process_exits_cleanly_with_a_compile_in_flight(gpu):
+    """A short process whose AUTO soft pass started a background NVRTC compile
+    exits with status 0 (the compile is joined before teardown: the Python
+    package's atexit -> sgx_jit_quiesce, and the library's own atexit)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for batch in ("4096", "1048576"):
+        r = subprocess.run([sys.executable, os.path.join(root, "tools", "exit_probe.py"), "c3a_or50", batch, "1"],
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, (batch, r.returncode, r.stderr[-2000:])
+        assert "done 1000" in r.stdout
