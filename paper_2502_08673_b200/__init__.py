@@ -10,7 +10,7 @@ from .circuit import (Circuit, Instance, PathClassification, SchemaError, classi
                       export_json, import_json, load_instance)
 from .extract import ExtractionResult, extract_circuit, instance_from_cnf
 from .sampler import (DeviceCircuit, Optimizer, RestartPolicy, SoftKernel, jit_source, RunResult, RunStats, Sampler, SamplerConfig,
-                      SolutionSet, layout_digest, layout_stats, run, run_instance, set_layout_cache_dir,
+                      SolutionSet, jit_quiesce, layout_digest, layout_stats, run, run_instance, set_layout_cache_dir,
                       verify_solutions)
 
 __all__ = [
@@ -18,6 +18,6 @@ __all__ = [
     "Circuit", "Instance", "PathClassification", "SchemaError", "classify_paths", "export_json",
     "import_json", "load_instance", "DeviceCircuit", "RestartPolicy", "RunResult", "RunStats",
     "Sampler", "SamplerConfig", "SolutionSet", "layout_digest", "layout_stats", "run", "run_instance",
-    "set_layout_cache_dir",
+    "set_layout_cache_dir", "jit_quiesce",
     "ExtractionResult", "extract_circuit", "instance_from_cnf", "verify_solutions",
 ]

@@ -1537,12 +1537,17 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
     s->cfg = *cfg;
     // The soft passes (st) outrank the harvest (sh) at the block scheduler:
     // the harvest has a whole iteration of slack (double-buffered input).
-    // Measured with the warp-synchronous harvest: C4 +2-3 %, C2 even.
-    // SGX_PRIO=0: equal priorities.
+    // Measured with the warp-synchronous harvest: C4 +2-3 %, C2 even.  Not
+    // for circuits the specialised soft pass runs (its step fills every SM,
+    // so a lower-priority harvest waits for it: C3a -3 %, C3b -1 %).
+    // SGX_PRIO=0 / 1: equal / prioritised always.
     int prio_lo = 0, prio_hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     const char* pe = std::getenv("SGX_PRIO");
-    const bool prio = !(pe && pe[0] == '0');
+    const char* je = std::getenv("SGX_JIT");
+    const bool jit_circuit = c->layout_ok && !c->L.unsat && cfg->soft_kernel != SGX_SOFT_HBM &&
+                             !(je && je[0] == '0') && sgx::jit_eligible(c->L);
+    const bool prio = pe ? pe[0] == '1' : !jit_circuit;
     {
       StreamKit k = kit_take(c->ctx->device, prio, prio_lo, prio_hi);
       s->kit_prio = prio;

@@ -241,6 +241,12 @@ def layout_stats(cnf, circuit, paths, unsat=False) -> dict:
     return dict(zip(keys, (int(x) for x in out)))
 
 
+def jit_quiesce() -> None:
+    """Wait for background compiles of the circuit-specialised soft pass
+    (sgx_jit_quiesce): afterwards every eligible sampler runs it."""
+    _lib.check(_lib.load().sgx_jit_quiesce())
+
+
 def set_layout_cache_dir(path: str | None) -> None:
     """On-disk layout cache for every later circuit upload (sgx_set_layout_cache_dir):
     <path>/<descriptor hash>.sgxlayout is read if valid, else compiled and written."""
