@@ -1713,8 +1713,8 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
         s->block_count.alloc_async(Bp / sgx::kThreads, st);
         s->K.alloc_async(static_cast<size_t>(L.key_words) * Bp, st);
         // Room for every row the run can harvest (restarts x (iterations + 1)
-        // batches, + 2 for the growth trigger) when that fits 24 GB and a
-        // quarter of the free device memory, else the old floor (16 harvests,
+        // batches, + 2 for the growth trigger) when that fits 48 GB and a
+        // third of the free device memory, else the old floor (16 harvests,
         // at most 4 GB): a growth waits for the host drain, copies the store
         // and allocates from the pool mid-run (C4: up to 1.7 s of fresh
         // mappings on a first run).  A quota caps it.
@@ -1731,7 +1731,13 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
             cudaGetLastError();
             fr = 0;
           }
-          const long long roomy = std::min<long long>((24ll << 30), static_cast<long long>(fr / 4)) / key_bytes;
+          {  // blocks the cache holds are as good as free
+            int dev = 0;
+            cudaGetDevice(&dev);
+            std::lock_guard<std::mutex> lk(blockcache::mu);
+            fr += blockcache::held_bytes[dev];
+          }
+          const long long roomy = std::min<long long>((48ll << 30), static_cast<long long>(fr / 3)) / key_bytes;
           if (bound <= roomy) want_rows = std::max(want_rows, bound);
         }
         if (cfg->max_solutions > 0) want_rows = std::min<long long>(want_rows, cfg->max_solutions + Bp);
