@@ -1264,6 +1264,7 @@ int sgx_close(sgx_ctx* ctx) {
     ctx->exp_tab.reset();
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
+    blockcache::flush();  // the device's cached sampler blocks back to the pool
   });
 }
 
