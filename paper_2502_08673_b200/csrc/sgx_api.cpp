@@ -814,7 +814,7 @@ void harvest_front(sgx_sampler* s, int restart, int iter, long long quota_left) 
 void harvest_back_launch(sgx_sampler* s, int loss_slot) {
   const auto& L = s->c->L;
   sgx::launch_append(s->sh, s->newmask.p, s->block_count.p, s->K.p, L.key_words, s->Bp, s->store.p,
-                     s->n_solutions, s->store_cap, s->hout.p);
+                     s->n_solutions, s->store_cap, s->hout.p, s->hlw > 0);
   s->launches += 1;
   CK(cudaEventRecord(s->ev[6], s->sh));
   CK(cudaGetLastError());
@@ -845,7 +845,7 @@ void harvest_back_finish(sgx_sampler* s, long long quota_left, long long* attemp
     s->host_ms[2] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     CK(cudaMemsetAsync(&s->hout.p->overflow, 0, sizeof(long long), s->sh));
     sgx::launch_append(s->sh, s->newmask.p, s->block_count.p, s->K.p, L.key_words, s->Bp, s->store.p,
-                       s->n_solutions, s->store_cap, s->hout.p);
+                       s->n_solutions, s->store_cap, s->hout.p, s->hlw > 0);
     s->launches += 1;
     CK(cudaMemcpyAsync(s->hpin, s->hout.p, sizeof(sgx::HarvestOut), cudaMemcpyDeviceToHost, s->sh));
     CK(cudaStreamSynchronize(s->sh));

@@ -2174,6 +2174,7 @@ __global__ void __launch_bounds__(256)
 k_keys_spill(const HarvestLiveArgs a) {
   __shared__ unsigned long long hsum[256];
   __shared__ uint32_t vw[8];
+  __shared__ unsigned long long kt[256 * 9];  // the round's 8 key words of the CTA's 256 rows, [row][8 (+1 pad)]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int w0 = blockIdx.x * 8;
   hsum[threadIdx.x] = 0ull;
@@ -2208,26 +2209,47 @@ k_keys_spill(const HarvestLiveArgs a) {
     }
   };
   fetch(warp);
-  for (int q = warp; q < a.key_words; q += 8) {
-    uint4 cx[2][2] = {{nx[0][0], nx[0][1]}, {nx[1][0], nx[1][1]}};
-    const uint32_t cm[2] = {nm[0], nm[1]};
-    fetch(q + 8);
-    uint32_t half[2][8];
+  // Rounds of 8 key words (warp w takes key word q0 + w), then the round's
+  // words of every valid row go out row-major -- K as [row][key_words], 64
+  // contiguous bytes per row per round -- so k_append_rows copies whole rows.
+  const int kwn = a.key_words;
+  for (int q0 = 0; q0 < kwn; q0 += 8) {
+    const int q = q0 + warp;
+    if (q < kwn) {
+      uint4 cx[2][2] = {{nx[0][0], nx[0][1]}, {nx[1][0], nx[1][1]}};
+      const uint32_t cm[2] = {nm[0], nm[1]};
+      fetch(q + 8);
+      uint32_t half[2][8];
 #pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
-      const uint4 A = cx[hf][0], Bv = cx[hf][1];
-      const uint32_t m = cm[hf];
-      const uint32_t x[8] = {A.x ^ m, A.y ^ m, A.z ^ m, A.w ^ m, Bv.x ^ m, Bv.y ^ m, Bv.z ^ m, Bv.w ^ m};
+      for (int hf = 0; hf < 2; ++hf) {
+        const uint4 A = cx[hf][0], Bv = cx[hf][1];
+        const uint32_t m = cm[hf];
+        const uint32_t x[8] = {A.x ^ m, A.y ^ m, A.z ^ m, A.w ^ m, Bv.x ^ m, Bv.y ^ m, Bv.z ^ m, Bv.w ^ m};
 #pragma unroll
-      for (int j = 0; j < 8; ++j) half[hf][j] = transpose32(x[j], lane);
+        for (int j = 0; j < 8; ++j) half[hf][j] = transpose32(x[j], lane);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (!vm[j]) continue;  // block-uniform
+        const uint64_t kw = static_cast<uint64_t>(half[0][j]) | (static_cast<uint64_t>(half[1][j]) << 32);
+        h[j] += key_term(kw, q);
+        kt[(j * 32 + lane) * 9 + warp] = kw;
+      }
     }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (!vm[j]) continue;  // block-uniform
-      const uint64_t kw = static_cast<uint64_t>(half[0][j]) | (static_cast<uint64_t>(half[1][j]) << 32);
-      h[j] += key_term(kw, q);
-      if ((vm[j] >> lane) & 1u) a.K[static_cast<size_t>(q) * a.Bp + (w0 + j) * 32 + lane] = kw;
+    __syncthreads();
+    {  // 4 threads per row, 16 bytes each: a warp stores 8 rows x 64 B
+      const int nq = min(8, kwn - q0);
+      for (int t = threadIdx.x; t < 256 * 4; t += blockDim.x) {
+        const int row = t >> 2, sub = t & 3, jj = row >> 5;
+        if (!((vm[jj] >> (row & 31)) & 1u) || 2 * sub >= nq) continue;
+        uint64_t* dst = a.K + static_cast<size_t>(w0 * 32 + row) * kwn + q0 + 2 * sub;
+        if (2 * sub + 1 < nq)
+          *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(kt[row * 9 + 2 * sub], kt[row * 9 + 2 * sub + 1]);
+        else
+          *dst = kt[row * 9 + 2 * sub];
+      }
     }
+    __syncthreads();
   }
 #pragma unroll
   for (int j = 0; j < 8; ++j)
@@ -2691,10 +2713,46 @@ void launch_commit(cudaStream_t st, const uint32_t* valid, const int* slot_of_ro
   k_scan_blocks<<<1, 1024, 0, st>>>(block_count, nb, quota_left, out);
 }
 
+// k_append for keys staged row-major (k_keys_spill: K as [row][key_words]):
+// warp j of the CTA takes the new rows of word j in row order and copies each
+// whole row -- key_words contiguous u64 -- with coalesced loads and stores.
+// Store position, quota cut, last row and overflow as in k_append.
+__global__ void __launch_bounds__(kThreads)
+k_append_rows(const uint32_t* __restrict__ newmask, const int* __restrict__ block_off, const uint64_t* __restrict__ Kr,
+              int key_words, int Bp, uint64_t* __restrict__ store, long long store_base, long long store_cap,
+              HarvestOut* out) {
+  __shared__ int warp_off[kThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int w = (blockIdx.x * kThreads >> 5) + wid;
+  const uint32_t m = w * 32 < Bp ? __ldg(newmask + w) : 0u;
+  if (lane == 0) warp_off[wid] = __popc(m);
+  __syncthreads();
+  if (!m) return;  // warp-uniform
+  int pos = __ldg(block_off + blockIdx.x);
+  for (int i = 0; i < wid; ++i) pos += warp_off[i];
+  const long long accepted = out->accepted;
+  for (uint32_t left = m; left; left &= left - 1, ++pos) {
+    const int r = w * 32 + __ffs(left) - 1;
+    if (pos >= accepted) return;  // (positions rise with the row)
+    const long long dst = store_base + pos;
+    if (dst >= store_cap) {
+      if (lane == 0) out->overflow = 1;
+      return;
+    }
+    if (pos == accepted - 1 && lane == 0) out->last_row = r;
+    const uint64_t* src = Kr + static_cast<size_t>(r) * key_words;
+    uint64_t* d = store + static_cast<size_t>(dst) * key_words;
+    for (int i = lane; i < key_words; i += 32) d[i] = __ldg(src + i);
+  }
+}
+
 void launch_append(cudaStream_t st, const uint32_t* newmask, const int* block_off, const uint64_t* K,
                    int key_words, int Bp, uint64_t* store, long long base, long long cap,
-                   HarvestOut* out) {
-  k_append<<<Bp / kThreads, kThreads, 0, st>>>(newmask, block_off, K, key_words, Bp, store, base, cap, out);
+                   HarvestOut* out, bool row_major) {
+  if (row_major)
+    k_append_rows<<<Bp / kThreads, kThreads, 0, st>>>(newmask, block_off, K, key_words, Bp, store, base, cap, out);
+  else
+    k_append<<<Bp / kThreads, kThreads, 0, st>>>(newmask, block_off, K, key_words, Bp, store, base, cap, out);
 }
 
 template <int WPC>

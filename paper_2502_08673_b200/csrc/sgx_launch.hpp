@@ -57,7 +57,8 @@ void launch_commit(cudaStream_t st, const uint32_t* valid, const int* slot_of_ro
                    int* block_count, long long quota_left, HarvestOut* out);
 void launch_append(cudaStream_t st, const uint32_t* newmask, const int* block_off, const uint64_t* K,
                    int key_words, int Bp, uint64_t* store, long long base, long long cap,
-                   HarvestOut* out);
+                   HarvestOut* out,
+                   bool row_major = false);
 struct HarvestSmemArgs {
   const uint32_t* hb;  // hardened V columns [word][ncpi]
   int ncpi, nucpi;
