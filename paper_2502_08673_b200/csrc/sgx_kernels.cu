@@ -2174,7 +2174,7 @@ __global__ void __launch_bounds__(256)
 k_keys_spill(const HarvestLiveArgs a) {
   __shared__ unsigned long long hsum[256];
   __shared__ uint32_t vw[8];
-  __shared__ unsigned long long kt[256 * 9];  // the round's 8 key words of the CTA's 256 rows, [row][8 (+1 pad)]
+  __shared__ unsigned long long kt[2][256 * 9];  // a round's 8 key words of the CTA's 256 rows, [row][8 (+1 pad)], double-buffered
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int w0 = blockIdx.x * 8;
   hsum[threadIdx.x] = 0ull;
@@ -2215,6 +2215,7 @@ k_keys_spill(const HarvestLiveArgs a) {
   const int kwn = a.key_words;
   for (int q0 = 0; q0 < kwn; q0 += 8) {
     const int q = q0 + warp;
+    unsigned long long* const kb = kt[(q0 >> 3) & 1];  // written this round, stored after the barrier
     if (q < kwn) {
       uint4 cx[2][2] = {{nx[0][0], nx[0][1]}, {nx[1][0], nx[1][1]}};
       const uint32_t cm[2] = {nm[0], nm[1]};
@@ -2233,7 +2234,7 @@ k_keys_spill(const HarvestLiveArgs a) {
         if (!vm[j]) continue;  // block-uniform
         const uint64_t kw = static_cast<uint64_t>(half[0][j]) | (static_cast<uint64_t>(half[1][j]) << 32);
         h[j] += key_term(kw, q);
-        kt[(j * 32 + lane) * 9 + warp] = kw;
+        kb[(j * 32 + lane) * 9 + warp] = kw;
       }
     }
     __syncthreads();
@@ -2244,12 +2245,13 @@ k_keys_spill(const HarvestLiveArgs a) {
         if (!((vm[jj] >> (row & 31)) & 1u) || 2 * sub >= nq) continue;
         uint64_t* dst = a.K + static_cast<size_t>(w0 * 32 + row) * kwn + q0 + 2 * sub;
         if (2 * sub + 1 < nq)
-          *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(kt[row * 9 + 2 * sub], kt[row * 9 + 2 * sub + 1]);
+          *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(kb[row * 9 + 2 * sub], kb[row * 9 + 2 * sub + 1]);
         else
-          *dst = kt[row * 9 + 2 * sub];
+          *dst = kb[row * 9 + 2 * sub];
       }
     }
-    __syncthreads();
+    // (no second barrier: the next round writes the other buffer, and this
+    // one is rewritten only after the next round's barrier)
   }
 #pragma unroll
   for (int j = 0; j < 8; ++j)
