@@ -2045,123 +2045,114 @@ k_harvest_lw(const HarvestLiveArgs a, const int4* __restrict__ lw, int n_iters) 
   __shared__ __align__(8) uint64_t full[kLwBuf], empty[kLwBuf];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
-  const int n_groups = (a.W + nw - 1) / nw;  // word groups; a CTA walks groups blockIdx.x + k * gridDim.x
-  const int my_groups = blockIdx.x < n_groups ? (n_groups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int w0 = blockIdx.x * nw;
+  const int active = min(nw, a.W - w0);  // warps with a word (the rest return at once)
   const int n_chunks = n_iters / kLwChunk;  // lw_ops is padded to whole chunks
-  const long long n_seq = static_cast<long long>(my_groups) * n_chunks;  // chunks this CTA consumes
   constexpr unsigned kChunkBytes = kLwChunk * 32 * sizeof(int4);
   if (threadIdx.x == 0) {
     for (int b = 0; b < kLwBuf; ++b) {
       mbar_init(&full[b], 1);
-      mbar_init(&empty[b], static_cast<unsigned>(nw));  // every warp releases every chunk
+      mbar_init(&empty[b], static_cast<unsigned>(active));
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  if (warp >= active) return;
   if (threadIdx.x == 0)
-    for (int b = 0; b < kLwBuf && b < n_seq; ++b)
-      bulk_load(lwsm + b * kLwChunk * 32, lw + static_cast<size_t>(b % n_chunks) * kLwChunk * 32, kChunkBytes / 16, &full[b]);
+    for (int b = 0; b < kLwBuf && b < n_chunks; ++b) bulk_load(lwsm + b * kLwChunk * 32, lw + static_cast<size_t>(b) * kLwChunk * 32, kChunkBytes / 16, &full[b]);
+  const int w = w0 + warp;
   uint32_t* bits = reinterpret_cast<uint32_t*>(lwsm + kLwBuf * kLwChunk * 32) + static_cast<size_t>(warp) * (a.slots + 1);
-  long long seq = 0;  // chunks consumed so far (ring position and parity)
-  for (int grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
-    const int w = grp * nw + warp;
-    const bool live = w < a.W;  // a warp past the last word still keeps the ring in step
-    const size_t Wz = static_cast<size_t>(a.W);
-    if (lane == 0) bits[0] = 0u;
-    if (live) {
-      // phase 0 inputs: hardened V (autodiff.cpp:292-297) and free bits (sampler.cpp:132-137)
-      for (int j = lane; j < a.ncpi; j += 32) {
-        const int2 cs = __ldg(a.cpi + j);
-        const uint32_t word = __ldg(a.hb + static_cast<size_t>(w) * a.ncpi + j);
-        bits[cs.x] = word;
-        if (cs.y >= 0) a.spill[cs.y * Wz + w] = word;
-      }
-      const int r = w * 32 + lane;
-      for (int k = 0; k < a.nucpi; ++k) {
-        const bool bit = fold(fold(a.free_prefix, static_cast<uint64_t>(a.row_offset + r)), static_cast<uint64_t>(k)) & 1;
-        const uint32_t word = __ballot_sync(kFull, bit);
-        if (lane == 0) {
-          const int2 cs = __ldg(a.ucpi + k);
-          bits[cs.x] = word;
-          if (cs.y >= 0) a.spill[cs.y * Wz + w] = word;
-        }
-      }
-    }  // live
-    __syncwarp();
-    uint32_t ok = kFull;
-    int ph = 0;
-    for (int c = 0; c < n_chunks; ++c, ++seq) {
-      const int b = static_cast<int>(seq % kLwBuf);
-      const unsigned par = static_cast<unsigned>(seq / kLwBuf) & 1u;
-      mbar_wait(&full[b], par);
-      const int4* R = lwsm + b * kLwChunk * 32 + lane;
-      // output checks and clauses of phase ph (read-only), at its last iteration
-      auto phase_end = [&](const int4 op) {
-        if (op.x & kLwChk) {
-          const int cb = __ldg(a.chk_ptr + ph), ce = __ldg(a.chk_ptr + ph + 1);
-          for (int i = cb + lane; i < ce; i += 32) {
-            const int4 rec = __ldg(a.chk + i);
-            uint32_t any = 0u;
-            if (rec.w == kLbBig) {  // a long clause, literal by literal
-              for (int l = rec.x; l < rec.x + rec.y; ++l) {
-                const int lit = __ldg(a.big_lits + l), sgn = lit >> 31;
-                any |= bits[lit ^ sgn] ^ static_cast<uint32_t>(sgn);
-              }
-            } else {
-              const int lit[4] = {rec.x, rec.y, rec.z, rec.w};
-  #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int sgn = lit[u] >> 31;
-                any |= bits[lit[u] ^ sgn] ^ static_cast<uint32_t>(sgn);
-              }
-            }
-            ok &= any;
-          }
-        }
-        ++ph;
-        __syncwarp();
-      };
-      // Iterations in pairs: when the first of a pair does not end its phase,
-      // both read only slots of earlier phases (and write slots no op of this
-      // phase reads), so the second's operand loads go out before the first's
-      // store -- two independent chains per lane.
-  #pragma unroll 2
-      for (int it = 0; it < kLwChunk && live; it += 2) {
-        const int4 o0 = R[it * 32], o1 = R[(it + 1) * 32];
-        const uint32_t X0 = bits[o0.y], Y0 = bits[o0.z];
-        const bool same = !(o0.x & kLwEnd);  // warp-uniform
-        uint32_t X1 = 0u, Y1 = 0u;
-        if (same) {
-          X1 = bits[o1.y];
-          Y1 = bits[o1.z];
-        }
-        const uint32_t v0 = anf_gate(o0.x, X0, Y0);
-        bits[(o0.x >> 4) & 0xffffff] = v0;
-        if (o0.w >= 0) a.spill[o0.w * Wz + w] = v0;
-        if (!same) {
-          phase_end(o0);
-          X1 = bits[o1.y];
-          Y1 = bits[o1.z];
-        }
-        const uint32_t v1 = anf_gate(o1.x, X1, Y1);
-        bits[(o1.x >> 4) & 0xffffff] = v1;
-        if (o1.w >= 0) a.spill[o1.w * Wz + w] = v1;
-        if (o1.x & kLwEnd) phase_end(o1);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[b]);
-      if (threadIdx.x == 0 && seq + kLwBuf < n_seq) {  // refill once every warp has released the chunk
-        mbar_wait(&empty[b], par);
-        bulk_load(lwsm + b * kLwChunk * 32, lw + static_cast<size_t>((seq + kLwBuf) % n_chunks) * kLwChunk * 32,
-                  kChunkBytes / 16, &full[b]);
-      }
+  const size_t Wz = static_cast<size_t>(a.W);
+  if (lane == 0) bits[0] = 0u;
+  // phase 0 inputs: hardened V (autodiff.cpp:292-297) and free bits (sampler.cpp:132-137)
+  for (int j = lane; j < a.ncpi; j += 32) {
+    const int2 cs = __ldg(a.cpi + j);
+    const uint32_t word = __ldg(a.hb + static_cast<size_t>(w) * a.ncpi + j);
+    bits[cs.x] = word;
+    if (cs.y >= 0) a.spill[cs.y * Wz + w] = word;
+  }
+  const int r = w * 32 + lane;
+  for (int k = 0; k < a.nucpi; ++k) {
+    const bool bit = fold(fold(a.free_prefix, static_cast<uint64_t>(a.row_offset + r)), static_cast<uint64_t>(k)) & 1;
+    const uint32_t word = __ballot_sync(kFull, bit);
+    if (lane == 0) {
+      const int2 cs = __ldg(a.ucpi + k);
+      bits[cs.x] = word;
+      if (cs.y >= 0) a.spill[cs.y * Wz + w] = word;
     }
-    const uint32_t v = __reduce_and_sync(kFull, ok);
-    const int r0 = w * 32;
-    const uint32_t mask = r0 + 32 <= a.batch ? kFull : (r0 >= a.batch ? 0u : ((1u << (a.batch - r0)) - 1u));
-    if (lane == 0 && live) a.valid[w] = v & mask;
-    __syncwarp();  // (bits are reused by this warp's next word)
-  }  // word groups
+  }
+  __syncwarp();
+  uint32_t ok = kFull;
+  int ph = 0;
+  for (int c = 0; c < n_chunks; ++c) {
+    const int b = c % kLwBuf;
+    const unsigned par = static_cast<unsigned>(c / kLwBuf) & 1u;
+    mbar_wait(&full[b], par);
+    const int4* R = lwsm + b * kLwChunk * 32 + lane;
+    // output checks and clauses of phase ph (read-only), at its last iteration
+    auto phase_end = [&](const int4 op) {
+      if (op.x & kLwChk) {
+        const int cb = __ldg(a.chk_ptr + ph), ce = __ldg(a.chk_ptr + ph + 1);
+        for (int i = cb + lane; i < ce; i += 32) {
+          const int4 rec = __ldg(a.chk + i);
+          uint32_t any = 0u;
+          if (rec.w == kLbBig) {  // a long clause, literal by literal
+            for (int l = rec.x; l < rec.x + rec.y; ++l) {
+              const int lit = __ldg(a.big_lits + l), sgn = lit >> 31;
+              any |= bits[lit ^ sgn] ^ static_cast<uint32_t>(sgn);
+            }
+          } else {
+            const int lit[4] = {rec.x, rec.y, rec.z, rec.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int sgn = lit[u] >> 31;
+              any |= bits[lit[u] ^ sgn] ^ static_cast<uint32_t>(sgn);
+            }
+          }
+          ok &= any;
+        }
+      }
+      ++ph;
+      __syncwarp();
+    };
+    // Iterations in pairs: when the first of a pair does not end its phase,
+    // both read only slots of earlier phases (and write slots no op of this
+    // phase reads), so the second's operand loads go out before the first's
+    // store -- two independent chains per lane.
+#pragma unroll 2
+    for (int it = 0; it < kLwChunk; it += 2) {
+      const int4 o0 = R[it * 32], o1 = R[(it + 1) * 32];
+      const uint32_t X0 = bits[o0.y], Y0 = bits[o0.z];
+      const bool same = !(o0.x & kLwEnd);  // warp-uniform
+      uint32_t X1 = 0u, Y1 = 0u;
+      if (same) {
+        X1 = bits[o1.y];
+        Y1 = bits[o1.z];
+      }
+      const uint32_t v0 = anf_gate(o0.x, X0, Y0);
+      bits[(o0.x >> 4) & 0xffffff] = v0;
+      if (o0.w >= 0) a.spill[o0.w * Wz + w] = v0;
+      if (!same) {
+        phase_end(o0);
+        X1 = bits[o1.y];
+        Y1 = bits[o1.z];
+      }
+      const uint32_t v1 = anf_gate(o1.x, X1, Y1);
+      bits[(o1.x >> 4) & 0xffffff] = v1;
+      if (o1.w >= 0) a.spill[o1.w * Wz + w] = v1;
+      if (o1.x & kLwEnd) phase_end(o1);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);
+    if (threadIdx.x == 0 && c + kLwBuf < n_chunks) {  // refill once every warp has released the chunk
+      mbar_wait(&empty[b], par);
+      bulk_load(lwsm + b * kLwChunk * 32, lw + static_cast<size_t>(c + kLwBuf) * kLwChunk * 32, kChunkBytes / 16, &full[b]);
+    }
+  }
+  const uint32_t v = __reduce_and_sync(kFull, ok);
+  const int r0 = w * 32;
+  const uint32_t mask = r0 + 32 <= a.batch ? kFull : (r0 >= a.batch ? 0u : ((1u << (a.batch - r0)) - 1u));
+  if (lane == 0) a.valid[w] = v & mask;
 }
 
 // Keys from the spill tape (dedupe_key, sampler.cpp:18-26): a CTA owns 8
@@ -2280,12 +2271,7 @@ bool launch_harvest_lw(cudaStream_t st, int warps_per_cta, const HarvestLiveArgs
   const size_t smem = static_cast<size_t>(a.slots + 1) * sizeof(uint32_t) * warps_per_cta + kLwRingBytes;
   if (smem > 226 * 1024 || n_iters % kLwChunk) return false;
   opt_in_smem(reinterpret_cast<const void*>(k_harvest_lw), smem);
-  static const int gcap = [] {  // SGX_LW_GRID=n: at most n CTAs, each walking several word groups
-    const char* e = std::getenv("SGX_LW_GRID");
-    return e ? std::max(1, std::atoi(e)) : (1 << 30);
-  }();
-  const int groups = (a.W + warps_per_cta - 1) / warps_per_cta;
-  k_harvest_lw<<<std::min(groups, gcap), 32 * warps_per_cta, smem, st>>>(a, lw, n_iters);
+  k_harvest_lw<<<(a.W + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, smem, st>>>(a, lw, n_iters);
   k_keys_spill<<<(a.W + 7) / 8, 256, 0, st>>>(a);
   return true;
 }

@@ -126,8 +126,6 @@ VARIANTS = [
     # (also where the full tape would win) at one and at two words per CTA
     {"SGX_HARVEST": "live"}, {"SGX_HARVEST": "lw"}, {"SGX_HARVEST": "lw", "SGX_LWW": "1"},
     {"SGX_HARVEST": "lw", "SGX_LWW": "2", "SGX_ALL_CLAUSES": "1"},
-    # the warp-synchronous harvest persistent on a capped grid (CTAs walk several word groups)
-    {"SGX_HARVEST": "lw", "SGX_LW_GRID": "3"}, {"SGX_HARVEST": "lw", "SGX_LWW": "3", "SGX_LW_GRID": "2"},
 ]
 
 
