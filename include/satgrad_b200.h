@@ -58,12 +58,18 @@ enum sgx_gate_kind {
   SGX_AND2, SGX_OR2, SGX_XOR2, SGX_XNOR2
 };
 
-/* RestartPolicy, sampler.hpp:21.  SGX_RESTART_REINIT_ROWS is an extension
- * (no reference counterpart, so no count parity): as
- * REINIT_ON_EXHAUST, plus after every harvest the rows that are valid but not
- * new redraw their logits; steps wait for the harvest (no overlap). */
+/* RestartPolicy, sampler.hpp:21.  SGX_RESTART_REINIT_ROWS and
+ * SGX_RESTART_REINIT_INVALID are extensions (SPEC.md:473
+ * "finer policies are future work"; no reference counterpart, so no count
+ * parity), both on top of REINIT_ON_EXHAUST:
+ *   REINIT_ROWS: after every harvest the rows that are valid but not new
+ *     redraw their logits;
+ *   REINIT_INVALID: as REINIT_ROWS, plus rows that are still invalid after
+ *     `reinit_age` GD steps since their last draw redraw theirs.
+ * Steps wait for the harvest (no harvest/step overlap). */
 enum sgx_restart_policy {
-  SGX_RESTART_NONE = 0, SGX_RESTART_REINIT_ON_EXHAUST = 1, SGX_RESTART_REINIT_ROWS = 2
+  SGX_RESTART_NONE = 0, SGX_RESTART_REINIT_ON_EXHAUST = 1, SGX_RESTART_REINIT_ROWS = 2,
+  SGX_RESTART_REINIT_INVALID = 3
 };
 
 typedef struct sgx_ctx sgx_ctx;
@@ -113,6 +119,8 @@ typedef struct {
   double adam_beta1;       /* SGX_OPT_ADAM only; 0 = 0.9                  */
   double adam_beta2;       /* 0 = 0.999                                   */
   double adam_eps;         /* 0 = 1e-8                                    */
+  int32_t reinit_age;      /* SGX_RESTART_REINIT_INVALID: GD steps an invalid
+                              row keeps its draw; 0 = 2                   */
 } sgx_sampler_cfg;
 
 /* Logit update.  GD is the reference's gd_step (V -= lr dV, autodiff.cpp:

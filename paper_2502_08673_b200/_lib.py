@@ -58,7 +58,7 @@ class SamplerCfg(C.Structure):
         ("restart_policy", C.c_int32), ("row_offset", C.c_int64),
         ("solution_capacity", C.c_int64), ("max_restarts", C.c_int32), ("soft_kernel", C.c_int32),
         ("optimizer", C.c_int32), ("adam_beta1", C.c_double), ("adam_beta2", C.c_double),
-        ("adam_eps", C.c_double),
+        ("adam_eps", C.c_double), ("reinit_age", C.c_int32),
     ]
 
 

@@ -441,6 +441,8 @@ struct sgx_sampler {
   int adam_t = 0;                                // steps since the last init
   DBuf<double> partial;
   DBuf<uint32_t> BT, valid, newmask;
+  DBuf<uint8_t> row_age;    // SGX_RESTART_REINIT_INVALID: GD steps since each row's last draw
+  DBuf<uint32_t> redraw;    // ... and the rows the next reinit redraws
   DBuf<uint32_t> HB;  // hardened V columns [word][ncpi] (shared-memory harvest input)
   DBuf<int> slot_of_row, block_count;
   DBuf<uint64_t> K, store;
@@ -536,6 +538,7 @@ void sampler_init(sgx_sampler* s, int restart) {
   sgx::launch_init_v(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, 32 * s->vec, prefix,
                      s->cfg.row_offset, hb_write(s));
   s->launches += L.cpi.empty() ? 0 : 1;
+  if (s->row_age.p) CK(cudaMemsetAsync(s->row_age.p, 0, s->row_age.n, s->st));
   if (s->cfg.optimizer == SGX_OPT_ADAM) {
     CK(cudaMemsetAsync(s->adam_m.p, 0, s->adam_m.n * sizeof(float), s->st));
     CK(cudaMemsetAsync(s->adam_v.p, 0, s->adam_v.n * sizeof(float), s->st));
@@ -547,6 +550,8 @@ void sampler_init(sgx_sampler* s, int restart) {
 
 // SGX_RESTART_REINIT_ROWS: redraw the logits of the rows the harvest just
 // found valid but not new (the harvest has finished: finish() waited on it).
+// SGX_RESTART_REINIT_INVALID: also the rows still invalid `reinit_age` steps
+// after their last draw (k_reinit_mask keeps the per-row ages).
 void reinit_rows(sgx_sampler* s, int restart, int it) {
   const auto& L = s->c->L;
   if (L.cpi.empty()) return;
@@ -570,10 +575,35 @@ void reinit_rows(sgx_sampler* s, int restart, int it) {
     std::fprintf(stderr, "[sgx] reinit restart %d it %d: valid %lld new %lld flagged %lld (W %d)\n", restart, it, nv,
                  nn, nf, s->W);
   }
-  sgx::launch_reinit_rows(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, 32 * s->vec, prefix,
-                          s->cfg.row_offset, s->valid.p, s->newmask.p);
-  s->launches += 1;
+  if (s->row_age.p) {
+    sgx::launch_reinit_mask(s->st, s->valid.p, s->newmask.p, s->row_age.p, s->W,
+                            s->cfg.reinit_age > 0 ? s->cfg.reinit_age : 2, s->redraw.p);
+    sgx::launch_reinit_rows(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, 32 * s->vec, prefix,
+                            s->cfg.row_offset, s->redraw.p, nullptr);
+    s->launches += 2;
+  } else {
+    sgx::launch_reinit_rows(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, 32 * s->vec, prefix,
+                            s->cfg.row_offset, s->valid.p, s->newmask.p);
+    s->launches += 1;
+  }
   CK(cudaGetLastError());
+}
+
+// How the harvest of iteration i overlaps the step of iteration i + 1
+// (SGX_OVERLAP): 0 = not at all (the step waits for the harvest), 1 = the
+// whole step, 2 = the forward only (the backward waits for the harvest; the
+// default).  Measured on B200 (bench.py, 3 alternations): C4 4.87 M/s (1),
+// 4.91-4.97 (0), 5.01-5.03 (2); C2 5.21-5.27 (1), 5.07 (0), 5.24-5.30 (2).
+// The backward is the pass most hurt by a harvest beside it (C4 163 ms per
+// run with it, 141 without), the forward hides it.
+int overlap_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("SGX_OVERLAP");
+    if (!e) return 2;
+    if (e[0] == 'f') return 2;
+    return e[0] == '0' ? 0 : 1;
+  }();
+  return m;
 }
 
 // One GD step; returns its parity slot (loss total in dloss[slot], timing in sev[slot]).
@@ -630,6 +660,7 @@ int sampler_step(sgx_sampler* s) {
                         s->tape.p, c->cone.n_rows, s->Bp, 0, tab, &c->cone.fb);
     CK(cudaEventRecord(ev[1], s->st));
     if (harvest_reads_v(s)) CK(cudaStreamWaitEvent(s->st, s->ev_front, 0));  // the running harvest reads V
+    if (overlap_mode() == 2) CK(cudaStreamWaitEvent(s->st, s->ev[6], 0));   // ... or all of it
     CK(cudaEventRecord(ev[2], s->st));
     if (s->cfg.optimizer == SGX_OPT_ADAM) {
       // dV out of the backward (its V update and hardening skipped), then Adam
@@ -923,12 +954,10 @@ void sampler_run(sgx_sampler* s) {
     if (iter > 0) s->loss_trace.push_back(s->hpin->loss_total / cfg.batch);
   };
   auto quota_left = [&] { return quota ? cfg.max_solutions - s->n_solutions : -1LL; };
-  static const bool overlap = [] {  // SGX_OVERLAP=0: the next step waits for the harvest (A/B)
-    const char* e = std::getenv("SGX_OVERLAP");
-    return !(e && e[0] == '0');
-  }();
+  const bool overlap = overlap_mode() != 0;  // SGX_OVERLAP=0: the next step waits for the harvest
   const int max_restarts = cfg.max_restarts > 0 ? cfg.max_restarts : 1000;
-  const bool per_row = cfg.restart_policy == SGX_RESTART_REINIT_ROWS;
+  const bool per_row =
+      cfg.restart_policy == SGX_RESTART_REINIT_ROWS || cfg.restart_policy == SGX_RESTART_REINIT_INVALID;
   bool timed_out = false;
   cudaEvent_t e0 = s->rev[0], e1 = s->rev[1], r0 = s->rev[2], r1 = s->rev[3];
   CK(cudaEventRecord(r0, s->st));
@@ -1124,10 +1153,7 @@ void sampler_run_sharded(sgx_sampler* s, const sgx_exchange* ex) {
     const auto all = gather1(now_s() >= cfg.timeout_s ? 1 : 0);
     return std::any_of(all.begin(), all.end(), [](int64_t v) { return v != 0; });
   };
-  const bool overlap = [] {
-    const char* e = std::getenv("SGX_OVERLAP");
-    return !(e && e[0] == '0');
-  }();
+  const bool overlap = overlap_mode() != 0;
   auto harvest = [&](int restart, int it, bool launch_next) {
     const auto h0 = clock::now();
     dist_local(s, restart, it);
@@ -1526,8 +1552,9 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
     need(out, "out");
     if (cfg->batch < 1) throw std::invalid_argument("batch must be positive");  // sampler.cpp:93
     if (cfg->iterations < 0) throw std::invalid_argument("iterations must be non-negative");
-    if (cfg->restart_policy < SGX_RESTART_NONE || cfg->restart_policy > SGX_RESTART_REINIT_ROWS)
+    if (cfg->restart_policy < SGX_RESTART_NONE || cfg->restart_policy > SGX_RESTART_REINIT_INVALID)
       throw std::invalid_argument("unknown restart policy");
+    if (cfg->reinit_age < 0 || cfg->reinit_age > 255) throw std::invalid_argument("reinit_age must be in [0, 255]");
     if (cfg->optimizer != SGX_OPT_GD && cfg->optimizer != SGX_OPT_ADAM) throw std::invalid_argument("unknown optimizer");
     if (cfg->optimizer == SGX_OPT_ADAM &&
         (cfg->adam_beta1 < 0 || cfg->adam_beta1 >= 1 || cfg->adam_beta2 < 0 || cfg->adam_beta2 >= 1 || cfg->adam_eps < 0))
@@ -1710,6 +1737,10 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
         if (s->hlive) s->SP.alloc_async(static_cast<size_t>(std::max(L.lb_n_spill, 1)) * s->W, st);
         s->valid.alloc_async(s->W, st);
         s->newmask.alloc_async(s->W, st);
+        if (cfg->restart_policy == SGX_RESTART_REINIT_INVALID) {
+          s->row_age.alloc_async(Bp, st);
+          s->redraw.alloc_async(s->W, st);
+        }
         s->slot_of_row.alloc_async(Bp, st);
         s->block_count.alloc_async(Bp / sgx::kThreads, st);
         s->K.alloc_async(static_cast<size_t>(L.key_words) * Bp, st);
@@ -2184,8 +2215,8 @@ int sgx_run_sharded(sgx_sampler* s, const sgx_exchange* ex, sgx_run_stats* stats
     need(ex, "exchange");
     if (ex->nranks < 1 || ex->rank < 0 || ex->rank >= ex->nranks) throw std::invalid_argument("bad rank / nranks");
     if (!ex->allgather_device || !ex->allgather_host) throw std::invalid_argument("exchange without collectives");
-    if (s->cfg.restart_policy == SGX_RESTART_REINIT_ROWS)
-      throw std::invalid_argument("SGX_RESTART_REINIT_ROWS is single-device only (sgx_run)");
+    if (s->cfg.restart_policy == SGX_RESTART_REINIT_ROWS || s->cfg.restart_policy == SGX_RESTART_REINIT_INVALID)
+      throw std::invalid_argument("SGX_RESTART_REINIT_ROWS / REINIT_INVALID are single-device only (sgx_run)");
     CK(cudaSetDevice(s->c->ctx->device));
     if (s->c->layout_ok && !s->c->L.unsat) {
       reset_solutions(s);

@@ -73,12 +73,32 @@ k_reinit_rows(float* __restrict__ V, int ncols, int Bp, int tile_rows, uint64_t 
     const int within = static_cast<int>(i - tile * ncols * tile_rows);
     const int c = within / tile_rows;
     const int r = static_cast<int>(tile * tile_rows) + within % tile_rows;
-    const uint32_t stuck = __ldg(valid + (r >> 5)) & ~__ldg(newmask + (r >> 5));
+    const uint32_t stuck =
+        newmask ? __ldg(valid + (r >> 5)) & ~__ldg(newmask + (r >> 5)) : __ldg(valid + (r >> 5));  // or a redraw mask
     if (!((stuck >> (r & 31)) & 1u)) continue;
     const uint64_t h = fold(fold(prefix, static_cast<uint64_t>(row_offset + r)), static_cast<uint64_t>(c));
     const double u = static_cast<double>(h >> 11) * 0x1.0p-53;
     V[i] = __double2float_rn(__dsub_rn(__dmul_rn(2.0, u), 1.0));
   }
+}
+
+// SGX_RESTART_REINIT_INVALID: the rows the next k_reinit_rows redraws --
+// valid but not new, or invalid `min_age` or more GD steps after their last
+// draw -- one thread per row, a warp per 32-row word.  age counts the steps
+// since a row's draw (zeroed by every init); a redrawn row restarts at 0,
+// every other row ages by the step that follows.
+__global__ void __launch_bounds__(kThreads)
+k_reinit_mask(const uint32_t* __restrict__ valid, const uint32_t* __restrict__ newmask, uint8_t* __restrict__ age,
+              int W, int min_age, uint32_t* __restrict__ redraw) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;  // W * 32 threads exactly (kThreads divides 32)
+  if (r >= W * 32) return;
+  const int w = r >> 5, b = r & 31;
+  const uint32_t v = (__ldg(valid + w) >> b) & 1u, n = (__ldg(newmask + w) >> b) & 1u;
+  const int a = age[r];
+  const bool go = (v && !n) || (!v && a >= min_age);
+  age[r] = go ? 0 : static_cast<uint8_t>(a < 255 ? a + 1 : 255);
+  const uint32_t m = __ballot_sync(kFull, go);
+  if (b == 0) redraw[w] = m;
 }
 
 // Vector access of V consecutive samples of one tape row.
@@ -2510,6 +2530,11 @@ void launch_reinit_rows(cudaStream_t st, float* V, int ncols, int Bp, int tile_r
   if (ncols == 0) return;
   k_reinit_rows<<<grid_for(static_cast<long long>(ncols) * Bp, kThreads, 148 * 64), kThreads, 0, st>>>(
       V, ncols, Bp, tile_rows, prefix, row_offset, valid, newmask);
+}
+
+void launch_reinit_mask(cudaStream_t st, const uint32_t* valid, const uint32_t* newmask, uint8_t* age, int W,
+                        int min_age, uint32_t* redraw) {
+  k_reinit_mask<<<(W * 32 + kThreads - 1) / kThreads, kThreads, 0, st>>>(valid, newmask, age, W, min_age, redraw);
 }
 
 // Forward variant (measured on B200, c2_iscas @ 64k rows): the

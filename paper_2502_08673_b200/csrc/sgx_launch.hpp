@@ -12,6 +12,8 @@ struct HarvestOut;
 
 void launch_reinit_rows(cudaStream_t st, float* V, int ncols, int Bp, int tile_rows, uint64_t prefix,
                         long long row_offset, const uint32_t* valid, const uint32_t* newmask);
+void launch_reinit_mask(cudaStream_t st, const uint32_t* valid, const uint32_t* newmask, uint8_t* age, int W,
+                        int min_age, uint32_t* redraw);
 void launch_init_v(cudaStream_t st, float* V, int ncols, int Bp, int tile_rows, uint64_t prefix,
                    long long row_offset, uint32_t* hb);
 // The TMA-fed forward's control stream (sgx_layout.hpp SoftProgram::fblk).

@@ -145,8 +145,8 @@ class ShardStats:
 
 def run_sharded(shard, ex, cfg, rank: int, world: int, stride: int) -> ShardStats:
     """run_impl (sampler.cpp:89-194) over the union of `world` shards."""
-    if int(cfg.restart) == 2:
-        raise ValueError("RestartPolicy.REINIT_ROWS is single-device only (sgx_run)")
+    if int(cfg.restart) in (2, 3):
+        raise ValueError("RestartPolicy.REINIT_ROWS / REINIT_INVALID are single-device only (sgx_run)")
     st = ShardStats()
     t0 = time.perf_counter()
     quota = cfg.max_solutions > 0

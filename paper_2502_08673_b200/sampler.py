@@ -42,6 +42,9 @@ class RestartPolicy(enum.IntEnum):
     # extension (no reference counterpart): REINIT_ON_EXHAUST plus, after every
     # harvest, valid-but-duplicate rows redraw their logits (SGX_RESTART_REINIT_ROWS)
     REINIT_ROWS = 2
+    # extension: REINIT_ROWS plus rows still invalid `reinit_age` GD steps after
+    # their last draw redraw theirs (SGX_RESTART_REINIT_INVALID)
+    REINIT_INVALID = 3
 
 
 @dataclass
@@ -63,6 +66,7 @@ class SamplerConfig:
     adam_beta1: float = 0.9
     adam_beta2: float = 0.999
     adam_eps: float = 1e-8
+    reinit_age: int = 2       # RestartPolicy.REINIT_INVALID only
 
 
 @dataclass
@@ -318,6 +322,7 @@ class Sampler:
         c.soft_kernel = int(cfg.soft_kernel)
         c.optimizer = int(cfg.optimizer)
         c.adam_beta1, c.adam_beta2, c.adam_eps = cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps
+        c.reinit_age = cfg.reinit_age
         self._cfg = c
         h = C.c_void_p()
         _lib.check(self.L.sgx_sampler_create(dc.h, C.byref(c), C.byref(h)))

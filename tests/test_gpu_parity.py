@@ -358,27 +358,29 @@ def test_device_format_matches_reference(gpu, name, batch, iters):
         dc.close()
 
 
+@pytest.mark.parametrize("policy", ["REINIT_ROWS", "REINIT_INVALID"])
 @pytest.mark.parametrize("name,batch", [("c2_iscas", 8192), ("c3a_or50", 1 << 16), ("mux_chain14", 4096)])
-def test_reinit_rows_policy(gpu, name, batch):
-    """RestartPolicy.REINIT_ROWS (no reference counterpart):
-    every stored solution satisfies the CNF and is distinct, runs are
-    deterministic, the first harvest equals the whole-batch policy's (re-init
-    starts after it), and redrawing converged duplicate rows does not lose
+def test_reinit_rows_policy(gpu, name, batch, policy):
+    """RestartPolicy.REINIT_ROWS / REINIT_INVALID (SURVEY 8(f) row 3, SPEC.md:473;
+    no reference counterpart): every stored solution satisfies the CNF and is
+    distinct, runs are deterministic, the first harvest equals the whole-batch
+    policy's (re-init starts after it), and redrawing rows does not lose
     solutions against REINIT_ON_EXHAUST at the same step count."""
     from paper_2502_08673_b200 import verify_keys
     i = inst(name)
+    pol = RestartPolicy[policy]
     base = dict(batch=batch, iterations=5, seed=5, max_restarts=3)
     dc = DeviceCircuit.from_instance(i)
     try:
         runs = {}
-        for pol in (RestartPolicy.REINIT_ROWS, RestartPolicy.REINIT_ROWS, RestartPolicy.REINIT_ON_EXHAUST):
-            s = Sampler(dc, SamplerConfig(restart=pol, **base))
+        for p in (pol, pol, RestartPolicy.REINIT_ON_EXHAUST):
+            s = Sampler(dc, SamplerConfig(restart=p, **base))
             try:
                 st = s.run()
-                runs.setdefault(pol, []).append((st, s.fetch(), list(st.new_unique)))
+                runs.setdefault(p, []).append((st, s.fetch(), list(st.new_unique)))
             finally:
                 s.close()
-        (a, ka, ta), (b, kb, tb) = runs[RestartPolicy.REINIT_ROWS]
+        (a, ka, ta), (b, kb, tb) = runs[pol]
         (w, kw, tw), = runs[RestartPolicy.REINIT_ON_EXHAUST]
         assert a.unique_count == b.unique_count and np.array_equal(ka, kb) and ta == tb
         assert len(ka) == a.unique_count > 0
@@ -386,7 +388,32 @@ def test_reinit_rows_policy(gpu, name, batch):
         assert verify_keys(i.cnf, ka).all()
         assert ta[0] == tw[0]
         assert a.unique_count >= 0.95 * w.unique_count, (a.unique_count, w.unique_count)
-        print(f"{name}: rows {a.unique_count} vs whole-batch {w.unique_count} "
+        print(f"{name} {policy}: rows {a.unique_count} vs whole-batch {w.unique_count} "
               f"({a.unique_count / max(1, w.unique_count):.3f}x)")
+    finally:
+        dc.close()
+
+
+@pytest.mark.parametrize("age", [1, 3])
+def test_reinit_invalid_age_redraws_only_old_invalid_rows(gpu, age):
+    """REINIT_INVALID's redraw rule, checked from the outside: with iterations
+    < reinit_age no invalid row is ever old enough, so the run equals
+    REINIT_ROWS key for key; with a smaller age it differs from it."""
+    i = inst("c2_iscas")
+    dc = DeviceCircuit.from_instance(i)
+    try:
+        out = {}
+        for p in (RestartPolicy.REINIT_ROWS, RestartPolicy.REINIT_INVALID):
+            s = Sampler(dc, SamplerConfig(batch=8192, iterations=2, seed=3, max_restarts=1, restart=p,
+                                          reinit_age=age))
+            try:
+                s.run()
+                out[p] = s.fetch()
+            finally:
+                s.close()
+        same = np.array_equal(out[RestartPolicy.REINIT_ROWS], out[RestartPolicy.REINIT_INVALID])
+        # iterations = 2: harvests after 0, 1, 2 steps; redraws are applied
+        # before steps 1 and 2, when invalid rows are 0 and 1 steps old.
+        assert same == (age > 1), age
     finally:
         dc.close()
