@@ -66,7 +66,9 @@ enum sgx_gate_kind {
  *     redraw their logits;
  *   REINIT_INVALID: as REINIT_ROWS, plus rows that are still invalid after
  *     `reinit_age` GD steps since their last draw redraw theirs.
- * Steps wait for the harvest (no harvest/step overlap). */
+ * The redraw decided at harvest h is applied before step h + 2, so steps keep
+ * overlapping harvests; with a quota (or SGX_OVERLAP=0) it is applied before
+ * step h + 1, which then waits for harvest h. */
 enum sgx_restart_policy {
   SGX_RESTART_NONE = 0, SGX_RESTART_REINIT_ON_EXHAUST = 1, SGX_RESTART_REINIT_ROWS = 2,
   SGX_RESTART_REINIT_INVALID = 3

@@ -441,8 +441,8 @@ struct sgx_sampler {
   int adam_t = 0;                                // steps since the last init
   DBuf<double> partial;
   DBuf<uint32_t> BT, valid, newmask;
-  DBuf<uint8_t> row_age;    // SGX_RESTART_REINIT_INVALID: GD steps since each row's last draw
-  DBuf<uint32_t> redraw;    // ... and the rows the next reinit redraws
+  DBuf<uint8_t> row_age;    // per-row restarts: GD steps since each row's last draw
+  DBuf<uint32_t> redraw;    // ... and the rows to redraw, [harvest parity][W]
   DBuf<uint32_t> HB;  // hardened V columns [word][ncpi] (shared-memory harvest input)
   DBuf<int> slot_of_row, block_count;
   DBuf<uint64_t> K, store;
@@ -548,45 +548,60 @@ void sampler_init(sgx_sampler* s, int restart) {
   CK(cudaGetLastError());
 }
 
-// SGX_RESTART_REINIT_ROWS: redraw the logits of the rows the harvest just
-// found valid but not new (the harvest has finished: finish() waited on it).
-// SGX_RESTART_REINIT_INVALID: also the rows still invalid `reinit_age` steps
-// after their last draw (k_reinit_mask keeps the per-row ages).
-void reinit_rows(sgx_sampler* s, int restart, int it) {
+// Per-row restarts.  SGX_RESTART_REINIT_ROWS redraws the logits of the rows a
+// harvest found valid but not new; SGX_RESTART_REINIT_INVALID also those
+// still invalid `reinit_age` steps after their last draw.  k_reinit_mask turns
+// a harvest's valid / new masks (and the per-row ages) into a redraw mask,
+// k_reinit_rows applies it.  Two schedules:
+//  * at once (with a quota, or SGX_OVERLAP=0): the mask of harvest it - 1 is
+//    applied before step it, which then waits for that harvest;
+//  * lagged (default): the mask of harvest h is built on the harvest stream
+//    right after it and applied before step h + 2, so step h + 1 still
+//    overlaps harvest h.  A flagged row takes one more step (and harvest) on
+//    its old draw; its age restarts at the flag, so it counts the new draw's
+//    steps from the harvest after it.
+int reinit_min_age(const sgx_sampler* s) {
+  if (s->cfg.restart_policy != SGX_RESTART_REINIT_INVALID) return 1 << 30;  // duplicates only
+  return s->cfg.reinit_age > 0 ? s->cfg.reinit_age : 2;
+}
+
+void reinit_mask(sgx_sampler* s, cudaStream_t stream, int h) {
+  if (s->c->L.cpi.empty()) return;
+  sgx::launch_reinit_mask(stream, s->valid.p, s->newmask.p, s->row_age.p, s->W, reinit_min_age(s),
+                          s->redraw.p + static_cast<size_t>(h & 1) * s->W);
+  s->launches += 1;
+  CK(cudaGetLastError());
+}
+
+void reinit_apply(sgx_sampler* s, int restart, int it, int h) {
   const auto& L = s->c->L;
   if (L.cpi.empty()) return;
   const uint64_t prefix =
       sgx::fold(sgx::fold(sgx::fold(sgx::fold(sgx::kPi, s->cfg.seed), sgx::kInitTag),
                           static_cast<uint64_t>(static_cast<int64_t>(restart))),
                 0x726f7773ull + static_cast<uint64_t>(it));  // "rows" + iteration
+  const uint32_t* mask = s->redraw.p + static_cast<size_t>(h & 1) * s->W;
+  if (std::getenv("SGX_REINIT_DEBUG")) {
+    std::vector<uint32_t> m(s->W);
+    CK(cudaStreamSynchronize(s->st));
+    CK(cudaMemcpy(m.data(), mask, s->W * 4, cudaMemcpyDeviceToHost));
+    long long nf = 0;
+    for (int w = 0; w < s->W; ++w) nf += __builtin_popcount(m[w]);
+    std::fprintf(stderr, "[sgx] reinit restart %d before step %d (harvest %d): %lld rows redrawn (W %d)\n", restart,
+                 it, h, nf, s->W);
+  }
+  sgx::launch_reinit_rows(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, 32 * s->vec, prefix,
+                          s->cfg.row_offset, mask, nullptr);
+  s->launches += 1;
+  CK(cudaGetLastError());
+}
+
+// At once: the harvest before step `it` has finished (finish() waited on it).
+void reinit_rows(sgx_sampler* s, int restart, int it) {
   CK(cudaEventRecord(s->ev_join, s->sh));  // valid / newmask of that harvest
   CK(cudaStreamWaitEvent(s->st, s->ev_join, 0));
-  if (std::getenv("SGX_REINIT_DEBUG")) {
-    std::vector<uint32_t> v(s->W), m(s->W);
-    CK(cudaStreamSynchronize(s->st));
-    CK(cudaMemcpy(v.data(), s->valid.p, s->W * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(m.data(), s->newmask.p, s->W * 4, cudaMemcpyDeviceToHost));
-    long long nv = 0, nn = 0, nf = 0;
-    for (int w = 0; w < s->W; ++w) {
-      nv += __builtin_popcount(v[w]);
-      nn += __builtin_popcount(m[w]);
-      nf += __builtin_popcount(v[w] & ~m[w]);
-    }
-    std::fprintf(stderr, "[sgx] reinit restart %d it %d: valid %lld new %lld flagged %lld (W %d)\n", restart, it, nv,
-                 nn, nf, s->W);
-  }
-  if (s->row_age.p) {
-    sgx::launch_reinit_mask(s->st, s->valid.p, s->newmask.p, s->row_age.p, s->W,
-                            s->cfg.reinit_age > 0 ? s->cfg.reinit_age : 2, s->redraw.p);
-    sgx::launch_reinit_rows(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, 32 * s->vec, prefix,
-                            s->cfg.row_offset, s->redraw.p, nullptr);
-    s->launches += 2;
-  } else {
-    sgx::launch_reinit_rows(s->st, s->V.p, static_cast<int>(L.cpi.size()), s->Bp, 32 * s->vec, prefix,
-                            s->cfg.row_offset, s->valid.p, s->newmask.p);
-    s->launches += 1;
-  }
-  CK(cudaGetLastError());
+  reinit_mask(s, s->st, it - 1);
+  reinit_apply(s, restart, it, it - 1);
 }
 
 // How the harvest of iteration i overlaps the step of iteration i + 1
@@ -958,6 +973,12 @@ void sampler_run(sgx_sampler* s) {
   const int max_restarts = cfg.max_restarts > 0 ? cfg.max_restarts : 1000;
   const bool per_row =
       cfg.restart_policy == SGX_RESTART_REINIT_ROWS || cfg.restart_policy == SGX_RESTART_REINIT_INVALID;
+  const bool lag = per_row && overlap && !quota;  // per-row redraws one harvest late (reinit_rows above)
+  auto lag_apply = [&](int restart, int it) {     // mask of harvest it - 2 (finished: finish() synced it)
+    if (it < 2) return;
+    if (harvest_reads_v(s)) CK(cudaStreamWaitEvent(s->st, s->ev_front, 0));  // harvest it - 1 reads V
+    reinit_apply(s, restart, it, it - 2);
+  };
   bool timed_out = false;
   cudaEvent_t e0 = s->rev[0], e1 = s->rev[1], r0 = s->rev[2], r1 = s->rev[3];
   CK(cudaEventRecord(r0, s->st));
@@ -982,12 +1003,16 @@ void sampler_run(sgx_sampler* s) {
     };
     harvest_front(s, restart, 0, h_quota);
     harvest_back_launch(s, -1);
+    if (lag) reinit_mask(s, s->sh, 0);
     hlap(3);
     int h_iter = 0, h_slot = -1;
     for (;;) {
       const int it = h_iter + 1;
       int slot = -1;
-      if (overlap && !per_row && !quota && it <= cfg.iterations && !out_of_time()) slot = sampler_step(s);
+      if (overlap && (!per_row || lag) && !quota && it <= cfg.iterations && !out_of_time()) {
+        if (lag) lag_apply(restart, it);
+        slot = sampler_step(s);
+      }
       hlap(4);
       finish(h_iter, h_quota, h_slot);
       if (h_iter == 0) s->phase_ms[0] += elapsed(e0, e1);
@@ -997,12 +1022,16 @@ void sampler_run(sgx_sampler* s) {
         timed_out = true;
         break;
       }
-      if (per_row && slot < 0) reinit_rows(s, restart, it);
-      if (slot < 0) slot = sampler_step(s);
+      if (per_row && !lag && slot < 0) reinit_rows(s, restart, it);
+      if (slot < 0) {
+        if (lag) lag_apply(restart, it);
+        slot = sampler_step(s);
+      }
       h_quota = quota_left();
       hlap(4);
       harvest_front(s, restart, it, h_quota);
       harvest_back_launch(s, slot);
+      if (lag) reinit_mask(s, s->sh, it);
       hlap(3);
       h_iter = it;
       h_slot = slot;
@@ -1737,9 +1766,9 @@ int sgx_sampler_create(sgx_circuit* c, const sgx_sampler_cfg* cfg, sgx_sampler**
         if (s->hlive) s->SP.alloc_async(static_cast<size_t>(std::max(L.lb_n_spill, 1)) * s->W, st);
         s->valid.alloc_async(s->W, st);
         s->newmask.alloc_async(s->W, st);
-        if (cfg->restart_policy == SGX_RESTART_REINIT_INVALID) {
+        if (cfg->restart_policy == SGX_RESTART_REINIT_ROWS || cfg->restart_policy == SGX_RESTART_REINIT_INVALID) {
           s->row_age.alloc_async(Bp, st);
-          s->redraw.alloc_async(s->W, st);
+          s->redraw.alloc_async(2 * static_cast<size_t>(s->W), st);  // one per harvest parity (lagged schedule)
         }
         s->slot_of_row.alloc_async(Bp, st);
         s->block_count.alloc_async(Bp / sgx::kThreads, st);

@@ -388,23 +388,35 @@ def test_reinit_rows_policy(gpu, name, batch, policy):
         assert verify_keys(i.cnf, ka).all()
         assert ta[0] == tw[0]
         assert a.unique_count >= 0.95 * w.unique_count, (a.unique_count, w.unique_count)
-        print(f"{name} {policy}: rows {a.unique_count} vs whole-batch {w.unique_count} "
-              f"({a.unique_count / max(1, w.unique_count):.3f}x)")
+        # a quota (never met) switches to the at-once schedule (redraw before
+        # the next step, no harvest/step overlap): same properties
+        s = Sampler(dc, SamplerConfig(restart=pol, max_solutions=1 << 40, **base))
+        try:
+            q = s.run()
+            kq = s.fetch()
+        finally:
+            s.close()
+        assert len(kq) == q.unique_count > 0 and len(np.unique(kq, axis=0)) == len(kq)
+        assert verify_keys(i.cnf, kq).all()
+        assert list(q.new_unique)[0] == tw[0]
+        print(f"{name} {policy}: rows {a.unique_count} (at once {q.unique_count}) vs whole-batch "
+              f"{w.unique_count} ({a.unique_count / max(1, w.unique_count):.3f}x)")
     finally:
         dc.close()
 
 
 @pytest.mark.parametrize("age", [1, 3])
 def test_reinit_invalid_age_redraws_only_old_invalid_rows(gpu, age):
-    """REINIT_INVALID's redraw rule, checked from the outside: with iterations
-    < reinit_age no invalid row is ever old enough, so the run equals
-    REINIT_ROWS key for key; with a smaller age it differs from it."""
+    """REINIT_INVALID's redraw rule, checked from the outside: with 3
+    iterations an invalid row is at most 2 steps old when a redraw is decided
+    (harvest 1 in the lagged schedule, harvests 1 and 2 at once), so at
+    reinit_age 3 the run equals REINIT_ROWS key for key, at age 1 it differs."""
     i = inst("c2_iscas")
     dc = DeviceCircuit.from_instance(i)
     try:
         out = {}
         for p in (RestartPolicy.REINIT_ROWS, RestartPolicy.REINIT_INVALID):
-            s = Sampler(dc, SamplerConfig(batch=8192, iterations=2, seed=3, max_restarts=1, restart=p,
+            s = Sampler(dc, SamplerConfig(batch=8192, iterations=3, seed=3, max_restarts=1, restart=p,
                                           reinit_age=age))
             try:
                 s.run()
@@ -412,8 +424,6 @@ def test_reinit_invalid_age_redraws_only_old_invalid_rows(gpu, age):
             finally:
                 s.close()
         same = np.array_equal(out[RestartPolicy.REINIT_ROWS], out[RestartPolicy.REINIT_INVALID])
-        # iterations = 2: harvests after 0, 1, 2 steps; redraws are applied
-        # before steps 1 and 2, when invalid rows are 0 and 1 steps old.
-        assert same == (age > 1), age
+        assert same == (age > 2), age
     finally:
         dc.close()
