@@ -66,9 +66,9 @@ enum sgx_gate_kind {
  *     redraw their logits;
  *   REINIT_INVALID: as REINIT_ROWS, plus rows that are still invalid after
  *     `reinit_age` GD steps since their last draw redraw theirs.
- * The redraw decided at harvest h is applied before step h + 2, so steps keep
- * overlapping harvests; with a quota (or SGX_OVERLAP=0) it is applied before
- * step h + 1, which then waits for harvest h. */
+ * The redraw decided at harvest h is applied before step h + 1, which then
+ * waits for harvest h (SGX_REINIT_LAG=1: before step h + 2, keeping the
+ * harvest/step overlap; slower to find solutions, measured in DESIGN.md). */
 enum sgx_restart_policy {
   SGX_RESTART_NONE = 0, SGX_RESTART_REINIT_ON_EXHAUST = 1, SGX_RESTART_REINIT_ROWS = 2,
   SGX_RESTART_REINIT_INVALID = 3

@@ -553,9 +553,9 @@ void sampler_init(sgx_sampler* s, int restart) {
 // still invalid `reinit_age` steps after their last draw.  k_reinit_mask turns
 // a harvest's valid / new masks (and the per-row ages) into a redraw mask,
 // k_reinit_rows applies it.  Two schedules:
-//  * at once (with a quota, or SGX_OVERLAP=0): the mask of harvest it - 1 is
-//    applied before step it, which then waits for that harvest;
-//  * lagged (default): the mask of harvest h is built on the harvest stream
+//  * at once (default): the mask of harvest it - 1 is applied before step
+//    it, which then waits for that harvest;
+//  * lagged (SGX_REINIT_LAG=1, no quota): the mask of harvest h is built on the harvest stream
 //    right after it and applied before step h + 2, so step h + 1 still
 //    overlaps harvest h.  A flagged row takes one more step (and harvest) on
 //    its old draw; its age restarts at the flag, so it counts the new draw's
@@ -610,7 +610,9 @@ void reinit_rows(sgx_sampler* s, int restart, int it) {
 // default).  Measured on B200 (bench.py, 3 alternations): C4 4.87 M/s (1),
 // 4.91-4.97 (0), 5.01-5.03 (2); C2 5.21-5.27 (1), 5.07 (0), 5.24-5.30 (2).
 // The backward is the pass most hurt by a harvest beside it (C4 163 ms per
-// run with it, 141 without), the forward hides it.
+// run with it, 141 without), the forward hides it.  Letting only the harvest's
+// commit / append run beside the backward (waiting on ev_front instead) was
+// even on C4 (4.99-5.01 vs 4.96-4.98 M/s) with a slower backward; not kept.
 int overlap_mode() {
   static const int m = [] {
     const char* e = std::getenv("SGX_OVERLAP");
@@ -973,7 +975,12 @@ void sampler_run(sgx_sampler* s) {
   const int max_restarts = cfg.max_restarts > 0 ? cfg.max_restarts : 1000;
   const bool per_row =
       cfg.restart_policy == SGX_RESTART_REINIT_ROWS || cfg.restart_policy == SGX_RESTART_REINIT_INVALID;
-  const bool lag = per_row && overlap && !quota;  // per-row redraws one harvest late (reinit_rows above)
+  // SGX_REINIT_LAG=1: per-row redraws one harvest late, keeping the overlap
+  // (reinit_rows above).  Opt-in: a row flagged at harvest h may turn valid
+  // at h + 1 and is redrawn anyway (C4 age 1: 1.13x against 1.20x at once;
+  // C2 loses solutions, tools/reinit_invalid_ab.py).
+  const char* lag_env = std::getenv("SGX_REINIT_LAG");
+  const bool lag = per_row && overlap && !quota && lag_env && lag_env[0] == '1';
   auto lag_apply = [&](int restart, int it) {     // mask of harvest it - 2 (finished: finish() synced it)
     if (it < 2) return;
     if (harvest_reads_v(s)) CK(cudaStreamWaitEvent(s->st, s->ev_front, 0));  // harvest it - 1 reads V

@@ -360,7 +360,7 @@ def test_device_format_matches_reference(gpu, name, batch, iters):
 
 @pytest.mark.parametrize("policy", ["REINIT_ROWS", "REINIT_INVALID"])
 @pytest.mark.parametrize("name,batch", [("c2_iscas", 8192), ("c3a_or50", 1 << 16), ("mux_chain14", 4096)])
-def test_reinit_rows_policy(gpu, name, batch, policy):
+def test_reinit_rows_policy(gpu, name, batch, policy, monkeypatch):
     """RestartPolicy.REINIT_ROWS / REINIT_INVALID (SURVEY 8(f) row 3, SPEC.md:473;
     no reference counterpart): every stored solution satisfies the CNF and is
     distinct, runs are deterministic, the first harvest equals the whole-batch
@@ -388,18 +388,21 @@ def test_reinit_rows_policy(gpu, name, batch, policy):
         assert verify_keys(i.cnf, ka).all()
         assert ta[0] == tw[0]
         assert a.unique_count >= 0.95 * w.unique_count, (a.unique_count, w.unique_count)
-        # a quota (never met) switches to the at-once schedule (redraw before
-        # the next step, no harvest/step overlap): same properties
-        s = Sampler(dc, SamplerConfig(restart=pol, max_solutions=1 << 40, **base))
+        # the lagged schedule (SGX_REINIT_LAG=1: redraw decided at harvest h
+        # applied before step h + 2, keeping the overlap): same properties
+        # except the solution count
+        monkeypatch.setenv("SGX_REINIT_LAG", "1")
+        s = Sampler(dc, SamplerConfig(restart=pol, **base))
         try:
             q = s.run()
             kq = s.fetch()
         finally:
             s.close()
+            monkeypatch.delenv("SGX_REINIT_LAG")
         assert len(kq) == q.unique_count > 0 and len(np.unique(kq, axis=0)) == len(kq)
         assert verify_keys(i.cnf, kq).all()
         assert list(q.new_unique)[0] == tw[0]
-        print(f"{name} {policy}: rows {a.unique_count} (at once {q.unique_count}) vs whole-batch "
+        print(f"{name} {policy}: rows {a.unique_count} (lagged {q.unique_count}) vs whole-batch "
               f"{w.unique_count} ({a.unique_count / max(1, w.unique_count):.3f}x)")
     finally:
         dc.close()
@@ -409,7 +412,7 @@ def test_reinit_rows_policy(gpu, name, batch, policy):
 def test_reinit_invalid_age_redraws_only_old_invalid_rows(gpu, age):
     """REINIT_INVALID's redraw rule, checked from the outside: with 3
     iterations an invalid row is at most 2 steps old when a redraw is decided
-    (harvest 1 in the lagged schedule, harvests 1 and 2 at once), so at
+    (at harvests 1 and 2), so at
     reinit_age 3 the run equals REINIT_ROWS key for key, at age 1 it differs."""
     i = inst("c2_iscas")
     dc = DeviceCircuit.from_instance(i)
