@@ -17,6 +17,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <condition_variable>
 #include <cstdint>
 #include <deque>
@@ -63,6 +64,7 @@ class HostDrain {
   std::condition_variable cv_, idle_cv_;
   std::deque<Job> q_;
   bool stop_ = false, busy_ = false;
+  std::atomic<bool> hurry_{false};  // someone waits for the drain: copy what is left in one go
   std::string err_;
   // worker-owned while busy
   char* buf_ = nullptr;

@@ -22,7 +22,7 @@ dst_d = torch.empty(n, dtype=torch.uint8, device="cuda:0")
 side = torch.cuda.Stream()
 
 
-def run(mode):
+def run(mode, chunk=n, gap=0.010):
     stop = threading.Event()
     count = [0]
 
@@ -31,10 +31,10 @@ def run(mode):
             while not stop.is_set():
                 if mode == "h2d_none":
                     break
-                (dst_h if mode == "d2h" else dst_d).copy_(src, non_blocking=True)
+                (dst_h if mode == "d2h" else dst_d)[:chunk].copy_(src[:chunk], non_blocking=True)
                 side.synchronize()
-                count[0] += 1
-                time.sleep(0.010)
+                count[0] += chunk / n
+                time.sleep(gap)
 
     th = threading.Thread(target=loop)
     s = Sampler(dc, cfg)
@@ -47,6 +47,8 @@ def run(mode):
 
 
 for rep in range(2):
-    for mode in ("h2d_none", "d2h", "d2d"):
-        ms, c = run(mode)
-        print(f"{mode:9s} device {ms:7.1f} ms  side copies {c}", flush=True)
+    for mode, chunk, gap in (("h2d_none", n, 0.01), ("d2h", n, 0.01), ("d2d", n, 0.01), ("d2h", 32 << 20, 0.0015),
+                             ("d2h", 4 << 20, 0.0002)):
+        ms, c = run(mode, chunk, gap)
+        print(f"{mode:9s} chunk {chunk >> 20:4d} MB gap {gap * 1e3:4.1f} ms: device {ms:7.1f} ms  "
+              f"side copies {c:.1f} x 220 MB", flush=True)
