@@ -343,13 +343,29 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
   // outputs are consecutive rows.
   // Last forward level reading each (materialized) node: operand loads at that
   // level are the row's last forward use and go to L2 as evict_first.
-  std::vector<int32_t> last_fwd(n, -1);
+  // A read also leaves first when the row's NEXT forward read is more than
+  // SGX_FWD_FAR levels later (default 48): the row would not survive in L2
+  // that long at 512 tiles in flight, and keeping it displaces rows that would
+  // (row-granular model, C4: forward DRAM reads 5.77 -> 4.98 GB).
+  // read_lv[row]: the levels reading it, ascending (each op at most once).
+  static const int far = [] {
+    const char* e = getenv("SGX_FWD_FAR");
+    const int v = e ? atoi(e) : 48;
+    return v > 0 ? v : (1 << 30);
+  }();
+  std::vector<std::vector<int32_t>> read_lv(n);
   for (int i = 0; i < n; ++i) {
     if (!in_set[i] || virt[i]) continue;
     const int oc = operand_count(L.kind[i]);
-    if (oc >= 1) last_fwd[base_of(L.a[i])] = std::max(last_fwd[base_of(L.a[i])], lev[i]);
-    if (oc == 2) last_fwd[base_of(L.b[i])] = std::max(last_fwd[base_of(L.b[i])], lev[i]);
+    if (oc >= 1) read_lv[base_of(L.a[i])].push_back(lev[i]);
+    if (oc == 2) read_lv[base_of(L.b[i])].push_back(lev[i]);
   }
+  for (auto& v : read_lv) std::sort(v.begin(), v.end());
+  auto cold_read = [&](int row_node, int l) {  // no read of row_node within `far` levels after l
+    const auto& v = read_lv[row_node];
+    auto it = std::upper_bound(v.begin(), v.end(), l);
+    return it == v.end() || *it - l > far;
+  };
   int32_t next_row = 0;
   auto enc = [&](int x) {  // operand encoding: row << 1 | negate
     int bse = base_of(x);
@@ -380,8 +396,8 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
           if (k == SGX_INPUT) operands[2 * (u - t)] = col_of_node[i];
           if (oc >= 1) operands[2 * (u - t)] = enc(L.a[i]);
           if (oc == 2) operands[2 * (u - t) + 1] = enc(L.b[i]);
-          if (oc >= 1 && last_fwd[base_of(L.a[i])] == lev[i]) head.w |= 1 << (2 * (u - t));
-          if (oc == 2 && last_fwd[base_of(L.b[i])] == lev[i]) head.w |= 1 << (2 * (u - t) + 1);
+          if (oc >= 1 && cold_read(base_of(L.a[i]), lev[i])) head.w |= 1 << (2 * (u - t));
+          if (oc == 2 && cold_read(base_of(L.b[i]), lev[i])) head.w |= 1 << (2 * (u - t) + 1);
         }
         P.fwd.push_back(head);
         for (int q = 0; q < kGroup / 2; ++q)
