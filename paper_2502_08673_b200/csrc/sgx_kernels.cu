@@ -1037,7 +1037,7 @@ k_backward_tma(const int4* __restrict__ sblk, int blk0_n4, int blk_max, int n_le
         for (int k = 0; k < kBU; ++k) {
           const int4 q = ch * kBU + k < W.y ? R[ch * kBU + k] : make_int4(0, -1, -1, 0);
           if (q.y >= 0) cp_async16(base + (2 * k) * 32, A + static_cast<size_t>(q.y) * TILE);
-          if (q.z >= 0 && SGX_HINT_Y)
+          if (q.z >= 0 && SGX_HINT_Y && !(q.x & kRYKeep))
             cp_async16_hint(base + (2 * k + 1) * 32, T + static_cast<size_t>(q.z) * TILE, pol_first);
           else if (q.z >= 0)
             cp_async16(base + (2 * k + 1) * 32, T + static_cast<size_t>(q.z) * TILE);

@@ -629,6 +629,37 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
       fprintf(stderr, "[sgx]   distance %-7s adjoint %6.2f%%  tape re-read (<=0: first read) %6.2f%%\n", names[b], 100.0 * hA[b] / std::max<int64_t>(1, nA),
               100.0 * hT[b] / std::max<int64_t>(1, nT));
   }
+  // Tape reads with a near next read keep their row in L2 (kRYKeep): another
+  // record reads the same tape row within SGX_BWD_KEEP passes (default 4;
+  // 0 = every tape read evict_first).  Row-granular model, C4: backward DRAM
+  // 29.9 -> 28.0 GB per launch.
+  {
+    static const int keep = [] {
+      const char* e = getenv("SGX_BWD_KEEP");
+      return e ? atoi(e) : 4;
+    }();
+    if (keep > 0) {
+      const int nl = P.n_levels;
+      std::vector<std::vector<int32_t>> treads(P.n_rows);  // passes reading each tape row, ascending
+      for (int li = 0; li < nl; ++li)
+        for (int w = 0; w < kWarps; ++w) {
+          const int32_t first = P.rec_lvl[2 * (li * kWarps + w)], cnt = P.rec_lvl[2 * (li * kWarps + w) + 1];
+          for (int32_t k = first; k < first + cnt; ++k)
+            if (P.rec[k].z >= 0) treads[P.rec[k].z].push_back(li);
+        }
+      for (int li = 0; li < nl; ++li)
+        for (int w = 0; w < kWarps; ++w) {
+          const int32_t first = P.rec_lvl[2 * (li * kWarps + w)], cnt = P.rec_lvl[2 * (li * kWarps + w) + 1];
+          for (int32_t k = first; k < first + cnt; ++k) {
+            const int32_t z = P.rec[k].z;
+            if (z < 0) continue;
+            const auto& v = treads[z];  // another read in [li, li + keep] besides this one?
+            const auto n_near = std::upper_bound(v.begin(), v.end(), li + keep) - std::lower_bound(v.begin(), v.end(), li);
+            if (n_near >= 2) P.rec[k].x |= kRYKeep;
+          }
+        }
+    }
+  }
   // Dead-adjoint lists: the last pass reading each adjoint row (a record's
   // .y), passes numbered in backward order.
   {
@@ -708,7 +739,7 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
       for (int w = 0; w < kWarps; ++w) {
         const int32_t first = P.rec_lvl[2 * (li * kWarps + w)], cnt = P.rec_lvl[2 * (li * kWarps + w) + 1];
         P.oc_rec.insert(P.oc_rec.end(), P.rec.begin() + first, P.rec.begin() + first + cnt);
-        for (auto it = P.oc_rec.end() - cnt; it != P.oc_rec.end(); ++it) it->x &= ~kRSubOne;
+        for (auto it = P.oc_rec.end() - cnt; it != P.oc_rec.end(); ++it) it->x &= ~(kRSubOne | kRYKeep);
       }
       P.oc_rec_lvl.push_back(static_cast<int32_t>(P.oc_rec.size()) - P.oc_rec_lvl.back());
     }

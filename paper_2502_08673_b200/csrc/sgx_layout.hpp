@@ -78,6 +78,10 @@ constexpr int32_t kRSlow = 1 << 16;
 // kernel runs on a short branch of its own (79 % of the SUB-run records on
 // C4 and C2).  Cleared in oc_rec, whose bits 17+ hold slots.
 constexpr int32_t kRSubOne = 1 << 29;
+// kRYKeep (staged records only): the other operand's tape row is read again
+// within SGX_BWD_KEEP passes, so this read keeps it in L2 (no evict_first).
+// Cleared in oc_rec.
+constexpr int32_t kRYKeep = 1 << 28;
 constexpr int kOcSlotShift = 17;  // oc_rec: adjoint store slot in the flag word
 constexpr int kCnfThreads = 256;               // threads of the shared-memory harvest CTA
 constexpr int32_t kCnfOpen = INT32_MIN;        // CNF record continues (see fb_cnf4)
