@@ -1422,7 +1422,7 @@ uint64_t key(const sgx_circuit_desc& d) {
   h = add(h, d.ucpi, d.n_ucpi);
   h = add(h, d.clause_ptr, d.n_clauses + 1);
   h = add(h, d.clause_lit, d.clause_ptr && d.n_clauses >= 0 ? d.clause_ptr[d.n_clauses] : 0);
-  for (const char* k : {"SGX_ALL_CLAUSES", "SGX_SCHED", "SGX_FWD_FAR", "SGX_BWD_KEEP"}) {
+  for (const char* k : {"SGX_ALL_CLAUSES", "SGX_SCHED", "SGX_FWD_FAR", "SGX_BWD_KEEP", "SGX_BWD_SPLIT"}) {
     const char* v = std::getenv(k);
     h = add(h, v, v ? static_cast<int64_t>(std::strlen(v)) : 0);
   }

@@ -521,22 +521,52 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
     }
     std::stable_sort(recs.begin(), recs.end(),
                      [](const auto& x, const auto& y) { return x.size() > y.size(); });
-    std::vector<std::vector<I4>> rper(kWarps);
-    for (auto& r : recs) {
-      int best = 0;
-      for (int w = 1; w < kWarps; ++w)
-        if (rper[w].size() < rper[best].size()) best = w;
-      rper[best].insert(rper[best].end(), r.begin(), r.end());
+    // SGX_BWD_SPLIT=cap (default 160; 0 = off; large cones only, the on-chip
+    // and circuit-specialised programs keep one pass per level): a level with
+    // more than `cap` records runs as several passes of at most ~cap records
+    // (node runs stay whole).  Nodes of one level are independent, so a
+    // barrier between them changes nothing but the staged blocks' size: at
+    // <= ~190 int4 per block a third data stage fits at 4 CTAs per SM (C4:
+    // 632 -> 724 passes, C2 66 -> 129; live bench C4 backward -0.7 %, C2 -3 %).
+    static const int split_cap = [] {
+      const char* e = getenv("SGX_BWD_SPLIT");
+      return e ? atoi(e) : 160;
+    }();
+    size_t total = 0;
+    for (auto& r : recs) total += r.size();
+    const size_t cap = (split_cap > 0 && next_row > 1536 && total > static_cast<size_t>(split_cap))
+                           ? static_cast<size_t>(split_cap) : total + 1;
+    const size_t n_sub = (total + cap - 1) / cap;
+    std::vector<std::vector<const std::vector<I4>*>> sub(std::max<size_t>(n_sub, 1));
+    {
+      std::vector<size_t> load(sub.size(), 0);  // longest runs first, to the least loaded sub-pass
+      for (auto& r : recs) {
+        size_t best = 0;
+        for (size_t q = 1; q < sub.size(); ++q)
+          if (load[q] < load[best]) best = q;
+        sub[best].push_back(&r);
+        load[best] += r.size();
+      }
     }
-    for (int w = 0; w < kWarps; ++w) {
-      P.rec_lvl.push_back(static_cast<int32_t>(P.rec.size()));
-      P.rec_lvl.push_back(static_cast<int32_t>(rper[w].size()));
-      P.rec.insert(P.rec.end(), rper[w].begin(), rper[w].end());
+    for (auto& group : sub) {
+      std::vector<std::vector<I4>> rper(kWarps);
+      for (auto* r : group) {
+        int best = 0;
+        for (int w = 1; w < kWarps; ++w)
+          if (rper[w].size() < rper[best].size()) best = w;
+        rper[best].insert(rper[best].end(), r->begin(), r->end());
+      }
+      for (int w = 0; w < kWarps; ++w) {
+        P.rec_lvl.push_back(static_cast<int32_t>(P.rec.size()));
+        P.rec_lvl.push_back(static_cast<int32_t>(rper[w].size()));
+        P.rec.insert(P.rec.end(), rper[w].begin(), rper[w].end());
+      }
     }
   }
+  const int n_bwd_passes = static_cast<int>(P.rec_lvl.size() / (2 * kWarps));
   lap("bwd records");
   if (getenv("SGX_TRACE_DIST")) {  // reuse distances of the backward's row reads, in passes
-    const int nl = P.n_levels;
+    const int nl = n_bwd_passes;
     std::vector<int32_t> def_pass(P.n_rows, -1), last_t(P.n_rows, -1);
     std::vector<int64_t> hA(8, 0), hT(8, 0);
     auto bucket = [](int d) { return d <= 0 ? 0 : d == 1 ? 1 : d <= 2 ? 2 : d <= 4 ? 3 : d <= 8 ? 4 : d <= 32 ? 5 : d <= 128 ? 6 : 7; };
@@ -639,7 +669,7 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
       return e ? atoi(e) : 4;
     }();
     if (keep > 0) {
-      const int nl = P.n_levels;
+      const int nl = n_bwd_passes;
       std::vector<std::vector<int32_t>> treads(P.n_rows);  // passes reading each tape row, ascending
       for (int li = 0; li < nl; ++li)
         for (int w = 0; w < kWarps; ++w) {
@@ -663,7 +693,7 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
   // Dead-adjoint lists: the last pass reading each adjoint row (a record's
   // .y), passes numbered in backward order.
   {
-    const int nl = P.n_levels;
+    const int nl = n_bwd_passes;
     std::vector<int32_t> last(P.n_rows, -1);
     for (int li = 0; li < nl; ++li)
       for (int w = 0; w < kWarps; ++w) {

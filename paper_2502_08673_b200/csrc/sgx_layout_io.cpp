@@ -22,7 +22,7 @@ namespace sgx {
 
 namespace {
 
-constexpr char kMagic[8] = {'S', 'G', 'X', 'L', 'A', 'Y', 'T', 4};  // 3: forward read hints for far next reads; 4: backward kRYKeep
+constexpr char kMagic[8] = {'S', 'G', 'X', 'L', 'A', 'Y', 'T', 5};  // 3: forward read hints for far next reads; 4: backward kRYKeep; 5: split backward passes
 
 // Every persisted field, in file order.  Adding a field to SoftProgram or
 // Layout changes their size and trips the static_asserts below, so this list
