@@ -348,7 +348,7 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
   // that long at 512 tiles in flight, and keeping it displaces rows that would
   // (row-granular model, C4: forward DRAM reads 5.77 -> 4.98 GB).
   // read_lv[row]: the levels reading it, ascending (each op at most once).
-  static const int far = [] {
+  const int far = [] {  // read per layout build (forced-variant tests set it per run)
     const char* e = getenv("SGX_FWD_FAR");
     const int v = e ? atoi(e) : 48;
     return v > 0 ? v : (1 << 30);
@@ -528,7 +528,7 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
     // barrier between them changes nothing but the staged blocks' size: at
     // <= ~190 int4 per block a third data stage fits at 4 CTAs per SM (C4:
     // 632 -> 724 passes, C2 66 -> 129; live bench C4 backward -0.7 %, C2 -3 %).
-    static const int split_cap = [] {
+    const int split_cap = [] {
       const char* e = getenv("SGX_BWD_SPLIT");
       return e ? atoi(e) : 160;
     }();
@@ -664,7 +664,7 @@ SoftProgram build_soft(const Layout& L, const std::vector<uint8_t>& in_set) {
   // 0 = every tape read evict_first).  Row-granular model, C4: backward DRAM
   // 29.9 -> 28.0 GB per launch.
   {
-    static const int keep = [] {
+    const int keep = [] {
       const char* e = getenv("SGX_BWD_KEEP");
       return e ? atoi(e) : 4;
     }();

@@ -126,6 +126,10 @@ VARIANTS = [
     # (also where the full tape would win) at one and at two words per CTA
     {"SGX_HARVEST": "live"}, {"SGX_HARVEST": "lw"}, {"SGX_HARVEST": "lw", "SGX_LWW": "1"},
     {"SGX_HARVEST": "lw", "SGX_LWW": "2", "SGX_ALL_CLAUSES": "1"},
+    # one backward pass per level (no split: two data stages), and the L2 read
+    # hints of round 2 off (every backward tape read evict_first, forward last
+    # reads only)
+    {"SGX_BWD_SPLIT": "0"}, {"SGX_BWD_KEEP": "0", "SGX_FWD_FAR": "0"},
 ]
 
 
